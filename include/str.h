@@ -1,0 +1,146 @@
+/*
+ * str.h — C ABI of the B200-native streaming tensor-ring (STR / rSTR) per-batch update.
+ *
+ * Method: Yu & Li, "Tracking Tensor Ring Decompositions of Streaming Tensors",
+ * arXiv 2307.00719 (cited as P:<line> of /root/reference/PAPER.md at build time; the
+ * file is not needed at run time).
+ *
+ * Problem statement: given the TR decomposition of X^old (temporal mode N)
+ * and the intermediate information kept by the method, update the decomposition with the
+ * new temporal block X^new only.  The library keeps, on one GPU (or sharded over several),
+ * the state of Alg. 4: the cores G_1..G_{N-1}, the temporal core G_N (one row
+ * per processed time step), the complementary matrices P_n (I_n x R_nR_{n+1}) and
+ * Q_n (R_nR_{n+1} x R_nR_{n+1}) of Eq. (partial), and the Gram tensors Z_n of
+ * Alg. 4 l.2.  rSTR (Alg. 6; Alg. 7; Alg. 8)
+ * keeps the same P_n/Q_n built from sampled rows and the sampled core slices.
+ *
+ * Conventions
+ *   - Modes are numbered 1..N as in the paper; mode N is time.  All indices are 0-based.
+ *   - Tensor data X (init, batches, fit input) use the paper's linearization P:119:
+ *     element (i_1, ..., i_{N-1}, t) at offset i_1 + I_1*(i_2 + I_2*(... + I_{N-1}*t)).
+ *   - Cores at this boundary use the paper layout G_n in R^{R_n x I_n x R_{n+1}}, first index
+ *     fastest: element (a, i, b) at offset a + R_n*(i + I_n*b), R_{N+1} = R_1.
+ *   - State is always fp64.  The data type of X (STR_F32 / STR_F64) and the precision of the
+ *     dense contraction (STR_CONTRACT_3XTF32 / STR_CONTRACT_F64) are chosen separately.
+ *
+ * Execution model
+ *   - Device work is enqueued on the stream given in the config (or an internal stream when
+ *     NULL) and the call returns without waiting; call str_sync() to wait.  Host-side argument
+ *     errors are reported immediately.  Device-side numerical failures (a non-positive
+ *     pivot in a Cholesky factorization of Q_n) are reported by the next str_sync(),
+ *     str_get_cores(), str_get_temporal_rows() or str_fit() as STR_E_NUMERIC, after which
+ *     the handle is poisoned (every later call returns STR_E_POISONED).
+ *   - A handle is used by one host thread at a time.  Distinct handles may run
+ *     concurrently on distinct streams.
+ *   - No C++ exception crosses this boundary.
+ */
+#ifndef STR_B200_H
+#define STR_B200_H
+
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define STR_API __attribute__((visibility("default")))
+#else
+#define STR_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct str_state str_state; /* opaque; owns all device state */
+
+typedef enum {
+  STR_OK = 0,
+  STR_E_ARG = 1,       /* invalid argument (NULL pointer, bad mode, capacity too small) */
+  STR_E_SHAPE = 2,     /* shape mismatch */
+  STR_E_PRECOND = 3,   /* rSTR with m < max_n R_nR_{n+1}, I_1 % world_size != 0 */
+  STR_E_NUMERIC = 4,   /* Cholesky of Q_n (or the sketched temporal Gram) failed */
+  STR_E_CUDA = 5,      /* CUDA runtime error */
+  STR_E_NCCL = 6,      /* NCCL error (multi-GPU) */
+  STR_E_OOM = 7,       /* device allocation failed */
+  STR_E_POISONED = 8   /* an earlier failure poisoned the handle */
+} str_status;
+
+typedef enum { STR_F32 = 0, STR_F64 = 1 } str_dtype;
+typedef enum { STR_CONTRACT_3XTF32 = 0, STR_CONTRACT_F64 = 1 } str_contract;
+typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2 } str_variant;
+
+typedef struct {
+  int32_t order;          /* N >= 3 */
+  const int64_t *dims;    /* I_1 .. I_{N-1}: GLOBAL sizes of the non-temporal modes */
+  const int32_t *ranks;   /* R_1 .. R_N, each in [1, 16]; R_n R_{n+1} <= 128 */
+  str_dtype dtype;        /* element type of every X passed in */
+  str_contract contract;  /* precision of the X contractions (state is always fp64) */
+  str_variant variant;    /* STR (Alg. 4) or rSTR with uniform (Alg. 7) / leverage (Alg. 8) rows */
+  int64_t sketch_rows;    /* rSTR m; must be >= max_n R_n R_{n+1} */
+  uint64_t seed;          /* rSTR sampler seed (reading R11) */
+  int64_t t_capacity;     /* initial capacity of temporal rows kept on the device (0 = 4096);
+                             grows automatically */
+  int32_t split_k;        /* two-pass split point k in [1, N-2] (0 = automatic) */
+  int32_t world_size;     /* >= 1: X is sharded along mode 1 across world_size processes */
+  int32_t rank;           /* this process' shard: rows [rank*I_1/p, (rank+1)*I_1/p) of mode 1 */
+  const void *nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (ignored if world_size == 1) */
+  int32_t device;         /* CUDA device ordinal */
+  void *stream;           /* cudaStream_t to enqueue on, or NULL for an internal stream */
+} str_config;
+
+/* Alg. 4 l.1-5, Alg. 7 l.1-16, Alg. 8 l.1-17.
+ * X_init: DEVICE pointer to this rank's shard (I_1/p x I_2 x ... x I_{N-1} x t_init), read
+ *         during the call only (caller keeps ownership).
+ * init_cores: HOST array of N pointers to GLOBAL cores in paper layout; core N holds t_init
+ *         temporal rows (R_N x t_init x R_1).  Remark P:386-392: any feasible initialization.
+ * out: receives the handle.  Errors: STR_E_ARG/SHAPE/PRECOND/CUDA/NCCL/OOM. */
+STR_API str_status str_init(const str_config *cfg, const void *X_init, int64_t t_init,
+                    const double *const *init_cores, str_state **out);
+
+/* One time step (Alg. 4 l.7-19; Alg. 7 l.17-41; Alg. 8 l.18-43).
+ * X_new: DEVICE pointer to this rank's shard (I_1/p x ... x I_{N-1} x t_new), t_new >= 1.
+ * Not retained after the enqueued work completes: the method never revisits old data
+ * (SPEC S:438).  Collective when world_size > 1 (every rank calls with the same t_new). */
+STR_API str_status str_update_batch(str_state *h, const void *X_new, int64_t t_new);
+
+/* Same step with X_new in HOST memory (pinned for full speed): the library copies it to the
+ * device on its stream (the copy is part of the enqueued work). */
+STR_API str_status str_update_batch_host(str_state *h, const void *X_new_host, int64_t t_new);
+
+/* Copies GLOBAL core n (1..N) into host_out in paper layout; n = N gives R_N x T x R_1 where
+ * T = str_processed().  capacity is in doubles.  Waits for the stream.  Collective for n = 1
+ * when world_size > 1 (G_1 is row-sharded). */
+STR_API str_status str_get_cores(str_state *h, int32_t n, double *host_out, int64_t capacity);
+
+/* Copies temporal rows [t0, t0+t) of G_N(2) (t x R_N R_1, column r_N + R_N r_1) to host. */
+STR_API str_status str_get_temporal_rows(str_state *h, int64_t t0, int64_t t, double *host_out);
+
+/* ||X - TR(G)||_F / ||X||_F over temporal rows [t0, t0+t), always in fp64 with
+ * direct differences.  X: DEVICE pointer to this rank's shard of those t slices.  Collective
+ * when world_size > 1.  ||X|| = 0 gives STR_E_ARG. Waits for the stream. */
+STR_API str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t, double *rel_err);
+
+/* Waits for all enqueued work; reports deferred numerical failures. */
+STR_API str_status str_sync(str_state *h);
+
+STR_API int64_t str_processed(const str_state *h);          /* T = temporal rows so far */
+STR_API const char *str_error_string(const str_state *h);   /* last error text ("" if none) */
+STR_API void str_destroy(str_state *h);                     /* idempotent on NULL */
+
+/* Number of CUDA kernels this library has launched on the handle's stream so far. */
+STR_API int64_t str_kernel_launches(const str_state *h);
+
+/* Profiling: when enabled, CUDA events bracket the dominant contraction kernels on the
+ * handle's stream; str_profile returns accumulated milliseconds and launch counts of the
+ * pass-1 and pass-2 contractions since the last reset (waits for the stream). */
+STR_API str_status str_set_profiling(str_state *h, int32_t enable);
+STR_API str_status str_profile(str_state *h, double *pass1_ms, int64_t *pass1_launches, double *pass2_ms,
+                       int64_t *pass2_launches);
+
+/* rSTR test hooks: the index table drawn for mode k (1..N) at the most
+ * recent draw (m entries), or force the table used at the next draw of mode k. */
+STR_API str_status str_get_index_table(str_state *h, int32_t mode, int32_t *idx, int64_t m);
+STR_API str_status str_set_index_table(str_state *h, int32_t mode, const int32_t *idx, int64_t m);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* STR_B200_H */

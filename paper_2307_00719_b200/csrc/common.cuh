@@ -1,0 +1,50 @@
+// common.cuh — shared device/host helpers for the STR library (sm_100a only).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#ifndef __CUDA_ARCH__
+#include <string>
+#endif
+
+#define STR_MAXR 16          // max TR rank per mode supported by the register-resident kernels
+#define STR_MAXW 128         // max R_n R_{n+1}
+
+namespace strb200 {
+
+// One factor of a chained slice product: slices G(i) of shape Ra x Rb stored in the
+// G(2) layout used on the device, element (a, b) of slice i at G[i*Ra*Rb + a + Ra*b]
+// (classical mode-2 unfolding, column r_n + R_n r_{n+1}).  The factor's index is
+// i = (e / stride) % I for a flat multi-index e.
+struct Factor {
+  const double *G;
+  int32_t I;
+  int32_t Ra, Rb;
+  int64_t stride;
+};
+
+constexpr int kMaxFactors = 8;
+
+struct FactorList {
+  Factor f[kMaxFactors];
+  int32_t n;
+};
+
+// Absorb descriptor: contract one index of a matrix-valued tensor Y with core slices.
+//   Y has multi-index dims d[0..nd-1] (first fastest) and entries P x Q row-major.
+//   left : Y'(rest)[p', q] = sum_i A(i)[p', p] Y(rest, i)[p, q]    (A: P' x P)
+//   right: Y'(rest)[p, q'] = sum_i Y(rest, i)[p, q] A(i)[q, q']    (A: Q x Q')
+struct AbsorbDesc {
+  int32_t nd;
+  int64_t d[8];
+  int32_t pos;     // which index of Y is contracted
+  int32_t P, Q;    // entry shape of Y
+  int32_t left;    // 1 = left, 0 = right
+  const double *A; // slices in G(2) layout
+  int32_t Ra, Rb;  // A slice shape
+};
+
+__host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+}  // namespace strb200

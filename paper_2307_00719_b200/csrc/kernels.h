@@ -1,0 +1,29 @@
+// kernels.h — host-side launchers of the STR device kernels (internal to libstr).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "common.cuh"
+
+namespace strb200 {
+
+// kernels_small.cu
+void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);
+void launch_absorb(const AbsorbDesc &ad, const double *Y, double *out, int accumulate, cudaStream_t s);
+void launch_gram_z(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
+void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, cudaStream_t s);
+void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate, cudaStream_t s);
+void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s);
+void launch_axpy(const double *x, double *y, int64_t n, cudaStream_t s);
+void launch_set_identity(double *A, int n, cudaStream_t s);
+
+// kernels_contract_f64.cu
+int launch_contract_f64(const void *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
+                        int64_t tn, double *out, double *ws, cudaStream_t s);
+size_t contract_f64_ws_doubles(int64_t M, int64_t K, int W);
+size_t fit_partials(int64_t L, int64_t Rr, int64_t tn);
+int launch_fit(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,
+               int64_t Rr, int64_t tn, double2 *partials, double *acc2, cudaStream_t s);
+
+}  // namespace strb200

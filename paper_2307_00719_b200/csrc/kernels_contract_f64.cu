@@ -1,0 +1,213 @@
+// kernels_contract_f64.cu — FP64 contraction of X_new with a chained-slice table.
+//
+// The two passes of the exact two-pass schedule evaluate
+// the products X^new_[n] G^{≠n}_[2] of Alg. 4 l.9 and l.14 for every mode:
+//   pass 1: Y_L[(l,t)][w] = sum_r  X[l + L r + L Rr t] T_R[r][w]       (M = L*t, K = Rr)
+//   pass 2: Y_R[r][w]     = sum_{l,t} X[l + L r + L Rr t] T_L[l + L t][w]  (M = Rr, K = L*t)
+// where l runs over the left modes (1..k), r over the right modes (k+1..N-1), and the tables
+// hold products of TR-core lateral slices (Def. 3).  This file is the FP64 path
+// (DFMA, fp64 accumulation; used where cond(Q_n) demands it and as the reference-precision
+// GPU path).  Split-K partials are reduced in a fixed order, so results are deterministic.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace strb200 {
+
+constexpr int BM = 64, BK = 16;
+
+template <typename T, int PASS, int WT>
+__global__ void __launch_bounds__(256) k_contract_f64(const T *__restrict__ X, const double *__restrict__ Btab, int W,
+                                                      int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
+                                                      int64_t kchunk, double *__restrict__ part) {
+  __shared__ double As[BK][BM + 1];
+  __shared__ double Bs[BK][WT];
+  const int tid = threadIdx.x;
+  const int tx = tid % 16, ty = tid / 16;
+  const int64_t m0 = (int64_t)blockIdx.x * BM;
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(K, k0 + kchunk);
+  const int64_t LRr = L * Rr;
+  constexpr int NJ = WT / 16;
+  double acc[4][NJ];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) acc[i][j] = 0.0;
+
+  for (int64_t kb = k0; kb < k1; kb += BK) {
+    // A tile: BM x BK
+    for (int e = tid; e < BM * BK; e += 256) {
+      int mm, kk;
+      if (PASS == 1) { mm = e % BM; kk = e / BM; }   // m (l) contiguous
+      else           { kk = e % BK; mm = e / BK; }   // k (l) contiguous
+      int64_t m = m0 + mm, k = kb + kk;
+      double v = 0.0;
+      if (m < M && k < k1) {
+        int64_t off;
+        if (PASS == 1) { int64_t l = m % L, t = m / L; off = l + L * k + LRr * t; }
+        else           { int64_t l = k % L, t = k / L; off = l + L * m + LRr * t; }
+        v = (double)X[off];
+      }
+      As[kk][mm] = v;
+    }
+    for (int e = tid; e < BK * WT; e += 256) {
+      int kk = e / WT, w = e % WT;
+      int64_t k = kb + kk;
+      Bs[kk][w] = (k < k1 && w < W) ? Btab[k * W + w] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < BK; ++kk) {
+      double a[4], b[NJ];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[j] = Bs[kk][tx + 16 * j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < NJ; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+  double *o = part + (int64_t)blockIdx.y * M * W;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    int64_t m = m0 + ty * 4 + i;
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int w = tx + 16 * j;
+      if (w < W) o[m * W + w] = acc[i][j];
+    }
+  }
+}
+
+__global__ void k_reduce_splits(const double *__restrict__ part, int splits, int64_t n, double *__restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int j = 0; j < splits; ++j) s += part[j * n + i];
+  out[i] = s;
+}
+
+template <typename T, int PASS>
+static void dispatch_w(const T *X, const double *B, int W, int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
+                       int64_t kchunk, int splits, double *part, cudaStream_t s) {
+  dim3 grid((unsigned)cdiv(M, BM), (unsigned)splits);
+  if (W <= 32)
+    k_contract_f64<T, PASS, 32><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
+  else if (W <= 64)
+    k_contract_f64<T, PASS, 64><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
+  else
+    k_contract_f64<T, PASS, 128><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
+}
+
+int contract_f64_splits(int64_t M, int64_t K) {
+  int64_t mt = cdiv(M, BM);
+  int64_t want = cdiv(2 * 148, mt);
+  int64_t maxs = cdiv(K, 4 * BK);
+  int64_t s = want < maxs ? want : maxs;
+  if (s < 1) s = 1;
+  if (s > 64) s = 64;
+  return (int)s;
+}
+
+// Returns the number of kernel launches.
+int launch_contract_f64(const void *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
+                        int64_t tn, double *out, double *ws, cudaStream_t s) {
+  int64_t M = pass == 1 ? L * tn : Rr;
+  int64_t K = pass == 1 ? Rr : L * tn;
+  int splits = contract_f64_splits(M, K);
+  int64_t kchunk = cdiv(cdiv(K, splits), BK) * BK;
+  splits = (int)cdiv(K, kchunk);
+  double *part = splits == 1 ? out : ws;
+  if (x_is_f64) {
+    if (pass == 1) dispatch_w<double, 1>((const double *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    else dispatch_w<double, 2>((const double *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+  } else {
+    if (pass == 1) dispatch_w<float, 1>((const float *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    else dispatch_w<float, 2>((const float *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+  }
+  if (splits == 1) return 1;
+  int64_t n = M * W;
+  k_reduce_splits<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(ws, splits, n, out);
+  return 2;
+}
+
+size_t contract_f64_ws_doubles(int64_t M, int64_t K, int W) {
+  int splits = contract_f64_splits(M, K);
+  return (size_t)splits * M * W;
+}
+
+// ------------------------------------------------------------------------------------------
+// Fit partial sums over temporal rows: X̂[l + L r + L Rr t] = sum_{p,q} TLf[(l,t)][p][q] TR[r][q][p]
+// (Tr(G_1...G_{N-1} G_N(t)) = Tr(TLf TR)).  Per block: sum (X - X̂)^2 and sum X^2.
+template <typename T>
+__global__ void __launch_bounds__(256) k_fit_partial(const T *__restrict__ X, const double *__restrict__ TLf,
+                                                     const double *__restrict__ TR, int Ra, int Rb, int64_t L,
+                                                     int64_t Rr, int64_t tn, double2 *__restrict__ out) {
+  // grid: x = l-blocks, y = r, z = t
+  extern __shared__ double trs[];   // Rb x Ra (TR[r] row-major q*Ra + p)
+  const int64_t r = blockIdx.y, t = blockIdx.z;
+  const int W = Ra * Rb;
+  for (int e = threadIdx.x; e < W; e += blockDim.x) trs[e] = TR[r * W + e];
+  __syncthreads();
+  int64_t l = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  double res = 0.0, nx = 0.0;
+  if (l < L) {
+    const double *tl = TLf + (l + L * t) * W;   // Ra x Rb row-major p*Rb + q
+    double xh = 0.0;
+    for (int p = 0; p < Ra; ++p)
+      for (int q = 0; q < Rb; ++q) xh = fma(tl[p * Rb + q], trs[q * Ra + p], xh);
+    double x = (double)X[l + L * r + L * Rr * t];
+    double d = x - xh;
+    res = d * d;
+    nx = x * x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    res += __shfl_xor_sync(0xffffffffu, res, o);
+    nx += __shfl_xor_sync(0xffffffffu, nx, o);
+  }
+  __shared__ double sr[8], sn[8];
+  int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  if (lane == 0) { sr[warp] = res; sn[warp] = nx; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0.0, b = 0.0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) { a += sr[w]; b += sn[w]; }
+    int64_t bid = blockIdx.x + (int64_t)gridDim.x * (blockIdx.y + (int64_t)gridDim.y * blockIdx.z);
+    out[bid] = make_double2(a, b);
+  }
+}
+
+__global__ void k_fit_reduce(const double2 *__restrict__ in, int64_t n, double *__restrict__ acc2) {
+  // single block, fixed-order strided sums then tree
+  __shared__ double sa[256], sb[256];
+  double a = 0.0, b = 0.0;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) { a += in[i].x; b += in[i].y; }
+  sa[threadIdx.x] = a;
+  sb[threadIdx.x] = b;
+  __syncthreads();
+  for (int o = 128; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) { sa[threadIdx.x] += sa[threadIdx.x + o]; sb[threadIdx.x] += sb[threadIdx.x + o]; }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) { acc2[0] += sa[0]; acc2[1] += sb[0]; }
+}
+
+size_t fit_partials(int64_t L, int64_t Rr, int64_t tn) { return (size_t)cdiv(L, 256) * Rr * tn; }
+
+int launch_fit(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,
+               int64_t Rr, int64_t tn, double2 *partials, double *acc2, cudaStream_t s) {
+  dim3 grid((unsigned)cdiv(L, 256), (unsigned)Rr, (unsigned)tn);
+  size_t smem = sizeof(double) * Ra * Rb;
+  if (x_is_f64)
+    k_fit_partial<double><<<grid, 256, smem, s>>>((const double *)X, TLf, TR, Ra, Rb, L, Rr, tn, partials);
+  else
+    k_fit_partial<float><<<grid, 256, smem, s>>>((const float *)X, TLf, TR, Ra, Rb, L, Rr, tn, partials);
+  k_fit_reduce<<<1, 256, 0, s>>>(partials, (int64_t)grid.x * grid.y * grid.z, acc2);
+  return 2;
+}
+
+}  // namespace strb200

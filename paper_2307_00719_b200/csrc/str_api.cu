@@ -1,0 +1,851 @@
+// str_api.cu — C ABI (include/str.h) and the per-batch orchestration of STR (Alg. 4,
+// PAPER.md P:353-384) on one B200 (and its mode-1-sharded multi-GPU form).
+//
+// Per batch ("exact two-pass schedule"):
+//   0. Gram-chain suffixes Sf_n = Z_{N-1} ... Z_{n+1} from the current Z's, and
+//      H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8).
+//   1. table T_R = G_{k+1}(i_{k+1}) ... G_{N-1}(i_{N-1}) (old cores) and pass 1 over X_new -> Y_L.
+//   2. temporal: M_N = sum_l (G_1...G_k)(l) Y_L(l,t); G_N^new = M_N (H^{≠N}_<2>)^{-1}
+//      (l.9); append (l.10); Z_N^new.
+//   3. left modes j = 1..k: M_j from Y_L, G_N^new and the current cores; P_j += M_j (l.14);
+//      Q_j += (Lp_j Z_N^new Sf_j)_<2> (l.15-16, Prop. 1); G_j = P_j Q_j^{-1} (l.17); Z_j (l.18).
+//   4. table T_L = G_N^new(t) G_1(i_1)...G_k(i_k) (new cores) and pass 2 over X_new -> Y_R.
+//   5. right modes j = k+1..N-1: as 3, from Y_R.
+// Everything is enqueued on one stream; no host synchronization inside a batch (STR).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "str.h"
+#include "str_internal.h"
+
+using namespace strb200;
+
+// ------------------------------------------------------------------------------------ helpers
+#define CU(call)                                                                     \
+  do {                                                                               \
+    cudaError_t _e = (call);                                                         \
+    if (_e != cudaSuccess) return fail(h, STR_E_CUDA, std::string(#call) + ": " +    \
+                                       cudaGetErrorString(_e));                     \
+  } while (0)
+
+#define TRY(call)                  \
+  do {                             \
+    str_status _s = (call);        \
+    if (_s != STR_OK) return _s;   \
+  } while (0)
+
+static str_status fail(str_state *h, str_status s, const std::string &msg) {
+  if (h) {
+    h->err = msg;
+    if (s == STR_E_CUDA || s == STR_E_NUMERIC || s == STR_E_NCCL || s == STR_E_OOM) h->poisoned = true;
+  }
+  return s;
+}
+
+static str_status ensure(str_state *h, DevBuf &b, size_t bytes) {
+  if (b.bytes >= bytes) return STR_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  if (bytes == 0) return STR_OK;
+  cudaError_t e = cudaMalloc(&b.p, bytes);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(h, STR_E_OOM, std::string("cudaMalloc failed: ") + cudaGetErrorString(e));
+  }
+  b.bytes = bytes;
+  return STR_OK;
+}
+
+static str_status check_launch(str_state *h, const char *what) {
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ NCCL (dlopen)
+#include <nccl.h>
+struct NcclApi {
+  void *lib = nullptr;
+  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
+  const char *(*getErrorString)(ncclResult_t) = nullptr;
+};
+static NcclApi g_nccl;
+
+static bool load_nccl(std::string &why) {
+  if (g_nccl.lib) return true;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *nm : names) {
+    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.lib) break;
+  }
+  if (!g_nccl.lib) {
+    why = "cannot dlopen libnccl.so.2";
+    return false;
+  }
+  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(g_nccl.lib, "ncclCommInitRank");
+  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(g_nccl.lib, "ncclAllReduce");
+  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(g_nccl.lib, "ncclAllGather");
+  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(g_nccl.lib, "ncclCommDestroy");
+  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(g_nccl.lib, "ncclGetErrorString");
+  if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy) {
+    why = "libnccl is missing symbols";
+    return false;
+  }
+  return true;
+}
+
+// Sum-allreduce of fp64 device data across the mode-1 shards (no-op on one GPU).
+static str_status allreduce(str_state *h, double *buf, size_t n) {
+  if (h->p == 1 || n == 0) return STR_OK;
+  ncclResult_t r = g_nccl.allReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)h->comm, h->st);
+  if (r != ncclSuccess)
+    return fail(h, STR_E_NCCL, std::string("ncclAllReduce: ") +
+                                   (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  h->collectives++;
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ geometry
+static inline int RR(const str_state *h, int n) { return h->R[(n - 1) % h->N]; }   // R_n, n in 1..N+1
+
+static Factor core_factor(const str_state *h, int n, int64_t stride) {
+  const ModeBuf &m = h->md[n - 1];
+  Factor f;
+  f.G = (const double *)m.G.p;
+  f.I = (int32_t)m.I;
+  f.Ra = m.Ra;
+  f.Rb = m.Rb;
+  f.stride = stride;
+  return f;
+}
+
+static Factor temporal_factor(const str_state *h, int64_t row0, int64_t rows, int64_t stride) {
+  Factor f;
+  f.G = (const double *)h->GN.p + row0 * (int64_t)h->SN;
+  f.I = (int32_t)rows;
+  f.Ra = RR(h, h->N);
+  f.Rb = RR(h, 1);
+  f.stride = stride;
+  return f;
+}
+
+// ------------------------------------------------------------------------------------ absorbs
+struct AOp {
+  int mode;      // mode id whose index is contracted (N = time)
+  int left;
+  Factor A;      // slices (stride unused)
+};
+
+// Runs a sequence of absorbs starting from Y (multi-index over `modes`, entries P x Q).
+// The final result is written (accumulate=0) or added (accumulate=1) into dst.
+static str_status run_absorbs(str_state *h, const double *Y, std::vector<int> modes, std::vector<int64_t> dims, int P,
+                              int Q, const std::vector<AOp> &ops, double *dst, int accumulate) {
+  if (ops.empty()) {
+    int64_t n = (int64_t)P * Q;
+    for (auto d : dims) n *= d;
+    if (accumulate) {
+      launch_axpy(Y, dst, n, h->st);
+      h->launches++;
+    } else {
+      CU(cudaMemcpyAsync(dst, Y, n * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
+    }
+    return check_launch(h, "axpy");
+  }
+  const double *cur = Y;
+  for (size_t s = 0; s < ops.size(); ++s) {
+    const AOp &op = ops[s];
+    AbsorbDesc ad;
+    ad.nd = (int)dims.size();
+    for (int j = 0; j < ad.nd; ++j) ad.d[j] = dims[j];
+    ad.pos = (int)(std::find(modes.begin(), modes.end(), op.mode) - modes.begin());
+    ad.P = P;
+    ad.Q = Q;
+    ad.left = op.left;
+    ad.A = op.A.G;
+    ad.Ra = op.A.Ra;
+    ad.Rb = op.A.Rb;
+    bool last = s + 1 == ops.size();
+    double *out = last ? dst : (double *)((s % 2 == 0) ? h->tmpA.p : h->tmpB.p);
+    launch_absorb(ad, cur, out, last ? accumulate : 0, h->st);
+    h->launches++;
+    TRY(check_launch(h, "absorb"));
+    if (op.left) P = op.A.Ra; else Q = op.A.Rb;
+    modes.erase(modes.begin() + ad.pos);
+    dims.erase(dims.begin() + ad.pos);
+    cur = out;
+  }
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ chains
+// out = A (MxK) * B (KxN), with identity flags.
+static str_status chain_mul(str_state *h, const double *A, bool A_id, const double *B, bool B_id, double *out, int M,
+                            int N, int K) {
+  if (A_id && B_id) {
+    launch_set_identity(out, M, h->st);
+  } else if (A_id) {
+    CU(cudaMemcpyAsync(out, B, sizeof(double) * K * N, cudaMemcpyDeviceToDevice, h->st));
+    return STR_OK;
+  } else if (B_id) {
+    CU(cudaMemcpyAsync(out, A, sizeof(double) * M * K, cudaMemcpyDeviceToDevice, h->st));
+    return STR_OK;
+  } else {
+    launch_dgemm(A, B, out, M, N, K, h->st);
+  }
+  h->launches++;
+  return check_launch(h, "dgemm");
+}
+
+// Sf_n = Z_{N-1} ... Z_{n+1} (Sf_{N-1} = I), from the current Z's (Alg. 4 l.15 right part).
+static str_status build_suffixes(str_state *h) {
+  const int N = h->N;
+  for (int n = N - 2; n >= 1; --n) {
+    // Sf_n = Sf_{n+1} * Zm_{n+1};  Sf_{n+1}: R_N^2 x R_{n+2}^2, Zm_{n+1}: R_{n+2}^2 x R_{n+1}^2
+    int M = RR(h, N) * RR(h, N), K = RR(h, n + 2) * RR(h, n + 2), Nc = RR(h, n + 1) * RR(h, n + 1);
+    bool id = (n + 1 == N - 1);
+    TRY(chain_mul(h, (const double *)h->Sf[n + 1].p, id, (const double *)h->md[n].Zm.p, false,
+                  (double *)h->Sf[n].p, M, Nc, K));
+  }
+  return STR_OK;
+}
+
+// H = Lp * Zmid * Sf_n, then Q (+)= H_<2>.
+static str_status q_update(str_state *h, int n, const double *Lp, bool Lp_id, const double *Zmid, int accumulate,
+                           double *Qout) {
+  const int N = h->N;
+  int a = RR(h, n) * RR(h, n), b = RR(h, 1) * RR(h, 1), c = RR(h, N) * RR(h, N), d = RR(h, n + 1) * RR(h, n + 1);
+  bool Sf_id = (n == N - 1);
+  TRY(chain_mul(h, Lp, Lp_id, Zmid, false, (double *)h->T1.p, a, c, b));
+  TRY(chain_mul(h, (const double *)h->T1.p, false, (const double *)h->Sf[n].p, Sf_id, (double *)h->H.p, a, d, c));
+  launch_q_accum((const double *)h->H.p, RR(h, n), RR(h, n + 1), Qout, accumulate, h->st);
+  h->launches++;
+  return check_launch(h, "q_accum");
+}
+
+// ------------------------------------------------------------------------------------ contraction
+static str_status contract(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out) {
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (h->profiling) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0, h->st);
+  }
+  int nl = 0;
+  if (h->contract == STR_CONTRACT_3XTF32 && h->tf32_ready) {
+    nl = launch_contract_tf32(h, X, pass, tab, W, tn, out);
+    if (nl < 0) return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
+  } else {
+    nl = launch_contract_f64(X, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn, out, (double *)h->ws.p, h->st);
+  }
+  h->launches += nl;
+  if (h->profiling) {
+    cudaEventRecord(e1, h->st);
+    h->prof_events.push_back({pass, e0, e1});
+  }
+  return check_launch(h, pass == 1 ? "contract pass 1" : "contract pass 2");
+}
+
+// ------------------------------------------------------------------------------------ workspaces
+static str_status ensure_workspace(str_state *h, int64_t tn) {
+  if (tn <= h->ws_t) return STR_OK;
+  const int N = h->N, k = h->k;
+  const int W1 = RR(h, k + 1) * RR(h, N);
+  const int64_t Lt = h->L * tn;
+  TRY(ensure(h, h->TR, sizeof(double) * h->Rr * W1));
+  TRY(ensure(h, h->TL, sizeof(double) * Lt * W1));
+  TRY(ensure(h, h->YL, sizeof(double) * Lt * W1));
+  TRY(ensure(h, h->YR, sizeof(double) * h->Rr * W1));
+  TRY(ensure(h, h->Wt, sizeof(double) * h->L * RR(h, k + 1) * RR(h, 1)));
+  int64_t big = std::max<int64_t>(Lt, h->Rr) * STR_MAXR * STR_MAXR;
+  TRY(ensure(h, h->tmpA, sizeof(double) * big));
+  TRY(ensure(h, h->tmpB, sizeof(double) * big));
+  int64_t mt = tn * h->SN;
+  for (auto &m : h->md) mt = std::max<int64_t>(mt, m.I * m.Ra * m.Rb);
+  TRY(ensure(h, h->Mt, sizeof(double) * mt));
+  size_t ws = std::max(contract_f64_ws_doubles(Lt, h->Rr, W1), contract_f64_ws_doubles(h->Rr, Lt, W1));
+  TRY(ensure(h, h->ws, sizeof(double) * ws));
+  if (h->contract == STR_CONTRACT_3XTF32) TRY(tf32_ensure_workspace(h, tn));
+  h->ws_t = tn;
+  return STR_OK;
+}
+
+static str_status ensure_temporal_capacity(str_state *h, int64_t need) {
+  if (need <= h->Tcap) return STR_OK;
+  int64_t cap = std::max<int64_t>(need, 2 * h->Tcap);
+  DevBuf nb;
+  TRY(ensure(h, nb, sizeof(double) * cap * h->SN));
+  if (h->T > 0) CU(cudaMemcpyAsync(nb.p, h->GN.p, sizeof(double) * h->T * h->SN, cudaMemcpyDeviceToDevice, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  cudaFree(h->GN.p);
+  h->GN = nb;
+  h->Tcap = cap;
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ left/right modes
+// Absorb ops producing M_j for a left-group mode j (1 <= j <= k) from W (modes 1..k, entries
+// R_{k+1} x R_1): right with G_1..G_{j-1} (current = new), left with G_k..G_{j+1} (old).
+static std::vector<AOp> left_ops(const str_state *h, int j) {
+  std::vector<AOp> ops;
+  for (int i = 1; i < j; ++i) ops.push_back({i, 0, core_factor(h, i, 1)});
+  for (int i = h->k; i > j; --i) ops.push_back({i, 1, core_factor(h, i, 1)});
+  return ops;
+}
+
+// M_j for a right-group mode j (k < j < N) from Y_R (modes k+1..N-1, entries R_N x R_{k+1}):
+// left with G_{N-1}..G_{j+1} (old), right with G_{k+1}..G_{j-1} (new).
+static std::vector<AOp> right_ops(const str_state *h, int j) {
+  std::vector<AOp> ops;
+  for (int i = h->N - 1; i > j; --i) ops.push_back({i, 1, core_factor(h, i, 1)});
+  for (int i = h->k + 1; i < j; ++i) ops.push_back({i, 0, core_factor(h, i, 1)});
+  return ops;
+}
+
+static void left_modes(const str_state *h, std::vector<int> &modes, std::vector<int64_t> &dims) {
+  modes.clear();
+  dims.clear();
+  for (int i = 1; i <= h->k; ++i) {
+    modes.push_back(i);
+    dims.push_back(h->md[i - 1].I);
+  }
+}
+
+static void right_modes(const str_state *h, std::vector<int> &modes, std::vector<int64_t> &dims) {
+  modes.clear();
+  dims.clear();
+  for (int i = h->k + 1; i <= h->N - 1; ++i) {
+    modes.push_back(i);
+    dims.push_back(h->md[i - 1].I);
+  }
+}
+
+// T_R[r] = G_{k+1}(i_{k+1}) ... G_{N-1}(i_{N-1})   (R_{k+1} x R_N, row-major)
+static str_status build_TR(str_state *h) {
+  FactorList fl;
+  fl.n = 0;
+  int64_t stride = 1;
+  for (int i = h->k + 1; i <= h->N - 1; ++i) {
+    fl.f[fl.n++] = core_factor(h, i, stride);
+    stride *= h->md[i - 1].I;
+  }
+  launch_build_table(fl, h->Rr, (double *)h->TR.p, h->st);
+  h->launches++;
+  return check_launch(h, "build_table TR");
+}
+
+// T_L[l + L t] = G_N(t0 + t) G_1(i_1) ... G_k(i_k)   (R_N x R_{k+1}, row-major)
+static str_status build_TL(str_state *h, int64_t t0, int64_t tn, double *out) {
+  FactorList fl;
+  fl.n = 0;
+  fl.f[fl.n++] = temporal_factor(h, t0, tn, h->L);
+  int64_t stride = 1;
+  for (int i = 1; i <= h->k; ++i) {
+    fl.f[fl.n++] = core_factor(h, i, stride);
+    stride *= h->md[i - 1].I;
+  }
+  launch_build_table(fl, h->L * tn, out, h->st);
+  h->launches++;
+  return check_launch(h, "build_table TL");
+}
+
+// Solve G_j = P_j Q_j^{-1} and refresh Z_j (Alg. 4 l.17-18).
+static str_status solve_mode(str_state *h, int j) {
+  ModeBuf &m = h->md[j - 1];
+  const int S = m.Ra * m.Rb;
+  launch_chol_solve((const double *)m.Q.p, S, (const double *)m.P.p, m.I, (double *)m.G.p, h->d_info, h->st);
+  h->launches++;
+  TRY(check_launch(h, "chol_solve"));
+  launch_gram_z((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
+  h->launches++;
+  TRY(check_launch(h, "gram_z"));
+  if (j == 1) TRY(allreduce(h, (double *)m.Zm.p, (size_t)m.Ra * m.Ra * m.Rb * m.Rb));   // G_1 row-sharded
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ update (STR)
+static str_status update_det(str_state *h, const void *X, int64_t tn) {
+  const int N = h->N, k = h->k;
+  const int W1 = RR(h, k + 1) * RR(h, N);
+  TRY(ensure_workspace(h, tn));
+  TRY(ensure_temporal_capacity(h, h->T + tn));
+  // 0. suffix chains and H^{≠N} (Alg. 4 l.8)
+  TRY(build_suffixes(h));
+  {
+    int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
+    TRY(chain_mul(h, (const double *)h->Sf[1].p, false, (const double *)h->md[0].Zm.p, false,
+                  (double *)h->H.p, M, Nc, K));
+    launch_q_accum((const double *)h->H.p, RR(h, N), RR(h, 1), (double *)h->Hq.p, 0, h->st);
+    h->launches++;
+  }
+  // 1. pass 1 with the old cores
+  TRY(build_TR(h));
+  TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
+  // 2. temporal mode: M_N = (G_1...G_k) Y_L summed over l
+  std::vector<int> modes;
+  std::vector<int64_t> dims;
+  left_modes(h, modes, dims);
+  modes.push_back(N);
+  dims.push_back(tn);
+  std::vector<AOp> ops;
+  for (int i = k; i >= 1; --i) ops.push_back({i, 1, core_factor(h, i, 1)});
+  double *Mt = (double *)h->Mt.p;
+  TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), ops, Mt, 0));
+  TRY(allreduce(h, Mt, (size_t)tn * h->SN));                                   // site C1
+  double *GN_new = (double *)h->GN.p + h->T * h->SN;
+  launch_chol_solve((const double *)h->Hq.p, h->SN, Mt, tn, GN_new, h->d_info, h->st);   // l.9 (+ l.10 append)
+  h->launches++;
+  TRY(check_launch(h, "chol_solve temporal"));
+  launch_gram_z(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);            // Z_N^new
+  h->launches++;
+  // W = Y_L absorbed over t with G_N^new on the right: modes 1..k, entries R_{k+1} x R_1
+  {
+    std::vector<AOp> o1 = {{N, 0, temporal_factor(h, h->T, tn, 1)}};
+    TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
+  }
+  // 3. left modes
+  bool Lp_id = true;
+  int lp_cur = 0;
+  for (int j = 1; j <= k; ++j) {
+    ModeBuf &m = h->md[j - 1];
+    left_modes(h, modes, dims);
+    auto lo = left_ops(h, j);
+    if (j == 1 || h->p == 1) {
+      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, (double *)m.P.p, 1));
+    } else {   // M_j sums over the sharded i_1: reduce before accumulating (site C2)
+      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
+      TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
+      launch_axpy(Mt, (double *)m.P.p, m.I * m.Ra * m.Rb, h->st);
+      h->launches++;
+    }
+    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
+    TRY(solve_mode(h, j));
+    // Lp_{j+1} = Zm_j * Lp_j
+    int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
+    TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
+                  (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
+    lp_cur = 1 - lp_cur;
+    Lp_id = false;
+  }
+  // 4. pass 2 with the new cores
+  TRY(build_TL(h, h->T, tn, (double *)h->TL.p));
+  TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
+  TRY(allreduce(h, (double *)h->YR.p, (size_t)h->Rr * W1));                  // site C2'
+  // 5. right modes
+  for (int j = k + 1; j <= N - 1; ++j) {
+    ModeBuf &m = h->md[j - 1];
+    right_modes(h, modes, dims);
+    TRY(run_absorbs(h, (const double *)h->YR.p, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p,
+                    1));
+    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
+    TRY(solve_mode(h, j));
+    if (j < N - 1) {
+      int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
+      TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
+                    (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
+      lp_cur = 1 - lp_cur;
+      Lp_id = false;
+    }
+  }
+  h->T += tn;
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ init (STR)
+// Alg. 4 l.1-5: Z_1..Z_N, P_n = X_init[n] G^{≠n}_[2], Q_n = H^{≠n}_<2> with all init cores.
+static str_status init_det(str_state *h, const void *X, int64_t tn) {
+  const int N = h->N, k = h->k;
+  const int W1 = RR(h, k + 1) * RR(h, N);
+  TRY(ensure_workspace(h, tn));
+  // Z_N over the whole init temporal core
+  launch_gram_z((const double *)h->GN.p, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);
+  h->launches++;
+  TRY(build_suffixes(h));
+  // pass 1 (init cores), W from the init temporal rows
+  TRY(build_TR(h));
+  TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
+  std::vector<int> modes;
+  std::vector<int64_t> dims;
+  left_modes(h, modes, dims);
+  modes.push_back(N);
+  dims.push_back(tn);
+  {
+    std::vector<AOp> o1 = {{N, 0, temporal_factor(h, 0, tn, 1)}};
+    TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
+  }
+  double *Mt = (double *)h->Mt.p;
+  bool Lp_id = true;
+  int lp_cur = 0;
+  for (int j = 1; j <= N - 1; ++j) {
+    ModeBuf &m = h->md[j - 1];
+    if (j <= k) {
+      left_modes(h, modes, dims);
+      auto lo = left_ops(h, j);
+      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
+      if (j > 1) TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
+    } else {
+      if (j == k + 1) {
+        TRY(build_TL(h, 0, tn, (double *)h->TL.p));
+        TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
+        TRY(allreduce(h, (double *)h->YR.p, (size_t)h->Rr * W1));
+      }
+      right_modes(h, modes, dims);
+      TRY(run_absorbs(h, (const double *)h->YR.p, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), Mt, 0));
+    }
+    CU(cudaMemcpyAsync(m.P.p, Mt, sizeof(double) * m.I * m.Ra * m.Rb, cudaMemcpyDeviceToDevice, h->st));
+    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 0, (double *)m.Q.p));
+    if (j < N - 1) {
+      int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
+      TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
+                    (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
+      lp_cur = 1 - lp_cur;
+      Lp_id = false;
+    }
+  }
+  return STR_OK;
+}
+
+// ------------------------------------------------------------------------------------ ABI
+static str_status deferred_check(str_state *h) {
+  if (h->poisoned) return STR_E_POISONED;
+  cudaError_t e = cudaStreamSynchronize(h->st);
+  if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("stream: ") + cudaGetErrorString(e));
+  int info = 0;
+  e = cudaMemcpy(&info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("info: ") + cudaGetErrorString(e));
+  if (info) return fail(h, STR_E_NUMERIC, "Cholesky of Q_n failed (non-positive pivot)");
+  return STR_OK;
+}
+
+static int auto_split(const std::vector<int64_t> &dims, int N) {
+  // choose k in [1, N-2] minimizing |Y_L| + |Y_R| relative sizes (prod of left dims ~ small)
+  int best = 1;
+  double bestc = 1e300;
+  for (int k = 1; k <= N - 2; ++k) {
+    double L = 1, Rr = 1;
+    for (int i = 0; i < k; ++i) L *= (double)dims[i];
+    for (int i = k; i < N - 1; ++i) Rr *= (double)dims[i];
+    double c = L + Rr;
+    if (c < bestc) {
+      bestc = c;
+      best = k;
+    }
+  }
+  return best;
+}
+
+extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_t t_init,
+                               const double *const *init_cores, str_state **out) {
+  if (!cfg || !out || !init_cores || !X_init) return STR_E_ARG;
+  *out = nullptr;
+  const int N = cfg->order;
+  if (N < 3 || !cfg->dims || !cfg->ranks) return STR_E_ARG;
+  if (t_init < 1) return STR_E_SHAPE;
+  for (int n = 0; n < N; ++n)
+    if (cfg->ranks[n] < 1 || cfg->ranks[n] > STR_MAXR) return STR_E_ARG;
+  for (int n = 0; n < N; ++n)
+    if (cfg->ranks[n] * cfg->ranks[(n + 1) % N] > STR_MAXW) return STR_E_ARG;
+  for (int n = 0; n < N - 1; ++n)
+    if (cfg->dims[n] < 1) return STR_E_SHAPE;
+  const int p = cfg->world_size < 1 ? 1 : cfg->world_size;
+  if (cfg->rank < 0 || cfg->rank >= p) return STR_E_ARG;
+  if (cfg->dims[0] % p != 0) return STR_E_PRECOND;
+  if (cfg->split_k < 0 || cfg->split_k > N - 2) return STR_E_ARG;
+  if (cfg->dtype != STR_F32 && cfg->dtype != STR_F64) return STR_E_ARG;
+  if (cfg->variant != STR_DET) {
+    int64_t need = 0;
+    for (int n = 0; n < N; ++n) need = std::max<int64_t>(need, (int64_t)cfg->ranks[n] * cfg->ranks[(n + 1) % N]);
+    if (cfg->sketch_rows < need) return STR_E_PRECOND;
+  }
+
+  str_state *h = new str_state();
+  h->N = N;
+  h->dims_g.assign(cfg->dims, cfg->dims + N - 1);
+  h->R.assign(cfg->ranks, cfg->ranks + N);
+  h->dtype = cfg->dtype;
+  h->contract = cfg->contract;
+  h->variant = cfg->variant;
+  h->m = cfg->sketch_rows;
+  h->seed = cfg->seed;
+  h->p = p;
+  h->rank = cfg->rank;
+  h->device = cfg->device;
+  h->k = cfg->split_k ? cfg->split_k : auto_split(h->dims_g, N);
+  h->xbytes = cfg->dtype == STR_F64 ? 8 : 4;
+
+  cudaError_t e = cudaSetDevice(cfg->device);
+  if (e != cudaSuccess) {
+    delete h;
+    return STR_E_CUDA;
+  }
+  if (cfg->stream) {
+    h->st = (cudaStream_t)cfg->stream;
+    h->own_stream = false;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+      delete h;
+      return STR_E_CUDA;
+    }
+    h->own_stream = true;
+  }
+  if (p > 1) {
+    std::string why;
+    if (!cfg->nccl_id || !load_nccl(why)) {
+      h->err = why.empty() ? "nccl_id required" : why;
+      str_destroy(h);
+      return STR_E_NCCL;
+    }
+    ncclUniqueId id;
+    memcpy(&id, cfg->nccl_id, sizeof(id));
+    ncclComm_t comm;
+    if (g_nccl.commInitRank(&comm, p, id, cfg->rank) != ncclSuccess) {
+      str_destroy(h);
+      return STR_E_NCCL;
+    }
+    h->comm = comm;
+  }
+  *out = h;
+
+  // geometry (mode 1 sharded)
+  h->md.resize(N - 1);
+  h->i1_off = (cfg->dims[0] / p) * cfg->rank;
+  for (int n = 1; n <= N - 1; ++n) {
+    ModeBuf &m = h->md[n - 1];
+    m.I = (n == 1) ? cfg->dims[0] / p : cfg->dims[n - 1];
+    m.I_glob = cfg->dims[n - 1];
+    m.Ra = RR(h, n);
+    m.Rb = RR(h, n + 1);
+  }
+  h->SN = RR(h, N) * RR(h, 1);
+  h->L = 1;
+  for (int i = 1; i <= h->k; ++i) h->L *= h->md[i - 1].I;
+  h->Rr = 1;
+  for (int i = h->k + 1; i <= N - 1; ++i) h->Rr *= h->md[i - 1].I;
+
+  // state buffers
+  for (int n = 1; n <= N - 1; ++n) {
+    ModeBuf &m = h->md[n - 1];
+    const int S = m.Ra * m.Rb;
+    TRY(ensure(h, m.G, sizeof(double) * m.I * S));
+    TRY(ensure(h, m.P, sizeof(double) * m.I * S));
+    TRY(ensure(h, m.Q, sizeof(double) * S * S));
+    TRY(ensure(h, m.Zm, sizeof(double) * S * S));
+  }
+  h->Tcap = std::max<int64_t>(cfg->t_capacity > 0 ? cfg->t_capacity : 4096, t_init);
+  TRY(ensure(h, h->GN, sizeof(double) * h->Tcap * h->SN));
+  int maxR2 = 0;
+  for (int n = 0; n < N; ++n) maxR2 = std::max(maxR2, h->R[n] * h->R[n]);
+  const size_t sq = (size_t)maxR2 * maxR2;
+  TRY(ensure(h, h->ZmN, sizeof(double) * sq));
+  h->Sf.resize(N);
+  for (int n = 1; n <= N - 1; ++n) TRY(ensure(h, h->Sf[n], sizeof(double) * sq));
+  TRY(ensure(h, h->Lp[0], sizeof(double) * sq));
+  TRY(ensure(h, h->Lp[1], sizeof(double) * sq));
+  TRY(ensure(h, h->T1, sizeof(double) * sq));
+  TRY(ensure(h, h->H, sizeof(double) * sq));
+  TRY(ensure(h, h->Hq, sizeof(double) * STR_MAXW * STR_MAXW));
+  {
+    DevBuf info;
+    TRY(ensure(h, info, sizeof(int)));
+    h->info_buf = info;
+    h->d_info = (int *)info.p;
+    CU(cudaMemsetAsync(h->d_info, 0, sizeof(int), h->st));
+  }
+  if (h->contract == STR_CONTRACT_3XTF32) TRY(tf32_prepare(h));
+
+  // upload init cores: paper layout (a, i, b) at a + Ra*(i + I*b) -> G(2) rows [i][a + Ra*b]
+  for (int n = 1; n <= N - 1; ++n) {
+    ModeBuf &m = h->md[n - 1];
+    const int S = m.Ra * m.Rb;
+    std::vector<double> buf((size_t)m.I * S);
+    int64_t off = (n == 1) ? h->i1_off : 0;
+    for (int64_t i = 0; i < m.I; ++i)
+      for (int b = 0; b < m.Rb; ++b)
+        for (int a = 0; a < m.Ra; ++a)
+          buf[i * S + a + m.Ra * b] = init_cores[n - 1][a + (int64_t)m.Ra * ((i + off) + m.I_glob * b)];
+    CU(cudaMemcpyAsync(m.G.p, buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+    launch_gram_z((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
+    h->launches++;
+    if (n == 1) TRY(allreduce(h, (double *)m.Zm.p, (size_t)S * S));
+  }
+  {
+    const int RN = RR(h, N), R1 = RR(h, 1);
+    std::vector<double> buf((size_t)t_init * h->SN);
+    for (int64_t t = 0; t < t_init; ++t)
+      for (int b = 0; b < R1; ++b)
+        for (int a = 0; a < RN; ++a) buf[t * h->SN + a + RN * b] = init_cores[N - 1][a + (int64_t)RN * (t + t_init * b)];
+    CU(cudaMemcpyAsync(h->GN.p, buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  }
+  h->T = t_init;
+  str_status s = (h->variant == STR_DET) ? init_det(h, X_init, t_init) : rstr_init(h, X_init, t_init);
+  if (s != STR_OK) return s;
+  return deferred_check(h);
+}
+
+extern "C" str_status str_update_batch(str_state *h, const void *X_new, int64_t t_new) {
+  if (!h) return STR_E_ARG;
+  if (h->poisoned) return STR_E_POISONED;
+  if (!X_new || t_new < 1) return fail(h, STR_E_ARG, "X_new must be non-NULL and t_new >= 1");
+  cudaSetDevice(h->device);
+  return (h->variant == STR_DET) ? update_det(h, X_new, t_new) : rstr_update(h, X_new, t_new);
+}
+
+extern "C" str_status str_update_batch_host(str_state *h, const void *X_host, int64_t t_new) {
+  if (!h) return STR_E_ARG;
+  if (h->poisoned) return STR_E_POISONED;
+  if (!X_host || t_new < 1) return fail(h, STR_E_ARG, "X_new must be non-NULL and t_new >= 1");
+  cudaSetDevice(h->device);
+  size_t bytes = (size_t)h->L * h->Rr * t_new * h->xbytes;
+  TRY(ensure(h, h->Xstage, bytes));
+  CU(cudaMemcpyAsync(h->Xstage.p, X_host, bytes, cudaMemcpyHostToDevice, h->st));
+  return str_update_batch(h, h->Xstage.p, t_new);
+}
+
+extern "C" str_status str_sync(str_state *h) {
+  if (!h) return STR_E_ARG;
+  return deferred_check(h);
+}
+
+extern "C" str_status str_get_cores(str_state *h, int32_t n, double *host_out, int64_t capacity) {
+  if (!h || !host_out) return STR_E_ARG;
+  if (n < 1 || n > h->N) return fail(h, STR_E_ARG, "mode out of range");
+  TRY(deferred_check(h));
+  if (n == h->N) {
+    const int RN = RR(h, h->N), R1 = RR(h, 1);
+    if (capacity < h->T * h->SN) return fail(h, STR_E_ARG, "capacity too small");
+    std::vector<double> buf((size_t)h->T * h->SN);
+    CU(cudaMemcpy(buf.data(), h->GN.p, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+    for (int64_t t = 0; t < h->T; ++t)
+      for (int b = 0; b < R1; ++b)
+        for (int a = 0; a < RN; ++a) host_out[a + (int64_t)RN * (t + h->T * b)] = buf[t * h->SN + a + RN * b];
+    return STR_OK;
+  }
+  ModeBuf &m = h->md[n - 1];
+  const int S = m.Ra * m.Rb;
+  if (capacity < m.I_glob * S) return fail(h, STR_E_ARG, "capacity too small");
+  std::vector<double> buf((size_t)m.I_glob * S);
+  if (n == 1 && h->p > 1) {
+    DevBuf gathered;
+    TRY(ensure(h, gathered, sizeof(double) * m.I_glob * S));
+    ncclResult_t r = g_nccl.allGather(m.G.p, gathered.p, (size_t)m.I * S, ncclFloat64, (ncclComm_t)h->comm, h->st);
+    if (r != ncclSuccess) {
+      cudaFree(gathered.p);
+      return fail(h, STR_E_NCCL, "ncclAllGather failed");
+    }
+    CU(cudaStreamSynchronize(h->st));
+    CU(cudaMemcpy(buf.data(), gathered.p, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+    cudaFree(gathered.p);
+  } else {
+    CU(cudaMemcpy(buf.data(), m.G.p, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
+  }
+  for (int64_t i = 0; i < m.I_glob; ++i)
+    for (int b = 0; b < m.Rb; ++b)
+      for (int a = 0; a < m.Ra; ++a) host_out[a + (int64_t)m.Ra * (i + m.I_glob * b)] = buf[i * S + a + m.Ra * b];
+  return STR_OK;
+}
+
+extern "C" str_status str_get_temporal_rows(str_state *h, int64_t t0, int64_t t, double *host_out) {
+  if (!h || !host_out) return STR_E_ARG;
+  if (t0 < 0 || t < 0 || t0 + t > h->T) return fail(h, STR_E_ARG, "temporal range out of bounds");
+  TRY(deferred_check(h));
+  CU(cudaMemcpyAsync(host_out, (double *)h->GN.p + t0 * h->SN, sizeof(double) * t * h->SN, cudaMemcpyDeviceToHost,
+                     h->st));
+  CU(cudaStreamSynchronize(h->st));
+  return STR_OK;
+}
+
+extern "C" str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t, double *rel_err) {
+  if (!h || !X || !rel_err) return STR_E_ARG;
+  if (t0 < 0 || t < 1 || t0 + t > h->T) return fail(h, STR_E_ARG, "temporal range out of bounds");
+  TRY(deferred_check(h));
+  const int N = h->N, k = h->k;
+  const int Ra = RR(h, N), Rb = RR(h, k + 1);
+  TRY(ensure_workspace(h, 1));
+  TRY(build_TR(h));
+  const int64_t chunk = 16;
+  DevBuf tl, parts, acc;
+  TRY(ensure(h, tl, sizeof(double) * h->L * chunk * Ra * Rb));
+  TRY(ensure(h, parts, sizeof(double2) * fit_partials(h->L, h->Rr, chunk)));
+  TRY(ensure(h, acc, sizeof(double) * 2));
+  CU(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2, h->st));
+  for (int64_t c0 = 0; c0 < t; c0 += chunk) {
+    int64_t tn = std::min(chunk, t - c0);
+    TRY(build_TL(h, t0 + c0, tn, (double *)tl.p));
+    const char *xp = (const char *)X + (size_t)h->L * h->Rr * c0 * h->xbytes;
+    h->launches += launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)h->TR.p, Ra, Rb, h->L,
+                              h->Rr, tn, (double2 *)parts.p, (double *)acc.p, h->st);
+    TRY(check_launch(h, "fit"));
+  }
+  TRY(allreduce(h, (double *)acc.p, 2));
+  double sums[2];
+  CU(cudaMemcpyAsync(sums, acc.p, sizeof(sums), cudaMemcpyDeviceToHost, h->st));
+  CU(cudaStreamSynchronize(h->st));
+  cudaFree(tl.p);
+  cudaFree(parts.p);
+  cudaFree(acc.p);
+  if (sums[1] == 0.0) return fail(h, STR_E_ARG, "||X|| = 0: relative error undefined");
+  *rel_err = std::sqrt(sums[0] / sums[1]);
+  return STR_OK;
+}
+
+extern "C" int64_t str_processed(const str_state *h) { return h ? h->T : 0; }
+extern "C" const char *str_error_string(const str_state *h) { return h ? h->err.c_str() : "null handle"; }
+extern "C" int64_t str_kernel_launches(const str_state *h) { return h ? h->launches : 0; }
+
+extern "C" str_status str_set_profiling(str_state *h, int32_t enable) {
+  if (!h) return STR_E_ARG;
+  cudaStreamSynchronize(h->st);
+  for (auto &pe : h->prof_events) {
+    cudaEventDestroy(pe.e0);
+    cudaEventDestroy(pe.e1);
+  }
+  h->prof_events.clear();
+  h->profiling = enable != 0;
+  return STR_OK;
+}
+
+extern "C" str_status str_profile(str_state *h, double *p1_ms, int64_t *p1_n, double *p2_ms, int64_t *p2_n) {
+  if (!h) return STR_E_ARG;
+  CU(cudaStreamSynchronize(h->st));
+  double a = 0, b = 0;
+  int64_t na = 0, nb = 0;
+  for (auto &pe : h->prof_events) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, pe.e0, pe.e1);
+    if (pe.pass == 1) { a += ms; na++; } else { b += ms; nb++; }
+  }
+  if (p1_ms) *p1_ms = a;
+  if (p1_n) *p1_n = na;
+  if (p2_ms) *p2_ms = b;
+  if (p2_n) *p2_n = nb;
+  return STR_OK;
+}
+
+extern "C" void str_destroy(str_state *h) {
+  if (!h) return;
+  cudaSetDevice(h->device);
+  cudaStreamSynchronize(h->st);
+  for (auto &pe : h->prof_events) {
+    cudaEventDestroy(pe.e0);
+    cudaEventDestroy(pe.e1);
+  }
+  h->free_all();
+  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)h->comm);
+  if (h->own_stream) cudaStreamDestroy(h->st);
+  delete h;
+}

@@ -1,0 +1,115 @@
+// str_internal.h — the opaque str_state and cross-file internal entry points.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "str.h"
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+};
+
+struct ModeBuf {
+  int64_t I = 0;        // local rows (mode 1 is sharded across ranks)
+  int64_t I_glob = 0;
+  int Ra = 0, Rb = 0;   // R_n, R_{n+1}
+  DevBuf G;             // I x Ra*Rb, G_n(2) rows (column r_n + R_n r_{n+1})
+  DevBuf P;             // I x Ra*Rb (Eq. partial)
+  DevBuf Q;             // (Ra*Rb)^2 (Eq. partial)
+  DevBuf Zm;            // Gram tensor Z_n as chain matrix: Rb^2 x Ra^2
+  // rSTR
+  DevBuf samp;          // sampled slices (G_n)_S: m x Ra*Rb (G(2) layout rows)
+  std::vector<int32_t> idx_host;
+};
+
+struct ProfEvent {
+  int pass;
+  cudaEvent_t e0, e1;
+};
+
+struct str_state {
+  // configuration
+  int N = 0;
+  std::vector<int64_t> dims_g;
+  std::vector<int> R;               // R_1..R_N
+  str_dtype dtype = STR_F32;
+  str_contract contract = STR_CONTRACT_F64;
+  str_variant variant = STR_DET;
+  int64_t m = 0;
+  uint64_t seed = 0;
+  int k = 1;                        // two-pass split
+  int p = 1, rank = 0, device = 0;
+  int xbytes = 4;
+  int64_t i1_off = 0;
+  cudaStream_t st = nullptr;
+  bool own_stream = false;
+  void *comm = nullptr;             // ncclComm_t
+
+  // geometry (local)
+  int64_t L = 1, Rr = 1;            // prod of left dims (modes 1..k), right dims (k+1..N-1)
+  int SN = 0;                       // R_N R_1
+
+  // state
+  std::vector<ModeBuf> md;          // modes 1..N-1
+  DevBuf GN;                        // temporal rows: Tcap x SN (G_N(2) rows)
+  int64_t T = 0, Tcap = 0;
+  DevBuf ZmN;                       // Z_N^new (update) / Z_N (init): R_1^2 x R_N^2
+  std::vector<DevBuf> Sf;           // suffix chains Sf_n (index n)
+  DevBuf Lp[2], T1, H, Hq;
+
+  // workspaces
+  int64_t ws_t = 0;
+  DevBuf TR, TL, YL, YR, Wt, tmpA, tmpB, Mt, ws, Xstage;
+  DevBuf info_buf;
+  int *d_info = nullptr;
+
+  // 3xTF32 path
+  bool tf32_ready = false;
+  DevBuf tab_split;                 // hi/lo fp32 table for the tensor-core passes
+  DevBuf tf_part;                   // split-K fp32->fp64 partials
+
+  // rSTR
+  DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev;
+  std::vector<int32_t> forced_idx[16];
+  std::vector<int32_t> last_idx[16];
+  int64_t tau = 0;
+
+  // bookkeeping
+  int64_t launches = 0;
+  int64_t collectives = 0;
+  bool profiling = false;
+  std::vector<ProfEvent> prof_events;
+  std::string err;
+  bool poisoned = false;
+
+  void free_all() {
+    auto fr = [](DevBuf &b) {
+      if (b.p) cudaFree(b.p);
+      b.p = nullptr;
+      b.bytes = 0;
+    };
+    for (auto &m : md) {
+      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.samp);
+    }
+    fr(GN); fr(ZmN);
+    for (auto &b : Sf) fr(b);
+    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq);
+    fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
+    fr(tab_split); fr(tf_part);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev);
+  }
+};
+
+// rstr.cu
+str_status rstr_init(str_state *h, const void *X, int64_t tn);
+str_status rstr_update(str_state *h, const void *X, int64_t tn);
+
+// contract_tf32.cu
+str_status tf32_prepare(str_state *h);
+str_status tf32_ensure_workspace(str_state *h, int64_t tn);
+int launch_contract_tf32(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out);
