@@ -1,0 +1,348 @@
+#!/usr/bin/env python
+"""STR update throughput on B200 (BASELINE.json metric), one JSON line on rank 0.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C5] [--impl ours|reference]
+
+A step is one ``str_update_batch`` — the whole per-batch STR update of Alg. 4:
+temporal solve, every non-temporal P/Q accumulation and re-solve — on one batch X_new of
+the workload (default C5: order-5 40^4 x t_new=8 fp32, TR ranks 10; BASELINE.json configs[4],
+the configuration on which BASELINE.json quotes multi-GPU throughput).  X_new is sharded along
+mode 1 across the N ranks (strong scaling: the global batch is fixed).  Inputs rotate through
+15 distinct device-resident batches (1.2 GB > 126 MB L2), so no step reads an L2-warm batch.
+
+Timing: W untimed warm-up steps, then K steps between CUDA events on the library's stream,
+bracketed by a barrier + synchronize; the max over ranks is reported.  `e2e` repeats the
+measurement through the public host-buffer API (pinned H2D of the shard + D2H of the new
+temporal rows every step).  `roofline` times the dominant kernels (the two contraction
+passes) with CUDA events on the library's stream.  `cpu_baseline` times the fp64 oracle
+(test infrastructure, rank 0 only, bounded sample).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "STR update throughput (tensor entries ingested/s)"
+UNIT = "entries/s"
+N_DISTINCT = 15
+
+
+def load_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) >= 7:
+                self.rows.append(parts)
+
+    def __exit__(self, *a):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=2)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[3 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_setup(n_gpus):
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != n_gpus:
+        raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={world}; launch with torchrun for N>1")
+    return world, rank, local
+
+
+def shard(slab: np.ndarray, world: int, rank: int) -> np.ndarray:
+    I1 = slab.shape[-1]
+    w = I1 // world
+    return np.ascontiguousarray(slab[..., rank * w:(rank + 1) * w])
+
+
+def bench_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2307_00719_b200 as lib
+    from workloads import get_config, make_stream
+
+    world, rank, local = dist_setup(args.gpus)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg = get_config(args.config)
+    contract = args.contract or cfg.contract
+    s = make_stream(cfg)
+    # inputs: init slab + N_DISTINCT rotating batches, this rank's mode-1 shard, device-resident
+    Xi = shard(s.init_slab(), world, rank)
+    nd = min(N_DISTINCT, cfg.n_batches)
+    host = [shard(s.batch(b), world, rank) for b in range(nd)]
+    dev_batches = [torch.from_numpy(x).to(dev) for x in host]
+    init = s.init_cores()
+    nccl_id = None
+    if world > 1:
+        obj = [torch.cuda.nccl.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nccl_id = obj[0]
+    stream = torch.cuda.Stream(dev)
+    total_steps = args.warmup + args.steps
+    cap = cfg.t_init + cfg.t_new * (2 * total_steps + 2 * args.e2e_steps + 64)
+    with torch.cuda.stream(stream):
+        h = lib.str_init(cfg.N, cfg.dims, cfg.ranks, torch.from_numpy(Xi).to(dev), cfg.t_init, init, dtype=cfg.dtype,
+                         contract=contract, split_k=cfg.split_k, t_capacity=cap, world_size=world, rank=rank,
+                         nccl_id=nccl_id, device=local, stream=stream.cuda_stream)
+    lib.str_sync(h)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def maxall(v):
+        if world == 1:
+            return v
+        t = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    step = [0]
+
+    def one_step():
+        lib.str_update_batch(h, dev_batches[step[0] % nd], cfg.t_new)
+        step[0] += 1
+
+    for _ in range(args.warmup):
+        one_step()
+    lib.str_sync(h)
+    barrier()
+    torch.cuda.synchronize(dev)
+    l0 = lib.str_kernel_launches(h)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        e0.record(stream)
+        for _ in range(args.steps):
+            one_step()
+        e1.record(stream)
+        lib.str_sync(h)
+        torch.cuda.synchronize(dev)
+    barrier()
+    launches = lib.str_kernel_launches(h) - l0
+    ms = maxall(e0.elapsed_time(e1))
+    global_entries = cfg.batch_entries
+    value = args.steps * global_entries / (ms / 1e3)
+
+    # ---- roofline of the dominant kernels (contraction passes), events on the library stream
+    lib.str_set_profiling(h, True)
+    kp = min(args.steps, 10)
+    for _ in range(kp):
+        one_step()
+    p1_ms, p1_n, p2_ms, p2_n = lib.str_profile(h)
+    lib.str_set_profiling(h, False)
+    peaks, peaks_src = load_peaks()
+    R2 = cfg.ranks[0] * cfg.ranks[-1]
+    local_entries = global_entries // world
+    flops_per_pass = 2.0 * local_entries * R2          # algorithmic: 2 |X_new| R^2 per pass
+    bytes_per_pass = local_entries * (4 if cfg.dtype == "f32" else 8)
+    avg_p1 = p1_ms / max(p1_n, 1)
+    avg_p2 = p2_ms / max(p2_n, 1)
+    avg_pass = 0.5 * (avg_p1 + avg_p2)
+    if contract == "3xtf32":
+        tf32 = peaks["bf16_tflops"] * 0.5            # nominal tf32/bf16 ratio (1.1 / 2.25 PF dense)
+        peak_tf = tf32 / 3.0                          # 3 tf32 MMAs per algorithmic MAC
+        bound, unit = "tensor", "TFLOP/s"
+        basis = f"{peaks_src} bf16 burst {peaks['bf16_tflops']} x 0.5 (tf32/bf16 nominal) / 3 (3xTF32)"
+    else:
+        peak_tf = 148 * 64 * 2 * 1.965e9 / 1e12       # FP64 FMA lanes x clock
+        bound, unit = "alu", "TFLOP/s"
+        basis = "FP64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz"
+    achieved = flops_per_pass / (avg_pass / 1e3) / 1e12
+    t_hbm = bytes_per_pass / (peaks["hbm_gbs"] * 1e9) * 1e3
+    t_cmp = flops_per_pass / (peak_tf * 1e12) * 1e3
+    if t_hbm > t_cmp:
+        bound, unit = "hbm", "GB/s"
+        achieved = bytes_per_pass / (avg_pass / 1e3) / 1e9
+        peak = peaks["hbm_gbs"]
+        basis = f"{peaks_src} HBM copy bandwidth"
+    else:
+        peak = peak_tf
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "traffic_latest.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(f"{args.config}:{contract}")
+        except Exception:
+            traffic = None
+    roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "contraction pass (avg of pass 1/2)",
+                "pass1_us": round(avg_p1 * 1e3, 2), "pass2_us": round(avg_p2 * 1e3, 2),
+                "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
+                "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
+                "peak_basis": basis}
+
+    # ---- e2e: public host-buffer API, pinned H2D + D2H of the step's result every step
+    pinned = [torch.from_numpy(x).pin_memory() for x in host[:min(nd, 4)]]
+    res = np.empty((cfg.t_new, R2))
+    for i in range(2):
+        lib.str_update_batch_host(h, pinned[i % len(pinned)], cfg.t_new)
+        res = lib.str_get_temporal_rows(h, lib.str_processed(h) - cfg.t_new, cfg.t_new)
+    barrier()
+    torch.cuda.synchronize(dev)
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record(stream)
+    for i in range(args.e2e_steps):
+        lib.str_update_batch_host(h, pinned[i % len(pinned)], cfg.t_new)
+        res = lib.str_get_temporal_rows(h, lib.str_processed(h) - cfg.t_new, cfg.t_new)
+    f1.record(stream)
+    torch.cuda.synchronize(dev)
+    barrier()
+    e2e_ms = maxall(f0.elapsed_time(f1))
+    e2e = {"value": args.e2e_steps * global_entries / (e2e_ms / 1e3), "unit": UNIT,
+           "h2d_bytes_per_step": int(pinned[0].numel() * pinned[0].element_size()),
+           "d2h_bytes_per_step": int(res.size * 8), "steps": args.e2e_steps}
+    lib.str_destroy(h)
+
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "3xtf32+f64" if contract == "3xtf32" else "f64",
+            "data": "synthetic (seeded TR stream, SURVEY.md §8(d).1)",
+            "config": {"workload": f"{cfg.name}: order-{cfg.N} {'x'.join(map(str, cfg.dims))} x t_new={cfg.t_new} "
+                                   f"{cfg.dtype}, TR ranks {cfg.ranks[0]}, STR (Alg. 4), X_new sharded on mode 1",
+                       "global_batch_entries": global_entries, "contract": contract, "split_k": cfg.split_k,
+                       "parallelism": f"mode-1 shard x{world}",
+                       "l2": f"rotating {nd} distinct device-resident batches ({nd * global_entries * 4 / 1e9:.2f} GB)"
+                             " > 126 MB L2"},
+            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline(cfg)
+    if world > 1:
+        dist.destroy_process_group()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg, budget_s=20.0):
+    """The oracle as it stands (fp64 numpy) on this host's cores: init + update steps on the
+    same workload until ~budget_s of update time; value = entries / update seconds."""
+    from oracle.stream import StreamingTR
+    from workloads import make_stream
+    from workloads.gen import paper_view
+    s = make_stream(cfg)
+    st = StreamingTR(paper_view(s.init_slab()), s.init_cores())
+    t_used, steps = 0.0, 0
+    while t_used < budget_s and steps < cfg.n_batches:
+        Xb = paper_view(s.batch(steps))
+        t = time.perf_counter()
+        st.update(Xb)
+        t_used += time.perf_counter() - t
+        steps += 1
+    return {"value": steps * cfg.batch_entries / t_used, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+            "sample": f"{cfg.name}: oracle init + {steps} full update steps ({t_used:.1f} s of update time; "
+                      f"numpy BLAS threads = all {os.cpu_count()} host cores)"}
+
+
+def bench_reference(args):
+    """--impl reference: the oracle (fp64 CPU, as it stands) on the same workload/metric."""
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    from oracle.stream import StreamingTR
+    from workloads import get_config, make_stream
+    from workloads.gen import paper_view
+    cfg = get_config(args.config)
+    s = make_stream(cfg)
+    st = StreamingTR(paper_view(s.init_slab()), s.init_cores())
+    nd = min(N_DISTINCT, cfg.n_batches)
+    for w in range(min(args.warmup, 1)):
+        st.update(paper_view(s.batch(w % nd)))
+    t_used, steps = 0.0, 0
+    while steps < args.steps and (t_used < args.ref_budget or steps == 0):
+        Xb = paper_view(s.batch(steps % nd))
+        t = time.perf_counter()
+        st.update(Xb)
+        t_used += time.perf_counter() - t
+        steps += 1
+    value = steps * cfg.batch_entries / t_used
+    sample = (f"{cfg.name}: {steps} of the requested {args.steps} oracle update steps "
+              f"(time budget {args.ref_budget:.0f} s), warm-up {min(args.warmup, 1)}")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * t_used / steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic (seeded TR stream, SURVEY.md §8(d).1)",
+            "config": {"workload": f"{cfg.name} (same as ours)", "global_batch_entries": cfg.batch_entries},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=30)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--contract", default=None, choices=[None, "3xtf32", "f64"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=10)
+    ap.add_argument("--ref-budget", type=float, default=60.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "ours":
+        args.warmup = 3
+    if args.impl == "reference":
+        bench_reference(args)
+    else:
+        bench_ours(args)
+
+
+if __name__ == "__main__":
+    main()
