@@ -16,31 +16,44 @@ namespace strb200 {
 // One thread per (entry, row p): a row vector is carried through the chain in registers.
 __global__ void k_build_table(FactorList fl, int64_t E, double *__restrict__ out) {
   const int R0 = fl.f[0].Ra;
-  const int Rl = fl.f[fl.n - 1].Rb;
+  int Rl = fl.f[0].Rb;
   int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (gid >= E * R0) return;
   int64_t e = gid / R0;
   int p = (int)(gid % R0);
   double v[STR_MAXR], w[STR_MAXR];
   {
-    const Factor &F = fl.f[0];
+    const Factor F = fl.f[0];
     int64_t i = (e / F.stride) % F.I;
     const double *S = F.G + i * (int64_t)F.Ra * F.Rb;
-    for (int b = 0; b < F.Rb; ++b) v[b] = S[p + F.Ra * b];
+#pragma unroll
+    for (int b = 0; b < STR_MAXR; ++b) v[b] = (b < F.Rb) ? S[p + F.Ra * b] : 0.0;
   }
-  for (int f = 1; f < fl.n; ++f) {
-    const Factor &F = fl.f[f];
-    int64_t i = (e / F.stride) % F.I;
-    const double *S = F.G + i * (int64_t)F.Ra * F.Rb;
-    for (int b = 0; b < F.Rb; ++b) {
-      double acc = 0.0;
-      for (int a = 0; a < F.Ra; ++a) acc = fma(v[a], S[a + F.Ra * b], acc);
-      w[b] = acc;
+#pragma unroll
+  for (int f = 1; f < kMaxFactors; ++f) {
+    if (f < fl.n) {
+      const Factor F = fl.f[f];
+      Rl = F.Rb;
+      int64_t i = (e / F.stride) % F.I;
+      const double *S = F.G + i * (int64_t)F.Ra * F.Rb;
+#pragma unroll
+      for (int b = 0; b < STR_MAXR; ++b) {
+        double acc = 0.0;
+        if (b < F.Rb) {
+#pragma unroll
+          for (int a = 0; a < STR_MAXR; ++a)
+            if (a < F.Ra) acc = fma(v[a], S[a + F.Ra * b], acc);
+        }
+        w[b] = acc;
+      }
+#pragma unroll
+      for (int b = 0; b < STR_MAXR; ++b) v[b] = w[b];
     }
-    for (int b = 0; b < F.Rb; ++b) v[b] = w[b];
   }
   double *o = out + e * (int64_t)R0 * Rl + (int64_t)p * Rl;
-  for (int q = 0; q < Rl; ++q) o[q] = v[q];
+#pragma unroll
+  for (int q = 0; q < STR_MAXR; ++q)
+    if (q < Rl) o[q] = v[q];
 }
 
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s) {
@@ -51,59 +64,78 @@ void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream
 
 // ------------------------------------------------------------------------------------------
 // Absorb: contract index `pos` of the matrix-valued tensor Y with core slices (AbsorbDesc).
-// One thread per output element.  accumulate != 0 adds into `out`.
-__global__ void k_absorb(AbsorbDesc ad, const double *__restrict__ Y, double *__restrict__ out,
-                         int64_t n_out, int accumulate) {
-  int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= n_out) return;
+// One CTA per remaining multi-index ("rest"); the Y entries and A slices of a chunk of the
+// contracted index are staged in shared memory; each output entry is accumulated by a group
+// of g threads (g | 32) that split the contracted index and combine with shuffles.
+constexpr int kAbsorbThreads = 256, kAbsorbSmemDoubles = 6144;
+
+__global__ void __launch_bounds__(kAbsorbThreads) k_absorb(AbsorbDesc ad, const double *__restrict__ Y,
+                                                           double *__restrict__ out, int accumulate, int g, int ichunk,
+                                                           int64_t before, int64_t I) {
+  __shared__ double sm[kAbsorbSmemDoubles];
   const int Po = ad.left ? ad.Ra : ad.P;
   const int Qo = ad.left ? ad.Q : ad.Rb;
-  int64_t rest = gid / (Po * Qo);
-  int pq = (int)(gid % (Po * Qo));
-  int po = pq / Qo, qo = pq % Qo;
-  // Decompose `rest` over the dims without pos; compute base offset of Y entries and stride of pos.
-  int64_t base = 0, stride = 1, pos_stride = 0;
-  int64_t r = rest;
-  for (int j = 0; j < ad.nd; ++j) {
-    if (j == ad.pos) {
-      pos_stride = stride;
-    } else {
-      int64_t ij = r % ad.d[j];
-      r /= ad.d[j];
-      base += ij * stride;
-    }
-    stride *= ad.d[j];
-  }
-  const int64_t esz = (int64_t)ad.P * ad.Q;
-  const int64_t I = ad.d[ad.pos];
-  const int64_t ssz = (int64_t)ad.Ra * ad.Rb;
+  const int O = Po * Qo;
+  const int PQ = ad.P * ad.Q, AB = ad.Ra * ad.Rb;
+  // Y multi-index = b + before*(i + I*a) with b < before, a < after; rest = b + before*a.
+  const int64_t rest = blockIdx.x;
+  const int64_t b0 = rest % before, a0 = rest / before;
+  const int64_t base = b0 + before * I * a0, pos_stride = before;
+  double *Ys = sm;
+  double *As = sm + (int64_t)ichunk * PQ;
+  const int tid = threadIdx.x;
+  const int o = tid / g, sub = tid % g;
+  const int po = o / Qo, qo = o % Qo;
   double acc = 0.0;
-  if (ad.left) {
-    // out[po][qo] = sum_i sum_p A(i)[po][p] Y(i)[p][qo]
-    for (int64_t i = 0; i < I; ++i) {
-      const double *y = Y + (base + i * pos_stride) * esz;
-      const double *A = ad.A + i * ssz;
-      for (int p = 0; p < ad.P; ++p) acc = fma(A[po + ad.Ra * p], y[p * ad.Q + qo], acc);
+  for (int64_t i0 = 0; i0 < I; i0 += ichunk) {
+    const int ic = (int)((I - i0) < ichunk ? (I - i0) : ichunk);
+    __syncthreads();
+    for (int e = tid; e < ic * PQ; e += kAbsorbThreads) {
+      int i = e / PQ, w = e % PQ;
+      Ys[e] = Y[(base + (i0 + i) * pos_stride) * PQ + w];
     }
-  } else {
-    // out[po][qo] = sum_i sum_q Y(i)[po][q] A(i)[q][qo]
-    for (int64_t i = 0; i < I; ++i) {
-      const double *y = Y + (base + i * pos_stride) * esz;
-      const double *A = ad.A + i * ssz;
-      for (int q = 0; q < ad.Q; ++q) acc = fma(y[po * ad.Q + q], A[q + ad.Ra * qo], acc);
+    const double *Ag = ad.A + i0 * AB;
+    for (int e = tid; e < ic * AB; e += kAbsorbThreads) As[e] = Ag[e];
+    __syncthreads();
+    if (o < O) {
+      if (ad.left) {
+        for (int i = sub; i < ic; i += g) {
+          const double *a = As + i * AB + po;
+          const double *y = Ys + i * PQ + qo;
+#pragma unroll 4
+          for (int p = 0; p < ad.P; ++p) acc = fma(a[ad.Ra * p], y[p * ad.Q], acc);
+        }
+      } else {
+        for (int i = sub; i < ic; i += g) {
+          const double *a = As + i * AB + ad.Ra * qo;
+          const double *y = Ys + i * PQ + po * ad.Q;
+#pragma unroll 4
+          for (int q = 0; q < ad.Q; ++q) acc = fma(y[q], a[q], acc);
+        }
+      }
     }
   }
-  if (accumulate) out[gid] += acc; else out[gid] = acc;
+  for (int sh = g / 2; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
+  if (o < O && sub == 0) {
+    double *dst = out + rest * O + o;
+    if (accumulate) *dst += acc; else *dst = acc;
+  }
 }
 
 void launch_absorb(const AbsorbDesc &ad, const double *Y, double *out, int accumulate, cudaStream_t s) {
-  int64_t rest = 1;
+  int64_t rest = 1, before = 1;
   for (int j = 0; j < ad.nd; ++j)
     if (j != ad.pos) rest *= ad.d[j];
+  for (int j = 0; j < ad.pos; ++j) before *= ad.d[j];
   const int Po = ad.left ? ad.Ra : ad.P;
   const int Qo = ad.left ? ad.Q : ad.Rb;
-  int64_t n = rest * Po * Qo;
-  k_absorb<<<(unsigned)cdiv(n, 128), 128, 0, s>>>(ad, Y, out, n, accumulate);
+  const int O = Po * Qo;
+  int g = 1;
+  while (g < 8 && O * g * 2 <= kAbsorbThreads) g *= 2;
+  int per = ad.P * ad.Q + ad.Ra * ad.Rb;
+  int ichunk = kAbsorbSmemDoubles / per;
+  if (ichunk > ad.d[ad.pos]) ichunk = (int)ad.d[ad.pos];
+  k_absorb<<<(unsigned)rest, kAbsorbThreads, 0, s>>>(ad, Y, out, accumulate, g, ichunk, before, ad.d[ad.pos]);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -177,78 +209,229 @@ void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate
 }
 
 // ------------------------------------------------------------------------------------------
-// G = P Q^{-1} for SPD Q (S x S, S <= 128) and I right-hand-side rows P (I x S), both
-// row-major.  Each CTA factors Q = L L^T in shared memory (right-looking), then solves
-// L L^T g^T = p^T for a chunk of rows.  A non-positive or non-finite pivot sets *info.
-constexpr int kSolveChunk = 32;
+// G = P Q^{-1} for SPD Q (S x S, S <= 128) and I right-hand-side rows P (I x S), row-major.
+// Blocked right-looking Cholesky (block 8): the packed lower triangle lives in registers
+// (entry e belongs to thread e % 256).  Per block column: the panel is published to shared
+// memory, every row thread factors the 8x8 diagonal block redundantly (rsqrt pivots) and solves
+// its own row, the first 8 threads also emit the inverse of the diagonal block, then a rank-8
+// update hits the trailing entries.  Forward / backward substitution use the inverted diagonal
+// blocks.  Each CTA factors Q (redundantly) and solves a chunk of <= 64 RHS rows.
+// A non-positive or non-finite pivot sets *info.
+constexpr int kNB = 8, kNT = 256, kMaxE = 33, kSolveChunk = 16;
 
-__global__ void __launch_bounds__(256) k_chol_solve(const double *__restrict__ Q, int S, const double *__restrict__ P,
-                                                     int64_t I, double *__restrict__ Gout, int *info) {
+__global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict__ Q, int S,
+                                                        const double *__restrict__ P, int64_t I,
+                                                        double *__restrict__ Gout, int *info) {
   extern __shared__ double sm[];
-  double *L = sm;              // S*S
-  double *B = sm + S * S;      // chunk*S, row-major [r][s]
-  __shared__ double piv;
-  const int tid = threadIdx.x, nt = blockDim.x;
+  const int S2 = (S * S + 3) & ~3;          // regions padded to 32-byte multiples
+  double *Lf = sm;                          // S*S, final L (lower), row-major
+  double *Bm = Lf + S2;                     // kSolveChunk * S RHS rows
+  double *Pn = Bm + kSolveChunk * S;        // S * 8 panel (input)
+  double *Ln = Pn + S * kNB;                // S * 8 panel (output)
+  double *Di = Ln + S * kNB;                // (S/8+1) * 64 inverted diagonal blocks (lower)
+  const int tid = threadIdx.x;
   const int64_t row0 = (int64_t)blockIdx.x * kSolveChunk;
   const int rows = (int)((I - row0) < kSolveChunk ? (I - row0) : kSolveChunk);
-  for (int e = tid; e < S * S; e += nt) L[e] = Q[e];
-  for (int e = tid; e < rows * S; e += nt) B[e] = P[(row0 + e / S) * S + e % S];
-  __syncthreads();
-  for (int k = 0; k < S; ++k) {
-    if (tid == 0) {
-      double d = L[k * S + k];
-      if (!(d > 0.0) || !isfinite(d)) {
-        if (info) atomicExch(info, 1);
-        d = nan("");
+  const int ntri = S * (S + 1) / 2;
+  double val[kMaxE];
+  int ij[kMaxE];
+#pragma unroll
+  for (int r = 0; r < kMaxE; ++r) {
+    int e = tid + kNT * r;
+    ij[r] = -1;
+    val[r] = 0.0;
+    if (e < ntri) {
+      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
+      while (i * (i + 1) / 2 > e) --i;
+      while ((i + 1) * (i + 2) / 2 <= e) ++i;
+      int j = e - i * (i + 1) / 2;
+      ij[r] = (i << 8) | j;
+      val[r] = Q[(int64_t)i * S + j];
+    }
+  }
+  for (int e = tid; e < rows * S; e += kNT) Bm[e] = P[(row0 + e / S) * S + e % S];
+  bool bad = false;
+  for (int kb = 0; kb < S; kb += kNB) {
+    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
+#pragma unroll
+    for (int r = 0; r < kMaxE; ++r) {
+      int i = ij[r] >> 8, j = ij[r] & 255;
+      if (ij[r] >= 0 && j >= kb && j < kb + nbk) Pn[i * kNB + (j - kb)] = val[r];
+    }
+    __syncthreads();
+    if (tid < S - kb) {
+      const int i = kb + tid;
+      double Ld[kNB][kNB], rd[kNB];
+#pragma unroll
+      for (int a = 0; a < kNB; ++a)
+#pragma unroll
+        for (int b = 0; b <= a; ++b) Ld[a][b] = (a < nbk) ? Pn[(kb + a) * kNB + b] : 0.0;
+#pragma unroll
+      for (int c = 0; c < kNB; ++c) {
+        double d = Ld[c][c], r = 0.0;
+        if (c < nbk) {
+          if (!(d > 0.0) || !isfinite(d)) bad = true;
+          r = rsqrt(d);
+          Ld[c][c] = d * r;
+        }
+        rd[c] = r;
+#pragma unroll
+        for (int a = c + 1; a < kNB; ++a) Ld[a][c] *= r;
+#pragma unroll
+        for (int a = c + 1; a < kNB; ++a)
+#pragma unroll
+          for (int b = c + 1; b <= a; ++b) Ld[a][b] = fma(-Ld[a][c], Ld[b][c], Ld[a][b]);
       }
-      piv = sqrt(d);
-      L[k * S + k] = piv;
+      double l[kNB];
+      if (i < kb + nbk) {
+#pragma unroll
+        for (int m = 0; m < kNB; ++m) {
+          double x = 0.0;
+#pragma unroll
+          for (int a = 0; a < kNB; ++a)
+            if (m <= a && a == i - kb) x = Ld[a][m];
+          l[m] = x;
+        }
+        // column (i - kb) of the inverse diagonal block
+        const int c = i - kb;
+        double x[kNB];
+#pragma unroll
+        for (int a = 0; a < kNB; ++a) {
+          double v = (a == c) ? 1.0 : 0.0;
+#pragma unroll
+          for (int q = 0; q < a; ++q) v = fma(-Ld[a][q], x[q], v);
+          x[a] = v * rd[a];
+        }
+        double *D = Di + (kb / kNB) * kNB * kNB;
+#pragma unroll
+        for (int a = 0; a < kNB; ++a) D[a * kNB + c] = x[a];
+      } else {
+#pragma unroll
+        for (int m = 0; m < kNB; ++m) {
+          double a = (m < nbk) ? Pn[i * kNB + m] : 0.0;
+#pragma unroll
+          for (int q = 0; q < m; ++q) a = fma(-l[q], Ld[m][q], a);
+          l[m] = a * rd[m];
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < kNB; ++m) Ln[i * kNB + m] = l[m];
     }
     __syncthreads();
-    const double inv = 1.0 / piv;
-    for (int i = k + 1 + tid; i < S; i += nt) L[i * S + k] *= inv;
+#pragma unroll
+    for (int r = 0; r < kMaxE; ++r) {
+      if (ij[r] < 0) continue;
+      int i = ij[r] >> 8, j = ij[r] & 255;
+      if (j >= kb && j < kb + nbk) {
+        val[r] = Ln[i * kNB + (j - kb)];
+      } else if (j >= kb + nbk) {
+        const double2 *li = (const double2 *)(Ln + i * kNB);
+        const double2 *lj = (const double2 *)(Ln + j * kNB);
+        double acc = val[r];
+#pragma unroll
+        for (int m = 0; m < kNB / 2; ++m) {
+          double2 x = li[m], y = lj[m];
+          acc = fma(-x.x, y.x, acc);
+          acc = fma(-x.y, y.y, acc);
+        }
+        val[r] = acc;
+      }
+    }
+  }
+  if (bad && info) atomicExch(info, 1);
+  for (int e = tid; e < S * S; e += kNT) Lf[e] = 0.0;
+  __syncthreads();
+#pragma unroll
+  for (int r = 0; r < kMaxE; ++r)
+    if (ij[r] >= 0) Lf[(ij[r] >> 8) * S + (ij[r] & 255)] = val[r];
+  __syncthreads();
+  const int ti = tid & 127, tr = tid >> 7;
+  const int nblk = (S + kNB - 1) / kNB;
+  // forward substitution, L y = b, for every RHS row (rows of Bm hold b^T)
+  for (int bi = 0; bi < nblk; ++bi) {
+    const int kb = bi * kNB;
+    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
+    const double *D = Di + bi * kNB * kNB;
+    double yv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
+      yv[u] = 0.0;
+      if (r1 < rows && m1 < nbk)
+#pragma unroll
+        for (int q = 0; q < kNB; ++q) yv[u] = fma(D[m1 * kNB + q], (q < nbk) ? Bm[r1 * S + kb + q] : 0.0, yv[u]);
+    }
     __syncthreads();
-    const int n = S - k - 1;
-    for (int e = tid; e < n * n; e += nt) {
-      int i = k + 1 + e / n, j = k + 1 + e % n;
-      if (j <= i) L[i * S + j] -= L[i * S + k] * L[j * S + k];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
+      if (r1 < rows && m1 < nbk) Bm[r1 * S + kb + m1] = yv[u];
+    }
+    __syncthreads();
+    if (ti >= kb + nbk && ti < S) {
+      double lrow[kNB];
+#pragma unroll
+      for (int m = 0; m < kNB; ++m) lrow[m] = (m < nbk) ? Lf[ti * S + kb + m] : 0.0;
+      for (int r = tr; r < rows; r += kNT / 128) {
+        double acc = Bm[r * S + ti];
+        const double *y = Bm + r * S + kb;
+#pragma unroll
+        for (int m = 0; m < kNB; ++m) acc = fma(-lrow[m], (m < nbk) ? y[m] : 0.0, acc);
+        Bm[r * S + ti] = acc;
+      }
     }
     __syncthreads();
   }
-  // forward: L y = b (row r of B holds b^T)
-  for (int k = 0; k < S; ++k) {
-    const double inv = 1.0 / L[k * S + k];
-    for (int r = tid; r < rows; r += nt) B[r * S + k] *= inv;
+  // backward substitution, L^T x = y
+  for (int bi = nblk - 1; bi >= 0; --bi) {
+    const int kb = bi * kNB;
+    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
+    const double *D = Di + bi * kNB * kNB;
+    double xv[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
+      xv[u] = 0.0;
+      if (r1 < rows && m1 < nbk)
+#pragma unroll
+        for (int q = 0; q < kNB; ++q) xv[u] = fma(D[q * kNB + m1], (q < nbk) ? Bm[r1 * S + kb + q] : 0.0, xv[u]);
+    }
     __syncthreads();
-    const int n = S - k - 1;
-    for (int e = tid; e < rows * n; e += nt) {
-      int r = e / n, i = k + 1 + e % n;
-      B[r * S + i] -= L[i * S + k] * B[r * S + k];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
+      if (r1 < rows && m1 < nbk) Bm[r1 * S + kb + m1] = xv[u];
+    }
+    __syncthreads();
+    if (ti < kb) {
+      double lcol[kNB];
+#pragma unroll
+      for (int m = 0; m < kNB; ++m) lcol[m] = (m < nbk) ? Lf[(kb + m) * S + ti] : 0.0;
+      for (int r = tr; r < rows; r += kNT / 128) {
+        double acc = Bm[r * S + ti];
+        const double *x = Bm + r * S + kb;
+#pragma unroll
+        for (int m = 0; m < kNB; ++m) acc = fma(-lcol[m], (m < nbk) ? x[m] : 0.0, acc);
+        Bm[r * S + ti] = acc;
+      }
     }
     __syncthreads();
   }
-  // backward: L^T x = y
-  for (int k = S - 1; k >= 0; --k) {
-    const double inv = 1.0 / L[k * S + k];
-    for (int r = tid; r < rows; r += nt) B[r * S + k] *= inv;
-    __syncthreads();
-    for (int e = tid; e < rows * k; e += nt) {
-      int r = e / k, i = e % k;
-      B[r * S + i] -= L[k * S + i] * B[r * S + k];
-    }
-    __syncthreads();
-  }
-  for (int e = tid; e < rows * S; e += nt) Gout[(row0 + e / S) * S + e % S] = B[e];
+  for (int e = tid; e < rows * S; e += kNT) Gout[(row0 + e / S) * S + e % S] = Bm[e];
+}
+
+size_t chol_solve_smem(int S) {
+  return sizeof(double) * ((size_t)((S * S + 3) & ~3) + (size_t)kSolveChunk * S + 2 * (size_t)S * kNB +
+                           (size_t)(S / kNB + 1) * kNB * kNB);
 }
 
 void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s) {
-  size_t smem = sizeof(double) * ((size_t)S * S + (size_t)kSolveChunk * S);
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     attr_set = true;
   }
-  k_chol_solve<<<(unsigned)cdiv(I, kSolveChunk), 256, smem, s>>>(Q, S, P, I, Gout, info);
+  k_chol_solve<<<(unsigned)cdiv(I, kSolveChunk), kNT, chol_solve_smem(S), s>>>(Q, S, P, I, Gout, info);
 }
 
 // ------------------------------------------------------------------------------------------

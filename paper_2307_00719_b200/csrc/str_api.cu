@@ -238,24 +238,25 @@ static str_status q_update(str_state *h, int n, const double *Lp, bool Lp_id, co
 
 // ------------------------------------------------------------------------------------ contraction
 static str_status contract(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out) {
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->profiling) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, h->st);
-  }
   int nl = 0;
-  if (h->contract == STR_CONTRACT_3XTF32 && h->tf32_ready) {
+  if (h->contract == STR_CONTRACT_3XTF32) {
+    // tensor-core path; profiling events bracket the contraction kernel itself
     nl = launch_contract_tf32(h, X, pass, tab, W, tn, out);
     if (nl < 0) return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
   } else {
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (h->profiling) {
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, h->st);
+    }
     nl = launch_contract_f64(X, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn, out, (double *)h->ws.p, h->st);
+    if (h->profiling) {
+      cudaEventRecord(e1, h->st);
+      h->prof_events.push_back({pass, e0, e1});
+    }
   }
   h->launches += nl;
-  if (h->profiling) {
-    cudaEventRecord(e1, h->st);
-    h->prof_events.push_back({pass, e0, e1});
-  }
   return check_launch(h, pass == 1 ? "contract pass 1" : "contract pass 2");
 }
 
@@ -848,4 +849,25 @@ extern "C" void str_destroy(str_state *h) {
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)h->comm);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
+}
+
+// ------------------------------------------------------------------------------------ test hook
+// Not part of include/str.h: runs one contraction pass with the current cores (pass 1: T_R;
+// pass 2: T_L over temporal rows [0, tn)) and copies Y (fp64) to host.  Used by the GPU unit
+// tests of the contraction kernels.
+extern "C" STR_API str_status strdbg_contract(str_state *h, const void *X, int32_t pass, int64_t tn, double *host_out) {
+  if (!h || !X || !host_out || (pass != 1 && pass != 2) || tn < 1 || tn > h->T) return STR_E_ARG;
+  TRY(ensure_workspace(h, tn));
+  const int W1 = RR(h, h->k + 1) * RR(h, h->N);
+  if (pass == 1) {
+    TRY(build_TR(h));
+    TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
+  } else {
+    TRY(build_TL(h, 0, tn, (double *)h->TL.p));
+    TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
+  }
+  CU(cudaStreamSynchronize(h->st));
+  size_t n = (size_t)(pass == 1 ? h->L * tn : h->Rr) * W1;
+  CU(cudaMemcpy(host_out, pass == 1 ? h->YL.p : h->YR.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  return STR_OK;
 }

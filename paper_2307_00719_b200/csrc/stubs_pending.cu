@@ -9,13 +9,6 @@ str_status rstr_update(str_state *h, const void *, int64_t) {
   h->err = "rSTR variants are not built yet";
   return STR_E_ARG;
 }
-str_status tf32_prepare(str_state *h) {
-  h->err = "3xTF32 contraction is not built yet; use STR_CONTRACT_F64";
-  return STR_E_ARG;
-}
-str_status tf32_ensure_workspace(str_state *, int64_t) { return STR_OK; }
-int launch_contract_tf32(str_state *, const void *, int, const double *, int, int64_t, double *) { return -1; }
-
 extern "C" str_status str_get_index_table(str_state *h, int32_t, int32_t *, int64_t) {
   if (h) h->err = "rSTR variants are not built yet";
   return STR_E_ARG;

@@ -19,7 +19,7 @@ def test_parity_f64_small(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,contract", [("P2", "f64"), ("P3", "f64"), ("P5", "f64")])
+@pytest.mark.parametrize("name,contract", [("P2", "f64"), ("P3", "f64"), ("P5", "f64"), ("P2", "3xtf32"), ("P5", "3xtf32")])
 def test_parity_multi_tile(name, contract):
     """Sizes spanning several 64/128-row tiles with ragged tails, unequal ranks."""
     for b, errs, fo, fg, h, orc in gpu_stream(name, contract=contract):

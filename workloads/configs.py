@@ -90,11 +90,11 @@ CONFIGS.update({
     "T5": StreamConfig("T5", (4, 3, 5, 3), (2, 3, 2, 4, 3), 5, 2, 3, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-2, seed=9, split_k=2),
     # GPU parity sizes: several 128-row tiles plus a ragged tail in every contraction.
-    "P2": StreamConfig("P2", (23, 19, 17), (3, 4, 5, 2), 6, 5, 4, "f32", "3xtf32",
+    "P2": StreamConfig("P2", (24, 19, 17), (3, 4, 5, 2), 6, 5, 4, "f32", "3xtf32",
                        core_scale=0.5, noise_abs=1e-2, seed=21),
     "P3": StreamConfig("P3", (37, 53), (4, 6, 5), 12, 7, 4, "f32", "f64",
                        kind="tr", core_scale=0.5, noise_abs=1e-2, seed=31),
-    "P5": StreamConfig("P5", (13, 11, 9, 7), (3, 4, 5, 3, 4), 5, 3, 3, "f32", "3xtf32",
+    "P5": StreamConfig("P5", (12, 11, 9, 7), (3, 4, 5, 3, 4), 5, 3, 3, "f32", "3xtf32",
                        core_scale=0.5, noise_abs=1e-2, seed=51, split_k=2),
     "P1": StreamConfig("P1", (20, 20), (3, 3, 3), 10, 2, 10, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-3, seed=111),
