@@ -10,7 +10,7 @@ namespace strb200 {
 
 // kernels_small.cu
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);
-void launch_absorb(const AbsorbDesc &ad, const double *Y, double *out, int accumulate, cudaStream_t s);
+void launch_absorb(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);
 void launch_gram_z(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
 void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, cudaStream_t s);
 void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate, cudaStream_t s);

@@ -64,78 +64,82 @@ void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream
 
 // ------------------------------------------------------------------------------------------
 // Absorb: contract index `pos` of the matrix-valued tensor Y with core slices (AbsorbDesc).
-// One CTA per remaining multi-index ("rest"); the Y entries and A slices of a chunk of the
-// contracted index are staged in shared memory; each output entry is accumulated by a group
-// of g threads (g | 32) that split the contracted index and combine with shuffles.
-constexpr int kAbsorbThreads = 256, kAbsorbSmemDoubles = 6144;
+//   left : out[rest][po][qo] = sum_i sum_p A(i)[po][p] Y(rest, i)[p][qo]
+//   right: out[rest][po][qo] = sum_i sum_q Y(rest, i)[po][q] A(i)[q][qo]
+// Thread layout: g adjacent lanes per output element split the contracted index i and reduce
+// with shuffles; a CTA covers 256/g consecutive outputs (several `rest` entries), with the A
+// slices of a chunk of i staged once per CTA in shared memory; Y is read through L1/L2.
+constexpr int kAbsorbThreads = 256, kAbsorbSmemDoubles = 4096;
 
-__global__ void __launch_bounds__(kAbsorbThreads) k_absorb(AbsorbDesc ad, const double *__restrict__ Y,
+template <typename TY>
+__global__ void __launch_bounds__(kAbsorbThreads) k_absorb(AbsorbDesc ad, const TY *__restrict__ Y,
                                                            double *__restrict__ out, int accumulate, int g, int ichunk,
-                                                           int64_t before, int64_t I) {
-  __shared__ double sm[kAbsorbSmemDoubles];
+                                                           int64_t before, int64_t I, int64_t n_out) {
+  __shared__ double As[kAbsorbSmemDoubles];
   const int Po = ad.left ? ad.Ra : ad.P;
   const int Qo = ad.left ? ad.Q : ad.Rb;
   const int O = Po * Qo;
   const int PQ = ad.P * ad.Q, AB = ad.Ra * ad.Rb;
-  // Y multi-index = b + before*(i + I*a) with b < before, a < after; rest = b + before*a.
-  const int64_t rest = blockIdx.x;
-  const int64_t b0 = rest % before, a0 = rest / before;
-  const int64_t base = b0 + before * I * a0, pos_stride = before;
-  double *Ys = sm;
-  double *As = sm + (int64_t)ichunk * PQ;
-  const int tid = threadIdx.x;
-  const int o = tid / g, sub = tid % g;
+  const int64_t gid = blockIdx.x * (int64_t)kAbsorbThreads + threadIdx.x;
+  const int64_t oi = gid / g;                 // global output index
+  const int sub = (int)(gid % g);
+  const bool active = oi < n_out;
+  const int64_t rest = active ? oi / O : 0;
+  const int o = (int)(oi % O);
   const int po = o / Qo, qo = o % Qo;
+  // Y multi-index = b + before*(i + I*a) with b < before, a < after; rest = b + before*a.
+  const int64_t b0 = rest % before, a0 = rest / before;
+  const TY *ybase = Y + (b0 + before * I * a0) * PQ;
+  const int64_t ystride = before * PQ;        // between consecutive i
   double acc = 0.0;
   for (int64_t i0 = 0; i0 < I; i0 += ichunk) {
     const int ic = (int)((I - i0) < ichunk ? (I - i0) : ichunk);
     __syncthreads();
-    for (int e = tid; e < ic * PQ; e += kAbsorbThreads) {
-      int i = e / PQ, w = e % PQ;
-      Ys[e] = Y[(base + (i0 + i) * pos_stride) * PQ + w];
-    }
     const double *Ag = ad.A + i0 * AB;
-    for (int e = tid; e < ic * AB; e += kAbsorbThreads) As[e] = Ag[e];
+    for (int e = threadIdx.x; e < ic * AB; e += kAbsorbThreads) As[e] = Ag[e];
     __syncthreads();
-    if (o < O) {
+    if (active) {
       if (ad.left) {
         for (int i = sub; i < ic; i += g) {
           const double *a = As + i * AB + po;
-          const double *y = Ys + i * PQ + qo;
-#pragma unroll 4
-          for (int p = 0; p < ad.P; ++p) acc = fma(a[ad.Ra * p], y[p * ad.Q], acc);
+          const TY *y = ybase + (i0 + i) * ystride + qo;
+          for (int p = 0; p < ad.P; ++p) acc = fma(a[ad.Ra * p], (double)y[p * ad.Q], acc);
         }
       } else {
         for (int i = sub; i < ic; i += g) {
           const double *a = As + i * AB + ad.Ra * qo;
-          const double *y = Ys + i * PQ + po * ad.Q;
-#pragma unroll 4
-          for (int q = 0; q < ad.Q; ++q) acc = fma(y[q], a[q], acc);
+          const TY *y = ybase + (i0 + i) * ystride + po * ad.Q;
+          for (int q = 0; q < ad.Q; ++q) acc = fma((double)y[q], a[q], acc);
         }
       }
     }
   }
   for (int sh = g / 2; sh > 0; sh >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, sh);
-  if (o < O && sub == 0) {
-    double *dst = out + rest * O + o;
+  if (active && sub == 0) {
+    double *dst = out + oi;
     if (accumulate) *dst += acc; else *dst = acc;
   }
 }
 
-void launch_absorb(const AbsorbDesc &ad, const double *Y, double *out, int accumulate, cudaStream_t s) {
+void launch_absorb(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s) {
   int64_t rest = 1, before = 1;
   for (int j = 0; j < ad.nd; ++j)
     if (j != ad.pos) rest *= ad.d[j];
   for (int j = 0; j < ad.pos; ++j) before *= ad.d[j];
   const int Po = ad.left ? ad.Ra : ad.P;
   const int Qo = ad.left ? ad.Q : ad.Rb;
-  const int O = Po * Qo;
-  int g = 1;
-  while (g < 8 && O * g * 2 <= kAbsorbThreads) g *= 2;
-  int per = ad.P * ad.Q + ad.Ra * ad.Rb;
-  int ichunk = kAbsorbSmemDoubles / per;
-  if (ichunk > ad.d[ad.pos]) ichunk = (int)ad.d[ad.pos];
-  k_absorb<<<(unsigned)rest, kAbsorbThreads, 0, s>>>(ad, Y, out, accumulate, g, ichunk, before, ad.d[ad.pos]);
+  const int64_t I = ad.d[ad.pos];
+  const int64_t K = I * (ad.left ? ad.P : ad.Q);
+  int g = K <= 64 ? 1 : (K <= 160 ? 2 : (K <= 320 ? 4 : (K <= 640 ? 8 : 16)));
+  const int64_t n_out = rest * Po * Qo;
+  int ichunk = kAbsorbSmemDoubles / (ad.Ra * ad.Rb);
+  if (ichunk > I) ichunk = (int)I;
+  const unsigned grid = (unsigned)cdiv(n_out * g, kAbsorbThreads);
+  if (y_f32)
+    k_absorb<float><<<grid, kAbsorbThreads, 0, s>>>(ad, (const float *)Y, out, accumulate, g, ichunk, before, I, n_out);
+  else
+    k_absorb<double><<<grid, kAbsorbThreads, 0, s>>>(ad, (const double *)Y, out, accumulate, g, ichunk, before, I,
+                                                     n_out);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -210,67 +214,47 @@ void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate
 
 // ------------------------------------------------------------------------------------------
 // G = P Q^{-1} for SPD Q (S x S, S <= 128) and I right-hand-side rows P (I x S), row-major.
-// Blocked right-looking Cholesky (block 8): the packed lower triangle lives in registers
-// (entry e belongs to thread e % 256).  Per block column: the panel is published to shared
-// memory, every row thread factors the 8x8 diagonal block redundantly (rsqrt pivots) and solves
-// its own row, the first 8 threads also emit the inverse of the diagonal block, then a rank-8
-// update hits the trailing entries.  Forward / backward substitution use the inverted diagonal
-// blocks.  Each CTA factors Q (redundantly) and solves a chunk of <= 64 RHS rows.
-// A non-positive or non-finite pivot sets *info.
-constexpr int kNB = 8, kNT = 256, kMaxE = 33, kSolveChunk = 16;
+// Blocked right-looking Cholesky (block 8) on the shared-memory copy of Q, written as compact
+// loops (the code must stay small: the kernel runs one CTA and is latency/I-cache bound):
+//   B-phase: one thread per row i >= kb factors the 8x8 diagonal block in registers
+//            (rsqrt pivots), solves its row of the panel and (rows in the block) emits one
+//            column of the inverted diagonal block;
+//   C-phase: warps own rows, lanes own columns: the panel is finalized and the trailing
+//            entries take the rank-8 update.
+// Forward / backward substitution then use the inverted diagonal blocks.  Each CTA factors Q
+// (cheap, redundant) and solves a chunk of <= 16 RHS rows.  A non-positive pivot sets *info.
+constexpr int kNB = 8, kNT = 512, kSolveChunk = 16;
 
 __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict__ Q, int S,
                                                         const double *__restrict__ P, int64_t I,
                                                         double *__restrict__ Gout, int *info) {
   extern __shared__ double sm[];
-  const int S2 = (S * S + 3) & ~3;          // regions padded to 32-byte multiples
-  double *Lf = sm;                          // S*S, final L (lower), row-major
-  double *Bm = Lf + S2;                     // kSolveChunk * S RHS rows
-  double *Pn = Bm + kSolveChunk * S;        // S * 8 panel (input)
-  double *Ln = Pn + S * kNB;                // S * 8 panel (output)
-  double *Di = Ln + S * kNB;                // (S/8+1) * 64 inverted diagonal blocks (lower)
-  const int tid = threadIdx.x;
+  const int LD = S + 1;                      // padded row stride of A
+  double *A = sm;                            // S x LD
+  double *Bm = A + ((S * LD + 3) & ~3);      // kSolveChunk x S
+  double *Ln = Bm + kSolveChunk * S;         // S x 8 panel of L
+  double *Di = Ln + S * kNB;                 // nblk x 64 inverted diagonal blocks
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kNT / 32;
   const int64_t row0 = (int64_t)blockIdx.x * kSolveChunk;
   const int rows = (int)((I - row0) < kSolveChunk ? (I - row0) : kSolveChunk);
-  const int ntri = S * (S + 1) / 2;
-  double val[kMaxE];
-  int ij[kMaxE];
-#pragma unroll
-  for (int r = 0; r < kMaxE; ++r) {
-    int e = tid + kNT * r;
-    ij[r] = -1;
-    val[r] = 0.0;
-    if (e < ntri) {
-      int i = (int)((sqrt(8.0 * e + 1.0) - 1.0) * 0.5);
-      while (i * (i + 1) / 2 > e) --i;
-      while ((i + 1) * (i + 2) / 2 <= e) ++i;
-      int j = e - i * (i + 1) / 2;
-      ij[r] = (i << 8) | j;
-      val[r] = Q[(int64_t)i * S + j];
-    }
-  }
+  for (int e = tid; e < S * S; e += kNT) A[(e / S) * LD + e % S] = Q[e];
   for (int e = tid; e < rows * S; e += kNT) Bm[e] = P[(row0 + e / S) * S + e % S];
+  __syncthreads();
   bool bad = false;
   for (int kb = 0; kb < S; kb += kNB) {
     const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
-#pragma unroll
-    for (int r = 0; r < kMaxE; ++r) {
-      int i = ij[r] >> 8, j = ij[r] & 255;
-      if (ij[r] >= 0 && j >= kb && j < kb + nbk) Pn[i * kNB + (j - kb)] = val[r];
-    }
-    __syncthreads();
     if (tid < S - kb) {
       const int i = kb + tid;
-      double Ld[kNB][kNB], rd[kNB];
+      double Ld[kNB][kNB], rd[kNB], l[kNB];
 #pragma unroll
       for (int a = 0; a < kNB; ++a)
 #pragma unroll
-        for (int b = 0; b <= a; ++b) Ld[a][b] = (a < nbk) ? Pn[(kb + a) * kNB + b] : 0.0;
+        for (int b = 0; b <= a; ++b) Ld[a][b] = (a < nbk) ? A[(kb + a) * LD + kb + b] : 0.0;
 #pragma unroll
       for (int c = 0; c < kNB; ++c) {
         double d = Ld[c][c], r = 0.0;
         if (c < nbk) {
-          if (!(d > 0.0) || !isfinite(d)) bad = true;
+          if (!(d > 0.0)) bad = true;
           r = rsqrt(d);
           Ld[c][c] = d * r;
         }
@@ -282,18 +266,18 @@ __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict_
 #pragma unroll
           for (int b = c + 1; b <= a; ++b) Ld[a][b] = fma(-Ld[a][c], Ld[b][c], Ld[a][b]);
       }
-      double l[kNB];
-      if (i < kb + nbk) {
+      const int c = i - kb;                    // < nbk for rows inside the diagonal block
 #pragma unroll
-        for (int m = 0; m < kNB; ++m) {
-          double x = 0.0;
+      for (int m = 0; m < kNB; ++m) {
+        double a = (m < nbk && m <= c) ? A[i * LD + kb + m] : 0.0;
 #pragma unroll
-          for (int a = 0; a < kNB; ++a)
-            if (m <= a && a == i - kb) x = Ld[a][m];
-          l[m] = x;
-        }
-        // column (i - kb) of the inverse diagonal block
-        const int c = i - kb;
+        for (int q = 0; q < m; ++q) a = fma(-l[q], Ld[m][q], a);
+        l[m] = (m <= c) ? a * rd[m] : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < kNB; ++m) Ln[i * kNB + m] = l[m];
+      if (c < nbk) {
+        // column c of the inverse of the lower-triangular diagonal block
         double x[kNB];
 #pragma unroll
         for (int a = 0; a < kNB; ++a) {
@@ -305,124 +289,67 @@ __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict_
         double *D = Di + (kb / kNB) * kNB * kNB;
 #pragma unroll
         for (int a = 0; a < kNB; ++a) D[a * kNB + c] = x[a];
-      } else {
-#pragma unroll
-        for (int m = 0; m < kNB; ++m) {
-          double a = (m < nbk) ? Pn[i * kNB + m] : 0.0;
-#pragma unroll
-          for (int q = 0; q < m; ++q) a = fma(-l[q], Ld[m][q], a);
-          l[m] = a * rd[m];
-        }
       }
-#pragma unroll
-      for (int m = 0; m < kNB; ++m) Ln[i * kNB + m] = l[m];
     }
     __syncthreads();
-#pragma unroll
-    for (int r = 0; r < kMaxE; ++r) {
-      if (ij[r] < 0) continue;
-      int i = ij[r] >> 8, j = ij[r] & 255;
-      if (j >= kb && j < kb + nbk) {
-        val[r] = Ln[i * kNB + (j - kb)];
-      } else if (j >= kb + nbk) {
-        const double2 *li = (const double2 *)(Ln + i * kNB);
-        const double2 *lj = (const double2 *)(Ln + j * kNB);
-        double acc = val[r];
-#pragma unroll
-        for (int m = 0; m < kNB / 2; ++m) {
-          double2 x = li[m], y = lj[m];
-          acc = fma(-x.x, y.x, acc);
-          acc = fma(-x.y, y.y, acc);
-        }
-        val[r] = acc;
+    for (int i = kb + warp; i < S; i += nw) {
+      const double4 *li4 = (const double4 *)(Ln + i * kNB);
+      const double4 x0 = li4[0], x1 = li4[1];
+      if (lane < nbk) A[i * LD + kb + lane] = Ln[i * kNB + lane];
+      for (int j = kb + nbk + lane; j <= i; j += 32) {
+        const double4 *lj4 = (const double4 *)(Ln + j * kNB);
+        const double4 y0 = lj4[0], y1 = lj4[1];
+        double acc = A[i * LD + j];
+        acc = fma(-x0.x, y0.x, acc);
+        acc = fma(-x0.y, y0.y, acc);
+        acc = fma(-x0.z, y0.z, acc);
+        acc = fma(-x0.w, y0.w, acc);
+        acc = fma(-x1.x, y1.x, acc);
+        acc = fma(-x1.y, y1.y, acc);
+        acc = fma(-x1.z, y1.z, acc);
+        acc = fma(-x1.w, y1.w, acc);
+        A[i * LD + j] = acc;
       }
     }
+    __syncthreads();
   }
   if (bad && info) atomicExch(info, 1);
-  for (int e = tid; e < S * S; e += kNT) Lf[e] = 0.0;
-  __syncthreads();
-#pragma unroll
-  for (int r = 0; r < kMaxE; ++r)
-    if (ij[r] >= 0) Lf[(ij[r] >> 8) * S + (ij[r] & 255)] = val[r];
-  __syncthreads();
-  const int ti = tid & 127, tr = tid >> 7;
   const int nblk = (S + kNB - 1) / kNB;
-  // forward substitution, L y = b, for every RHS row (rows of Bm hold b^T)
-  for (int bi = 0; bi < nblk; ++bi) {
-    const int kb = bi * kNB;
-    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
-    const double *D = Di + bi * kNB * kNB;
-    double yv[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
-      yv[u] = 0.0;
-      if (r1 < rows && m1 < nbk)
-#pragma unroll
-        for (int q = 0; q < kNB; ++q) yv[u] = fma(D[m1 * kNB + q], (q < nbk) ? Bm[r1 * S + kb + q] : 0.0, yv[u]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
-      if (r1 < rows && m1 < nbk) Bm[r1 * S + kb + m1] = yv[u];
-    }
-    __syncthreads();
-    if (ti >= kb + nbk && ti < S) {
-      double lrow[kNB];
-#pragma unroll
-      for (int m = 0; m < kNB; ++m) lrow[m] = (m < nbk) ? Lf[ti * S + kb + m] : 0.0;
-      for (int r = tr; r < rows; r += kNT / 128) {
-        double acc = Bm[r * S + ti];
-        const double *y = Bm + r * S + kb;
-#pragma unroll
-        for (int m = 0; m < kNB; ++m) acc = fma(-lrow[m], (m < nbk) ? y[m] : 0.0, acc);
-        Bm[r * S + ti] = acc;
+  // forward substitution L y = b (rows of Bm hold b^T), then backward L^T x = y
+  for (int pass = 0; pass < 2; ++pass) {
+    for (int bb = 0; bb < nblk; ++bb) {
+      const int bi = pass == 0 ? bb : nblk - 1 - bb;
+      const int kb = bi * kNB;
+      const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
+      const double *D = Di + bi * kNB * kNB;
+      const int r1 = tid / kNB, m1 = tid % kNB;
+      const bool act = (r1 < rows) && (m1 < nbk);
+      double v = 0.0;
+      if (act) {
+        for (int q = 0; q < nbk; ++q)
+          v = fma(pass == 0 ? D[m1 * kNB + q] : D[q * kNB + m1], Bm[r1 * S + kb + q], v);
       }
-    }
-    __syncthreads();
-  }
-  // backward substitution, L^T x = y
-  for (int bi = nblk - 1; bi >= 0; --bi) {
-    const int kb = bi * kNB;
-    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
-    const double *D = Di + bi * kNB * kNB;
-    double xv[2];
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
-      xv[u] = 0.0;
-      if (r1 < rows && m1 < nbk)
-#pragma unroll
-        for (int q = 0; q < kNB; ++q) xv[u] = fma(D[q * kNB + m1], (q < nbk) ? Bm[r1 * S + kb + q] : 0.0, xv[u]);
-    }
-    __syncthreads();
-#pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      int w = tid + kNT * u, r1 = w / kNB, m1 = w % kNB;
-      if (r1 < rows && m1 < nbk) Bm[r1 * S + kb + m1] = xv[u];
-    }
-    __syncthreads();
-    if (ti < kb) {
-      double lcol[kNB];
-#pragma unroll
-      for (int m = 0; m < kNB; ++m) lcol[m] = (m < nbk) ? Lf[(kb + m) * S + ti] : 0.0;
-      for (int r = tr; r < rows; r += kNT / 128) {
-        double acc = Bm[r * S + ti];
-        const double *x = Bm + r * S + kb;
-#pragma unroll
-        for (int m = 0; m < kNB; ++m) acc = fma(-lcol[m], (m < nbk) ? x[m] : 0.0, acc);
-        Bm[r * S + ti] = acc;
+      __syncthreads();
+      if (act) Bm[r1 * S + kb + m1] = v;
+      __syncthreads();
+      const int lo = pass == 0 ? kb + nbk : 0, hi = pass == 0 ? S : kb;
+      for (int e = tid; e < rows * (hi - lo); e += kNT) {
+        const int r = e / (hi - lo), i = lo + e % (hi - lo);
+        double acc = Bm[r * S + i];
+        for (int m = 0; m < nbk; ++m)
+          acc = fma(-(pass == 0 ? A[i * LD + kb + m] : A[(kb + m) * LD + i]), Bm[r * S + kb + m], acc);
+        Bm[r * S + i] = acc;
       }
+      __syncthreads();
     }
-    __syncthreads();
   }
   for (int e = tid; e < rows * S; e += kNT) Gout[(row0 + e / S) * S + e % S] = Bm[e];
 }
 
 size_t chol_solve_smem(int S) {
-  return sizeof(double) * ((size_t)((S * S + 3) & ~3) + (size_t)kSolveChunk * S + 2 * (size_t)S * kNB +
-                           (size_t)(S / kNB + 1) * kNB * kNB);
+  const int nblk = (S + kNB - 1) / kNB;
+  return sizeof(double) * ((size_t)((S * (S + 1) + 3) & ~3) + (size_t)kSolveChunk * S + (size_t)S * kNB +
+                           (size_t)nblk * kNB * kNB);
 }
 
 void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s) {

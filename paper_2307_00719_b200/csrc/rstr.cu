@@ -1,0 +1,414 @@
+// rstr.cu — randomized streaming TR (rSTR) with uniform (Alg. 7) and
+// leverage-score (Alg. 8) row sampling.
+//
+// Per draw (mode k, time step tau) the host draws m indices with replacement from a SplitMix64
+// stream keyed by (seed, tau, k) (reading R11; the oracle re-implements the same
+// generator independently).  Leverage probabilities p_k(i) = l_i(G_k(2)) / rank (Lemma 1,
+// P:567) are computed on the device (Gram + Cholesky: l_i = g_i^T (G^T G)^{-1} g_i when
+// I_k > R_kR_{k+1}; uniform when I_k <= R_kR_{k+1}, reading R10) and copied to the host for the
+// inverse-CDF draw.  Everything else runs in device kernels:
+//   * sampled slices (G_k)_S = G_k(:, idxs(:,k), :)                       (Alg. 7 l.4)
+//   * sampled subchain G^{≠n}_S by the ⊡₂ chain of sampled slices         (Alg. 3 l.5-7, Def. 7)
+//   * zipped fibers X_S[n] (I_n x m) gathered from X                      (reading R7)
+//   * P_n += X_S[n] G_S[2], Q_n += G_S[2]^T G_S[2], G_n = P_n Q_n^{-1}     (Alg. 7 l.36-38)
+//   * temporal rows G_N^new = X_S[N] G_S (G_S^T G_S)^{-1}                (reading R4)
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "str_internal.h"
+
+namespace strb200 {
+
+// ------------------------------------------------------------------------------------------ kernels
+// out[s][c] = G[idx[s]][c]  (rows of a G(2) matrix with S columns)
+__global__ void k_gather_rows(const double *__restrict__ G, int S, const int32_t *__restrict__ idx, int64_t m,
+                              double *__restrict__ out) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * S) return;
+  int64_t s = e / S;
+  int c = (int)(e % S);
+  out[e] = G[(int64_t)idx[s] * S + c];
+}
+
+// Zipped fibers: XS[i][s] = X(idx(s,1), ..., i (mode n), ..., idx(s,N)), X in the P:119 layout.
+// idx is [N][m] (mode-major); strides[j] = element stride of mode j+1 (time last).
+struct GatherDesc {
+  int N, n;                 // order, target mode (1-based)
+  int64_t stride[8];
+  int64_t In, m;
+};
+
+template <typename T>
+__global__ void k_gather_fibers(const T *__restrict__ X, const int32_t *__restrict__ idx, GatherDesc gd,
+                                double *__restrict__ XS) {
+  int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= gd.In * gd.m) return;
+  int64_t s = e % gd.m, i = e / gd.m;
+  int64_t off = 0;
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (j < gd.N) {
+      int64_t ij = (j == gd.n - 1) ? i : (int64_t)idx[j * gd.m + s];
+      off += ij * gd.stride[j];
+    }
+  }
+  XS[e] = (double)X[off];
+}
+
+// C[M][N] (+)= sum_k A(i,k) B(k,j) with strided operands (fp64), 16x16 tiles.
+__global__ void k_gemm_strided(const double *__restrict__ A, int64_t sai, int64_t sak, const double *__restrict__ B,
+                               int64_t sbk, int64_t sbj, double *__restrict__ C, int M, int N, int64_t K,
+                               int accumulate) {
+  __shared__ double As[16][17], Bs[16][17];
+  int tx = threadIdx.x, ty = threadIdx.y;
+  int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double acc = 0.0;
+  for (int64_t k0 = 0; k0 < K; k0 += 16) {
+    As[ty][tx] = (row < M && k0 + tx < K) ? A[row * sai + (k0 + tx) * sak] : 0.0;
+    Bs[ty][tx] = (k0 + ty < K && col < N) ? B[(k0 + ty) * sbk + col * sbj] : 0.0;
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
+    __syncthreads();
+  }
+  if (row < M && col < N) {
+    double *c = C + (int64_t)row * N + col;
+    *c = accumulate ? *c + acc : acc;
+  }
+}
+
+// Symmetrize: Q = (Q + Q^T)/2 (reading R5).
+__global__ void k_symmetrize(double *Q, int S) {
+  int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= S * S) return;
+  int x = e / S, y = e % S;
+  if (y <= x) return;
+  double v = 0.5 * (Q[x * S + y] + Q[y * S + x]);
+  Q[x * S + y] = v;
+  Q[y * S + x] = v;
+}
+
+// p_i = (sum_c Y[i][c] G[i][c]) / rank   (leverage of row i, Def. 8 via g_i^T (G^T G)^{-1} g_i)
+__global__ void k_rowdot_scale(const double *__restrict__ Y, const double *__restrict__ G, int64_t I, int S,
+                               double inv_rank, double *__restrict__ p) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= I) return;
+  double acc = 0.0;
+  for (int c = 0; c < S; ++c) acc = fma(Y[i * S + c], G[i * S + c], acc);
+  p[i] = acc * inv_rank;
+}
+
+}  // namespace strb200
+
+using namespace strb200;
+
+#define RCU(call)                                                        \
+  do {                                                                   \
+    cudaError_t _e = (call);                                             \
+    if (_e != cudaSuccess) {                                             \
+      h->err = std::string(#call) + ": " + cudaGetErrorString(_e);       \
+      h->poisoned = true;                                                \
+      return STR_E_CUDA;                                                 \
+    }                                                                    \
+  } while (0)
+#define RTRY(call)                 \
+  do {                             \
+    str_status _s = (call);        \
+    if (_s != STR_OK) return _s;   \
+  } while (0)
+
+// ------------------------------------------------------------------------------------------ sampler
+// SplitMix64 (reading R11): key = seed ^ (GOLDEN * (1 + tau*(N+1) + k)); uniform index =
+// (u * I) >> 64; weighted: first i with cdf[i] > (u >> 11) * 2^-53 * cdf[I-1].
+static const uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+
+static inline uint64_t splitmix_next(uint64_t &s) {
+  s += kGolden;
+  uint64_t z = s;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+static void draw_uniform(uint64_t seed, int64_t tau, int k, int N, int64_t I, int64_t m, std::vector<int32_t> &out) {
+  uint64_t s = seed ^ (kGolden * (uint64_t)(1 + tau * (N + 1) + k));
+  out.resize(m);
+  for (int64_t j = 0; j < m; ++j) {
+    unsigned __int128 prod = (unsigned __int128)splitmix_next(s) * (unsigned __int128)(uint64_t)I;
+    out[j] = (int32_t)(uint64_t)(prod >> 64);
+  }
+}
+
+static void draw_weighted(uint64_t seed, int64_t tau, int k, int N, const std::vector<double> &p, int64_t m,
+                          std::vector<int32_t> &out) {
+  uint64_t s = seed ^ (kGolden * (uint64_t)(1 + tau * (N + 1) + k));
+  const int64_t I = (int64_t)p.size();
+  std::vector<double> c(I);
+  double acc = 0.0;
+  for (int64_t i = 0; i < I; ++i) {
+    acc = acc + p[i];
+    c[i] = acc;
+  }
+  out.resize(m);
+  for (int64_t j = 0; j < m; ++j) {
+    uint64_t u = splitmix_next(s);
+    double target = (double)(u >> 11) * 0x1.0p-53 * c[I - 1];
+    int64_t idx = std::upper_bound(c.begin(), c.end(), target) - c.begin();
+    out[j] = (int32_t)std::min<int64_t>(idx, I - 1);
+  }
+}
+
+// ------------------------------------------------------------------------------------------ helpers
+static inline int RRr(const str_state *h, int n) { return h->R[(n - 1) % h->N]; }
+
+static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
+  if (b.bytes >= bytes) return STR_OK;
+  if (b.p) cudaFree(b.p);
+  b.p = nullptr;
+  b.bytes = 0;
+  if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    h->err = "cudaMalloc failed (rSTR workspace)";
+    h->poisoned = true;
+    return STR_E_OOM;
+  }
+  b.bytes = bytes;
+  return STR_OK;
+}
+
+static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj,
+                 double *C, int M, int N, int64_t K, int acc) {
+  dim3 blk(16, 16), grd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
+  k_gemm_strided<<<grd, blk, 0, h->st>>>(A, sai, sak, B, sbk, sbj, C, M, N, K, acc);
+  h->launches++;
+}
+
+// Core k's slices as G(2) rows: k < N -> current core; k == N -> temporal rows [t0, t0 + rows).
+static const double *core_rows(const str_state *h, int k, int64_t t0) {
+  if (k == h->N) return (const double *)h->GN.p + t0 * h->SN;
+  return (const double *)h->md[k - 1].G.p;
+}
+
+// Leverage probabilities of an I x S matrix G (device rows) -> host vector p.
+static str_status leverage_probs(str_state *h, const double *G, int64_t I, int S, std::vector<double> &p) {
+  p.assign(I, 1.0 / (double)I);
+  if (I <= S) return STR_OK;   // full row rank: every score is 1 (reading R10)
+  RTRY(ensure_dev(h, h->sGram, sizeof(double) * S * S));
+  RTRY(ensure_dev(h, h->sTmp, sizeof(double) * (I * S + I)));
+  double *K = (double *)h->sGram.p;
+  double *Y = (double *)h->sTmp.p;
+  double *pd = Y + I * S;
+  gemm(h, G, 1, S, G, S, 1, K, S, S, I, 0);                         // K = G^T G
+  launch_chol_solve(K, S, G, I, Y, h->d_info, h->st);                // Y = G K^{-1}
+  h->launches++;
+  k_rowdot_scale<<<(unsigned)cdiv(I, 128), 128, 0, h->st>>>(Y, G, I, S, 1.0 / (double)S, pd);
+  h->launches++;
+  RCU(cudaMemcpyAsync(p.data(), pd, sizeof(double) * I, cudaMemcpyDeviceToHost, h->st));
+  RCU(cudaStreamSynchronize(h->st));
+  int info = 0;
+  RCU(cudaMemcpy(&info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost));
+  if (info) {
+    h->err = "leverage: G^T G not positive definite";
+    h->poisoned = true;
+    return STR_E_NUMERIC;
+  }
+  return STR_OK;
+}
+
+// idxs(:,k) <- Randsample(I_k, m[, p_k]); (G_k)_S <- G_k(:, idxs(:,k), :)
+static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) {
+  const int S = RRr(h, k) * RRr(h, k + 1);
+  std::vector<int32_t> &ix = h->last_idx[k];
+  if (!h->forced_idx[k].empty()) {
+    ix = h->forced_idx[k];
+  } else if (h->variant == STR_SAMPLE_UNIFORM) {
+    draw_uniform(h->seed, h->tau, k, h->N, I, h->m, ix);
+  } else {
+    std::vector<double> p;
+    RTRY(leverage_probs(h, rows, I, S, p));
+    draw_weighted(h->seed, h->tau, k, h->N, p, h->m, ix);
+  }
+  int32_t *dix = (int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
+  RCU(cudaMemcpyAsync(dix, ix.data(), sizeof(int32_t) * h->m, cudaMemcpyHostToDevice, h->st));
+  // pageable source: make sure the copy has consumed `ix` before it can change
+  RCU(cudaStreamSynchronize(h->st));
+  ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
+  double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
+  k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
+  h->launches++;
+  return STR_OK;
+}
+
+// G_S[2] (m x R_nR_{n+1}) = ⊡₂ chain of sampled slices in order n+1..N, 1..n-1 (identity start).
+static str_status sampled_chain(str_state *h, int n, double *out) {
+  FactorList fl;
+  fl.n = 0;
+  const int N = h->N;
+  for (int k = n + 1; k <= N; ++k) {
+    Factor f;
+    f.G = (k == N) ? (const double *)h->sG.p : (const double *)h->md[k - 1].samp.p;
+    f.I = (int32_t)h->m;
+    f.Ra = RRr(h, k);
+    f.Rb = RRr(h, k + 1);
+    f.stride = 1;
+    fl.f[fl.n++] = f;
+  }
+  for (int k = 1; k < n; ++k) {
+    Factor f;
+    f.G = (const double *)h->md[k - 1].samp.p;
+    f.I = (int32_t)h->m;
+    f.Ra = RRr(h, k);
+    f.Rb = RRr(h, k + 1);
+    f.stride = 1;
+    fl.f[fl.n++] = f;
+  }
+  launch_build_table(fl, h->m, out, h->st);
+  h->launches++;
+  return STR_OK;
+}
+
+static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, double *XS) {
+  GatherDesc gd;
+  gd.N = h->N;
+  gd.n = n;
+  int64_t st = 1;
+  for (int j = 0; j < h->N - 1; ++j) {
+    gd.stride[j] = st;
+    st *= h->md[j].I;
+  }
+  gd.stride[h->N - 1] = st;
+  for (int j = h->N; j < 8; ++j) gd.stride[j] = 0;
+  gd.In = (n == h->N) ? tn : h->md[n - 1].I;
+  gd.m = h->m;
+  const unsigned grid = (unsigned)cdiv(gd.In * gd.m, 256);
+  if (h->dtype == STR_F64)
+    k_gather_fibers<double><<<grid, 256, 0, h->st>>>((const double *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
+  else
+    k_gather_fibers<float><<<grid, 256, 0, h->st>>>((const float *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
+  h->launches++;
+  return STR_OK;
+}
+
+static str_status rstr_workspace(str_state *h, int64_t tn) {
+  int64_t maxI = tn;
+  int maxS = 0;
+  for (auto &mb : h->md) {
+    maxI = std::max<int64_t>(maxI, mb.I);
+    maxS = std::max(maxS, mb.Ra * mb.Rb);
+  }
+  maxS = std::max(maxS, h->SN);
+  RTRY(ensure_dev(h, h->sIdxDev, sizeof(int32_t) * h->N * h->m));
+  RTRY(ensure_dev(h, h->sX, sizeof(double) * maxI * h->m));
+  RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS));
+  RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS));   // G_S[2]
+  RTRY(ensure_dev(h, h->sGram, sizeof(double) * maxS * maxS));
+  RTRY(ensure_dev(h, h->Mt, sizeof(double) * std::max<int64_t>(maxI, tn) * maxS));
+  for (auto &mb : h->md) RTRY(ensure_dev(h, mb.samp, sizeof(double) * h->m * mb.Ra * mb.Rb));
+  return STR_OK;
+}
+
+// Accumulate the sampled normal equations of mode n (1..N-1) from X (tn slices): P_n (+)= X_S G_S,
+// Q_n (+)= G_S^T G_S (Alg. 7 l.15-16 / l.36-37).
+static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t tn, int acc) {
+  ModeBuf &mb = h->md[n - 1];
+  const int S = mb.Ra * mb.Rb;
+  double *GS = (double *)h->sidx.p;
+  double *XS = (double *)h->sX.p;
+  RTRY(sampled_chain(h, n, GS));
+  RTRY(gather_fibers(h, X, n, tn, XS));
+  gemm(h, XS, h->m, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, h->m, acc);
+  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, h->m, acc);
+  k_symmetrize<<<(unsigned)cdiv(S * S, 256), 256, 0, h->st>>>((double *)mb.Q.p, S);
+  h->launches++;
+  return STR_OK;
+}
+
+str_status rstr_init(str_state *h, const void *X, int64_t tn) {
+  RTRY(rstr_workspace(h, tn));
+  h->tau = 0;
+  const int N = h->N;
+  // Alg. 7 l.2-5 / Alg. 8 l.2-6: draws for k = 1..N (I_N = t_init)
+  for (int k = 1; k <= N; ++k) RTRY(draw_mode(h, k, core_rows(h, k, 0), k == N ? tn : h->md[k - 1].I));
+  for (int n = 1; n < N; ++n) RTRY(sampled_normal_eq(h, X, n, tn, 0));
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->err = std::string("rstr_init: ") + cudaGetErrorString(e);
+    h->poisoned = true;
+    return STR_E_CUDA;
+  }
+  return STR_OK;
+}
+
+str_status rstr_update(str_state *h, const void *X, int64_t tn) {
+  RTRY(rstr_workspace(h, tn));
+  const int N = h->N;
+  h->tau++;
+  RTRY(ensure_temporal_capacity(h, h->T + tn));
+  // temporal: G_N^new = X_S[N] G_S (G_S^T G_S)^{-1}  (Alg. 7 l.17-23, reading R4)
+  const int SN = h->SN;
+  double *GS = (double *)h->sidx.p;
+  double *XS = (double *)h->sX.p;
+  double *K = (double *)h->sGram.p;
+  double *M = (double *)h->Mt.p;
+  RTRY(sampled_chain(h, N, GS));
+  RTRY(gather_fibers(h, X, N, tn, XS));
+  gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
+  gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0);
+  k_symmetrize<<<(unsigned)cdiv(SN * SN, 256), 256, 0, h->st>>>(K, SN);
+  h->launches++;
+  double *GN_new = (double *)h->GN.p + h->T * SN;
+  launch_chol_solve(K, SN, M, tn, GN_new, h->d_info, h->st);
+  h->launches++;
+  // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
+  RTRY(draw_mode(h, N, GN_new, tn));
+  for (int n = 1; n < N; ++n) {
+    ModeBuf &mb = h->md[n - 1];
+    RTRY(sampled_normal_eq(h, X, n, tn, 1));
+    launch_chol_solve((const double *)mb.Q.p, mb.Ra * mb.Rb, (const double *)mb.P.p, mb.I, (double *)mb.G.p,
+                      h->d_info, h->st);
+    h->launches++;
+    RTRY(draw_mode(h, n, (const double *)mb.G.p, mb.I));
+  }
+  h->T += tn;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    h->err = std::string("rstr_update: ") + cudaGetErrorString(e);
+    h->poisoned = true;
+    return STR_E_CUDA;
+  }
+  return STR_OK;
+}
+
+extern "C" STR_API str_status str_get_index_table(str_state *h, int32_t mode, int32_t *idx, int64_t m) {
+  if (!h || !idx) return STR_E_ARG;
+  if (h->variant == STR_DET || mode < 1 || mode > h->N || m != h->m || h->last_idx[mode].empty()) {
+    h->err = "no index table for this mode";
+    return STR_E_ARG;
+  }
+  std::copy(h->last_idx[mode].begin(), h->last_idx[mode].end(), idx);
+  return STR_OK;
+}
+
+extern "C" STR_API str_status str_set_index_table(str_state *h, int32_t mode, const int32_t *idx, int64_t m) {
+  if (!h) return STR_E_ARG;
+  if (h->variant == STR_DET || mode < 1 || mode > h->N) {
+    h->err = "index tables exist only for rSTR modes 1..N";
+    return STR_E_ARG;
+  }
+  if (!idx || m == 0) {
+    h->forced_idx[mode].clear();
+    return STR_OK;
+  }
+  if (m != h->m) {
+    h->err = "index table length must equal sketch_rows";
+    return STR_E_ARG;
+  }
+  h->forced_idx[mode].assign(idx, idx + m);
+  return STR_OK;
+}

@@ -180,7 +180,7 @@ static str_status run_absorbs(str_state *h, const double *Y, std::vector<int> mo
     ad.Rb = op.A.Rb;
     bool last = s + 1 == ops.size();
     double *out = last ? dst : (double *)((s % 2 == 0) ? h->tmpA.p : h->tmpB.p);
-    launch_absorb(ad, cur, out, last ? accumulate : 0, h->st);
+    launch_absorb(ad, cur, false, out, last ? accumulate : 0, h->st);
     h->launches++;
     TRY(check_launch(h, "absorb"));
     if (op.left) P = op.A.Ra; else Q = op.A.Rb;
@@ -284,7 +284,7 @@ static str_status ensure_workspace(str_state *h, int64_t tn) {
   return STR_OK;
 }
 
-static str_status ensure_temporal_capacity(str_state *h, int64_t need) {
+str_status ensure_temporal_capacity(str_state *h, int64_t need) {
   if (need <= h->Tcap) return STR_OK;
   int64_t cap = std::max<int64_t>(need, 2 * h->Tcap);
   DevBuf nb;
@@ -566,6 +566,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   if (cfg->dims[0] % p != 0) return STR_E_PRECOND;
   if (cfg->split_k < 0 || cfg->split_k > N - 2) return STR_E_ARG;
   if (cfg->dtype != STR_F32 && cfg->dtype != STR_F64) return STR_E_ARG;
+  if (cfg->variant != STR_DET && p > 1) return STR_E_PRECOND;   // rSTR runs as replicas only
   if (cfg->variant != STR_DET) {
     int64_t need = 0;
     for (int n = 0; n < N; ++n) need = std::max<int64_t>(need, (int64_t)cfg->ranks[n] * cfg->ranks[(n + 1) % N]);

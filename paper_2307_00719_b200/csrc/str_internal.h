@@ -105,6 +105,9 @@ struct str_state {
   }
 };
 
+// str_api.cu
+str_status ensure_temporal_capacity(str_state *h, int64_t need);
+
 // rstr.cu
 str_status rstr_init(str_state *h, const void *X, int64_t tn);
 str_status rstr_update(str_state *h, const void *X, int64_t tn);

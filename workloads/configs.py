@@ -98,6 +98,11 @@ CONFIGS.update({
                        core_scale=0.5, noise_abs=1e-2, seed=51, split_k=2),
     "P1": StreamConfig("P1", (20, 20), (3, 3, 3), 10, 2, 10, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-3, seed=111),
+    # rSTR parity: I_k > R_kR_{k+1} so leverage scores are non-uniform; m >= max R_nR_{n+1}.
+    "R4": StreamConfig("R4", (30, 25, 20), (2, 3, 2, 3), 6, 4, 3, "f32", "f64",
+                       core_scale=0.7, noise_abs=1e-2, seed=41, sketch_rows=200),
+    "R5": StreamConfig("R5", (12, 9, 10, 8), (2, 3, 2, 2, 3), 5, 3, 3, "f64", "f64",
+                       core_scale=0.7, noise_abs=1e-2, seed=42, sketch_rows=150),
 })
 
 
