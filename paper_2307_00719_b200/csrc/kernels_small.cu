@@ -223,26 +223,42 @@ void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate
 //            entries take the rank-8 update.
 // Forward / backward substitution then use the inverted diagonal blocks.  Each CTA factors Q
 // (cheap, redundant) and solves a chunk of <= 16 RHS rows.  A non-positive pivot sets *info.
-constexpr int kNB = 8, kNT = 512, kSolveChunk = 16;
+constexpr int kNB = 8, kNT = 512, kSolveChunk = 16;   // rows per CTA = 4 * (kNT / 128)
+#ifdef STR_CHOL_PROBE
+__device__ long long *g_probe = nullptr;
+#endif
 
 __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict__ Q, int S,
                                                         const double *__restrict__ P, int64_t I,
                                                         double *__restrict__ Gout, int *info) {
   extern __shared__ double sm[];
   const int LD = S + 1;                      // padded row stride of A
+  const int nblk = (S + kNB - 1) / kNB;
   double *A = sm;                            // S x LD
-  double *Bm = A + ((S * LD + 3) & ~3);      // kSolveChunk x S
-  double *Ln = Bm + kSolveChunk * S;         // S x 8 panel of L
-  double *Di = Ln + S * kNB;                 // nblk x 64 inverted diagonal blocks
+  double *Bm = A + ((S * LD + 3) & ~3);      // kSolveChunk x LD (RHS rows)
+  double *LnT = Bm + ((kSolveChunk * LD + 3) & ~3);   // 8 x S panel of L, m-major
+  double *Ln = LnT + ((kNB * S + 3) & ~3);            // S x 8 panel of L, row-major
+  double *Di = Ln + kNB * S;                          // nblk x 64 inverted diagonal blocks (zero padded)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kNT / 32;
   const int64_t row0 = (int64_t)blockIdx.x * kSolveChunk;
   const int rows = (int)((I - row0) < kSolveChunk ? (I - row0) : kSolveChunk);
+#ifdef STR_CHOL_PROBE
+  long long t_start = clock64();
+#endif
   for (int e = tid; e < S * S; e += kNT) A[(e / S) * LD + e % S] = Q[e];
-  for (int e = tid; e < rows * S; e += kNT) Bm[e] = P[(row0 + e / S) * S + e % S];
+  for (int e = tid; e < rows * S; e += kNT) Bm[(e / S) * LD + e % S] = P[(row0 + e / S) * S + e % S];
+  for (int e = tid; e < nblk * kNB * kNB; e += kNT) Di[e] = 0.0;
   __syncthreads();
+#ifdef STR_CHOL_PROBE
+  long long t_loaded = clock64();
+  long long tB = 0, tC = 0;
+#endif
   bool bad = false;
   for (int kb = 0; kb < S; kb += kNB) {
     const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
+#ifdef STR_CHOL_PROBE
+    long long t0 = clock64();
+#endif
     if (tid < S - kb) {
       const int i = kb + tid;
       double Ld[kNB][kNB], rd[kNB], l[kNB];
@@ -275,9 +291,11 @@ __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict_
         l[m] = (m <= c) ? a * rd[m] : 0.0;
       }
 #pragma unroll
-      for (int m = 0; m < kNB; ++m) Ln[i * kNB + m] = l[m];
+      for (int m = 0; m < kNB; ++m) LnT[m * S + i] = l[m];
+      double4 *lr = (double4 *)(Ln + i * kNB);
+      lr[0] = make_double4(l[0], l[1], l[2], l[3]);
+      lr[1] = make_double4(l[4], l[5], l[6], l[7]);
       if (c < nbk) {
-        // column c of the inverse of the lower-triangular diagonal block
         double x[kNB];
 #pragma unroll
         for (int a = 0; a < kNB; ++a) {
@@ -292,64 +310,115 @@ __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict_
       }
     }
     __syncthreads();
-    for (int i = kb + warp; i < S; i += nw) {
-      const double4 *li4 = (const double4 *)(Ln + i * kNB);
-      const double4 x0 = li4[0], x1 = li4[1];
-      if (lane < nbk) A[i * LD + kb + lane] = Ln[i * kNB + lane];
-      for (int j = kb + nbk + lane; j <= i; j += 32) {
-        const double4 *lj4 = (const double4 *)(Ln + j * kNB);
-        const double4 y0 = lj4[0], y1 = lj4[1];
-        double acc = A[i * LD + j];
-        acc = fma(-x0.x, y0.x, acc);
-        acc = fma(-x0.y, y0.y, acc);
-        acc = fma(-x0.z, y0.z, acc);
-        acc = fma(-x0.w, y0.w, acc);
-        acc = fma(-x1.x, y1.x, acc);
-        acc = fma(-x1.y, y1.y, acc);
-        acc = fma(-x1.z, y1.z, acc);
-        acc = fma(-x1.w, y1.w, acc);
-        A[i * LD + j] = acc;
+#ifdef STR_CHOL_PROBE
+    long long t1 = clock64();
+    tB += t1 - t0;
+#endif
+    // panel write-back, then rank-8 update of the trailing lower triangle: a warp task is a strip
+    // of up to 8 rows x 32 columns; lane j keeps y = L[j][kb..kb+7] in registers and reads the
+    // row values x = L[i][kb..kb+7] as broadcasts from the row-major copy Ln.
+    for (int e = tid; e < (S - kb) * nbk; e += kNT) {
+      const int i = kb + e / nbk, m = e % nbk;
+      A[i * LD + kb + m] = LnT[m * S + i];
+    }
+    {
+      const int j0 = kb + nbk;
+      const int nch = (S - j0 + 31) / 32;
+      const int nrg = (S - j0 + 7) / 8;
+      for (int task = warp; task < nch * nrg; task += nw) {
+        const int ch = task % nch, rg = task / nch;
+        const int j = j0 + ch * 32 + lane;
+        const int ib = j0 + rg * 8;
+        if (ib + 7 < j0 + ch * 32) continue;               // strip entirely above the diagonal
+        double y[kNB];
+#pragma unroll
+        for (int m = 0; m < kNB; ++m) y[m] = (j < S && m < nbk) ? LnT[m * S + j] : 0.0;
+#pragma unroll 2
+        for (int a = 0; a < 8; ++a) {
+          const int i = ib + a;
+          if (i >= S) break;
+          const double4 *xr = (const double4 *)(Ln + i * kNB);
+          const double4 x0 = xr[0], x1 = xr[1];
+          if (j <= i) {
+            double acc0 = A[i * LD + j], acc1 = 0.0;
+            acc0 = fma(-x0.x, y[0], acc0);
+            acc1 = fma(-x0.y, y[1], acc1);
+            acc0 = fma(-x0.z, y[2], acc0);
+            acc1 = fma(-x0.w, y[3], acc1);
+            acc0 = fma(-x1.x, y[4], acc0);
+            acc1 = fma(-x1.y, y[5], acc1);
+            acc0 = fma(-x1.z, y[6], acc0);
+            acc1 = fma(-x1.w, y[7], acc1);
+            A[i * LD + j] = acc0 + acc1;
+          }
+        }
       }
     }
     __syncthreads();
+#ifdef STR_CHOL_PROBE
+    tC += clock64() - t1;
+#endif
   }
   if (bad && info) atomicExch(info, 1);
-  const int nblk = (S + kNB - 1) / kNB;
-  // forward substitution L y = b (rows of Bm hold b^T), then backward L^T x = y
+#ifdef STR_CHOL_PROBE
+  long long t_fact = clock64();
+#endif
+  // forward substitution L y = b (rows of Bm hold b^T), then backward L^T x = y, block by block:
+  // (1) threads (r, m) form y_blk = Dinv b_blk, (2) store, (3) threads (i, r) take the rank-8 update.
+  const int ti = tid & 127, tr = tid >> 7;
   for (int pass = 0; pass < 2; ++pass) {
     for (int bb = 0; bb < nblk; ++bb) {
       const int bi = pass == 0 ? bb : nblk - 1 - bb;
       const int kb = bi * kNB;
       const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
       const double *D = Di + bi * kNB * kNB;
-      const int r1 = tid / kNB, m1 = tid % kNB;
+      const int r1 = tid >> 3, m1 = tid & 7;
       const bool act = (r1 < rows) && (m1 < nbk);
-      double v = 0.0;
+      double v0 = 0.0, v1 = 0.0;
       if (act) {
-        for (int q = 0; q < nbk; ++q)
-          v = fma(pass == 0 ? D[m1 * kNB + q] : D[q * kNB + m1], Bm[r1 * S + kb + q], v);
+#pragma unroll
+        for (int q = 0; q < kNB; q += 2) {
+          const double d0 = pass == 0 ? D[m1 * kNB + q] : D[q * kNB + m1];
+          const double d1 = pass == 0 ? D[m1 * kNB + q + 1] : D[(q + 1) * kNB + m1];
+          v0 = fma(d0, (q < nbk) ? Bm[r1 * LD + kb + q] : 0.0, v0);
+          v1 = fma(d1, (q + 1 < nbk) ? Bm[r1 * LD + kb + q + 1] : 0.0, v1);
+        }
       }
       __syncthreads();
-      if (act) Bm[r1 * S + kb + m1] = v;
+      if (act) Bm[r1 * LD + kb + m1] = v0 + v1;
       __syncthreads();
-      const int lo = pass == 0 ? kb + nbk : 0, hi = pass == 0 ? S : kb;
-      for (int e = tid; e < rows * (hi - lo); e += kNT) {
-        const int r = e / (hi - lo), i = lo + e % (hi - lo);
-        double acc = Bm[r * S + i];
-        for (int m = 0; m < nbk; ++m)
-          acc = fma(-(pass == 0 ? A[i * LD + kb + m] : A[(kb + m) * LD + i]), Bm[r * S + kb + m], acc);
-        Bm[r * S + i] = acc;
+      const bool upd = ti < S && (pass == 0 ? (ti >= kb + nbk) : (ti < kb));
+      if (upd) {
+        double lv[kNB];
+#pragma unroll
+        for (int m = 0; m < kNB; ++m)
+          lv[m] = (m < nbk) ? (pass == 0 ? A[ti * LD + kb + m] : A[(kb + m) * LD + ti]) : 0.0;
+        for (int r = tr; r < rows; r += kNT / 128) {
+          const double *yb = Bm + r * LD + kb;
+          double acc0 = Bm[r * LD + ti], acc1 = 0.0;
+#pragma unroll
+          for (int m = 0; m < kNB; m += 2) {
+            acc0 = fma(-lv[m], (m < nbk) ? yb[m] : 0.0, acc0);
+            acc1 = fma(-lv[m + 1], (m + 1 < nbk) ? yb[m + 1] : 0.0, acc1);
+          }
+          Bm[r * LD + ti] = acc0 + acc1;
+        }
       }
       __syncthreads();
     }
   }
-  for (int e = tid; e < rows * S; e += kNT) Gout[(row0 + e / S) * S + e % S] = Bm[e];
+  for (int e = tid; e < rows * S; e += kNT) Gout[(row0 + e / S) * S + e % S] = Bm[(e / S) * LD + e % S];
+#ifdef STR_CHOL_PROBE
+  if (tid == 0 && blockIdx.x == 0 && g_probe) {
+    g_probe[0] = t_loaded - t_start; g_probe[1] = tB; g_probe[2] = tC; g_probe[3] = clock64() - t_fact;
+  }
+#endif
 }
 
 size_t chol_solve_smem(int S) {
   const int nblk = (S + kNB - 1) / kNB;
-  return sizeof(double) * ((size_t)((S * (S + 1) + 3) & ~3) + (size_t)kSolveChunk * S + (size_t)S * kNB +
-                           (size_t)nblk * kNB * kNB);
+  return sizeof(double) * ((size_t)((S * (S + 1) + 3) & ~3) + (size_t)((kSolveChunk * (S + 1) + 3) & ~3) +
+                           (size_t)((S * kNB + 3) & ~3) + (size_t)S * kNB + (size_t)nblk * kNB * kNB);
 }
 
 void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s) {
