@@ -99,17 +99,28 @@ __global__ void __launch_bounds__(kAbsorbThreads) k_absorb(AbsorbDesc ad, const 
     for (int e = threadIdx.x; e < ic * AB; e += kAbsorbThreads) As[e] = Ag[e];
     __syncthreads();
     if (active) {
+      // fully unrolled (predicated) inner loop: the STR_MAXR loads of one i issue back to back
       if (ad.left) {
         for (int i = sub; i < ic; i += g) {
           const double *a = As + i * AB + po;
           const TY *y = ybase + (i0 + i) * ystride + qo;
-          for (int p = 0; p < ad.P; ++p) acc = fma(a[ad.Ra * p], (double)y[p * ad.Q], acc);
+          double yv[STR_MAXR];
+#pragma unroll
+          for (int p = 0; p < STR_MAXR; ++p) yv[p] = (p < ad.P) ? (double)y[p * ad.Q] : 0.0;
+#pragma unroll
+          for (int p = 0; p < STR_MAXR; ++p)
+            if (p < ad.P) acc = fma(a[ad.Ra * p], yv[p], acc);
         }
       } else {
         for (int i = sub; i < ic; i += g) {
           const double *a = As + i * AB + ad.Ra * qo;
           const TY *y = ybase + (i0 + i) * ystride + po * ad.Q;
-          for (int q = 0; q < ad.Q; ++q) acc = fma((double)y[q], a[q], acc);
+          double yv[STR_MAXR];
+#pragma unroll
+          for (int q = 0; q < STR_MAXR; ++q) yv[q] = (q < ad.Q) ? (double)y[q] : 0.0;
+#pragma unroll
+          for (int q = 0; q < STR_MAXR; ++q)
+            if (q < ad.Q) acc = fma(yv[q], a[q], acc);
         }
       }
     }
@@ -154,8 +165,17 @@ __global__ void k_gram_z(const double *__restrict__ G, int64_t I, int Ra, int Rb
   int row = gid / cols, col = gid % cols;
   int a = row % Rb, c = row / Rb, b = col % Ra, d = col / Ra;
   const int64_t ssz = (int64_t)Ra * Rb;
-  double acc = 0.0;
-  for (int64_t i = 0; i < I; ++i) acc = fma(G[i * ssz + b + Ra * a], G[i * ssz + d + Ra * c], acc);
+  const double *g1 = G + b + Ra * a, *g2 = G + d + Ra * c;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  int64_t i = 0;
+  for (; i + 4 <= I; i += 4) {
+    acc0 = fma(g1[i * ssz], g2[i * ssz], acc0);
+    acc1 = fma(g1[(i + 1) * ssz], g2[(i + 1) * ssz], acc1);
+    acc2 = fma(g1[(i + 2) * ssz], g2[(i + 2) * ssz], acc2);
+    acc3 = fma(g1[(i + 3) * ssz], g2[(i + 3) * ssz], acc3);
+  }
+  for (; i < I; ++i) acc0 = fma(g1[i * ssz], g2[i * ssz], acc0);
+  const double acc = (acc0 + acc1) + (acc2 + acc3);
   if (accumulate) Zm[gid] += acc; else Zm[gid] = acc;
 }
 
@@ -165,22 +185,34 @@ void launch_gram_z(const double *G, int64_t I, int Ra, int Rb, double *Zm, int a
 }
 
 // ------------------------------------------------------------------------------------------
-// Small row-major fp64 GEMM C[M][N] = A[M][K] B[K][N] (Gram-chain links).  16x16 tiles.
-__global__ void k_dgemm(const double *__restrict__ A, const double *__restrict__ B, double *__restrict__ C, int M,
-                        int N, int K) {
-  __shared__ double As[16][17], Bs[16][17];
-  int tx = threadIdx.x, ty = threadIdx.y;
-  int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
-  double acc = 0.0;
-  for (int k0 = 0; k0 < K; k0 += 16) {
-    As[ty][tx] = (row < M && k0 + tx < K) ? A[(int64_t)row * K + k0 + tx] : 0.0;
-    Bs[ty][tx] = (k0 + ty < K && col < N) ? B[(int64_t)(k0 + ty) * N + col] : 0.0;
+// Small row-major fp64 GEMM C[M][N] = A[M][K] B[K][N] (Gram-chain links).  16x16 output tiles
+// (one per thread block of 256), K staged 32 at a time, 4 independent accumulator chains.
+__global__ void __launch_bounds__(256) k_dgemm(const double *__restrict__ A, const double *__restrict__ B,
+                                               double *__restrict__ C, int M, int N, int K) {
+  __shared__ double As[16][33], Bs[32][17];
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * 16 + tx;
+  const int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
+  double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0, acc3 = 0.0;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    for (int e = tid; e < 16 * 32; e += 256) {
+      const int r = e / 32, kk = e % 32;
+      const int gr = blockIdx.y * 16 + r;
+      As[r][kk] = (gr < M && k0 + kk < K) ? A[(int64_t)gr * K + k0 + kk] : 0.0;
+      const int kr = e / 16, cc = e % 16;
+      const int gc = blockIdx.x * 16 + cc;
+      Bs[kr][cc] = (k0 + kr < K && gc < N) ? B[(int64_t)(k0 + kr) * N + gc] : 0.0;
+    }
     __syncthreads();
 #pragma unroll
-    for (int kk = 0; kk < 16; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
+    for (int kk = 0; kk < 32; kk += 4) {
+      acc0 = fma(As[ty][kk], Bs[kk][tx], acc0);
+      acc1 = fma(As[ty][kk + 1], Bs[kk + 1][tx], acc1);
+      acc2 = fma(As[ty][kk + 2], Bs[kk + 2][tx], acc2);
+      acc3 = fma(As[ty][kk + 3], Bs[kk + 3][tx], acc3);
+    }
     __syncthreads();
   }
-  if (row < M && col < N) C[(int64_t)row * N + col] = acc;
+  if (row < M && col < N) C[(int64_t)row * N + col] = (acc0 + acc1) + (acc2 + acc3);
 }
 
 void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, cudaStream_t s) {

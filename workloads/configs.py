@@ -83,9 +83,9 @@ CONFIGS = {
 # Small variants for the oracle suite and for GPU parity at sizes the oracle finishes in
 # seconds.  Unequal ranks catch index-pairing mistakes; ragged dims span several tiles.
 CONFIGS.update({
-    "T3": StreamConfig("T3", (5, 4), (2, 3, 4), 6, 2, 3, "f64", "f64",
+    "T3": StreamConfig("T3", (6, 4), (2, 3, 4), 6, 2, 3, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-2, seed=7),
-    "T4": StreamConfig("T4", (5, 4, 3), (2, 3, 4, 2), 6, 3, 3, "f64", "f64",
+    "T4": StreamConfig("T4", (6, 4, 3), (2, 3, 4, 2), 6, 3, 3, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-2, seed=8),
     "T5": StreamConfig("T5", (4, 3, 5, 3), (2, 3, 2, 4, 3), 5, 2, 3, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-2, seed=9, split_k=2),
