@@ -255,7 +255,7 @@ void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate
 //            entries take the rank-8 update.
 // Forward / backward substitution then use the inverted diagonal blocks.  Each CTA factors Q
 // (cheap, redundant) and solves a chunk of <= 16 RHS rows.  A non-positive pivot sets *info.
-constexpr int kNB = 8, kNT = 512, kSolveChunk = 16;   // rows per CTA = 4 * (kNT / 128)
+constexpr int kNB = 8, kNT = 512, kSolveChunk = 4;    // RHS rows per CTA (the factorization is repeated per CTA)
 #ifdef STR_CHOL_PROBE
 __device__ long long *g_probe = nullptr;
 #endif
@@ -365,23 +365,33 @@ __global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict_
         double y[kNB];
 #pragma unroll
         for (int m = 0; m < kNB; ++m) y[m] = (j < S && m < nbk) ? LnT[m * S + j] : 0.0;
-#pragma unroll 2
-        for (int a = 0; a < 8; ++a) {
-          const int i = ib + a;
-          if (i >= S) break;
-          const double4 *xr = (const double4 *)(Ln + i * kNB);
-          const double4 x0 = xr[0], x1 = xr[1];
-          if (j <= i) {
-            double acc0 = A[i * LD + j], acc1 = 0.0;
-            acc0 = fma(-x0.x, y[0], acc0);
-            acc1 = fma(-x0.y, y[1], acc1);
-            acc0 = fma(-x0.z, y[2], acc0);
-            acc1 = fma(-x0.w, y[3], acc1);
-            acc0 = fma(-x1.x, y[4], acc0);
-            acc1 = fma(-x1.y, y[5], acc1);
-            acc0 = fma(-x1.z, y[6], acc0);
-            acc1 = fma(-x1.w, y[7], acc1);
-            A[i * LD + j] = acc0 + acc1;
+        // two groups of 4 rows: all shared loads of a group are issued before its stores
+#pragma unroll
+        for (int g4 = 0; g4 < 8; g4 += 4) {
+          double4 xa[4][2];
+          double av[4];
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int i = ib + g4 + a;
+            const bool ok = i < S;
+            const double4 *xr = (const double4 *)(Ln + (ok ? i : kb) * kNB);
+            xa[a][0] = xr[0];
+            xa[a][1] = xr[1];
+            av[a] = (ok && j <= i) ? A[i * LD + j] : 0.0;
+          }
+#pragma unroll
+          for (int a = 0; a < 4; ++a) {
+            const int i = ib + g4 + a;
+            double acc0 = av[a], acc1 = 0.0;
+            acc0 = fma(-xa[a][0].x, y[0], acc0);
+            acc1 = fma(-xa[a][0].y, y[1], acc1);
+            acc0 = fma(-xa[a][0].z, y[2], acc0);
+            acc1 = fma(-xa[a][0].w, y[3], acc1);
+            acc0 = fma(-xa[a][1].x, y[4], acc0);
+            acc1 = fma(-xa[a][1].y, y[5], acc1);
+            acc0 = fma(-xa[a][1].z, y[6], acc0);
+            acc1 = fma(-xa[a][1].w, y[7], acc1);
+            if (i < S && j <= i) A[i * LD + j] = acc0 + acc1;
           }
         }
       }
