@@ -45,6 +45,21 @@ struct AbsorbDesc {
   int32_t Ra, Rb;  // A slice shape
 };
 
+// Chained-slice table over work units (t', l-block of 32): entries e = l + Lk t', l < Lk, t' < tk.
+// Npad > 0 additionally emits the pre-tiled 3xTF32 operand blocks (2 Npad rows x 32 k).
+struct TableDesc {
+  FactorList fl;
+  int64_t Lk, tk;
+  int32_t Npad;
+};
+
+// Epilogue of k_chain_gemm: mode 0 = store C; 1 = Q = H_<2>; 2 = Q += H_<2> (Rn = R_n, Rn1 = R_{n+1}).
+struct QEpi {
+  double *Q;
+  int32_t Rn, Rn1;
+  int32_t mode;
+};
+
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
 }  // namespace strb200

@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 
 #include "common.cuh"
@@ -278,43 +279,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (warp == 2) tc::tmem_dealloc(tbase, 512);
 }
 
-// ---------------------------------------------------------------------------------------------
-// fp64 table [k][w] (k = l' + Lk t') -> pre-tiled 3xTF32 operand blocks: block kt = t' nlb + l'/32
-// holds rows n in [0, 2 Npad) x 32 k-columns; row n < Npad is hi(w = n), row n >= Npad is
-// lo(w = n - Npad); 16-byte chunk c of row n is stored at chunk c ^ (n % 8) (128B swizzle).
-__global__ void k_split_table(const double *__restrict__ tab, int64_t Lk, int64_t tk, int W, int Npad,
-                              float *__restrict__ out) {
-  const int nlb = (int)cdiv(Lk, 32);
-  const int64_t total = tk * nlb * (int64_t)(2 * Npad) * 32;
-  int64_t gid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (gid >= total) return;
-  const int kk = (int)(gid % 32);
-  const int n = (int)((gid / 32) % (2 * Npad));
-  const int64_t kt = gid / (32 * 2 * Npad);
-  const int64_t tp = kt / nlb, lb = kt % nlb;
-  const int64_t lp = lb * 32 + kk;
-  const int w = n < Npad ? n : n - Npad;
-  float v = 0.0f;
-  if (lp < Lk && w < W) {
-    double x = tab[(lp + Lk * tp) * W + w];
-    float hi = __uint_as_float((__float_as_uint((float)x) + 0x1000u) & 0xFFFFE000u);   // round to tf32
-    if (n < Npad) {
-      v = hi;
-    } else {
-      float lo = (float)(x - (double)hi);
-      v = __uint_as_float((__float_as_uint(lo) + 0x1000u) & 0xFFFFE000u);
-    }
-  }
-  const int chunk = kk / 4, within = kk % 4;
-  const int64_t off = kt * (2 * Npad) * 32 + (int64_t)n * 32 + ((chunk ^ (n % 8)) * 4) + within;
-  out[off] = v;
-}
-
-__global__ void k_f32_to_f64(const float *__restrict__ a, double *__restrict__ b, int64_t n) {
-  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i < n) b[i] = (double)a[i];
-}
-
 }  // namespace strb200
 
 // =============================================================================================
@@ -375,41 +339,59 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
     b.bytes = bytes;
     return true;
   };
-  if (!grow(h->tab_split, tiles) || !grow(h->tf_part, yf)) {
+  if (!grow(h->tab_split, tiles) || !grow(h->tf_part, yf) || !grow(h->tf_part2, yf)) {
     h->err = "cudaMalloc failed (3xTF32 workspace)";
     return STR_E_OOM;
   }
   return STR_OK;
 }
 
-int launch_contract_tf32(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out) {
+int tf32_npad(int W) { return npad_of(W); }
+
+static bool encode_x_map(str_state *h, CUtensorMap *tmap, const void *X, int pass, int64_t tn) {
+  const int64_t L = h->L, Rr = h->Rr;
+  cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)Rr, (cuuint64_t)tn};
+  cuuint64_t strides[2] = {(cuuint64_t)L * 4, (cuuint64_t)L * Rr * 4};
+  cuuint32_t box[3] = {32, (cuuint32_t)(pass == 1 ? 32 : 128), 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(X), dims, strides, box, es,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    h->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
+str_status tf32_graph_update(str_state *h, cudaGraphExec_t exec, int pass, const void *X, int64_t tn) {
+  CUtensorMap tmap;
+  if (!encode_x_map(h, &tmap, X, pass, tn)) return STR_E_CUDA;
+  TcParams p;
+  memcpy(&p, h->tf_params[pass - 1], sizeof(TcParams));
+  void *args[2] = {&tmap, &p};
+  cudaKernelNodeParams kp = {};
+  kp.func = pass == 1 ? (void *)k_contract_tf32<1> : (void *)k_contract_tf32<2>;
+  kp.gridDim = dim3(h->tf_grid[pass - 1]);
+  kp.blockDim = dim3(kTcThreads);
+  kp.sharedMemBytes = (unsigned)h->tf_smem[pass - 1];
+  kp.kernelParams = args;
+  kp.extra = nullptr;
+  cudaError_t e = cudaGraphExecKernelNodeSetParams(exec, h->tf_node[pass - 1], &kp);
+  if (e != cudaSuccess) {
+    h->err = std::string("cudaGraphExecKernelNodeSetParams: ") + cudaGetErrorString(e);
+    return STR_E_CUDA;
+  }
+  return STR_OK;
+}
+
+int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y) {
   cudaStream_t st = h->st;
   const int Np = npad_of(W);
   const int64_t L = h->L, Rr = h->Rr;
-  int launches = 0;
-  // 1. table -> pre-tiled hi/lo fp32 blocks
-  const int64_t Lk = pass == 1 ? Rr : L, tk = pass == 1 ? 1 : tn;
-  const int64_t KT = tk * cdiv(Lk, 32);
-  {
-    int64_t total = KT * 2 * Np * 32;
-    k_split_table<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(tab, Lk, tk, W, Np, (float *)h->tab_split.p);
-    launches++;
-  }
-  // 2. tensor map over X: dims (l, r, t), 128B swizzle, box {32, 32|128, 1}
+  // tensor map over X: dims (l, r, t), 128B swizzle, box {32, 32|128, 1}
   CUtensorMap tmap;
-  {
-    cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)Rr, (cuuint64_t)tn};
-    cuuint64_t strides[2] = {(cuuint64_t)L * 4, (cuuint64_t)L * Rr * 4};
-    cuuint32_t box[3] = {32, (cuuint32_t)(pass == 1 ? 32 : 128), 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    CUresult r = g_encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(X), dims, strides, box, es,
-                          CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                          CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    if (r != CUDA_SUCCESS) {
-      h->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
-      return -1;
-    }
-  }
+  if (!encode_x_map(h, &tmap, X, pass, tn)) return -1;
   // 3. the persistent stream-K contraction
   TcParams p;
   p.L = L;
@@ -428,9 +410,10 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, const double *ta
   p.upc = cdiv(p.U, grid);
   grid = (int)cdiv(p.U, p.upc);
   p.Btiles = (const float *)h->tab_split.p;
-  p.Y = (float *)h->tf_part.p;
+  p.Y = Y;
   const int64_t M = pass == 1 ? L * tn : Rr;
   cudaMemsetAsync(p.Y, 0, (size_t)M * W * sizeof(float), st);
+  tl_mark(h, "memset", 0);
   const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 256;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->profiling) {
@@ -442,13 +425,25 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, const double *ta
     k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, p);
   else
     k_contract_tf32<2><<<grid, kTcThreads, smem, st>>>(tmap, p);
-  launches++;
+  if (h->capturing) {
+    // remember the node so that graph replays can re-point it at new X (tf32_graph_update)
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    if (cudaStreamGetCaptureInfo(st, &cs, nullptr, nullptr, &deps, &nd) != cudaSuccess || nd != 1) {
+      h->err = "cannot locate the captured contraction node";
+      return -1;
+    }
+    h->tf_node[pass - 1] = deps[0];
+    static_assert(sizeof(TcParams) <= sizeof(h->tf_params[0]), "TcParams too large");
+    memcpy(h->tf_params[pass - 1], &p, sizeof(TcParams));
+    h->tf_grid[pass - 1] = grid;
+    h->tf_smem[pass - 1] = smem;
+  }
+  tl_mark(h, pass == 1 ? "contract_tf32_p1" : "contract_tf32_p2");
   if (h->profiling) {
     cudaEventRecord(e1, st);
     h->prof_events.push_back({pass, e0, e1});
   }
-  // 4. fp32 rows -> fp64 Y for the fp64 second-level contractions
-  k_f32_to_f64<<<(unsigned)cdiv(M * W, 256), 256, 0, st>>>(p.Y, out, M * W);
-  launches++;
-  return launches;
+  return 0;
 }

@@ -18,9 +18,22 @@ void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, doubl
 void launch_axpy(const double *x, double *y, int64_t n, cudaStream_t s);
 void launch_set_identity(double *A, int n, cudaStream_t s);
 
+// kernels_chain.cu
+void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s);
+void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s);
+void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s);
+void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
+void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);
+int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaStream_t s);
+void launch_axpy_any(const void *x, bool x_f32, double *y, int64_t n, int accumulate, cudaStream_t s);
+
 // kernels_contract_f64.cu
-int launch_contract_f64(const void *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
+int launch_contract_f64(const void *const *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
                         int64_t tn, double *out, double *ws, cudaStream_t s);
+void launch_set_ptr(const void **slot, const void *p, cudaStream_t s);
+void *set_ptr_kernel();
+void prepare_kernel_attrs();
+void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn, int SN, cudaStream_t s);
 size_t contract_f64_ws_doubles(int64_t M, int64_t K, int W);
 size_t fit_partials(int64_t L, int64_t Rr, int64_t tn);
 int launch_fit(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,

@@ -1,0 +1,610 @@
+// kernels_chain.cu — the fp64 kernels on the serial part of an STR batch (everything R^2-sized):
+//   k_spd_inv      Q^{-1} of the SPD normal-equation matrix by an in-place symmetric sweep
+//                  (Gauss-Jordan without pivoting; pivots are Schur-complement diagonals, > 0 for
+//                  SPD Q), one CTA, register-resident 4x4 tiles of the lower triangle;
+//   (rows_mm)      G = P Q^{-1} row blocks (the "G_n(2) = P_n Q_n^†" of Alg. 4 l.9/l.17);
+//   k_chain_gemm   Gram-chain links (×_{2,4}^{1,3} as a matrix product, Def. 5 / Prop. 1)
+//                  with the Q_n (+)= H_<2> epilogue (Alg. 4 l.16);
+//   k_gram_z2      core Grams Z_n (Alg. 4 l.2/l.18);
+//   k_absorb2      second-level contractions of the two-pass intermediates with core slices;
+//   k_build_table2 chained-slice tables (⊠₂ chains, Def. 6), fp64 rows and/or the
+//                  pre-tiled 3xTF32 hi/lo operand blocks of the tensor-core contraction.
+#include "common.cuh"
+#include "kernels.h"
+
+namespace strb200 {
+
+void prepare_kernel_attrs();
+
+__device__ __forceinline__ void cp_async8(void *smem, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
+}
+
+// ------------------------------------------------------------------------------------------
+// Q^{-1} of an SPD matrix (S <= 128) by the blocked symmetric sweep (Gauss-Jordan without
+// pivoting on 8x8 pivot blocks; the pivot blocks are Schur complements of an SPD matrix, hence
+// SPD).  Step kb with pivot block P (tile kb), V = A[:, P], D = A_PP^{-1}, W = V D:
+//   A_RR -= W_R V_R^T,   A_RP = W_R,   A_PR = W_R^T,   A_PP = -D          (R = the other indices)
+// after the last step A = -Q^{-1}.  The lower-triangle 8x8 tiles live in registers as FP64
+// tensor-core accumulator fragments (mma.sync m8n8k4 f64: lane holds C[lane/4][2(lane%4)+{0,1}]),
+// so the rank-8 update of a tile is two DMMAs with W and V fragments read from shared memory.
+// Warp w < nt owns diagonal tile (w, w) only; the off-diagonal tiles are spread over the other
+// warps.  Look-ahead: in step kb the owner of tile (kb+1, kb+1) updates it first and inverts it at
+// once (8-pivot scalar sweep in registers, shuffles) while the other warps update their tiles;
+// the next pivot column block V' is published by its owners, then all threads form W' = V' D'.
+// Q is staged in shared memory (coalesced) and symmetrized on load ((Q + Q^T)/2, DESIGN.md
+// reading R5); the result goes out through shared memory as well.  A non-positive or NaN pivot
+// sets *info = 1.
+constexpr int kInvThreads = 1024;              // 32 warps
+#ifdef INV_PROBE
+__device__ long long g_inv_probe[8];
+#endif
+
+__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ double rcp_nr(double d) {
+  // reciprocal: hardware approximation + two Newton steps (full double precision for normal d)
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
+  r = fma(r, fma(-d, r, 1.0), r);
+  r = fma(r, fma(-d, r, 1.0), r);
+  return r;
+}
+
+// In-register inverse of the SPD 8x8 block held by one warp in accumulator layout
+// (lane (g, t) holds M[g][2t], M[g][2t+1]): 8-pivot scalar sweep; returns -M^{-1} in d.
+__device__ __forceinline__ bool warp_sweep8(double (&d)[2], int g, int tg) {
+  bool bad = false;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const int src = m >> 1;
+    const double piv = __shfl_sync(0xffffffffu, d[m & 1], m * 4 + src);
+    const double vg = __shfl_sync(0xffffffffu, d[m & 1], g * 4 + src);
+    const double v0 = __shfl_sync(0xffffffffu, d[m & 1], (2 * tg) * 4 + src);
+    const double v1 = __shfl_sync(0xffffffffu, d[m & 1], (2 * tg + 1) * 4 + src);
+    bad = bad || !(piv > 0.0);
+    const double p = rcp_nr(piv);
+    const double sg = vg * p;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int j = 2 * tg + e;
+      const double vj = e ? v1 : v0;
+      double nv = fma(-sg, vj, d[e]);
+      if (j == m) nv = sg;
+      if (g == m) nv = vj * p;
+      if (g == m && j == m) nv = -p;
+      d[e] = nv;
+    }
+  }
+  return bad;
+}
+
+// SLOTS = off-diagonal tiles per warp: ceil(nt(nt-1)/2 / (32 - nt)) = 5 for nt <= 13, 8 for nt <= 16
+template <int kInvMaxSlots>
+__global__ void __launch_bounds__(kInvThreads, 1) k_spd_inv(const double *__restrict__ Q, int S,
+                                                              double *__restrict__ Qinv, int *info) {
+  extern __shared__ __align__(16) double ism[];
+  double *Qs = ism;                                   // S x S staging (in and out)
+  double *Vs0 = Qs + ((S * S + 1) & ~1);              // [2][128*8] pivot column blocks V[i][m]
+  double *Ws = Vs0 + 2 * STR_MAXW * 8;                // [128*8] W = V D
+  double *Ds0 = Ws + STR_MAXW * 8;                    // [2][64] D = A_PP^{-1}
+  __shared__ int s_bad;
+  const int nt = (S + 7) >> 3, Sp = nt * 8;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int noff = nt * (nt - 1) / 2, nwoff = 32 - nt;
+  if (threadIdx.x == 0) s_bad = 0;
+#ifdef INV_PROBE
+  long long tp0 = clock64();
+#endif
+  for (int e = threadIdx.x; e < S * S; e += kInvThreads) cp_async8(Qs + e, Q + e);
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- owned tiles: diagonal warps hold (w, w); the others hold off-diagonal slots
+  const bool diag = warp < nt;
+  double c[kInvMaxSlots][2];
+  int TI[kInvMaxSlots], TJ[kInvMaxSlots];
+#pragma unroll
+  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+    int I = -1, J = 0;
+    if (diag) {
+      if (sl == 0) I = J = warp;
+    } else {
+      const int tt = (warp - nt) + nwoff * sl;      // off-diagonal tiles, row-major (I > J)
+      if (tt < noff) {
+        I = 1;
+        while (I * (I + 1) / 2 <= tt) ++I;
+        J = tt - I * (I - 1) / 2;
+      }
+    }
+    TI[sl] = I;
+    TJ[sl] = J;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
+      c[sl][e] = (I >= 0 && i < S && j < S) ? 0.5 * (Qs[i * S + j] + Qs[j * S + i]) : (i == j ? 1.0 : 0.0);
+    }
+  }
+  // ---- prologue: V_0 = A[:, 0], D_0 by warp 0, W_0 = V_0 D_0
+#pragma unroll
+  for (int sl = 0; sl < kInvMaxSlots; ++sl)
+    if (TI[sl] >= 0 && TJ[sl] == 0) {
+      Vs0[(8 * TI[sl] + g) * 8 + 2 * tg] = c[sl][0];
+      Vs0[(8 * TI[sl] + g) * 8 + 2 * tg + 1] = c[sl][1];
+    }
+  if (warp == 0) {
+    double d[2] = {c[0][0], c[0][1]};
+    if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
+    Ds0[g * 8 + 2 * tg] = -d[0];
+    Ds0[g * 8 + 2 * tg + 1] = -d[1];
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < Sp * 8; e += kInvThreads) {
+    const int i = e >> 3, m = e & 7;
+    double acc = 0.0;
+#pragma unroll
+    for (int l = 0; l < 8; ++l) acc = fma(Vs0[i * 8 + l], Ds0[l * 8 + m], acc);
+    Ws[e] = acc;
+  }
+  __syncthreads();
+#ifdef INV_PROBE
+  long long tp1 = clock64();
+#endif
+  for (int kb = 0; kb < nt; ++kb) {
+    const int cur = kb & 1, nxt = cur ^ 1;
+    const double *V = Vs0 + cur * STR_MAXW * 8;
+    double *Vn = Vs0 + nxt * STR_MAXW * 8;
+    const double *D = Ds0 + cur * 64;
+    double *Dn = Ds0 + nxt * 64;
+    const int kn = kb + 1;
+#pragma unroll
+    for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+      const int I = TI[sl], J = TJ[sl];
+      if (I < 0) continue;
+      if (I != kb && J != kb) {
+        const double a0 = Ws[(8 * I + g) * 8 + tg], b0 = V[(8 * J + g) * 8 + tg];
+        const double a1 = Ws[(8 * I + g) * 8 + 4 + tg], b1 = V[(8 * J + g) * 8 + 4 + tg];
+        dmma884(c[sl][0], c[sl][1], -a0, b0);
+        dmma884(c[sl][0], c[sl][1], -a1, b1);
+      } else if (I != kb) {          // J == kb: A_RP = W_R
+        c[sl][0] = Ws[(8 * I + g) * 8 + 2 * tg];
+        c[sl][1] = Ws[(8 * I + g) * 8 + 2 * tg + 1];
+      } else if (J != kb) {          // I == kb: A_PR = W_R^T
+        c[sl][0] = Ws[(8 * J + 2 * tg) * 8 + g];
+        c[sl][1] = Ws[(8 * J + 2 * tg + 1) * 8 + g];
+      } else {                        // pivot block: -D
+        c[sl][0] = -D[g * 8 + 2 * tg];
+        c[sl][1] = -D[g * 8 + 2 * tg + 1];
+      }
+      if (kn < nt) {
+        if (J == kn) {
+          Vn[(8 * I + g) * 8 + 2 * tg] = c[sl][0];
+          Vn[(8 * I + g) * 8 + 2 * tg + 1] = c[sl][1];
+          if (I == kn) {              // look-ahead: invert the next pivot block right away
+            double d[2] = {c[sl][0], c[sl][1]};
+            if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
+            Dn[g * 8 + 2 * tg] = -d[0];
+            Dn[g * 8 + 2 * tg + 1] = -d[1];
+          }
+        } else if (I == kn) {        // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
+          Vn[(8 * J + 2 * tg) * 8 + g] = c[sl][0];
+          Vn[(8 * J + 2 * tg + 1) * 8 + g] = c[sl][1];
+        }
+      }
+    }
+    __syncthreads();
+    if (kn < nt) {
+      for (int e = threadIdx.x; e < Sp * 8; e += kInvThreads) {
+        const int i = e >> 3, m = e & 7;
+        double acc = 0.0;
+#pragma unroll
+        for (int l = 0; l < 8; ++l) acc = fma(Vn[i * 8 + l], Dn[l * 8 + m], acc);
+        Ws[e] = acc;
+      }
+      __syncthreads();
+    }
+  }
+#ifdef INV_PROBE
+  long long tp2 = clock64();
+#endif
+  if (threadIdx.x == 0 && s_bad && info) atomicExch(info, 1);
+  // ---- -A -> Qinv through shared memory (both triangles), coalesced store
+#pragma unroll
+  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+    const int I = TI[sl], J = TJ[sl];
+    if (I < 0) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
+      if (i < S && j < S && (I != J || j <= i)) {
+        const double xv = -c[sl][e];
+        Qs[i * S + j] = xv;
+        Qs[j * S + i] = xv;
+      }
+    }
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < S * S; e += kInvThreads) Qinv[e] = Qs[e];
+#ifdef INV_PROBE
+  __syncthreads();
+  if (threadIdx.x == 0) { g_inv_probe[0] = tp1 - tp0; g_inv_probe[1] = tp2 - tp1; g_inv_probe[2] = clock64() - tp2; }
+#endif
+}
+
+size_t spd_inv_smem(int S) {
+  return sizeof(double) * ((size_t)((S * S + 1) & ~1) + 3 * STR_MAXW * 8 + 2 * 64);
+}
+
+void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {
+  prepare_kernel_attrs();
+  if (S <= 104)
+    k_spd_inv<5><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
+  else
+    k_spd_inv<8><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
+}
+
+// ------------------------------------------------------------------------------------------
+// C = A (M x K) B (K x N), row-major fp64, K <= 256: one 32x32 output tile per CTA with the whole
+// A row block and B column block staged in shared memory by cp.async (every load in flight at
+// once; these small products are latency-bound).  Thread (tx, ty) owns rows 4ty..4ty+3 of
+// column tx; A is stored k-major so a thread's 4 rows are two 16-byte broadcast loads.
+// Epilogue (q.mode): 0 store C; 1 Q = H_<2>; 2 Q += H_<2>, where C is the chain matrix Hm
+// (rows (i1 + Rn r1), columns (i2 + Rn1 r2)) and H_<2>[i1 + Rn i2][r1 + Rn r2] = Hm[..][..]
+// (Def. 1 P:126 applied to the chain result).  Q is left unsymmetrized; k_spd_inv symmetrizes.
+// Used for the Gram-chain links and for G = P Q^{-1} (M = I rows).
+
+__global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A, const double *__restrict__ B,
+                                                    double *__restrict__ C, int M, int N, int K, QEpi q) {
+  extern __shared__ __align__(16) double gsm[];
+  double *AsT = gsm;            // [K][32]  (k-major A block)
+  double *Bs = gsm + K * 32;    // [K][32]
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
+  for (int e = threadIdx.x; e < 32 * K; e += 256) {
+    const int r = e / K, k = e % K;          // A row-major: consecutive threads read consecutive k
+    if (row0 + r < M) cp_async8(AsT + k * 32 + r, A + (int64_t)(row0 + r) * K + k);
+    else AsT[k * 32 + r] = 0.0;
+  }
+  for (int e = threadIdx.x; e < 32 * K; e += 256) {
+    const int k = e >> 5, c = e & 31;
+    if (col0 + c < N) cp_async8(Bs + k * 32 + c, B + (int64_t)k * N + col0 + c);
+    else Bs[k * 32 + c] = 0.0;
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+#pragma unroll 4
+  for (int k = 0; k < K; ++k) {
+    const double b = Bs[k * 32 + tx];
+    const double2 a01 = *(const double2 *)(AsT + k * 32 + 4 * ty);
+    const double2 a23 = *(const double2 *)(AsT + k * 32 + 4 * ty + 2);
+    acc[0] = fma(a01.x, b, acc[0]);
+    acc[1] = fma(a01.y, b, acc[1]);
+    acc[2] = fma(a23.x, b, acc[2]);
+    acc[3] = fma(a23.y, b, acc[3]);
+  }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int row = row0 + 4 * ty + u, col = col0 + tx;
+    if (row < M && col < N) {
+      if (q.mode == 0) {
+        C[(int64_t)row * N + col] = acc[u];
+      } else {
+        const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
+        const int S = q.Rn * q.Rn1;
+        double *dst = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
+        *dst = (q.mode == 1) ? acc[u] : *dst + acc[u];
+      }
+    }
+  }
+}
+
+void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
+  prepare_kernel_attrs();
+  dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32));
+  k_chain_gemm<<<grid, 256, (size_t)2 * K * 32 * sizeof(double), s>>>(A, B, C, M, N, K, q);
+}
+
+void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s) {
+  if (I <= 0) return;
+  launch_chain_gemm(P, B, out, (int)I, S, S, QEpi{nullptr, 0, 0, 0}, s);
+}
+
+// ------------------------------------------------------------------------------------------
+// Gram tensor as a chain matrix: Zm[(a + Rb c)][(b + Ra d)] = sum_i G(i)(b,a) G(i)(d,c) (Z of
+// P:228, rows = (1st,3rd) index pair, columns = (2nd,4th)); G(i) = Ra x Rb slices in G(2) layout.
+// Thread per output entry; rows of G staged in shared memory in chunks.
+constexpr int kGramSmem = 6144;   // doubles
+
+__global__ void __launch_bounds__(256) k_gram_z2(const double *__restrict__ G, int64_t I, int Ra, int Rb,
+                                                 double *__restrict__ Zm, int accumulate) {
+  __shared__ double Gs[kGramSmem];
+  const int AB = Ra * Rb;
+  const int ch = kGramSmem / AB;
+  const int rows = Rb * Rb, cols = Ra * Ra;
+  const int gid = blockIdx.x * 256 + threadIdx.x;
+  const bool act = gid < rows * cols;
+  const int row = act ? gid / cols : 0, col = act ? gid % cols : 0;
+  const int a = row % Rb, c = row / Rb, b = col % Ra, d = col / Ra;
+  const int o1 = b + Ra * a, o2 = d + Ra * c;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t i0 = 0; i0 < I; i0 += ch) {
+    const int ic = (int)((I - i0) < ch ? (I - i0) : ch);
+    __syncthreads();
+    for (int e = threadIdx.x; e < ic * AB; e += 256) Gs[e] = G[i0 * AB + e];
+    __syncthreads();
+    int i = 0;
+    for (; i + 2 <= ic; i += 2) {
+      acc0 = fma(Gs[i * AB + o1], Gs[i * AB + o2], acc0);
+      acc1 = fma(Gs[(i + 1) * AB + o1], Gs[(i + 1) * AB + o2], acc1);
+    }
+    if (i < ic) acc0 = fma(Gs[i * AB + o1], Gs[i * AB + o2], acc0);
+  }
+  if (act) {
+    const double v = acc0 + acc1;
+    if (accumulate) Zm[gid] += v; else Zm[gid] = v;
+  }
+}
+
+void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s) {
+  const int n = Ra * Ra * Rb * Rb;
+  k_gram_z2<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(G, I, Ra, Rb, Zm, accumulate);
+}
+
+// ------------------------------------------------------------------------------------------
+// Absorb (AbsorbDesc): one CTA per `rest` multi-index, thread per output entry (po, qo); chunks
+// of the contracted index i of both A slices and Y(rest, i) are staged in shared memory.
+//   left : out[rest][po][qo] = sum_i sum_p A(i)[po][p] Y(rest, i)[p][qo]
+//   right: out[rest][po][qo] = sum_i sum_q Y(rest, i)[po][q] A(i)[q][qo]
+constexpr int kAbsorbSmem = 6144;   // doubles
+
+template <typename TY>
+__global__ void __launch_bounds__(256) k_absorb2(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
+                                                 int accumulate, int64_t before, int64_t I, int ic_max) {
+  __shared__ double sm[kAbsorbSmem];
+  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
+  double *As = sm, *Ys = sm + ic_max * AB;
+  const int Po = ad.left ? ad.Ra : ad.P;
+  const int Qo = ad.left ? ad.Q : ad.Rb;
+  const int O = Po * Qo;
+  const int64_t rest = blockIdx.x;
+  const int64_t b0 = rest % before, a0 = rest / before;
+  const TY *ybase = Y + (b0 + before * I * a0) * PQ;
+  const int64_t ystride = before * PQ;
+  const int o = threadIdx.x;
+  const bool act = o < O;
+  const int po = act ? o / Qo : 0, qo = act ? o % Qo : 0;
+  double acc0 = 0.0, acc1 = 0.0;
+  for (int64_t i0 = 0; i0 < I; i0 += ic_max) {
+    const int ic = (int)((I - i0) < ic_max ? (I - i0) : ic_max);
+    __syncthreads();
+    for (int e = threadIdx.x; e < ic * AB; e += blockDim.x) As[e] = ad.A[i0 * AB + e];
+    for (int e = threadIdx.x; e < ic * PQ; e += blockDim.x) {
+      const int i = e / PQ, w = e % PQ;
+      Ys[e] = (double)ybase[(i0 + i) * ystride + w];
+    }
+    __syncthreads();
+    if (act) {
+      if (ad.left) {
+        for (int i = 0; i < ic; ++i) {
+          const double *a = As + i * AB + po;
+          const double *y = Ys + i * PQ + qo;
+          double s = 0.0;
+#pragma unroll
+          for (int p = 0; p < STR_MAXR; ++p)
+            if (p < ad.P) s = fma(a[ad.Ra * p], y[p * ad.Q], s);
+          if (i & 1) acc1 += s; else acc0 += s;
+        }
+      } else {
+        for (int i = 0; i < ic; ++i) {
+          const double *a = As + i * AB + ad.Ra * qo;
+          const double *y = Ys + i * PQ + po * ad.Q;
+          double s = 0.0;
+#pragma unroll
+          for (int q = 0; q < STR_MAXR; ++q)
+            if (q < ad.Q) s = fma(y[q], a[q], s);
+          if (i & 1) acc1 += s; else acc0 += s;
+        }
+      }
+    }
+  }
+  if (act) {
+    double *dst = out + rest * O + o;
+    const double v = acc0 + acc1;
+    if (accumulate) *dst += v; else *dst = v;
+  }
+}
+
+void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s) {
+  int64_t rest = 1, before = 1;
+  for (int j = 0; j < ad.nd; ++j)
+    if (j != ad.pos) rest *= ad.d[j];
+  for (int j = 0; j < ad.pos; ++j) before *= ad.d[j];
+  const int64_t I = ad.d[ad.pos];
+  const int Po = ad.left ? ad.Ra : ad.P;
+  const int Qo = ad.left ? ad.Q : ad.Rb;
+  const int threads = (int)cdiv(Po * Qo, 32) * 32;
+  int ic = kAbsorbSmem / (ad.Ra * ad.Rb + ad.P * ad.Q);
+  if (ic > I) ic = (int)I;
+  if (ic < 1) ic = 1;
+  if (y_f32)
+    k_absorb2<float><<<(unsigned)rest, threads, 0, s>>>(ad, (const float *)Y, out, accumulate, before, I, ic);
+  else
+    k_absorb2<double><<<(unsigned)rest, threads, 0, s>>>(ad, (const double *)Y, out, accumulate, before, I, ic);
+}
+
+// ------------------------------------------------------------------------------------------
+// Chained slice table over work units (t', lb): entries e = l + Lk t' for l in [32 lb, 32 lb + 32)
+// ∩ [0, Lk).  Entry e is F_0(i_0) F_1(i_1) ... (i_f = (e / stride_f) % I_f), R0 x Rl.  The slices
+// a unit touches (a contiguous index range per factor) are staged in shared memory; thread
+// (entry, row p) carries row p through the chain in registers.  Outputs: fp64 rows
+// out64[e][p][q] (optional) and/or the pre-tiled 3xTF32 operand block kt = t' nlb + lb: rows
+// n < Np hold hi(w = p Rl + q), rows Np + n hold lo, 32 k-columns, 16-byte chunk c of row n at
+// chunk c ^ (n % 8) (128B swizzle) — assembled in shared memory, stored contiguously.
+__device__ __forceinline__ float tf32_rna(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
+
+__global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
+  extern __shared__ __align__(16) double tsm[];
+  const int nlb = (int)cdiv(td.Lk, 32);
+  const int64_t unit = blockIdx.x;
+  const int64_t tp = unit / nlb;
+  const int lb = (int)(unit % nlb);
+  const int64_t l0 = (int64_t)lb * 32;
+  const int64_t l1 = (l0 + 32 < td.Lk) ? l0 + 32 : td.Lk;
+  const int64_t e_lo = l0 + td.Lk * tp, e_hi = l1 - 1 + td.Lk * tp;
+  const FactorList &fl = td.fl;
+  // stage slices
+  double *base[kMaxFactors];
+  int64_t first[kMaxFactors];
+  int cnt[kMaxFactors];
+  {
+    double *p = tsm;
+    for (int f = 0; f < fl.n; ++f) {
+      const Factor &F = fl.f[f];
+      const int64_t q0 = e_lo / F.stride, q1 = e_hi / F.stride;
+      int c = (int)((q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I);
+      base[f] = p;
+      first[f] = q0;
+      cnt[f] = c;
+      const int AB = F.Ra * F.Rb;
+      for (int e = threadIdx.x; e < c * AB; e += blockDim.x) {
+        const int j = e / AB, w = e % AB;
+        p[e] = F.G[((q0 + j) % F.I) * AB + w];
+      }
+      p += ((c * AB + 1) & ~1);
+    }
+  }
+  const int R0 = fl.f[0].Ra;
+  const int Rl = fl.f[fl.n - 1].Rb;
+  const int W = R0 * Rl;
+  float *tile = nullptr;
+  const int Np = td.Npad;
+  if (tiles) {
+    // tile staging area after the slices (float, 2 Np x 32)
+    double *p = tsm;
+    for (int f = 0; f < fl.n; ++f) p += ((cnt[f] * fl.f[f].Ra * fl.f[f].Rb + 1) & ~1);
+    tile = (float *)p;
+    for (int e = threadIdx.x; e < 2 * Np * 32; e += blockDim.x) tile[e] = 0.0f;
+  }
+  __syncthreads();
+  const int el = threadIdx.x / R0, pr = threadIdx.x % R0;
+  const int64_t l = l0 + el;
+  if (el < 32 && l < l1) {
+    const int64_t e = l + td.Lk * tp;
+    double v[STR_MAXR], w[STR_MAXR];
+    {
+      const Factor &F = fl.f[0];
+      const int64_t q = e / F.stride;
+      const double *S = base[0] + ((q - first[0]) % cnt[0]) * (F.Ra * F.Rb);
+#pragma unroll
+      for (int b = 0; b < STR_MAXR; ++b) v[b] = (b < F.Rb) ? S[pr + F.Ra * b] : 0.0;
+    }
+#pragma unroll
+    for (int f = 1; f < kMaxFactors; ++f) {
+      if (f < fl.n) {
+        const Factor &F = fl.f[f];
+        const int64_t q = e / F.stride;
+        const double *S = base[f] + ((q - first[f]) % cnt[f]) * (F.Ra * F.Rb);
+#pragma unroll
+        for (int b = 0; b < STR_MAXR; ++b) {
+          double acc = 0.0;
+          if (b < F.Rb) {
+#pragma unroll
+            for (int a = 0; a < STR_MAXR; ++a)
+              if (a < F.Ra) acc = fma(v[a], S[a + F.Ra * b], acc);
+          }
+          w[b] = acc;
+        }
+#pragma unroll
+        for (int b = 0; b < STR_MAXR; ++b) v[b] = w[b];
+      }
+    }
+    if (out64) {
+      double *o = out64 + e * (int64_t)W + (int64_t)pr * Rl;
+#pragma unroll
+      for (int q = 0; q < STR_MAXR; ++q)
+        if (q < Rl) o[q] = v[q];
+    }
+    if (tiles) {
+      const int kk = el, chunk = kk >> 2, within = kk & 3;
+#pragma unroll
+      for (int q = 0; q < STR_MAXR; ++q) {
+        if (q < Rl) {
+          const int n = pr * Rl + q;
+          const float hi = tf32_rna((float)v[q]);
+          const float lo = tf32_rna((float)(v[q] - (double)hi));
+          tile[n * 32 + ((chunk ^ (n & 7)) << 2) + within] = hi;
+          const int n2 = Np + n;
+          tile[n2 * 32 + ((chunk ^ (n2 & 7)) << 2) + within] = lo;
+        }
+      }
+    }
+  }
+  if (tiles) {
+    __syncthreads();
+    float4 *dst = (float4 *)(tiles + unit * (int64_t)(2 * Np * 32));
+    const float4 *src = (const float4 *)tile;
+    for (int e = threadIdx.x; e < 2 * Np * 8; e += blockDim.x) dst[e] = src[e];
+  }
+}
+
+size_t table2_smem(const TableDesc &td) {
+  size_t n = 0;
+  for (int f = 0; f < td.fl.n; ++f) {
+    const Factor &F = td.fl.f[f];
+    int64_t c = 31 / F.stride + 2;
+    if (c > F.I) c = F.I;
+    n += (size_t)((c * F.Ra * F.Rb + 1) & ~1);
+  }
+  size_t bytes = n * sizeof(double);
+  if (td.Npad > 0) bytes += (size_t)2 * td.Npad * 32 * sizeof(float);
+  return bytes;
+}
+
+int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaStream_t s) {
+  const size_t smem = table2_smem(td);
+  if (smem > 200 * 1024) return -1;
+  prepare_kernel_attrs();
+  const int64_t units = td.tk * cdiv(td.Lk, 32);
+  const int threads = (int)cdiv(32 * td.fl.f[0].Ra, 32) * 32;
+  k_build_table2<<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
+  return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// dst (+)= x for fp32 or fp64 x (accumulate = 0 copies).
+template <typename T>
+__global__ void k_axpy_any(const T *__restrict__ x, double *__restrict__ y, int64_t n, int accumulate) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) y[i] = accumulate ? y[i] + (double)x[i] : (double)x[i];
+}
+
+void launch_axpy_any(const void *x, bool x_f32, double *y, int64_t n, int accumulate, cudaStream_t s) {
+  if (x_f32)
+    k_axpy_any<float><<<(unsigned)cdiv(n, 256), 256, 0, s>>>((const float *)x, y, n, accumulate);
+  else
+    k_axpy_any<double><<<(unsigned)cdiv(n, 256), 256, 0, s>>>((const double *)x, y, n, accumulate);
+}
+
+// Dynamic shared-memory opt-ins, done once outside any stream capture.
+void prepare_kernel_attrs() {
+  static bool done = false;
+  if (done) return;
+  cudaFuncSetAttribute(k_spd_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
+  cudaFuncSetAttribute(k_spd_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
+  cudaFuncSetAttribute(k_chain_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
+  cudaFuncSetAttribute(k_build_table2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  done = true;
+}
+
+}  // namespace strb200

@@ -16,9 +16,11 @@ namespace strb200 {
 constexpr int BM = 64, BK = 16;
 
 template <typename T, int PASS, int WT>
-__global__ void __launch_bounds__(256) k_contract_f64(const T *__restrict__ X, const double *__restrict__ Btab, int W,
+__global__ void __launch_bounds__(256) k_contract_f64(const void *const *Xp, const double *__restrict__ Btab, int W,
                                                       int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
                                                       int64_t kchunk, double *__restrict__ part) {
+  // X is read through a device-side pointer slot so that a captured CUDA graph replays on new data
+  const T *__restrict__ X = (const T *)*Xp;
   __shared__ double As[BK][BM + 1];
   __shared__ double Bs[BK][WT];
   const int tid = threadIdx.x;
@@ -92,7 +94,7 @@ __global__ void k_reduce_splits(const double *__restrict__ part, int splits, int
 }
 
 template <typename T, int PASS>
-static void dispatch_w(const T *X, const double *B, int W, int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
+static void dispatch_w(const void *const *X, const double *B, int W, int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
                        int64_t kchunk, int splits, double *part, cudaStream_t s) {
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)splits);
   if (W <= 32)
@@ -114,7 +116,7 @@ int contract_f64_splits(int64_t M, int64_t K) {
 }
 
 // Returns the number of kernel launches.
-int launch_contract_f64(const void *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
+int launch_contract_f64(const void *const *X, bool x_is_f64, int pass, const double *Btab, int W, int64_t L, int64_t Rr,
                         int64_t tn, double *out, double *ws, cudaStream_t s) {
   int64_t M = pass == 1 ? L * tn : Rr;
   int64_t K = pass == 1 ? Rr : L * tn;
@@ -123,11 +125,11 @@ int launch_contract_f64(const void *X, bool x_is_f64, int pass, const double *Bt
   splits = (int)cdiv(K, kchunk);
   double *part = splits == 1 ? out : ws;
   if (x_is_f64) {
-    if (pass == 1) dispatch_w<double, 1>((const double *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
-    else dispatch_w<double, 2>((const double *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    if (pass == 1) dispatch_w<double, 1>(X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    else dispatch_w<double, 2>(X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
   } else {
-    if (pass == 1) dispatch_w<float, 1>((const float *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
-    else dispatch_w<float, 2>((const float *)X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    if (pass == 1) dispatch_w<float, 1>(X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
+    else dispatch_w<float, 2>(X, Btab, W, L, Rr, tn, M, K, kchunk, splits, part, s);
   }
   if (splits == 1) return 1;
   int64_t n = M * W;
@@ -208,6 +210,26 @@ int launch_fit(const void *X, bool x_is_f64, const double *TLf, const double *TR
     k_fit_partial<float><<<grid, 256, smem, s>>>((const float *)X, TLf, TR, Ra, Rb, L, Rr, tn, partials);
   k_fit_reduce<<<1, 256, 0, s>>>(partials, (int64_t)grid.x * grid.y * grid.z, acc2);
   return 2;
+}
+
+__global__ void k_set_ptr(const void **slot, const void *p) { *slot = p; }
+
+void launch_set_ptr(const void **slot, const void *p, cudaStream_t s) { k_set_ptr<<<1, 1, 0, s>>>(slot, p); }
+void *set_ptr_kernel() { return (void *)k_set_ptr; }
+
+// Appends the t_new fresh temporal rows (scratch GNnew) to the temporal core at the device-side
+// row counter *dT (graph-invariant: no host T in the arguments), then advances *dT.
+__global__ void k_append_rows(double *__restrict__ GN, int64_t *dT, const double *__restrict__ GNnew, int64_t n,
+                              int64_t tn, int SN) {
+  const int64_t T = *dT;
+  double *dst = GN + T * SN;
+  for (int64_t i = threadIdx.x; i < n; i += blockDim.x) dst[i] = GNnew[i];
+  __syncthreads();
+  if (threadIdx.x == 0) *dT = T + tn;
+}
+
+void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn, int SN, cudaStream_t s) {
+  k_append_rows<<<1, 512, 0, s>>>(GN, dT, GNnew, tn * SN, tn, SN);
 }
 
 }  // namespace strb200

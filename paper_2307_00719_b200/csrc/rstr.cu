@@ -186,7 +186,7 @@ static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const 
                  double *C, int M, int N, int64_t K, int acc) {
   dim3 blk(16, 16), grd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
   k_gemm_strided<<<grd, blk, 0, h->st>>>(A, sai, sak, B, sbk, sbj, C, M, N, K, acc);
-  h->launches++;
+  tl_mark(h, "k_gemm_strided");
 }
 
 // Core k's slices as G(2) rows: k < N -> current core; k == N -> temporal rows [t0, t0 + rows).
@@ -206,9 +206,9 @@ static str_status leverage_probs(str_state *h, const double *G, int64_t I, int S
   double *pd = Y + I * S;
   gemm(h, G, 1, S, G, S, 1, K, S, S, I, 0);                         // K = G^T G
   launch_chol_solve(K, S, G, I, Y, h->d_info, h->st);                // Y = G K^{-1}
-  h->launches++;
+  tl_mark(h, "chol_solve");
   k_rowdot_scale<<<(unsigned)cdiv(I, 128), 128, 0, h->st>>>(Y, G, I, S, 1.0 / (double)S, pd);
-  h->launches++;
+  tl_mark(h, "k_rowdot_scale");
   RCU(cudaMemcpyAsync(p.data(), pd, sizeof(double) * I, cudaMemcpyDeviceToHost, h->st));
   RCU(cudaStreamSynchronize(h->st));
   int info = 0;
@@ -241,7 +241,7 @@ static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) 
   ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
   double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
   k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
-  h->launches++;
+  tl_mark(h, "k_gather_rows");
   return STR_OK;
 }
 
@@ -269,7 +269,7 @@ static str_status sampled_chain(str_state *h, int n, double *out) {
     fl.f[fl.n++] = f;
   }
   launch_build_table(fl, h->m, out, h->st);
-  h->launches++;
+  tl_mark(h, "build_table");
   return STR_OK;
 }
 
@@ -291,7 +291,7 @@ static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, 
     k_gather_fibers<double><<<grid, 256, 0, h->st>>>((const double *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
   else
     k_gather_fibers<float><<<grid, 256, 0, h->st>>>((const float *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
-  h->launches++;
+  tl_mark(h, "gather_fibers");
   return STR_OK;
 }
 
@@ -325,7 +325,7 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   gemm(h, XS, h->m, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, h->m, acc);
   gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, h->m, acc);
   k_symmetrize<<<(unsigned)cdiv(S * S, 256), 256, 0, h->st>>>((double *)mb.Q.p, S);
-  h->launches++;
+  tl_mark(h, "k_symmetrize");
   return STR_OK;
 }
 
@@ -361,10 +361,10 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
   gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0);
   k_symmetrize<<<(unsigned)cdiv(SN * SN, 256), 256, 0, h->st>>>(K, SN);
-  h->launches++;
+  tl_mark(h, "k_symmetrize");
   double *GN_new = (double *)h->GN.p + h->T * SN;
   launch_chol_solve(K, SN, M, tn, GN_new, h->d_info, h->st);
-  h->launches++;
+  tl_mark(h, "chol_solve");
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
   RTRY(draw_mode(h, N, GN_new, tn));
   for (int n = 1; n < N; ++n) {
@@ -372,7 +372,7 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
     RTRY(sampled_normal_eq(h, X, n, tn, 1));
     launch_chol_solve((const double *)mb.Q.p, mb.Ra * mb.Rb, (const double *)mb.P.p, mb.I, (double *)mb.G.p,
                       h->d_info, h->st);
-    h->launches++;
+    tl_mark(h, "chol_solve");
     RTRY(draw_mode(h, n, (const double *)mb.G.p, mb.I));
   }
   h->T += tn;

@@ -18,6 +18,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -108,10 +109,10 @@ static bool load_nccl(std::string &why) {
   return true;
 }
 
-// Sum-allreduce of fp64 device data across the mode-1 shards (no-op on one GPU).
-static str_status allreduce(str_state *h, double *buf, size_t n) {
+// Sum-allreduce of device data across the mode-1 shards (no-op on one GPU).
+static str_status allreduce(str_state *h, void *buf, size_t n, bool f32 = false) {
   if (h->p == 1 || n == 0) return STR_OK;
-  ncclResult_t r = g_nccl.allReduce(buf, buf, n, ncclFloat64, ncclSum, (ncclComm_t)h->comm, h->st);
+  ncclResult_t r = g_nccl.allReduce(buf, buf, n, f32 ? ncclFloat32 : ncclFloat64, ncclSum, (ncclComm_t)h->comm, h->st);
   if (r != ncclSuccess)
     return fail(h, STR_E_NCCL, std::string("ncclAllReduce: ") +
                                    (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
@@ -133,6 +134,16 @@ static Factor core_factor(const str_state *h, int n, int64_t stride) {
   return f;
 }
 
+static Factor temporal_factor_at(const str_state *h, const double *rows0, int64_t rows, int64_t stride) {
+  Factor f;
+  f.G = rows0;
+  f.I = (int32_t)rows;
+  f.Ra = RR(h, h->N);
+  f.Rb = RR(h, 1);
+  f.stride = stride;
+  return f;
+}
+
 static Factor temporal_factor(const str_state *h, int64_t row0, int64_t rows, int64_t stride) {
   Factor f;
   f.G = (const double *)h->GN.p + row0 * (int64_t)h->SN;
@@ -150,22 +161,20 @@ struct AOp {
   Factor A;      // slices (stride unused)
 };
 
-// Runs a sequence of absorbs starting from Y (multi-index over `modes`, entries P x Q).
-// The final result is written (accumulate=0) or added (accumulate=1) into dst.
-static str_status run_absorbs(str_state *h, const double *Y, std::vector<int> modes, std::vector<int64_t> dims, int P,
-                              int Q, const std::vector<AOp> &ops, double *dst, int accumulate) {
+// Runs a sequence of absorbs starting from Y (multi-index over `modes`, entries P x Q; fp32 when
+// y_f32, else fp64).  The final result is written (accumulate=0) or added (accumulate=1) into dst.
+static str_status run_absorbs(str_state *h, const void *Y, bool y_f32, std::vector<int> modes,
+                              std::vector<int64_t> dims, int P, int Q, const std::vector<AOp> &ops, double *dst,
+                              int accumulate) {
   if (ops.empty()) {
     int64_t n = (int64_t)P * Q;
     for (auto d : dims) n *= d;
-    if (accumulate) {
-      launch_axpy(Y, dst, n, h->st);
-      h->launches++;
-    } else {
-      CU(cudaMemcpyAsync(dst, Y, n * sizeof(double), cudaMemcpyDeviceToDevice, h->st));
-    }
+    launch_axpy_any(Y, y_f32, dst, n, accumulate, h->st);
+    tl_mark(h, "axpy");
     return check_launch(h, "axpy");
   }
-  const double *cur = Y;
+  const void *cur = Y;
+  bool cur_f32 = y_f32;
   for (size_t s = 0; s < ops.size(); ++s) {
     const AOp &op = ops[s];
     AbsorbDesc ad;
@@ -180,19 +189,20 @@ static str_status run_absorbs(str_state *h, const double *Y, std::vector<int> mo
     ad.Rb = op.A.Rb;
     bool last = s + 1 == ops.size();
     double *out = last ? dst : (double *)((s % 2 == 0) ? h->tmpA.p : h->tmpB.p);
-    launch_absorb(ad, cur, false, out, last ? accumulate : 0, h->st);
-    h->launches++;
+    launch_absorb2(ad, cur, cur_f32, out, last ? accumulate : 0, h->st);
+    tl_mark(h, "absorb");
     TRY(check_launch(h, "absorb"));
     if (op.left) P = op.A.Ra; else Q = op.A.Rb;
     modes.erase(modes.begin() + ad.pos);
     dims.erase(dims.begin() + ad.pos);
     cur = out;
+    cur_f32 = false;
   }
   return STR_OK;
 }
 
 // ------------------------------------------------------------------------------------ chains
-// out = A (MxK) * B (KxN), with identity flags.
+// out = A (MxK) * B (KxN) (Gram-chain matrices), with identity flags.
 static str_status chain_mul(str_state *h, const double *A, bool A_id, const double *B, bool B_id, double *out, int M,
                             int N, int K) {
   if (A_id && B_id) {
@@ -204,10 +214,10 @@ static str_status chain_mul(str_state *h, const double *A, bool A_id, const doub
     CU(cudaMemcpyAsync(out, A, sizeof(double) * M * K, cudaMemcpyDeviceToDevice, h->st));
     return STR_OK;
   } else {
-    launch_dgemm(A, B, out, M, N, K, h->st);
+    launch_chain_gemm(A, B, out, M, N, K, QEpi{nullptr, 0, 0, 0}, h->st);
   }
-  h->launches++;
-  return check_launch(h, "dgemm");
+  tl_mark(h, "chain_gemm");
+  return check_launch(h, "chain_gemm");
 }
 
 // Sf_n = Z_{N-1} ... Z_{n+1} (Sf_{N-1} = I), from the current Z's (Alg. 4 l.15 right part).
@@ -223,40 +233,107 @@ static str_status build_suffixes(str_state *h) {
   return STR_OK;
 }
 
-// H = Lp * Zmid * Sf_n, then Q (+)= H_<2>.
+// H = Lp * Zmid * Sf_n (Prop. 1 chain), then Q (+)= H_<2> (l.16) in the epilogue
+// of the last chain product.  Lp and Sf are never both identities for N >= 3.
 static str_status q_update(str_state *h, int n, const double *Lp, bool Lp_id, const double *Zmid, int accumulate,
                            double *Qout) {
   const int N = h->N;
   int a = RR(h, n) * RR(h, n), b = RR(h, 1) * RR(h, 1), c = RR(h, N) * RR(h, N), d = RR(h, n + 1) * RR(h, n + 1);
   bool Sf_id = (n == N - 1);
-  TRY(chain_mul(h, Lp, Lp_id, Zmid, false, (double *)h->T1.p, a, c, b));
-  TRY(chain_mul(h, (const double *)h->T1.p, false, (const double *)h->Sf[n].p, Sf_id, (double *)h->H.p, a, d, c));
-  launch_q_accum((const double *)h->H.p, RR(h, n), RR(h, n + 1), Qout, accumulate, h->st);
-  h->launches++;
-  return check_launch(h, "q_accum");
+  QEpi q{Qout, RR(h, n), RR(h, n + 1), accumulate ? 2 : 1};
+  if (Lp_id) {
+    launch_chain_gemm(Zmid, (const double *)h->Sf[n].p, nullptr, b, d, c, q, h->st);
+  } else if (Sf_id) {
+    launch_chain_gemm(Lp, Zmid, nullptr, a, c, b, q, h->st);
+  } else {
+    TRY(chain_mul(h, Lp, false, Zmid, false, (double *)h->T1.p, a, c, b));
+    launch_chain_gemm((const double *)h->T1.p, (const double *)h->Sf[n].p, nullptr, a, d, c, q, h->st);
+  }
+  tl_mark(h, "chain_gemm_q");
+  return check_launch(h, "chain_gemm_q");
+}
+
+// ------------------------------------------------------------------------------------ tables
+// T_R[r] = G_{k+1}(i_{k+1}) ... G_{N-1}(i_{N-1})   (R_{k+1} x R_N) over the right multi-index r.
+static TableDesc desc_TR(const str_state *h) {
+  TableDesc td;
+  td.fl.n = 0;
+  int64_t stride = 1;
+  for (int i = h->k + 1; i <= h->N - 1; ++i) {
+    td.fl.f[td.fl.n++] = core_factor(h, i, stride);
+    stride *= h->md[i - 1].I;
+  }
+  td.Lk = h->Rr;
+  td.tk = 1;
+  td.Npad = 0;
+  return td;
+}
+
+// T_L[l + L t] = G_N(t0 + t) G_1(i_1) ... G_k(i_k)   (R_N x R_{k+1}) over (l, t).
+static TableDesc desc_TL_at(const str_state *h, const double *rows0, int64_t tn) {
+  TableDesc td;
+  td.fl.n = 0;
+  td.fl.f[td.fl.n++] = temporal_factor_at(h, rows0, tn, h->L);
+  int64_t stride = 1;
+  for (int i = 1; i <= h->k; ++i) {
+    td.fl.f[td.fl.n++] = core_factor(h, i, stride);
+    stride *= h->md[i - 1].I;
+  }
+  td.Lk = h->L;
+  td.tk = tn;
+  td.Npad = 0;
+  return td;
+}
+
+static str_status build_table(str_state *h, TableDesc td, double *out64, float *tiles, const char *name) {
+  if (launch_build_table2(td, out64, tiles, h->st) != 0)
+    return fail(h, STR_E_ARG, "chained-slice table needs too much shared memory for this shape");
+  tl_mark(h, name);
+  return check_launch(h, name);
+}
+
+static TableDesc desc_TL(const str_state *h, int64_t t0, int64_t tn) {
+  return desc_TL_at(h, (const double *)h->GN.p + t0 * (int64_t)h->SN, tn);
 }
 
 // ------------------------------------------------------------------------------------ contraction
-static str_status contract(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out) {
-  int nl = 0;
+// One pass of the two-pass schedule over X: builds the pass's table operand
+// (pass 1: T_R from the current = old cores; pass 2: T_L from the new temporal rows [t0, t0+tn)
+// and the updated left cores), contracts, and returns the output Y (fp32 in 3xTF32 mode).
+// trows: the tn temporal rows that pass 2 contracts with (unused by pass 1).  The f64 path reads X
+// through the device slot h->dX, which the caller has set (set_x).
+static str_status contract(str_state *h, const void *X, int pass, const double *trows, int64_t tn, const void **Y,
+                           bool *y_f32) {
+  const int W = RR(h, h->k + 1) * RR(h, h->N);
+  TableDesc td = pass == 1 ? desc_TR(h) : desc_TL_at(h, trows, tn);
   if (h->contract == STR_CONTRACT_3XTF32) {
-    // tensor-core path; profiling events bracket the contraction kernel itself
-    nl = launch_contract_tf32(h, X, pass, tab, W, tn, out);
-    if (nl < 0) return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
+    td.Npad = tf32_npad(W);
+    TRY(build_table(h, td, nullptr, (float *)h->tab_split.p, pass == 1 ? "table_TR" : "table_TL"));
+    float *out = (float *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
+    if (launch_contract_tf32(h, X, pass, W, tn, out) != 0)
+      return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
+    *Y = out;
+    *y_f32 = true;
   } else {
+    double *tab = (double *)(pass == 1 ? h->TR.p : h->TL.p);
+    TRY(build_table(h, td, tab, nullptr, pass == 1 ? "table_TR" : "table_TL"));
+    double *out = (double *)(pass == 1 ? h->YL.p : h->YR.p);
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (h->profiling) {
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, h->st);
     }
-    nl = launch_contract_f64(X, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn, out, (double *)h->ws.p, h->st);
+    int nl = launch_contract_f64((const void *const *)h->dX.p, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn,
+                                 out, (double *)h->ws.p, h->st);
+    tl_mark(h, pass == 1 ? "contract_f64_p1" : "contract_f64_p2", nl);
     if (h->profiling) {
       cudaEventRecord(e1, h->st);
       h->prof_events.push_back({pass, e0, e1});
     }
+    *Y = out;
+    *y_f32 = false;
   }
-  h->launches += nl;
   return check_launch(h, pass == 1 ? "contract pass 1" : "contract pass 2");
 }
 
@@ -266,10 +343,6 @@ static str_status ensure_workspace(str_state *h, int64_t tn) {
   const int N = h->N, k = h->k;
   const int W1 = RR(h, k + 1) * RR(h, N);
   const int64_t Lt = h->L * tn;
-  TRY(ensure(h, h->TR, sizeof(double) * h->Rr * W1));
-  TRY(ensure(h, h->TL, sizeof(double) * Lt * W1));
-  TRY(ensure(h, h->YL, sizeof(double) * Lt * W1));
-  TRY(ensure(h, h->YR, sizeof(double) * h->Rr * W1));
   TRY(ensure(h, h->Wt, sizeof(double) * h->L * RR(h, k + 1) * RR(h, 1)));
   int64_t big = std::max<int64_t>(Lt, h->Rr) * STR_MAXR * STR_MAXR;
   TRY(ensure(h, h->tmpA, sizeof(double) * big));
@@ -277,9 +350,17 @@ static str_status ensure_workspace(str_state *h, int64_t tn) {
   int64_t mt = tn * h->SN;
   for (auto &m : h->md) mt = std::max<int64_t>(mt, m.I * m.Ra * m.Rb);
   TRY(ensure(h, h->Mt, sizeof(double) * mt));
-  size_t ws = std::max(contract_f64_ws_doubles(Lt, h->Rr, W1), contract_f64_ws_doubles(h->Rr, Lt, W1));
-  TRY(ensure(h, h->ws, sizeof(double) * ws));
-  if (h->contract == STR_CONTRACT_3XTF32) TRY(tf32_ensure_workspace(h, tn));
+  TRY(ensure(h, h->GNnew, sizeof(double) * tn * h->SN));
+  if (h->contract == STR_CONTRACT_3XTF32) {
+    TRY(tf32_ensure_workspace(h, tn));
+  } else {
+    TRY(ensure(h, h->TR, sizeof(double) * h->Rr * W1));
+    TRY(ensure(h, h->TL, sizeof(double) * Lt * W1));
+    TRY(ensure(h, h->YL, sizeof(double) * Lt * W1));
+    TRY(ensure(h, h->YR, sizeof(double) * h->Rr * W1));
+    size_t ws = std::max(contract_f64_ws_doubles(Lt, h->Rr, W1), contract_f64_ws_doubles(h->Rr, Lt, W1));
+    TRY(ensure(h, h->ws, sizeof(double) * ws));
+  }
   h->ws_t = tn;
   return STR_OK;
 }
@@ -294,7 +375,29 @@ str_status ensure_temporal_capacity(str_state *h, int64_t need) {
   cudaFree(h->GN.p);
   h->GN = nb;
   h->Tcap = cap;
+  if (h->gexec) {   // the captured append node points at the old buffer
+    cudaGraphExecDestroy(h->gexec);
+    cudaGraphDestroy(h->graph);
+    h->gexec = nullptr;
+    h->graph = nullptr;
+  }
   return STR_OK;
+}
+
+// X into the device slot h->dX (read by the f64 contraction); recorded as a graph node when
+// capturing so that replays can point it at the new batch.
+static str_status set_x(str_state *h, const void *X) {
+  launch_set_ptr((const void **)h->dX.p, X, h->st);
+  tl_mark(h, "set_x");
+  if (h->capturing) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    CU(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, nullptr, &deps, &nd));
+    if (nd != 1) return fail(h, STR_E_CUDA, "cannot locate the captured set_x node");
+    h->g_setx = deps[0];
+  }
+  return check_launch(h, "set_x");
 }
 
 // ------------------------------------------------------------------------------------ left/right modes
@@ -334,67 +437,43 @@ static void right_modes(const str_state *h, std::vector<int> &modes, std::vector
   }
 }
 
-// T_R[r] = G_{k+1}(i_{k+1}) ... G_{N-1}(i_{N-1})   (R_{k+1} x R_N, row-major)
-static str_status build_TR(str_state *h) {
-  FactorList fl;
-  fl.n = 0;
-  int64_t stride = 1;
-  for (int i = h->k + 1; i <= h->N - 1; ++i) {
-    fl.f[fl.n++] = core_factor(h, i, stride);
-    stride *= h->md[i - 1].I;
-  }
-  launch_build_table(fl, h->Rr, (double *)h->TR.p, h->st);
-  h->launches++;
-  return check_launch(h, "build_table TR");
-}
-
-// T_L[l + L t] = G_N(t0 + t) G_1(i_1) ... G_k(i_k)   (R_N x R_{k+1}, row-major)
-static str_status build_TL(str_state *h, int64_t t0, int64_t tn, double *out) {
-  FactorList fl;
-  fl.n = 0;
-  fl.f[fl.n++] = temporal_factor(h, t0, tn, h->L);
-  int64_t stride = 1;
-  for (int i = 1; i <= h->k; ++i) {
-    fl.f[fl.n++] = core_factor(h, i, stride);
-    stride *= h->md[i - 1].I;
-  }
-  launch_build_table(fl, h->L * tn, out, h->st);
-  h->launches++;
-  return check_launch(h, "build_table TL");
-}
-
-// Solve G_j = P_j Q_j^{-1} and refresh Z_j (Alg. 4 l.17-18).
+// Q_j^{-1} (sweep), G_j = P_j Q_j^{-1} (Alg. 4 l.17) and Z_j (l.18).
 static str_status solve_mode(str_state *h, int j) {
   ModeBuf &m = h->md[j - 1];
   const int S = m.Ra * m.Rb;
-  launch_chol_solve((const double *)m.Q.p, S, (const double *)m.P.p, m.I, (double *)m.G.p, h->d_info, h->st);
-  h->launches++;
-  TRY(check_launch(h, "chol_solve"));
-  launch_gram_z((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
-  h->launches++;
+  launch_spd_inv((const double *)m.Q.p, S, (double *)m.Qi.p, h->d_info, h->st);
+  tl_mark(h, "spd_inv");
+  TRY(check_launch(h, "spd_inv"));
+  launch_rows_mm((const double *)m.P.p, (const double *)m.Qi.p, S, m.I, (double *)m.G.p, h->st);
+  tl_mark(h, "rows_mm");
+  TRY(check_launch(h, "rows_mm"));
+  launch_gram_z2((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
+  tl_mark(h, "gram_z");
   TRY(check_launch(h, "gram_z"));
-  if (j == 1) TRY(allreduce(h, (double *)m.Zm.p, (size_t)m.Ra * m.Ra * m.Rb * m.Rb));   // G_1 row-sharded
+  if (j == 1) TRY(allreduce(h, m.Zm.p, (size_t)m.Ra * m.Ra * m.Rb * m.Rb));   // G_1 row-sharded
   return STR_OK;
 }
 
 // ------------------------------------------------------------------------------------ update (STR)
-static str_status update_det(str_state *h, const void *X, int64_t tn) {
+// Enqueues one STR step (everything on h->st, no host synchronization, no host-side T): the new
+// temporal rows go to the scratch GNnew and are appended at the device row counter at the end.
+static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   const int N = h->N, k = h->k;
-  const int W1 = RR(h, k + 1) * RR(h, N);
-  TRY(ensure_workspace(h, tn));
-  TRY(ensure_temporal_capacity(h, h->T + tn));
-  // 0. suffix chains and H^{≠N} (Alg. 4 l.8)
+  TRY(set_x(h, X));
+  // 0. suffix chains and H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq, Hq^{-1}
   TRY(build_suffixes(h));
   {
     int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
-    TRY(chain_mul(h, (const double *)h->Sf[1].p, false, (const double *)h->md[0].Zm.p, false,
-                  (double *)h->H.p, M, Nc, K));
-    launch_q_accum((const double *)h->H.p, RR(h, N), RR(h, 1), (double *)h->Hq.p, 0, h->st);
-    h->launches++;
+    launch_chain_gemm((const double *)h->Sf[1].p, (const double *)h->md[0].Zm.p, nullptr, M, Nc, K,
+                      QEpi{(double *)h->Hq.p, RR(h, N), RR(h, 1), 1}, h->st);
+    tl_mark(h, "chain_gemm_q");
+    launch_spd_inv((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, h->d_info, h->st);
+    tl_mark(h, "spd_inv");
   }
   // 1. pass 1 with the old cores
-  TRY(build_TR(h));
-  TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
+  const void *YL;
+  bool yl32;
+  TRY(contract(h, X, 1, nullptr, tn, &YL, &yl32));
   // 2. temporal mode: M_N = (G_1...G_k) Y_L summed over l
   std::vector<int> modes;
   std::vector<int64_t> dims;
@@ -404,18 +483,18 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
   std::vector<AOp> ops;
   for (int i = k; i >= 1; --i) ops.push_back({i, 1, core_factor(h, i, 1)});
   double *Mt = (double *)h->Mt.p;
-  TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), ops, Mt, 0));
+  TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), ops, Mt, 0));
   TRY(allreduce(h, Mt, (size_t)tn * h->SN));                                   // site C1
-  double *GN_new = (double *)h->GN.p + h->T * h->SN;
-  launch_chol_solve((const double *)h->Hq.p, h->SN, Mt, tn, GN_new, h->d_info, h->st);   // l.9 (+ l.10 append)
-  h->launches++;
-  TRY(check_launch(h, "chol_solve temporal"));
-  launch_gram_z(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);            // Z_N^new
-  h->launches++;
+  double *GN_new = (double *)h->GNnew.p;
+  launch_rows_mm(Mt, (const double *)h->Hi.p, h->SN, tn, GN_new, h->st);       // l.9
+  tl_mark(h, "rows_mm");
+  TRY(check_launch(h, "temporal solve"));
+  launch_gram_z2(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);  // Z_N^new
+  tl_mark(h, "gram_z");
   // W = Y_L absorbed over t with G_N^new on the right: modes 1..k, entries R_{k+1} x R_1
   {
-    std::vector<AOp> o1 = {{N, 0, temporal_factor(h, h->T, tn, 1)}};
-    TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
+    std::vector<AOp> o1 = {{N, 0, temporal_factor_at(h, GN_new, tn, 1)}};
+    TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
   }
   // 3. left modes
   bool Lp_id = true;
@@ -425,12 +504,12 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
     left_modes(h, modes, dims);
     auto lo = left_ops(h, j);
     if (j == 1 || h->p == 1) {
-      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, (double *)m.P.p, 1));
+      TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, (double *)m.P.p, 1));
     } else {   // M_j sums over the sharded i_1: reduce before accumulating (site C2)
-      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
+      TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
       TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
-      launch_axpy(Mt, (double *)m.P.p, m.I * m.Ra * m.Rb, h->st);
-      h->launches++;
+      launch_axpy_any(Mt, false, (double *)m.P.p, m.I * m.Ra * m.Rb, 1, h->st);
+      tl_mark(h, "axpy");
     }
     TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
     TRY(solve_mode(h, j));
@@ -442,15 +521,15 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
     Lp_id = false;
   }
   // 4. pass 2 with the new cores
-  TRY(build_TL(h, h->T, tn, (double *)h->TL.p));
-  TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
-  TRY(allreduce(h, (double *)h->YR.p, (size_t)h->Rr * W1));                  // site C2'
+  const void *YR;
+  bool yr32;
+  TRY(contract(h, X, 2, GN_new, tn, &YR, &yr32));
+  TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));   // site C2'
   // 5. right modes
   for (int j = k + 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
     right_modes(h, modes, dims);
-    TRY(run_absorbs(h, (const double *)h->YR.p, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p,
-                    1));
+    TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p, 1));
     TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
     TRY(solve_mode(h, j));
     if (j < N - 1) {
@@ -461,6 +540,68 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
       Lp_id = false;
     }
   }
+  // l.10: append the new temporal rows
+  launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, h->SN, h->st);
+  tl_mark(h, "append");
+  return check_launch(h, "append");
+}
+
+// One STR step: replays the captured graph of update_det_enqueue (capturing it on first use or
+// when t_new changes); eager when profiling / timeline diagnostics are on.
+static str_status update_det(str_state *h, const void *X, int64_t tn) {
+  TRY(ensure_workspace(h, tn));
+  TRY(ensure_temporal_capacity(h, h->T + tn));
+  const bool graph = h->use_graph && !h->profiling && !h->timeline;
+  if (!graph) {
+    TRY(update_det_enqueue(h, X, tn));
+  } else {
+    if (!h->gexec || h->g_tn != tn) {
+      if (h->gexec) {
+        cudaGraphExecDestroy(h->gexec);
+        cudaGraphDestroy(h->graph);
+        h->gexec = nullptr;
+        h->graph = nullptr;
+      }
+      CU(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+      h->capturing = true;
+      const int64_t l0 = h->launches;
+      str_status st = update_det_enqueue(h, X, tn);
+      h->capturing = false;
+      cudaGraph_t g = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->st, &g);
+      if (st != STR_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st;
+      }
+      if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
+      e = cudaGraphInstantiate(&h->gexec, g, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(g);
+        return fail(h, STR_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
+      }
+      h->graph = g;
+      h->g_tn = tn;
+      h->g_launches = h->launches - l0;
+      h->launches = l0;
+    } else {
+      // point the replay at this batch
+      void *slot = h->dX.p;
+      const void *xp = X;
+      void *args[2] = {&slot, &xp};
+      cudaKernelNodeParams kp = {};
+      kp.func = set_ptr_kernel();
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(1);
+      kp.kernelParams = args;
+      CU(cudaGraphExecKernelNodeSetParams(h->gexec, h->g_setx, &kp));
+      if (h->contract == STR_CONTRACT_3XTF32) {
+        TRY(tf32_graph_update(h, h->gexec, 1, X, tn));
+        TRY(tf32_graph_update(h, h->gexec, 2, X, tn));
+      }
+    }
+    CU(cudaGraphLaunch(h->gexec, h->st));
+    h->launches += h->g_launches;
+  }
   h->T += tn;
   return STR_OK;
 }
@@ -469,15 +610,16 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
 // Alg. 4 l.1-5: Z_1..Z_N, P_n = X_init[n] G^{≠n}_[2], Q_n = H^{≠n}_<2> with all init cores.
 static str_status init_det(str_state *h, const void *X, int64_t tn) {
   const int N = h->N, k = h->k;
-  const int W1 = RR(h, k + 1) * RR(h, N);
   TRY(ensure_workspace(h, tn));
   // Z_N over the whole init temporal core
-  launch_gram_z((const double *)h->GN.p, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);
-  h->launches++;
+  launch_gram_z2((const double *)h->GN.p, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);
+  tl_mark(h, "gram_z");
   TRY(build_suffixes(h));
   // pass 1 (init cores), W from the init temporal rows
-  TRY(build_TR(h));
-  TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
+  TRY(set_x(h, X));
+  const void *YL;
+  bool yl32;
+  TRY(contract(h, X, 1, nullptr, tn, &YL, &yl32));
   std::vector<int> modes;
   std::vector<int64_t> dims;
   left_modes(h, modes, dims);
@@ -485,26 +627,27 @@ static str_status init_det(str_state *h, const void *X, int64_t tn) {
   dims.push_back(tn);
   {
     std::vector<AOp> o1 = {{N, 0, temporal_factor(h, 0, tn, 1)}};
-    TRY(run_absorbs(h, (const double *)h->YL.p, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
+    TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
   }
   double *Mt = (double *)h->Mt.p;
   bool Lp_id = true;
   int lp_cur = 0;
+  const void *YR = nullptr;
+  bool yr32 = false;
   for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
     if (j <= k) {
       left_modes(h, modes, dims);
       auto lo = left_ops(h, j);
-      TRY(run_absorbs(h, (const double *)h->Wt.p, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
+      TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
       if (j > 1) TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
     } else {
       if (j == k + 1) {
-        TRY(build_TL(h, 0, tn, (double *)h->TL.p));
-        TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
-        TRY(allreduce(h, (double *)h->YR.p, (size_t)h->Rr * W1));
+        TRY(contract(h, X, 2, (const double *)h->GN.p, tn, &YR, &yr32));
+        TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));
       }
       right_modes(h, modes, dims);
-      TRY(run_absorbs(h, (const double *)h->YR.p, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), Mt, 0));
+      TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), Mt, 0));
     }
     CU(cudaMemcpyAsync(m.P.p, Mt, sizeof(double) * m.I * m.Ra * m.Rb, cudaMemcpyDeviceToDevice, h->st));
     TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 0, (double *)m.Q.p));
@@ -645,6 +788,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     TRY(ensure(h, m.P, sizeof(double) * m.I * S));
     TRY(ensure(h, m.Q, sizeof(double) * S * S));
     TRY(ensure(h, m.Zm, sizeof(double) * S * S));
+    TRY(ensure(h, m.Qi, sizeof(double) * S * S));
   }
   h->Tcap = std::max<int64_t>(cfg->t_capacity > 0 ? cfg->t_capacity : 4096, t_init);
   TRY(ensure(h, h->GN, sizeof(double) * h->Tcap * h->SN));
@@ -659,6 +803,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   TRY(ensure(h, h->T1, sizeof(double) * sq));
   TRY(ensure(h, h->H, sizeof(double) * sq));
   TRY(ensure(h, h->Hq, sizeof(double) * STR_MAXW * STR_MAXW));
+  TRY(ensure(h, h->Hi, sizeof(double) * STR_MAXW * STR_MAXW));
   {
     DevBuf info;
     TRY(ensure(h, info, sizeof(int)));
@@ -667,6 +812,13 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     CU(cudaMemsetAsync(h->d_info, 0, sizeof(int), h->st));
   }
   if (h->contract == STR_CONTRACT_3XTF32) TRY(tf32_prepare(h));
+  TRY(ensure(h, h->dT, sizeof(int64_t)));
+  TRY(ensure(h, h->dX, sizeof(void *)));
+  prepare_kernel_attrs();
+  {
+    const char *ev = getenv("STR_NO_GRAPH");
+    h->use_graph = !(ev && ev[0] == '1');
+  }
 
   // upload init cores: paper layout (a, i, b) at a + Ra*(i + I*b) -> G(2) rows [i][a + Ra*b]
   for (int n = 1; n <= N - 1; ++n) {
@@ -680,9 +832,9 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
           buf[i * S + a + m.Ra * b] = init_cores[n - 1][a + (int64_t)m.Ra * ((i + off) + m.I_glob * b)];
     CU(cudaMemcpyAsync(m.G.p, buf.data(), sizeof(double) * buf.size(), cudaMemcpyHostToDevice, h->st));
     CU(cudaStreamSynchronize(h->st));
-    launch_gram_z((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
-    h->launches++;
-    if (n == 1) TRY(allreduce(h, (double *)m.Zm.p, (size_t)S * S));
+    launch_gram_z2((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
+    tl_mark(h, "gram_z");
+    if (n == 1) TRY(allreduce(h, m.Zm.p, (size_t)S * S));
   }
   {
     const int RN = RR(h, N), R1 = RR(h, 1);
@@ -694,6 +846,10 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     CU(cudaStreamSynchronize(h->st));
   }
   h->T = t_init;
+  {
+    int64_t t0 = t_init;
+    CU(cudaMemcpy(h->dT.p, &t0, sizeof(t0), cudaMemcpyHostToDevice));
+  }
   str_status s = (h->variant == STR_DET) ? init_det(h, X_init, t_init) : rstr_init(h, X_init, t_init);
   if (s != STR_OK) return s;
   return deferred_check(h);
@@ -777,26 +933,28 @@ extern "C" str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t
   TRY(deferred_check(h));
   const int N = h->N, k = h->k;
   const int Ra = RR(h, N), Rb = RR(h, k + 1);
-  TRY(ensure_workspace(h, 1));
-  TRY(build_TR(h));
   const int64_t chunk = 16;
-  DevBuf tl, parts, acc;
+  DevBuf tr, tl, parts, acc;
+  TRY(ensure(h, tr, sizeof(double) * h->Rr * Ra * Rb));
+  TRY(build_table(h, desc_TR(h), (double *)tr.p, nullptr, "table_TR"));
   TRY(ensure(h, tl, sizeof(double) * h->L * chunk * Ra * Rb));
   TRY(ensure(h, parts, sizeof(double2) * fit_partials(h->L, h->Rr, chunk)));
   TRY(ensure(h, acc, sizeof(double) * 2));
   CU(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2, h->st));
   for (int64_t c0 = 0; c0 < t; c0 += chunk) {
     int64_t tn = std::min(chunk, t - c0);
-    TRY(build_TL(h, t0 + c0, tn, (double *)tl.p));
+    TRY(build_table(h, desc_TL(h, t0 + c0, tn), (double *)tl.p, nullptr, "table_TL"));
     const char *xp = (const char *)X + (size_t)h->L * h->Rr * c0 * h->xbytes;
-    h->launches += launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)h->TR.p, Ra, Rb, h->L,
+    int nf = launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
                               h->Rr, tn, (double2 *)parts.p, (double *)acc.p, h->st);
+    tl_mark(h, "fit", nf);
     TRY(check_launch(h, "fit"));
   }
   TRY(allreduce(h, (double *)acc.p, 2));
   double sums[2];
   CU(cudaMemcpyAsync(sums, acc.p, sizeof(sums), cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
+  cudaFree(tr.p);
   cudaFree(tl.p);
   cudaFree(parts.p);
   cudaFree(acc.p);
@@ -819,6 +977,46 @@ extern "C" str_status str_set_profiling(str_state *h, int32_t enable) {
   h->prof_events.clear();
   h->profiling = enable != 0;
   return STR_OK;
+}
+
+// Launch timeline (diagnostic, not in include/str.h): enable clears it; dump aggregates the
+// in-stream time between consecutive marks per kernel name as "name total_ms count" lines.
+extern "C" STR_API str_status strdbg_timeline(str_state *h, int32_t enable) {
+  if (!h) return STR_E_ARG;
+  cudaStreamSynchronize(h->st);
+  for (auto &e : h->tl) cudaEventDestroy(e.second);
+  h->tl.clear();
+  h->timeline = enable != 0;
+  if (h->timeline) tl_mark(h, "begin", 0);
+  return STR_OK;
+}
+
+extern "C" STR_API int64_t strdbg_timeline_dump(str_state *h, char *buf, int64_t cap) {
+  if (!h || !buf || cap < 1) return -1;
+  cudaStreamSynchronize(h->st);
+  std::vector<std::string> names;
+  std::vector<double> ms;
+  std::vector<int64_t> cnt;
+  for (size_t i = 1; i < h->tl.size(); ++i) {
+    float t = 0;
+    cudaEventElapsedTime(&t, h->tl[i - 1].second, h->tl[i].second);
+    std::string nm = h->tl[i].first;
+    size_t j = std::find(names.begin(), names.end(), nm) - names.begin();
+    if (j == names.size()) {
+      names.push_back(nm);
+      ms.push_back(0);
+      cnt.push_back(0);
+    }
+    ms[j] += t;
+    cnt[j]++;
+  }
+  std::string out;
+  for (size_t j = 0; j < names.size(); ++j)
+    out += names[j] + " " + std::to_string(ms[j]) + " " + std::to_string(cnt[j]) + "\n";
+  int64_t n = std::min<int64_t>((int64_t)out.size(), cap - 1);
+  memcpy(buf, out.data(), n);
+  buf[n] = 0;
+  return n;
 }
 
 extern "C" str_status str_profile(str_state *h, double *p1_ms, int64_t *p1_n, double *p2_ms, int64_t *p2_n) {
@@ -860,15 +1058,18 @@ extern "C" STR_API str_status strdbg_contract(str_state *h, const void *X, int32
   if (!h || !X || !host_out || (pass != 1 && pass != 2) || tn < 1 || tn > h->T) return STR_E_ARG;
   TRY(ensure_workspace(h, tn));
   const int W1 = RR(h, h->k + 1) * RR(h, h->N);
-  if (pass == 1) {
-    TRY(build_TR(h));
-    TRY(contract(h, X, 1, (const double *)h->TR.p, W1, tn, (double *)h->YL.p));
-  } else {
-    TRY(build_TL(h, 0, tn, (double *)h->TL.p));
-    TRY(contract(h, X, 2, (const double *)h->TL.p, W1, tn, (double *)h->YR.p));
-  }
+  const void *Y;
+  bool y32;
+  TRY(set_x(h, X));
+  TRY(contract(h, X, pass, (const double *)h->GN.p, tn, &Y, &y32));
   CU(cudaStreamSynchronize(h->st));
   size_t n = (size_t)(pass == 1 ? h->L * tn : h->Rr) * W1;
-  CU(cudaMemcpy(host_out, pass == 1 ? h->YL.p : h->YR.p, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (y32) {
+    std::vector<float> f(n);
+    CU(cudaMemcpy(f.data(), Y, n * sizeof(float), cudaMemcpyDeviceToHost));
+    for (size_t i = 0; i < n; ++i) host_out[i] = f[i];
+  } else {
+    CU(cudaMemcpy(host_out, Y, n * sizeof(double), cudaMemcpyDeviceToHost));
+  }
   return STR_OK;
 }

@@ -22,6 +22,7 @@ struct ModeBuf {
   DevBuf P;             // I x Ra*Rb (Eq. partial)
   DevBuf Q;             // (Ra*Rb)^2 (Eq. partial)
   DevBuf Zm;            // Gram tensor Z_n as chain matrix: Rb^2 x Ra^2
+  DevBuf Qi;            // Q_n^{-1} (full symmetric)
   // rSTR
   DevBuf samp;          // sampled slices (G_n)_S: m x Ra*Rb (G(2) layout rows)
   std::vector<int32_t> idx_host;
@@ -60,7 +61,7 @@ struct str_state {
   int64_t T = 0, Tcap = 0;
   DevBuf ZmN;                       // Z_N^new (update) / Z_N (init): R_1^2 x R_N^2
   std::vector<DevBuf> Sf;           // suffix chains Sf_n (index n)
-  DevBuf Lp[2], T1, H, Hq;
+  DevBuf Lp[2], T1, H, Hq, Hi;       // Hq = H^{≠N}_<2> (temporal normal matrix), Hi = Hq^{-1}
 
   // workspaces
   int64_t ws_t = 0;
@@ -71,7 +72,24 @@ struct str_state {
   // 3xTF32 path
   bool tf32_ready = false;
   DevBuf tab_split;                 // hi/lo fp32 table for the tensor-core passes
-  DevBuf tf_part;                   // split-K fp32->fp64 partials
+  DevBuf tf_part, tf_part2;         // pass-1 / pass-2 fp32 outputs (stream-K red.add targets)
+
+  // CUDA-graph replay of the STR step: the step is captured once per t_new and
+  // replayed; X enters through the device slot dX (f64 path) or by re-pointing the two tensor-core
+  // contraction nodes (3xTF32 path).  New temporal rows go to the fixed scratch GNnew and are
+  // appended at the device-side row counter dT.
+  DevBuf GNnew, dT, dX;
+  bool use_graph = true;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int64_t g_tn = 0;
+  int64_t g_launches = 0;
+  cudaGraphNode_t g_setx = nullptr;
+  cudaGraphNode_t tf_node[2] = {nullptr, nullptr};
+  alignas(16) unsigned char tf_params[2][256];
+  int tf_grid[2] = {0, 0};
+  size_t tf_smem[2] = {0, 0};
+  bool capturing = false;
 
   // rSTR
   DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev;
@@ -84,6 +102,9 @@ struct str_state {
   int64_t collectives = 0;
   bool profiling = false;
   std::vector<ProfEvent> prof_events;
+  // launch timeline (diagnostic): an event after every launch, named by kernel
+  bool timeline = false;
+  std::vector<std::pair<const char *, cudaEvent_t>> tl;
   std::string err;
   bool poisoned = false;
 
@@ -94,16 +115,33 @@ struct str_state {
       b.bytes = 0;
     };
     for (auto &m : md) {
-      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.samp);
+      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.Qi); fr(m.samp);
     }
     fr(GN); fr(ZmN);
     for (auto &b : Sf) fr(b);
-    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq);
+    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi);
     fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
-    fr(tab_split); fr(tf_part);
+    fr(tab_split); fr(tf_part); fr(tf_part2);
+    fr(GNnew); fr(dT); fr(dX);
+    if (gexec) cudaGraphExecDestroy(gexec);
+    if (graph) cudaGraphDestroy(graph);
+    gexec = nullptr;
+    graph = nullptr;
     fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev);
   }
 };
+
+// Count a launch (n kernels) and, when the timeline is on, record a named event after it on the
+// handle's stream: consecutive events bracket each launch's in-stream time (incl. its gap).
+inline void tl_mark(str_state *h, const char *name, int n = 1) {
+  h->launches += n;
+  if (h->timeline) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, h->st);
+    h->tl.push_back({name, e});
+  }
+}
 
 // str_api.cu
 str_status ensure_temporal_capacity(str_state *h, int64_t need);
@@ -115,4 +153,9 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn);
 // contract_tf32.cu
 str_status tf32_prepare(str_state *h);
 str_status tf32_ensure_workspace(str_state *h, int64_t tn);
-int launch_contract_tf32(str_state *h, const void *X, int pass, const double *tab, int W, int64_t tn, double *out);
+// Tensor-core pass over X with the pre-tiled table operand already in h->tab_split; fp32 output Y
+// (zeroed and accumulated here).  Returns 0, or -1 with h->err set.
+int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y);
+int tf32_npad(int W);
+// Re-point captured contraction node `pass` of exec at new data X (3xTF32 path).
+str_status tf32_graph_update(str_state *h, cudaGraphExec_t exec, int pass, const void *X, int64_t tn);

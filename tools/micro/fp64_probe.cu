@@ -66,5 +66,12 @@ int main() {
   printf("LDS.64 pointer-chase latency: %.1f cyc\n", (double)hc[3] / n);
   printf("DFMA throughput (1024 thr, 8 indep chains): %.1f DFMA/cyc/SM\n", 1024.0 * 8 * n / hc[4]);
   printf("__syncthreads (512 thr) cost: %.1f cyc\n", (double)hc[5] / n);
+  for (int thr : {32, 64, 128, 256, 512}) {
+    tput_dfma<<<1, thr>>>(d, c, n);
+    cudaDeviceSynchronize();
+    cudaMemcpy(hc, c, 64, cudaMemcpyDeviceToHost);
+    printf("DFMA throughput %4d threads: %.2f DFMA/cyc/SM  (%.2f cyc per warp-instr per warp)\n", thr,
+           (double)thr * 8 * n / hc[4], (double)hc[4] / (8.0 * n));
+  }
   return 0;
 }
