@@ -9,6 +9,8 @@
 //   k_absorb2      second-level contractions of the two-pass intermediates with core slices;
 //   k_build_table2 chained-slice tables (⊠₂ chains, Def. 6), fp64 rows and/or the
 //                  pre-tiled 3xTF32 hi/lo operand blocks of the tensor-core contraction.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -19,6 +21,14 @@ void prepare_kernel_attrs();
 __device__ __forceinline__ void cp_async8(void *smem, const void *g) {
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
                : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *smem, const void *g) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+template <typename T>
+__device__ __forceinline__ void cp_async_el(T *smem, const T *g) {
+  if (sizeof(T) == 8) cp_async8(smem, g); else cp_async4(smem, g);
 }
 __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\n\tcp.async.wait_group 0;" ::: "memory");
@@ -339,7 +349,8 @@ __global__ void __launch_bounds__(256) k_gram_z2(const double *__restrict__ G, i
   for (int64_t i0 = 0; i0 < I; i0 += ch) {
     const int ic = (int)((I - i0) < ch ? (I - i0) : ch);
     __syncthreads();
-    for (int e = threadIdx.x; e < ic * AB; e += 256) Gs[e] = G[i0 * AB + e];
+    for (int e = threadIdx.x; e < ic * AB; e += 256) cp_async8(Gs + e, G + i0 * AB + e);
+    cp_async_wait_all();
     __syncthreads();
     int i = 0;
     for (; i + 2 <= ic; i += 2) {
@@ -360,85 +371,179 @@ void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int 
 }
 
 // ------------------------------------------------------------------------------------------
-// Absorb (AbsorbDesc): one CTA per `rest` multi-index, thread per output entry (po, qo); chunks
-// of the contracted index i of both A slices and Y(rest, i) are staged in shared memory.
+// Absorb (AbsorbDesc): contract index `pos` of the matrix-valued tensor Y with core slices.
 //   left : out[rest][po][qo] = sum_i sum_p A(i)[po][p] Y(rest, i)[p][qo]
 //   right: out[rest][po][qo] = sum_i sum_q Y(rest, i)[po][q] A(i)[q][qo]
-constexpr int kAbsorbSmem = 6144;   // doubles
+// Generic form: out vector index u (po | qo, length L), vector index v (qo | po, V of them),
+// contracted p (p | q, R).  A thread owns VB consecutive v of one rest and one k-split ks of the
+// contracted index i; it keeps VB x L accumulators in registers (register-blocked micro-GEMM:
+// per (i, p) L broadcast loads of A from shared memory and VB loads of Y feed VB x L FMAs).  The
+// A slices are staged in shared memory (cp.async) in chunks of i; the KS partials are reduced in
+// shared memory in a fixed order (deterministic).
+constexpr int kAbsVB = 2;
 
-template <typename TY>
-__global__ void __launch_bounds__(256) k_absorb2(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
-                                                 int accumulate, int64_t before, int64_t I, int ic_max) {
-  __shared__ double sm[kAbsorbSmem];
+template <typename TY, int MR, bool LEFT>
+__global__ void __launch_bounds__(256) k_absorb4(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
+                                                 int accumulate, int64_t before, int64_t I, int64_t nrest, int KS,
+                                                 int ic_max) {
+  extern __shared__ __align__(16) double asm_[];
   const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
-  double *As = sm, *Ys = sm + ic_max * AB;
-  const int Po = ad.left ? ad.Ra : ad.P;
-  const int Qo = ad.left ? ad.Q : ad.Rb;
-  const int O = Po * Qo;
-  const int64_t rest = blockIdx.x;
-  const int64_t b0 = rest % before, a0 = rest / before;
-  const TY *ybase = Y + (b0 + before * I * a0) * PQ;
+  const int Po = LEFT ? ad.Ra : ad.P, Qo = LEFT ? ad.Q : ad.Rb;
+  const int L = LEFT ? Po : Qo, V = LEFT ? Qo : Po, R = LEFT ? ad.P : ad.Q;
+  const int nvb = (V + kAbsVB - 1) / kAbsVB;
+  const int per_ks = blockDim.x / KS;                      // (rest, vblk) pairs per CTA
+  double *As = asm_;                                        // ic_max * AB
+  double *red = asm_ + ((ic_max * AB + 1) & ~1);           // KS * per_ks * kAbsVB * MR
+  const int tid = threadIdx.x;
+  const int ks = tid / per_ks, pr = tid % per_ks;
+  const int64_t pair = (int64_t)blockIdx.x * per_ks + pr;
+  const int64_t rest = pair / nvb;
+  const int v0 = (int)(pair % nvb) * kAbsVB;
+  const bool act = rest < nrest && ks < KS;        // (threads beyond KS * per_ks idle)
+  const int64_t b0 = act ? rest % before : 0, a0 = act ? rest / before : 0;
+  const TY *yb = Y + (b0 + before * I * a0) * PQ;
   const int64_t ystride = before * PQ;
-  const int o = threadIdx.x;
-  const bool act = o < O;
-  const int po = act ? o / Qo : 0, qo = act ? o % Qo : 0;
-  double acc0 = 0.0, acc1 = 0.0;
+  const int a_ps = LEFT ? ad.Ra : 1, a_us = LEFT ? 1 : ad.Ra;     // A(i): p and u strides
+  const int y_ps = LEFT ? ad.Q : 1, y_vs = LEFT ? 1 : ad.Q;       // Y(rest,i): p and v strides
+  double acc[kAbsVB][MR];
+#pragma unroll
+  for (int b = 0; b < kAbsVB; ++b)
+#pragma unroll
+    for (int u = 0; u < MR; ++u) acc[b][u] = 0.0;
   for (int64_t i0 = 0; i0 < I; i0 += ic_max) {
     const int ic = (int)((I - i0) < ic_max ? (I - i0) : ic_max);
     __syncthreads();
-    for (int e = threadIdx.x; e < ic * AB; e += blockDim.x) As[e] = ad.A[i0 * AB + e];
-    for (int e = threadIdx.x; e < ic * PQ; e += blockDim.x) {
-      const int i = e / PQ, w = e % PQ;
-      Ys[e] = (double)ybase[(i0 + i) * ystride + w];
-    }
+    for (int e = tid; e < ic * AB; e += blockDim.x) cp_async8(As + e, ad.A + i0 * AB + e);
+    cp_async_wait_all();
     __syncthreads();
     if (act) {
-      if (ad.left) {
-        for (int i = 0; i < ic; ++i) {
-          const double *a = As + i * AB + po;
-          const double *y = Ys + i * PQ + qo;
-          double s = 0.0;
+      // this thread's i in the chunk: i = i0 + j with (i0 + j) % KS == ks
+      int j = (int)((ks - i0 % KS + KS) % KS);
+      for (; j < ic; j += KS) {
+        const double *Ai = As + j * AB;
+        const TY *yi = yb + (i0 + j) * ystride;
+        // all Y loads of this slice first (one memory latency per slice), then the FMAs
+        double yv[MR][kAbsVB];
 #pragma unroll
-          for (int p = 0; p < STR_MAXR; ++p)
-            if (p < ad.P) s = fma(a[ad.Ra * p], y[p * ad.Q], s);
-          if (i & 1) acc1 += s; else acc0 += s;
-        }
-      } else {
-        for (int i = 0; i < ic; ++i) {
-          const double *a = As + i * AB + ad.Ra * qo;
-          const double *y = Ys + i * PQ + po * ad.Q;
-          double s = 0.0;
+        for (int p = 0; p < MR; ++p)
 #pragma unroll
-          for (int q = 0; q < STR_MAXR; ++q)
-            if (q < ad.Q) s = fma(y[q], a[q], s);
-          if (i & 1) acc1 += s; else acc0 += s;
+          for (int b = 0; b < kAbsVB; ++b)
+            yv[p][b] = (p < R && v0 + b < V) ? (double)__ldg(yi + p * y_ps + (v0 + b) * y_vs) : 0.0;
+#pragma unroll
+        for (int p = 0; p < MR; ++p) {
+          if (p < R) {
+            double av[MR];
+#pragma unroll
+            for (int u = 0; u < MR; ++u) av[u] = (u < L) ? Ai[p * a_ps + u * a_us] : 0.0;
+#pragma unroll
+            for (int b = 0; b < kAbsVB; ++b)
+#pragma unroll
+              for (int u = 0; u < MR; ++u) acc[b][u] = fma(av[u], yv[p][b], acc[b][u]);
+          }
         }
       }
     }
   }
-  if (act) {
-    double *dst = out + rest * O + o;
-    const double v = acc0 + acc1;
-    if (accumulate) *dst += v; else *dst = v;
+  if (KS > 1) {
+    __syncthreads();
+    if (ks < KS) {
+      double *rp = red + ((int64_t)ks * per_ks + pr) * (kAbsVB * MR);
+#pragma unroll
+      for (int b = 0; b < kAbsVB; ++b)
+#pragma unroll
+        for (int u = 0; u < MR; ++u) rp[b * MR + u] = acc[b][u];
+    }
+    __syncthreads();
+    if (ks != 0) return;
+    for (int k = 1; k < KS; ++k) {
+      const double *rk = red + ((int64_t)k * per_ks + pr) * (kAbsVB * MR);
+#pragma unroll
+      for (int b = 0; b < kAbsVB; ++b)
+#pragma unroll
+        for (int u = 0; u < MR; ++u) acc[b][u] += rk[b * MR + u];
+    }
+  }
+  if (!act) return;
+  const int O = Po * Qo;
+#pragma unroll
+  for (int b = 0; b < kAbsVB; ++b) {
+    if (v0 + b >= V) continue;
+#pragma unroll
+    for (int u = 0; u < MR; ++u) {
+      if (u < L) {
+        const int po = LEFT ? u : v0 + b, qo = LEFT ? v0 + b : u;
+        double *dst = out + rest * O + po * Qo + qo;
+        if (accumulate) *dst += acc[b][u]; else *dst = acc[b][u];
+      }
+    }
   }
 }
 
+template <typename TY, int MR>
+static void absorb_launch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest,
+                          int64_t before, int64_t I, cudaStream_t s) {
+  const bool left = ad.left != 0;
+  const int Po = left ? ad.Ra : ad.P, Qo = left ? ad.Q : ad.Rb;
+  const int V = left ? Qo : Po;
+  const int nvb = (V + kAbsVB - 1) / kAbsVB;
+  const int64_t pairs = nrest * nvb;
+  // k-splits: aim for ~148 x 128 threads, each thread >= 2 contracted slices
+  int KS = (int)std::max<int64_t>(1, std::min<int64_t>(cdiv(148 * 128, pairs), I / 2));
+  if (KS > 32) KS = 32;
+  int threads = 128;
+  while (threads < 256 && threads / KS < 4) threads *= 2;
+  if (KS > threads) KS = threads;
+  const int per_ks = threads / KS;
+  const int AB = ad.Ra * ad.Rb;
+  int ic = (int)std::min<int64_t>(I, std::max<int64_t>(1, 8192 / AB));   // <= 64 KB of A per chunk
+  const size_t smem = sizeof(double) * (((size_t)ic * AB + 1) & ~1) +
+                      (KS > 1 ? sizeof(double) * KS * per_ks * kAbsVB * MR : 0);
+  const unsigned grid = (unsigned)cdiv(pairs, per_ks);
+  if (left)
+    k_absorb4<TY, MR, true><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, before, I, nrest, KS, ic);
+  else
+    k_absorb4<TY, MR, false><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, before, I, nrest, KS, ic);
+}
+
+template <typename TY>
+static void absorb_dispatch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest,
+                            int64_t before, int64_t I, cudaStream_t s) {
+  // MR bounds both the accumulator length (Ra | Rb) and the contracted rank (P | Q)
+  const int L = std::max(ad.left ? ad.Ra : ad.Rb, ad.left ? ad.P : ad.Q);
+  if (L <= 4)
+    absorb_launch<TY, 4>(ad, Y, out, accumulate, nrest, before, I, s);
+  else if (L <= 8)
+    absorb_launch<TY, 8>(ad, Y, out, accumulate, nrest, before, I, s);
+  else if (L <= 10)
+    absorb_launch<TY, 10>(ad, Y, out, accumulate, nrest, before, I, s);
+  else
+    absorb_launch<TY, STR_MAXR>(ad, Y, out, accumulate, nrest, before, I, s);
+}
+
+template <typename TY>
+static void absorb_attrs() {
+  const int mx = 160 * 1024;
+  cudaFuncSetAttribute(k_absorb4<TY, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, 8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, 10, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, 10, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, STR_MAXR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb4<TY, STR_MAXR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+}
+
 void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s) {
+  prepare_kernel_attrs();
   int64_t rest = 1, before = 1;
   for (int j = 0; j < ad.nd; ++j)
     if (j != ad.pos) rest *= ad.d[j];
   for (int j = 0; j < ad.pos; ++j) before *= ad.d[j];
   const int64_t I = ad.d[ad.pos];
-  const int Po = ad.left ? ad.Ra : ad.P;
-  const int Qo = ad.left ? ad.Q : ad.Rb;
-  const int threads = (int)cdiv(Po * Qo, 32) * 32;
-  int ic = kAbsorbSmem / (ad.Ra * ad.Rb + ad.P * ad.Q);
-  if (ic > I) ic = (int)I;
-  if (ic < 1) ic = 1;
   if (y_f32)
-    k_absorb2<float><<<(unsigned)rest, threads, 0, s>>>(ad, (const float *)Y, out, accumulate, before, I, ic);
+    absorb_dispatch<float>(ad, (const float *)Y, out, accumulate, rest, before, I, s);
   else
-    k_absorb2<double><<<(unsigned)rest, threads, 0, s>>>(ad, (const double *)Y, out, accumulate, before, I, ic);
+    absorb_dispatch<double>(ad, (const double *)Y, out, accumulate, rest, before, I, s);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -453,6 +558,7 @@ __device__ __forceinline__ float tf32_rna(float x) {
   return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
 }
 
+template <int MR>
 __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
   extern __shared__ __align__(16) double tsm[];
   const int nlb = (int)cdiv(td.Lk, 32);
@@ -479,7 +585,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
       const int AB = F.Ra * F.Rb;
       for (int e = threadIdx.x; e < c * AB; e += blockDim.x) {
         const int j = e / AB, w = e % AB;
-        p[e] = F.G[((q0 + j) % F.I) * AB + w];
+        cp_async8(p + e, F.G + ((q0 + j) % F.I) * AB + w);
       }
       p += ((c * AB + 1) & ~1);
     }
@@ -496,18 +602,19 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
     tile = (float *)p;
     for (int e = threadIdx.x; e < 2 * Np * 32; e += blockDim.x) tile[e] = 0.0f;
   }
+  cp_async_wait_all();
   __syncthreads();
   const int el = threadIdx.x / R0, pr = threadIdx.x % R0;
   const int64_t l = l0 + el;
   if (el < 32 && l < l1) {
     const int64_t e = l + td.Lk * tp;
-    double v[STR_MAXR], w[STR_MAXR];
+    double v[MR], w[MR];
     {
       const Factor &F = fl.f[0];
       const int64_t q = e / F.stride;
       const double *S = base[0] + ((q - first[0]) % cnt[0]) * (F.Ra * F.Rb);
 #pragma unroll
-      for (int b = 0; b < STR_MAXR; ++b) v[b] = (b < F.Rb) ? S[pr + F.Ra * b] : 0.0;
+      for (int b = 0; b < MR; ++b) v[b] = (b < F.Rb) ? S[pr + F.Ra * b] : 0.0;
     }
 #pragma unroll
     for (int f = 1; f < kMaxFactors; ++f) {
@@ -516,29 +623,29 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
         const int64_t q = e / F.stride;
         const double *S = base[f] + ((q - first[f]) % cnt[f]) * (F.Ra * F.Rb);
 #pragma unroll
-        for (int b = 0; b < STR_MAXR; ++b) {
+        for (int b = 0; b < MR; ++b) {
           double acc = 0.0;
           if (b < F.Rb) {
 #pragma unroll
-            for (int a = 0; a < STR_MAXR; ++a)
+            for (int a = 0; a < MR; ++a)
               if (a < F.Ra) acc = fma(v[a], S[a + F.Ra * b], acc);
           }
           w[b] = acc;
         }
 #pragma unroll
-        for (int b = 0; b < STR_MAXR; ++b) v[b] = w[b];
+        for (int b = 0; b < MR; ++b) v[b] = w[b];
       }
     }
     if (out64) {
       double *o = out64 + e * (int64_t)W + (int64_t)pr * Rl;
 #pragma unroll
-      for (int q = 0; q < STR_MAXR; ++q)
+      for (int q = 0; q < MR; ++q)
         if (q < Rl) o[q] = v[q];
     }
     if (tiles) {
       const int kk = el, chunk = kk >> 2, within = kk & 3;
 #pragma unroll
-      for (int q = 0; q < STR_MAXR; ++q) {
+      for (int q = 0; q < MR; ++q) {
         if (q < Rl) {
           const int n = pr * Rl + q;
           const float hi = tf32_rna((float)v[q]);
@@ -577,7 +684,16 @@ int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaSt
   prepare_kernel_attrs();
   const int64_t units = td.tk * cdiv(td.Lk, 32);
   const int threads = (int)cdiv(32 * td.fl.f[0].Ra, 32) * 32;
-  k_build_table2<<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
+  int mr = 0;
+  for (int f = 0; f < td.fl.n; ++f) mr = std::max(mr, std::max(td.fl.f[f].Ra, td.fl.f[f].Rb));
+  if (mr <= 4)
+    k_build_table2<4><<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
+  else if (mr <= 8)
+    k_build_table2<8><<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
+  else if (mr <= 10)
+    k_build_table2<10><<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
+  else
+    k_build_table2<STR_MAXR><<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
   return 0;
 }
 
@@ -603,7 +719,12 @@ void prepare_kernel_attrs() {
   cudaFuncSetAttribute(k_spd_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
   cudaFuncSetAttribute(k_spd_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
   cudaFuncSetAttribute(k_chain_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
-  cudaFuncSetAttribute(k_build_table2, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  absorb_attrs<float>();
+  absorb_attrs<double>();
+  cudaFuncSetAttribute(k_build_table2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table2<STR_MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   done = true;
 }
 

@@ -437,13 +437,18 @@ static void right_modes(const str_state *h, std::vector<int> &modes, std::vector
   }
 }
 
-// Q_j^{-1} (sweep), G_j = P_j Q_j^{-1} (Alg. 4 l.17) and Z_j (l.18).
-static str_status solve_mode(str_state *h, int j) {
+// Q_j^{-1} by the blocked sweep (the "^{-1}" of Alg. 4 l.17).
+static str_status invert_mode(str_state *h, int j) {
+  ModeBuf &m = h->md[j - 1];
+  launch_spd_inv((const double *)m.Q.p, m.Ra * m.Rb, (double *)m.Qi.p, h->d_info, h->st);
+  tl_mark(h, "spd_inv");
+  return check_launch(h, "spd_inv");
+}
+
+// G_j = P_j Q_j^{-1} (Alg. 4 l.17) and Z_j (l.18).
+static str_status finish_mode(str_state *h, int j) {
   ModeBuf &m = h->md[j - 1];
   const int S = m.Ra * m.Rb;
-  launch_spd_inv((const double *)m.Q.p, S, (double *)m.Qi.p, h->d_info, h->st);
-  tl_mark(h, "spd_inv");
-  TRY(check_launch(h, "spd_inv"));
   launch_rows_mm((const double *)m.P.p, (const double *)m.Qi.p, S, m.I, (double *)m.G.p, h->st);
   tl_mark(h, "rows_mm");
   TRY(check_launch(h, "rows_mm"));
@@ -454,13 +459,32 @@ static str_status solve_mode(str_state *h, int j) {
   return STR_OK;
 }
 
+// Fork / join of the side stream (independent branches of one step; graph branches when
+// capturing).  Between fork() and main_again() launches go to the side stream.
+static str_status fork(str_state *h) {
+  CU(cudaEventRecord(h->ev_fork, h->st));
+  CU(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  h->st_main = h->st;
+  h->st = h->st2;
+  return STR_OK;
+}
+static void main_again(str_state *h) { h->st = h->st_main; }
+static str_status join(str_state *h) {
+  CU(cudaEventRecord(h->ev_join, h->st2));
+  CU(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  return STR_OK;
+}
+
 // ------------------------------------------------------------------------------------ update (STR)
-// Enqueues one STR step (everything on h->st, no host synchronization, no host-side T): the new
-// temporal rows go to the scratch GNnew and are appended at the device row counter at the end.
+// Enqueues one STR step (no host synchronization, no host-side T): the new temporal rows go to the
+// scratch GNnew and are appended at the device row counter at the end.  The Gram-chain / inverse
+// work of each mode (which needs only Z's) runs on the side stream, concurrently with the
+// contraction / absorb work (which needs X and the cores); the two join before G_n = P_n Q_n^{-1}.
 static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   const int N = h->N, k = h->k;
   TRY(set_x(h, X));
-  // 0. suffix chains and H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq, Hq^{-1}
+  // side: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq, Hq^{-1} (old state only)
+  TRY(fork(h));
   TRY(build_suffixes(h));
   {
     int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
@@ -470,11 +494,11 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     launch_spd_inv((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, h->d_info, h->st);
     tl_mark(h, "spd_inv");
   }
-  // 1. pass 1 with the old cores
+  main_again(h);
+  // main: pass 1 with the old cores, then M_N = (G_1...G_k) Y_L summed over l
   const void *YL;
   bool yl32;
   TRY(contract(h, X, 1, nullptr, tn, &YL, &yl32));
-  // 2. temporal mode: M_N = (G_1...G_k) Y_L summed over l
   std::vector<int> modes;
   std::vector<int64_t> dims;
   left_modes(h, modes, dims);
@@ -485,54 +509,57 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   double *Mt = (double *)h->Mt.p;
   TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), ops, Mt, 0));
   TRY(allreduce(h, Mt, (size_t)tn * h->SN));                                   // site C1
+  TRY(join(h));
   double *GN_new = (double *)h->GNnew.p;
   launch_rows_mm(Mt, (const double *)h->Hi.p, h->SN, tn, GN_new, h->st);       // l.9
   tl_mark(h, "rows_mm");
   TRY(check_launch(h, "temporal solve"));
   launch_gram_z2(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);  // Z_N^new
   tl_mark(h, "gram_z");
-  // W = Y_L absorbed over t with G_N^new on the right: modes 1..k, entries R_{k+1} x R_1
-  {
-    std::vector<AOp> o1 = {{N, 0, temporal_factor_at(h, GN_new, tn, 1)}};
-    TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
-  }
-  // 3. left modes
+  // modes 1..N-1 in order (Gauss-Seidel)
   bool Lp_id = true;
   int lp_cur = 0;
-  for (int j = 1; j <= k; ++j) {
+  const void *YR = nullptr;
+  bool yr32 = false;
+  for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
-    left_modes(h, modes, dims);
-    auto lo = left_ops(h, j);
-    if (j == 1 || h->p == 1) {
-      TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, (double *)m.P.p, 1));
-    } else {   // M_j sums over the sharded i_1: reduce before accumulating (site C2)
-      TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
-      TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
-      launch_axpy_any(Mt, false, (double *)m.P.p, m.I * m.Ra * m.Rb, 1, h->st);
-      tl_mark(h, "axpy");
+    // side: Q_j += H^{≠j}_new (l.15-16), Q_j^{-1}
+    TRY(fork(h));
+    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
+    TRY(invert_mode(h, j));
+    main_again(h);
+    // main: P_j += X_new[j] G^{≠j}_new (l.13-14)
+    if (j <= k) {
+      left_modes(h, modes, dims);
+      if (j == 1) {
+        // W = Y_L absorbed over t with G_N^new on the right: modes 1..k, entries R_{k+1} x R_1
+        std::vector<int> m2 = modes;
+        std::vector<int64_t> d2 = dims;
+        m2.push_back(N);
+        d2.push_back(tn);
+        std::vector<AOp> o1 = {{N, 0, temporal_factor_at(h, GN_new, tn, 1)}};
+        TRY(run_absorbs(h, YL, yl32, m2, d2, RR(h, k + 1), RR(h, N), o1, (double *)h->Wt.p, 0));
+      }
+      auto lo = left_ops(h, j);
+      if (j == 1 || h->p == 1) {
+        TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, (double *)m.P.p, 1));
+      } else {   // M_j sums over the sharded i_1: reduce before accumulating (site C2)
+        TRY(run_absorbs(h, h->Wt.p, false, modes, dims, RR(h, k + 1), RR(h, 1), lo, Mt, 0));
+        TRY(allreduce(h, Mt, (size_t)m.I * m.Ra * m.Rb));
+        launch_axpy_any(Mt, false, (double *)m.P.p, m.I * m.Ra * m.Rb, 1, h->st);
+        tl_mark(h, "axpy");
+      }
+    } else {
+      if (j == k + 1) {   // pass 2 with the new cores
+        TRY(contract(h, X, 2, GN_new, tn, &YR, &yr32));
+        TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));   // site C2'
+      }
+      right_modes(h, modes, dims);
+      TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p, 1));
     }
-    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
-    TRY(solve_mode(h, j));
-    // Lp_{j+1} = Zm_j * Lp_j
-    int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
-    TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
-                  (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
-    lp_cur = 1 - lp_cur;
-    Lp_id = false;
-  }
-  // 4. pass 2 with the new cores
-  const void *YR;
-  bool yr32;
-  TRY(contract(h, X, 2, GN_new, tn, &YR, &yr32));
-  TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));   // site C2'
-  // 5. right modes
-  for (int j = k + 1; j <= N - 1; ++j) {
-    ModeBuf &m = h->md[j - 1];
-    right_modes(h, modes, dims);
-    TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p, 1));
-    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
-    TRY(solve_mode(h, j));
-    if (j < N - 1) {
+    TRY(join(h));
+    TRY(finish_mode(h, j));
+    if (j < N - 1) {   // Lp_{j+1} = Zm_j * Lp_j
       int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
       TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
                     (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
@@ -733,6 +760,12 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
 
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) {
+    delete h;
+    return STR_E_CUDA;
+  }
+  if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return STR_E_CUDA;
   }
@@ -1046,6 +1079,12 @@ extern "C" void str_destroy(str_state *h) {
   }
   h->free_all();
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)h->comm);
+  if (h->st2) {
+    cudaStreamSynchronize(h->st2);
+    cudaStreamDestroy(h->st2);
+  }
+  if (h->ev_fork) cudaEventDestroy(h->ev_fork);
+  if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
 }

@@ -49,6 +49,8 @@ struct str_state {
   int64_t i1_off = 0;
   cudaStream_t st = nullptr;
   bool own_stream = false;
+  cudaStream_t st2 = nullptr, st_main = nullptr;   // side stream for the independent branches
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   void *comm = nullptr;             // ncclComm_t
 
   // geometry (local)

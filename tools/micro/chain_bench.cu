@@ -64,7 +64,31 @@ __global__ void k_skel8(double *out, int steps, long long *cyc) {
   out[t] = sacc;
 }
 
+__global__ void k_empty_n() {}
+__global__ void k_copy_d(const double *__restrict__ a, double *__restrict__ b, int64_t n) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < n) b[i] = a[i];
+}
+__global__ void k_dep_loads(const double *__restrict__ a, double *__restrict__ b, int n) {
+  // one thread chain of n dependent L2 loads
+  int idx = threadIdx.x;
+  double acc = 0;
+  for (int i = 0; i < n; ++i) { double v = a[idx]; acc += v; idx = ((int)v + i * 97 + threadIdx.x) & 4095; }
+  b[threadIdx.x] = acc;
+}
+
 int main(int argc, char **argv) {
+  {
+    double *a, *b; cudaMalloc(&a, 8 << 20); cudaMalloc(&b, 8 << 20); cudaMemset(a, 0, 8 << 20);
+    float e1 = time_us([&] { k_empty_n<<<1, 32>>>(); });
+    float e2 = time_us([&] { k_empty_n<<<1600, 512>>>(); });
+    float e3 = time_us([&] { k_empty_n<<<148, 1024>>>(); });
+    float c1 = time_us([&] { k_copy_d<<<625, 256>>>(a, b, 160000); });
+    float c2 = time_us([&] { k_copy_d<<<4096, 256>>>(a, b, 1 << 20); });
+    float d1 = time_us([&] { k_dep_loads<<<1, 32>>>(a, b, 100); });
+    printf("empty 1x32 %.2f | empty 1600x512 %.2f | empty 148x1024 %.2f | copy 1.28MB %.2f | copy 8MB %.2f | 100 dep loads %.2f us\n",
+           e1, e2, e3, c1, c2, d1);
+  }
   {
     double *o; long long *cy; cudaMalloc(&o, 8 * 1024); cudaMalloc(&cy, 64);
     for (int thr : {32, 96}) {
@@ -129,6 +153,37 @@ int main(int argc, char **argv) {
   float t_ginv = time_us([&] { cudaGraphLaunch(ge, st); }, 10) / 10.f;
   cudaStreamSynchronize(st);
   printf("graph: %.2f us per empty node, %.2f us per spd_inv node\n", t_graph, t_ginv);
+  {
+    // C5-shaped absorbs: Y_L (i1, i2, t) 40 x 40 x 8 entries 10x10 (fp32), contract i2 with G_2 slices
+    float *Yf; double *Ad, *Od, *Wd;
+    cudaMalloc(&Yf, sizeof(float) * 12800 * 100);
+    cudaMalloc(&Ad, sizeof(double) * 40 * 100);
+    cudaMalloc(&Od, sizeof(double) * 12800 * 100);
+    cudaMalloc(&Wd, sizeof(double) * 1600 * 100);
+    cudaMemset(Yf, 0, sizeof(float) * 12800 * 100);
+    cudaMemset(Ad, 0, sizeof(double) * 40 * 100);
+    cudaMemset(Wd, 0, sizeof(double) * 1600 * 100);
+    AbsorbDesc ad{};
+    ad.nd = 3; ad.d[0] = 40; ad.d[1] = 40; ad.d[2] = 8; ad.pos = 1; ad.P = 10; ad.Q = 10; ad.left = 1; ad.A = Ad; ad.Ra = 10; ad.Rb = 10;
+    float t1 = time_us([&] { launch_absorb2(ad, Yf, true, Od, 0, 0); });
+    ad.pos = 2; ad.left = 0;   // W: contract t (I = 8) on the right
+    ad.A = Ad;
+    float t2 = time_us([&] { launch_absorb2(ad, Yf, true, Od, 0, 0); });
+    AbsorbDesc am{};
+    am.nd = 2; am.d[0] = 40; am.d[1] = 40; am.pos = 1; am.P = 10; am.Q = 10; am.left = 1; am.A = Ad; am.Ra = 10; am.Rb = 10;
+    float t3 = time_us([&] { launch_absorb2(am, Wd, false, Od, 1, 0); });
+    // T_L table: 12800 entries of G_N(t) G_1(i1) G_2(i2), tf32 tiles
+    TableDesc td{};
+    td.fl.n = 3;
+    td.fl.f[0] = Factor{Ad, 8, 10, 10, 1600};
+    td.fl.f[1] = Factor{Ad, 40, 10, 10, 1};
+    td.fl.f[2] = Factor{Ad, 40, 10, 10, 40};
+    td.Lk = 1600; td.tk = 8; td.Npad = 112;
+    float *tiles; cudaMalloc(&tiles, sizeof(float) * 400 * 2 * 112 * 32);
+    float t4 = time_us([&] { launch_build_table2(td, nullptr, tiles, 0); });
+    printf("absorb Y_L->mode2 (320 rest) %.2f us | absorb W over t (1600 rest) %.2f us | mode absorb (40 rest) %.2f us | table T_L %.2f us\n",
+           t1, t2, t3, t4);
+  }
   // correctness: G Q = P
   std::vector<double> G(I * S);
   cudaMemcpy(G.data(), dG, 8 * I * S, cudaMemcpyDeviceToHost);
