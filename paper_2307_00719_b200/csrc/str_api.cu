@@ -462,6 +462,8 @@ static str_status finish_mode(str_state *h, int j) {
 // Fork / join of the side stream (independent branches of one step; graph branches when
 // capturing).  Between fork() and main_again() launches go to the side stream.
 static str_status fork(str_state *h) {
+  h->st_main = h->st;
+  if (h->timeline) return STR_OK;   // the diagnostic timeline serializes everything on one stream
   CU(cudaEventRecord(h->ev_fork, h->st));
   CU(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
   h->st_main = h->st;
@@ -470,6 +472,7 @@ static str_status fork(str_state *h) {
 }
 static void main_again(str_state *h) { h->st = h->st_main; }
 static str_status join(str_state *h) {
+  if (h->timeline) return STR_OK;
   CU(cudaEventRecord(h->ev_join, h->st2));
   CU(cudaStreamWaitEvent(h->st, h->ev_join, 0));
   return STR_OK;
