@@ -3,20 +3,24 @@
 // 3xTF32 splitting for fp32-level accuracy.
 //
 // Math: the two passes of the exact two-pass schedule evaluate
-//   pass 1: Y_L[(l,t)][w] = sum_r X[l + L r + L Rr t] T_R[r][w]         A = X_t^T (M = l; loaded MN-major, transposed to K-major by the converters)
-//   pass 2: Y_R[r][w]     = sum_{l,t} X[l + L r + L Rr t] T_L[(l,t)][w]  A = X      (M = r, K-major)
+//   pass 1: Y_L[(l,t)][w] = sum_r X[l + L r + L Rr t] T_R[r][w]         A = X_t^T (M = l; MN-major tile)
+//   pass 2: Y_R[r][w]     = sum_{l,t} X[l + L r + L Rr t] T_L[(l,t)][w]  A = X      (M = r, K-major tile)
 // i.e. the products X^new_[n] G^{≠n}_[2] of Alg. 4 l.9 / l.14, grouped.
 // 3xTF32: A = A_hi + A_lo (A_hi = A with the low 13 mantissa bits cleared, A_lo = A - A_hi exact
 // in fp32), B = B_hi + B_lo (rounded from the fp64 table), and
-//   A B ~= A_hi [B_hi | B_lo] + A_lo B_hi      (two UMMAs per k-step, N = 2 Npad and Npad).
+//   A B ~= A_hi B_hi + A_hi B_lo + A_lo B_hi      (three UMMAs per k-step into one accumulator).
 //
-// Structure (one CTA per SM, persistent "stream-K" over units (M-tile, K-tile)):
-//   warp 0      TMA producer: X tile via cp.async.bulk.tensor (128B swizzle, OOB zero-fill) and
-//               the pre-tiled table block via cp.async.bulk, both on the stage's mbarrier
-//   warp 1      UMMA issuer (one thread): 4 k-steps x 2 tcgen05.mma per stage, commit -> empty
-//   warp 2      TMEM allocator (512 columns: two accumulator buffers)
-//   warps 4-7   split converters: A_hi / A_lo (K-major) in shared memory, fence.proxy.async, arrive
-//   warps 8-11  epilogue: tcgen05.ld the accumulator, hi+lo sum, fp32 red.add into Y
+// Structure (one CTA per SM, persistent "stream-K" over units (M-block of 256 rows, K-tile of 32)):
+//   warp 0       TMA producer: the two 128-row X tiles (cp.async.bulk.tensor, 128B swizzle, OOB
+//                zero-fill) and the pre-tiled hi/lo table block (cp.async.bulk) on one mbarrier
+//   warp 1       UMMA issuer (one thread): per M-tile and k-step 3 x tcgen05.mma.kind::tf32 with A
+//                from TMEM (A_hi | A_lo) and B from shared memory (B_hi | B_lo); one B stage feeds
+//                both M-tiles, halving the table traffic per FLOP
+//   warp 2       TMEM allocator (512 columns: 2 accumulators of Npad, 2 slots of A_hi|A_lo per M-tile)
+//   warps 4-11   split converters: each thread reads its X row from the stage, splits hi / lo and
+//                writes them to TMEM (tcgen05.st), so neither the split operands nor the MMA's A
+//                reads touch shared memory
+//   warps 12-15  epilogue: tcgen05.ld the accumulators, fp32 red.add into Y (stream-K partials)
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -33,35 +37,100 @@
 
 namespace strb200 {
 
-constexpr int kTcThreads = 384;
+constexpr int kTcThreads = 512;
 constexpr int kBM = 128;       // UMMA M
+constexpr int kMT = 2;         // M-tiles per CTA (share every B stage)
 constexpr int kBK = 32;        // K per stage (one 128-byte swizzle row of fp32)
-constexpr int kABytes = kBM * kBK * 4;   // 16 KB
+constexpr int kABytes = kBM * kBK * 4;   // 16 KB per X tile
+constexpr uint32_t kAccCols = 256;       // accumulators at [0, 256): M-tile mt at mt * 128
+constexpr uint32_t kASlot0 = 256;        // A slots at [256, 512): slot a, M-tile mt at 256 + (2a + mt) * 64
 
 struct TcParams {
   int64_t L, Rr, tn;
-  int W, Npad, stages;
-  int mb_per_t;    // pass 1: ceil(L/128) M-tiles per t
+  int W, Npad, stages, bstages;   // X ring / table ring depths
+  int mb_per_t;    // pass 1: ceil(L/256) M-blocks per t
   int nlb;         // pass 2: ceil(L/32) K-tiles per t
   int64_t KT, U, upc;
   const float *Btiles;   // [KT][2 Npad rows][32 k] fp32, 128B-swizzled K-major blocks
   float *Y;              // fp32 output rows (zeroed), row stride W
+  long long *dbg;        // optional pipeline trace of CTA 0 (diagnostic; nullptr in production)
+  int dbg_flags;         // diagnostic: bit0 skip table loads, bit1 skip X loads, bit2 skip TMEM stores, bit3 one commit per unit, bit4 spin waits, bit5 converters skip smem reads (wrong results)
 };
+
+__device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,"
+      "%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]), "r"(v[9]),
+      "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]), "r"(v[16]), "r"(v[17]), "r"(v[18]),
+      "r"(v[19]), "r"(v[20]), "r"(v[21]), "r"(v[22]), "r"(v[23]), "r"(v[24]), "r"(v[25]), "r"(v[26]), "r"(v[27]),
+      "r"(v[28]), "r"(v[29]), "r"(v[30]), "r"(v[31])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,"
+      "%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+__device__ __forceinline__ void tmem_st_wait() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+// D[tmem] (+)= A[tmem] * B[smem], kind::tf32 (fp32 accumulate), one CTA.  Executed by a whole
+// warp with warp-uniform operands (kept in uniform registers); one elected lane issues.
+__device__ __forceinline__ void mma_tf32_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc, uint32_t idesc,
+                                            uint32_t accumulate) {
+  asm volatile(
+      "{\n\t.reg .pred p, e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "@e tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accumulate)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_elect(uint64_t *bar) {
+  asm volatile(
+      "{\n\t.reg .pred e;\n\t"
+      "elect.sync _|e, 0xffffffff;\n\t"
+      "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(tc::smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ long long gtimer() {
+  long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 template <int PASS>
 __global__ void __launch_bounds__(kTcThreads, 1)
     k_contract_tf32(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
+  if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // X ring (HBM stream; slots freed by the converters as soon as the tile is in TMEM) and a
+  // shallower table ring (L2-resident; slots freed by the MMA commit).
   const int BBYTES = 2 * p.Npad * 128;
-  const int STAGE = 2 * kABytes + BBYTES;
-  const int S = p.stages;
-  uint64_t *full = (uint64_t *)(smem + (size_t)S * STAGE);
-  uint64_t *conv = full + S;
-  uint64_t *empty = conv + S;
-  uint64_t *accf = empty + S;
-  uint64_t *acce = accf + 2;
-  uint32_t *tslot = (uint32_t *)(acce + 2);
+  const int XSTAGE = kMT * kABytes;
+  const int SX = p.stages, SB = p.bstages;
+  uint8_t *xbuf = smem;
+  uint8_t *bbuf = smem + (size_t)SX * XSTAGE;
+  uint64_t *xfull = (uint64_t *)(bbuf + (size_t)SB * BBYTES);
+  uint64_t *xempty = xfull + SX;
+  uint64_t *bfull = xempty + SX;
+  uint64_t *bempty = bfull + SB;
+  uint64_t *conv = bempty + SB;    // [2] A slot filled (converters -> MMA)
+  uint64_t *aempty = conv + 2;     // [2] A slot free   (MMA -> converters)
+  uint64_t *accf = aempty + 2;     // accumulators complete (MMA -> epilogue)
+  uint64_t *acce = accf + 1;       // accumulators drained  (epilogue -> MMA)
+  uint32_t *tslot = (uint32_t *)(acce + 1);
 
   const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
   const int64_t u0 = (int64_t)blockIdx.x * p.upc;
@@ -69,207 +138,282 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (u0 >= u1) return;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < S; ++s) {
-      tc::mbar_init(&full[s], 1);
-      tc::mbar_init(&conv[s], 128);
-      tc::mbar_init(&empty[s], 1);
+    for (int s = 0; s < SX; ++s) {
+      tc::mbar_init(&xfull[s], 1);
+      tc::mbar_init(&xempty[s], 8);    // one arrival per converter warp
     }
-    for (int b = 0; b < 2; ++b) {
-      tc::mbar_init(&accf[b], 1);
-      tc::mbar_init(&acce[b], 128);
+    for (int s = 0; s < SB; ++s) {
+      tc::mbar_init(&bfull[s], 1);
+      tc::mbar_init(&bempty[s], 1);
     }
+    for (int a = 0; a < 2; ++a) {
+      tc::mbar_init(&conv[a], 8);
+      tc::mbar_init(&aempty[a], 1);
+    }
+    tc::mbar_init(accf, 1);
+    tc::mbar_init(acce, 4);          // one arrival per epilogue warp
     tc::fence_barrier_init();
     tc::prefetch_tmap(&tmap);
   }
   if (warp == 2) tc::tmem_alloc(tslot, 512);
+  if (p.W < p.Npad) {   // table padding rows are never loaded: zero them once (read by the MMA)
+    for (int i = threadIdx.x; i < SB * BBYTES / 16; i += blockDim.x) ((float4 *)bbuf)[i] = make_float4(0, 0, 0, 0);
+    tc::fence_proxy_async_smem();
+  }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = *tslot;
+  if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 1] = gtimer();
 
-  if (warp == 0) {
+  if ((p.dbg_flags & 256) && warp != 1 && !(p.dbg_flags & 512)) {
+    // diagnostic mode: every other role idles (with bit 9 they run their loops)
+  } else if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      int s = 0;
-      uint32_t ph = 0;
-      for (int64_t u = u0; u < u1; ++u) {
-        tc::mbar_wait(&empty[s], ph ^ 1);
-        const int64_t tile = u / p.KT, kt = u % p.KT;
-        uint8_t *A = smem + (size_t)s * STAGE;
-        uint8_t *B = A + 2 * kABytes;
-        tc::mbar_arrive_expect_tx(&full[s], kABytes + BBYTES);
-        if (PASS == 1) {
-          const int t = (int)(tile / p.mb_per_t), mb = (int)(tile % p.mb_per_t);
-#pragma unroll
-          for (int j = 0; j < 4; ++j) tc::tma_load_3d(A + j * 4096, &tmap, &full[s], mb * kBM + 32 * j, (int)kt * kBK, t);
+      int sx = 0, sb = 0;
+      uint32_t phx = 0, phb = 0;
+      int mblk = (int)(u0 / p.KT), kt = (int)(u0 % p.KT);   // 32-bit, advanced incrementally
+      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0, ++mblk) : 0) {
+        tc::mbar_wait(&xempty[sx], phx ^ 1);
+        if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 0] = clock64();
+        uint8_t *A = xbuf + (size_t)sx * XSTAGE;
+        if (p.dbg_flags & 2) {
+          tc::mbar_arrive(&xfull[sx]);
         } else {
-          const int t = (int)(kt / p.nlb), lb = (int)(kt % p.nlb);
-          tc::tma_load_3d(A, &tmap, &full[s], lb * kBK, (int)tile * kBM, t);
+        tc::mbar_arrive_expect_tx(&xfull[sx], kMT * kABytes);
+        if (PASS == 1) {
+          const int t = mblk / p.mb_per_t, mb = mblk - t * p.mb_per_t;
+#pragma unroll
+          for (int mt = 0; mt < kMT; ++mt)
+            tc::tma_load_3d(A + mt * kABytes, &tmap, &xfull[sx], (mb * kMT + mt) * kBM, (int)kt * kBK, t);
+        } else {
+          const int t = kt / p.nlb, lb = kt - t * p.nlb;
+#pragma unroll
+          for (int mt = 0; mt < kMT; ++mt)
+            tc::tma_load_3d(A + mt * kABytes, &tmap, &xfull[sx], lb * kBK, (int)(mblk * kMT + mt) * kBM, t);
         }
-        tc::bulk_load(B, p.Btiles + kt * (int64_t)(BBYTES / 4), BBYTES, &full[s]);
-        if (++s == S) { s = 0; ph ^= 1; }
+        }
+        if (++sx == SX) { sx = 0; phx ^= 1; }
+        tc::mbar_wait(&bempty[sb], phb ^ 1);
+        if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 8] = clock64();
+        uint8_t *B = bbuf + (size_t)sb * BBYTES;
+        {   // only the W real rows of B_hi and B_lo travel; the padding rows stay zero in smem
+          const int rb = p.W * 128;
+          const uint8_t *src = (const uint8_t *)(p.Btiles + kt * (int64_t)(BBYTES / 4));
+          if (p.dbg_flags & 1) {
+            tc::mbar_arrive(&bfull[sb]);
+          } else {
+            tc::mbar_arrive_expect_tx(&bfull[sb], 2 * rb);
+            tc::bulk_load(B, src, rb, &bfull[sb]);
+            tc::bulk_load(B + p.Npad * 128, src + p.Npad * 128, rb, &bfull[sb]);
+          }
+        }
+        if (++sb == SB) { sb = 0; phb ^= 1; }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
+    {   // the whole warp walks the loop (warp-uniform operands); mma / commit elect one lane
       // ------------------------------------------------------------ UMMA issuer
-      const uint32_t idesc2 = tc::idesc_tf32(kBM, 2 * p.Npad, 0, 0);
-      const uint32_t idesc1 = tc::idesc_tf32(kBM, p.Npad, 0, 0);
-      int s = 0;
-      uint32_t ph = 0;
-      int seg = 0;
-      uint32_t use0 = 0, use1 = 0;
-      for (int64_t u = u0; u < u1; ++u) {
-        const bool first = (u == u0) || (u % p.KT == 0);
-        const bool last = (u == u1 - 1) || ((u + 1) % p.KT == 0);
-        const int buf = seg & 1;
+      const uint32_t idesc = tc::idesc_tf32(kBM, p.Npad, 0, 0);
+      if (p.dbg_flags & 256) {   // diagnostic: the bare MMA sequence, no waits (probe inside the kernel)
+        const uint32_t b0 = tc::smem_u32(bbuf);
+        long long t0 = clock64();
+        for (int64_t u = u0; u < u1; ++u) {
+          const int a = (int)(u & 1);
+#pragma unroll
+          for (int mt = 0; mt < kMT; ++mt) {
+            const uint32_t d = tbase + (uint32_t)(mt * 128);
+            const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * a + mt) * 64);
+#pragma unroll
+            for (int ks = 0; ks < kBK / 8; ++ks) {
+              const uint64_t bhi = tc::smem_desc_sw128(b0 + ks * 32, 16, 1024);
+              const uint64_t blo = tc::smem_desc_sw128(b0 + p.Npad * 128 + ks * 32, 16, 1024);
+              mma_tf32_ts(d, ahi + ks * 8, bhi, idesc, 1u);
+              mma_tf32_ts(d, ahi + ks * 8, blo, idesc, 1u);
+              mma_tf32_ts(d, ahi + 32 + ks * 8, bhi, idesc, 1u);
+            }
+          }
+          mma_commit_elect(&bempty[(int)((u - u0) % SB)]);
+          mma_commit_elect(&aempty[(int)((u - u0) & 1)]);
+        }
+        mma_commit_elect(accf);
+        tc::mbar_wait(accf, 0);
+        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2) p.dbg[63 * 16 + 0] = clock64() - t0;
+      } else {
+      int s = 0, a = 0;
+      uint32_t ph = 0, pha = 0, phe = 0;
+      int kt = (int)(u0 % p.KT);
+      // The commits of unit u are issued after the barrier waits of unit u+1 (deferred), so the
+      // waits do not queue behind the commit bookkeeping while unit u's MMAs still run.
+      int ps = -1, pa = 0;
+      bool plast = false;
+      auto flush = [&]() {
+        if (ps >= 0) {
+          mma_commit_elect(&bempty[ps]);
+          if (!(p.dbg_flags & 8)) mma_commit_elect(&aempty[pa]);
+          else if (lane == 0) tc::mbar_arrive(&aempty[pa]);
+          if (plast) mma_commit_elect(accf);
+          ps = -1;
+        }
+      };
+      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0) : 0) {   // s: table slot, a: TMEM A slot
+        const bool first = (u == u0) || (kt == 0);
+        const bool last = (u == u1 - 1) || (kt == (int)p.KT - 1);
         if (first) {
-          tc::mbar_wait(&acce[buf], ((buf ? use1 : use0) & 1) ^ 1);
+          flush();                         // the previous segment's accf must go out first
+          tc::mbar_wait(acce, phe ^ 1);   // previous segment drained by the epilogue
+          phe ^= 1;
           tc::tc_fence_after();
         }
-        tc::mbar_wait(&conv[s], ph);
+        // (the table block of this unit has landed: the converters arrive on conv only after bfull)
+        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 4] = clock64();
+        if (p.dbg_flags & 128) {} else if (p.dbg_flags & 16) tc::mbar_spin(&conv[a], pha); else tc::mbar_wait(&conv[a], pha);
+        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 5] = clock64();
+        flush();
         tc::tc_fence_after();
-        const uint32_t a_hi = tc::smem_u32(smem + (size_t)s * STAGE);
-        const uint32_t a_lo = a_hi + kABytes;
-        const uint32_t b0 = a_hi + 2 * kABytes;
-        const uint32_t d = tbase + (uint32_t)(buf * 256);
+        const uint32_t b0 = tc::smem_u32(bbuf + (size_t)s * BBYTES);
 #pragma unroll
-        for (int ks = 0; ks < kBK / 8; ++ks) {
-          // K-major (both passes): advance 32 B (8 fp32) inside the 128-byte swizzle row
-          const uint64_t ah = tc::smem_desc_sw128(a_hi + ks * 32, 16, 1024);
-          const uint64_t al = tc::smem_desc_sw128(a_lo + ks * 32, 16, 1024);
-          const uint64_t bd = tc::smem_desc_sw128(b0 + ks * 32, 16, 1024);
-          tc::mma_tf32(d, ah, bd, idesc2, (first && ks == 0) ? 0u : 1u);
-          tc::mma_tf32(d, al, bd, idesc1, 1u);
-        }
-        tc::mma_commit(&empty[s]);
-        if (last) {
-          tc::mma_commit(&accf[buf]);
-          if (buf) use1++; else use0++;
-          seg++;
-        }
-        if (++s == S) { s = 0; ph ^= 1; }
-      }
-    }
-  } else if (warp >= 4 && warp < 8) {
-    // -------------------------------------------------------------- 3xTF32 split converters
-    // Pass 2: the TMA tile is already K-major; split in place (hi) and into the lo buffer.
-    // Pass 1: the TMA tile is MN-major (4 boxes of [32 k][32 m]); each thread loads two 4x4
-    // blocks, the 128 converter threads sync on a named barrier, then hi / lo are written
-    // transposed into the K-major 128B-swizzled layout [128 m][32 k] (same as pass 2), so both
-    // passes feed the tensor core through K-major descriptors.
-    const int ct = threadIdx.x - 128;
-    int s = 0;
-    uint32_t ph = 0;
-    for (int64_t u = u0; u < u1; ++u) {
-      tc::mbar_wait(&full[s], ph);
-      uint8_t *abase = smem + (size_t)s * STAGE;
-      if (PASS == 2) {
-        float4 *a = (float4 *)abase;
-        float4 *alo = (float4 *)(abase + kABytes);
+        for (int mt = 0; mt < kMT; ++mt) {
+          const uint32_t d = tbase + (uint32_t)(mt * 128);
+          const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * a + mt) * 64);
 #pragma unroll
-        for (int i = ct; i < kABytes / 16; i += 128) {
-          float4 x = a[i], h, l;
-          h.x = __uint_as_float(__float_as_uint(x.x) & 0xFFFFE000u);
-          h.y = __uint_as_float(__float_as_uint(x.y) & 0xFFFFE000u);
-          h.z = __uint_as_float(__float_as_uint(x.z) & 0xFFFFE000u);
-          h.w = __uint_as_float(__float_as_uint(x.w) & 0xFFFFE000u);
-          l.x = x.x - h.x;
-          l.y = x.y - h.y;
-          l.z = x.z - h.z;
-          l.w = x.w - h.w;
-          a[i] = h;
-          alo[i] = l;
-        }
-      } else {
-        float v[2][4][4];   // [block][d = k offset][e = m offset]
-#pragma unroll
-        for (int bI = 0; bI < 2; ++bI) {
-          const int b = ct + 128 * bI;
-          const int kq = b % 8, mq = b / 8;             // 4x4 block: k = 4kq.., m = 4mq..
-          const int box = mq / 8, mc = mq % 8;          // m chunk inside the 32-wide box
-#pragma unroll
-          for (int d = 0; d < 4; ++d) {
-            const int k = 4 * kq + d;
-            const float4 x = *(const float4 *)(abase + box * 4096 + k * 128 + ((mc ^ (k % 8)) * 16));
-            v[bI][d][0] = x.x;
-            v[bI][d][1] = x.y;
-            v[bI][d][2] = x.z;
-            v[bI][d][3] = x.w;
+          for (int ks = 0; ks < kBK / 8; ++ks) {
+            const uint64_t bhi = tc::smem_desc_sw128(b0 + ks * 32, 16, 1024);
+            const uint64_t blo = tc::smem_desc_sw128(b0 + p.Npad * 128 + ks * 32, 16, 1024);
+            mma_tf32_ts(d, ahi + ks * 8, bhi, idesc, (first && ks == 0) ? 0u : 1u);
+            mma_tf32_ts(d, ahi + ks * 8, blo, idesc, 1u);
+            mma_tf32_ts(d, ahi + 32 + ks * 8, bhi, idesc, 1u);
           }
         }
-        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 6] = clock64();
+        if (p.dbg && lane == 0 && u == u1 - 1) p.dbg[1024 + blockIdx.x * 4 + 2] = gtimer();
+        ps = s;
+        pa = a;
+        plast = last;
+        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 7] = clock64();
+        if (++s == SB) { s = 0; ph ^= 1; }
+        if (++a == 2) { a = 0; pha ^= 1; }
+      }
+      flush();
+      }
+    }
+  } else if (warp >= 4 && warp < 12) {
+    // -------------------------------------------------------------- 3xTF32 split converters
+    // thread = row m of M-tile mt; reads its 32 k-values from the stage, writes hi / lo to TMEM.
+    const int mt = (warp - 4) / 4, q = warp % 4;
+    const int m = q * 32 + lane;
+    int s = 0, a = 0, sb = 0;
+    uint32_t ph = 0, pha = 0, phb = 0;
+    for (int64_t u = u0; u < u1; ++u) {   // s: X ring slot, a: TMEM A slot, sb: table ring slot
+      if (p.dbg_flags & 2048) tc::mbar_wait_sleep(&xfull[s], ph); else tc::mbar_wait(&xfull[s], ph);
+      if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 1] = clock64();
+      if (p.dbg_flags & 2048) tc::mbar_wait_sleep(&aempty[a], pha ^ 1); else tc::mbar_wait(&aempty[a], pha ^ 1);
+      if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 2] = clock64();
+      const uint8_t *xt = xbuf + (size_t)s * XSTAGE + mt * kABytes;
+      uint32_t hi[32], lo[32];
+      if (p.dbg_flags & 32) {
 #pragma unroll
-        for (int bI = 0; bI < 2; ++bI) {
-          const int b = ct + 128 * bI;
-          const int kq = b % 8, mq = b / 8;
+        for (int k = 0; k < 32; ++k) { hi[k] = 0; lo[k] = 0; }
+      } else if (PASS == 2) {
+        // K-major [128 m][32 k]: row m at m*128, 16-byte chunk c at (c ^ (m % 8))
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float4 x = *(const float4 *)(xt + m * 128 + ((c ^ (m & 7)) << 4));
+          const float xv[4] = {x.x, x.y, x.z, x.w};
 #pragma unroll
           for (int e = 0; e < 4; ++e) {
-            const int m = 4 * mq + e;
-            float4 h, l;
-            float *hp = &h.x, *lp = &l.x;
-#pragma unroll
-            for (int d = 0; d < 4; ++d) {
-              const float x = v[bI][d][e];
-              hp[d] = __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
-              lp[d] = x - hp[d];
-            }
-            const int off = m * 128 + ((kq ^ (m % 8)) * 16);
-            *(float4 *)(abase + off) = h;
-            *(float4 *)(abase + kABytes + off) = l;
+            const uint32_t h = __float_as_uint(xv[e]) & 0xFFFFE000u;
+            hi[4 * c + e] = h;
+            lo[4 * c + e] = __float_as_uint(xv[e] - __uint_as_float(h));
           }
         }
+      } else {
+        // MN-major [32 k][128 m], unswizzled: (k, m) at (k * 128 + m) * 4
+        const float *bx = (const float *)xt + m;
+#pragma unroll
+        for (int k = 0; k < 32; ++k) {
+          const float xv = bx[k * 128];
+          const uint32_t h = __float_as_uint(xv) & 0xFFFFE000u;
+          hi[k] = h;
+          lo[k] = __float_as_uint(xv - __uint_as_float(h));
+        }
       }
-      tc::fence_proxy_async_smem();
-      tc::mbar_arrive(&conv[s]);
-      if (++s == S) { s = 0; ph ^= 1; }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&xempty[s]);   // the X slot is free once the tile sits in registers
+      const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + kASlot0 + (uint32_t)((2 * a + mt) * 64);
+      if (!(p.dbg_flags & 4)) {
+        tmem_st32(ta, hi);
+        tmem_st32(ta + 32, lo);
+        tmem_st_wait();
+      }
+      tc::tc_fence_before();
+      if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 3] = clock64();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&conv[a]);
+      if (++s == SX) { s = 0; ph ^= 1; }
+      if (++a == 2) { a = 0; pha ^= 1; }
     }
-  } else if (warp >= 8) {
+  } else if (warp >= 12) {
     // -------------------------------------------------------------- epilogue
     const int q = warp % 4;
     const int row = q * 32 + lane;
-    int seg = 0;
+    uint32_t phf = 0;
     int64_t u = u0;
     while (u < u1) {
-      const int64_t tile = u / p.KT;
-      const int64_t uend = ((tile + 1) * p.KT < u1) ? (tile + 1) * p.KT : u1;
-      const int buf = seg & 1;
-      tc::mbar_wait(&accf[buf], (uint32_t)((seg >> 1) & 1));
+      const int64_t mblk = u / p.KT;
+      const int64_t uend = ((mblk + 1) * p.KT < u1) ? (mblk + 1) * p.KT : u1;
+      if (p.dbg_flags & 1024) tc::mbar_wait_sleep(accf, phf); else tc::mbar_wait(accf, phf);
+      phf ^= 1;
       tc::tc_fence_after();
-      int64_t yrow;
-      bool valid;
-      if (PASS == 1) {
-        const int64_t t = tile / p.mb_per_t, mb = tile % p.mb_per_t;
-        const int64_t l = mb * kBM + row;
-        valid = l < p.L;
-        yrow = l + p.L * t;
-      } else {
-        const int64_t r = tile * kBM + row;
-        valid = r < p.Rr;
-        yrow = r;
-      }
-      const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(buf * 256);
-      float *yr = p.Y + yrow * p.W;
-      for (int c0 = 0; c0 < p.Npad; c0 += 16) {
-        float hi[16], lo[16];
-        tc::tmem_ld16(taddr + c0, hi);
-        tc::tmem_ld16(taddr + p.Npad + c0, lo);
-        if (valid) {
-          if ((p.W & 3) == 0 && c0 + 16 <= p.W) {
 #pragma unroll
-            for (int i = 0; i < 16; i += 4)
-              atomicAdd((float4 *)(yr + c0 + i),
-                        make_float4(hi[i] + lo[i], hi[i + 1] + lo[i + 1], hi[i + 2] + lo[i + 2], hi[i + 3] + lo[i + 3]));
+      for (int mt = 0; mt < kMT; ++mt) {
+        int64_t yrow;
+        bool valid;
+        if (PASS == 1) {
+          const int64_t t = mblk / p.mb_per_t, mb = mblk % p.mb_per_t;
+          const int64_t l = (mb * kMT + mt) * kBM + row;
+          valid = l < p.L;
+          yrow = l + p.L * t;
+        } else {
+          const int64_t r = (mblk * kMT + mt) * kBM + row;
+          valid = r < p.Rr;
+          yrow = r;
+        }
+        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * 128);
+        float *yr = p.Y + yrow * p.W;
+        for (int c0 = 0; c0 < p.Npad; c0 += 32) {
+          float v[32];
+          if (c0 + 32 <= p.Npad) {
+            tmem_ld32(taddr + c0, v);
           } else {
+            float w16[16];
+            tc::tmem_ld16(taddr + c0, w16);
 #pragma unroll
-            for (int i = 0; i < 16; ++i)
-              if (c0 + i < p.W) atomicAdd(yr + c0 + i, hi[i] + lo[i]);
+            for (int i = 0; i < 16; ++i) v[i] = w16[i];
+#pragma unroll
+            for (int i = 16; i < 32; ++i) v[i] = 0.0f;
+          }
+          if (valid) {
+            if ((p.W & 3) == 0 && c0 + 32 <= p.W) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                atomicAdd((float4 *)(yr + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+            } else if ((p.W & 3) == 0) {
+#pragma unroll
+              for (int i = 0; i < 32; i += 4)
+                if (c0 + i < p.W) atomicAdd((float4 *)(yr + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
+            } else {
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                if (c0 + i < p.W) atomicAdd(yr + c0 + i, v[i]);
+            }
           }
         }
       }
       tc::tc_fence_before();
-      tc::mbar_arrive(&acce[buf]);
-      seg++;
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(acce);
       u = uend;
     }
   }
@@ -277,6 +421,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   if (warp == 2) tc::tmem_dealloc(tbase, 512);
+  if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 3] = gtimer();
 }
 
 }  // namespace strb200
@@ -314,6 +459,7 @@ str_status tf32_prepare(str_state *h) {
   if (!attr) {
     cudaFuncSetAttribute(k_contract_tf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_contract_tf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    // (Npad <= 128 keeps 2 Npad x 128 B of table per stage; 3 stages fit)
     attr = true;
   }
   h->tf32_ready = true;
@@ -352,11 +498,13 @@ static bool encode_x_map(str_state *h, CUtensorMap *tmap, const void *X, int pas
   const int64_t L = h->L, Rr = h->Rr;
   cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)Rr, (cuuint64_t)tn};
   cuuint64_t strides[2] = {(cuuint64_t)L * 4, (cuuint64_t)L * Rr * 4};
-  cuuint32_t box[3] = {32, (cuuint32_t)(pass == 1 ? 32 : 128), 1};
+  // pass 1: one [32 k][128 m] box per M-tile, unswizzled (only the converters read it: lanes take
+  // consecutive m, conflict-free); pass 2: one [128 m][32 k] box, 128B-swizzled (lanes take rows)
+  cuuint32_t box[3] = {(cuuint32_t)(pass == 1 ? 128 : 32), (cuuint32_t)(pass == 1 ? 32 : 128), 1};
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void *>(X), dims, strides, box, es,
-                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, pass == 1 ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) {
     h->err = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
     return false;
@@ -399,11 +547,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.tn = tn;
   p.W = W;
   p.Npad = Np;
-  const int stage_bytes = 2 * kABytes + 2 * Np * 128;
-  p.stages = std::min(6, (int)((220 * 1024 - 1024 - 256) / stage_bytes));
-  p.mb_per_t = (int)cdiv(L, kBM);
+  const int bbytes = 2 * Np * 128;
+  p.bstages = 4;
+  p.stages = std::min(6, (int)((224 * 1024 - 1024 - 256 - p.bstages * bbytes) / (kMT * kABytes)));
+  p.mb_per_t = (int)cdiv(L, kMT * kBM);
   p.nlb = (int)cdiv(L, 32);
-  const int64_t tiles = pass == 1 ? (int64_t)p.mb_per_t * tn : cdiv(Rr, kBM);
+  const int64_t tiles = pass == 1 ? (int64_t)p.mb_per_t * tn : cdiv(Rr, kMT * kBM);
   p.KT = pass == 1 ? cdiv(Rr, kBK) : tn * p.nlb;
   p.U = tiles * p.KT;
   int grid = (int)std::min<int64_t>(148, p.U);
@@ -411,10 +560,16 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   grid = (int)cdiv(p.U, p.upc);
   p.Btiles = (const float *)h->tab_split.p;
   p.Y = Y;
+  p.dbg = h->tf_dbg;
+  p.dbg_flags = 0;
+  if (h->tf_dbg) {
+    const char *ev = getenv("STR_TF_DBGFLAGS");
+    if (ev) p.dbg_flags = atoi(ev);
+  }
   const int64_t M = pass == 1 ? L * tn : Rr;
   cudaMemsetAsync(p.Y, 0, (size_t)M * W * sizeof(float), st);
   tl_mark(h, "memset", 0);
-  const size_t smem = (size_t)p.stages * stage_bytes + 1024 + 256;
+  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + 1024 + 256;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
   if (h->profiling) {
     cudaEventCreate(&e0);

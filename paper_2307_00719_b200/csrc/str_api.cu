@@ -1015,6 +1015,24 @@ extern "C" str_status str_set_profiling(str_state *h, int32_t enable) {
   return STR_OK;
 }
 
+// Contraction pipeline trace (diagnostic, not in include/str.h): enable allocates a device buffer
+// the tensor-core kernel fills for CTA 0 (per unit: producer / converter / MMA timestamps).
+extern "C" STR_API str_status strdbg_tftrace(str_state *h, int32_t enable, long long *host_out) {
+  if (!h) return STR_E_ARG;
+  cudaStreamSynchronize(h->st);
+  if (enable) {
+    if (!h->tf_dbg) {
+      CU(cudaMalloc(&h->tf_dbg, (1024 + 4 * 160) * sizeof(long long)));
+    }
+    CU(cudaMemset(h->tf_dbg, 0, (1024 + 4 * 160) * sizeof(long long)));
+  } else if (h->tf_dbg) {
+    if (host_out) CU(cudaMemcpy(host_out, h->tf_dbg, (1024 + 4 * 160) * sizeof(long long), cudaMemcpyDeviceToHost));
+    cudaFree(h->tf_dbg);
+    h->tf_dbg = nullptr;
+  }
+  return STR_OK;
+}
+
 // Launch timeline (diagnostic, not in include/str.h): enable clears it; dump aggregates the
 // in-stream time between consecutive marks per kernel name as "name total_ms count" lines.
 extern "C" STR_API str_status strdbg_timeline(str_state *h, int32_t enable) {

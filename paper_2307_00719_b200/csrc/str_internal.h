@@ -92,6 +92,7 @@ struct str_state {
   int tf_grid[2] = {0, 0};
   size_t tf_smem[2] = {0, 0};
   bool capturing = false;
+  long long *tf_dbg = nullptr;      // device buffer for the contraction pipeline trace (diagnostic)
 
   // rSTR
   DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev;

@@ -34,8 +34,35 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t addr, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+__device__ __forceinline__ bool mbar_test(uint32_t addr, uint32_t parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+      "selp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(ok)
+      : "r"(addr), "r"(parity)
+      : "memory");
+  return ok != 0;
+}
+// Spin with the non-blocking test (for the single MMA-issuing thread).
+__device__ __forceinline__ void mbar_spin(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  while (!mbar_test(a, parity)) {
+  }
+}
+// Wait with exponential nanosleep back-off (roles off the critical path).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t *bar, uint32_t parity) {
+  const uint32_t a = smem_u32(bar);
+  uint32_t ns = 32;
+  while (!mbar_try_wait(a, parity)) {
+    __nanosleep(ns);
+    if (ns < 256) ns <<= 1;
+  }
+}
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
   const uint32_t a = smem_u32(bar);
+  if (mbar_test(a, parity)) return;   // fast path: phase already complete (non-blocking probe)
   while (!mbar_try_wait(a, parity)) {
   }
 }

@@ -1,4 +1,1 @@
-cd tools/micro && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -I../../include -I../../paper_2307_00719_b200/csrc -o /tmp/chain_bench chain_bench.cu && /tmp/chain_bench 100 40
-timeout 300 ncu --set full --import-source on --warp-sampling-interval 0 --clock-control none -k regex:k_build_table2 -s 5 -c 1 -o gpurun_out/prof_tab /tmp/chain_bench 100 40 > gpurun_out/ncu_tab.log 2>&1; \
-timeout 300 ncu --set full --import-source on --warp-sampling-interval 0 --clock-control none -k regex:k_absorb4 -s 112 -c 1 -o gpurun_out/prof_abs4 /tmp/chain_bench 100 40 > gpurun_out/ncu_abs4.log 2>&1; \
-timeout 300 ncu --set full --import-source on --warp-sampling-interval 0 --clock-control none -k regex:k_chain_gemm -s 60 -c 1 -o gpurun_out/prof_gemm /tmp/chain_bench 100 40 > gpurun_out/ncu_gemm.log 2>&1; ls gpurun_out
+cd tools/micro && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -o /tmp/umma_probe2 umma_probe2.cu && timeout 60 /tmp/umma_probe2
