@@ -132,7 +132,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t *acce = accf + 1;       // accumulators drained  (epilogue -> MMA)
   uint32_t *tslot = (uint32_t *)(acce + 1);
 
-  const int warp = threadIdx.x / 32, lane = threadIdx.x % 32;
+  // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform and the
+  // MMA warp keeps its descriptors / TMEM addresses in uniform registers (no per-MMA R2UR)
+  const int warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x / 32), 0), lane = threadIdx.x % 32;
   const int64_t u0 = (int64_t)blockIdx.x * p.upc;
   const int64_t u1 = (u0 + p.upc < p.U) ? (u0 + p.upc) : p.U;
   if (u0 >= u1) return;
@@ -157,13 +159,19 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
   if (warp == 2) tc::tmem_alloc(tslot, 512);
   if (p.W < p.Npad) {   // table padding rows are never loaded: zero them once (read by the MMA)
-    for (int i = threadIdx.x; i < SB * BBYTES / 16; i += blockDim.x) ((float4 *)bbuf)[i] = make_float4(0, 0, 0, 0);
+    const int prow = p.Npad - p.W;                       // padding rows per half, 128 B each
+    const int per = 2 * prow * 8;                        // float4 per slot
+    for (int i = threadIdx.x; i < SB * per; i += blockDim.x) {
+      const int slot = i / per, r = i % per, half = r / (prow * 8), w = r % (prow * 8);
+      ((float4 *)(bbuf + (size_t)slot * BBYTES + (size_t)half * p.Npad * 128 + (size_t)p.W * 128))[w] =
+          make_float4(0, 0, 0, 0);
+    }
     tc::fence_proxy_async_smem();
   }
   tc::tc_fence_before();
   __syncthreads();
   tc::tc_fence_after();
-  const uint32_t tbase = *tslot;
+  const uint32_t tbase = __shfl_sync(0xffffffffu, *tslot, 0);
   if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 1] = gtimer();
 
   if ((p.dbg_flags & 256) && warp != 1 && !(p.dbg_flags & 512)) {
@@ -251,8 +259,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       auto flush = [&]() {
         if (ps >= 0) {
           mma_commit_elect(&bempty[ps]);
-          if (!(p.dbg_flags & 8)) mma_commit_elect(&aempty[pa]);
-          else if (lane == 0) tc::mbar_arrive(&aempty[pa]);
           if (plast) mma_commit_elect(accf);
           ps = -1;
         }
@@ -288,6 +294,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         }
         if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 6] = clock64();
         if (p.dbg && lane == 0 && u == u1 - 1) p.dbg[1024 + blockIdx.x * 4 + 2] = gtimer();
+        mma_commit_elect(&aempty[a]);    // the converters may refill this A slot as soon as possible
         ps = s;
         pa = a;
         plast = last;
