@@ -25,6 +25,9 @@ void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
 void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);
 int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaStream_t s);
+int launch_gemm_sk(const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj, double *C,
+                   int M, int N, int64_t K, int acc, double *ws, cudaStream_t s, int sym = 0);
+size_t gemm_sk_ws_doubles(int M, int N, int64_t K);
 void launch_axpy_any(const void *x, bool x_f32, double *y, int64_t n, int accumulate, cudaStream_t s);
 
 // kernels_contract_f64.cu

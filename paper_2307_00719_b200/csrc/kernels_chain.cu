@@ -712,6 +712,89 @@ void launch_axpy_any(const void *x, bool x_f32, double *y, int64_t n, int accumu
     k_axpy_any<double><<<(unsigned)cdiv(n, 256), 256, 0, s>>>((const double *)x, y, n, accumulate);
 }
 
+// ------------------------------------------------------------------------------------------
+// Split-K fp64 GEMM with strided operands (rSTR sampled normal equations, Alg. 7 l.15-16:
+// P_n += X_S G_S, Q_n += G_S^T G_S, temporal G_S^T G_S and X_S[N] G_S with K = m sampled rows):
+//   part[ks][i][j] = sum_{k in range ks} A(i, k) B(k, j),  A(i,k) = A[i sai + k sak], B(k,j) = B[k sbk + j sbj]
+// One 32x32 output tile per CTA and K-range; chunks of 32 k staged in shared memory by cp.async;
+// then k_reduce_sk sums the KS partials in a fixed order into C (= or +=): deterministic.
+constexpr int kSkKC = 32;
+
+__global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, int64_t sai, int64_t sak,
+                                                 const double *__restrict__ B, int64_t sbk, int64_t sbj, int M, int N,
+                                                 int64_t K, int64_t kper, double *__restrict__ part) {
+  __shared__ __align__(16) double As[kSkKC][32], Bs[kSkKC][32];
+  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
+  const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
+  const int64_t k0 = (int64_t)blockIdx.z * kper;
+  const int64_t k1 = (k0 + kper < K) ? k0 + kper : K;
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  for (int64_t kc = k0; kc < k1; kc += kSkKC) {
+    __syncthreads();
+    for (int e = threadIdx.x; e < 32 * kSkKC; e += 256) {
+      const int kk = e >> 5, r = e & 31;
+      const int64_t k = kc + kk;
+      if (k < k1 && row0 + r < M) cp_async8(&As[kk][r], A + (int64_t)(row0 + r) * sai + k * sak);
+      else As[kk][r] = 0.0;
+      if (k < k1 && col0 + r < N) cp_async8(&Bs[kk][r], B + k * sbk + (int64_t)(col0 + r) * sbj);
+      else Bs[kk][r] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
+#pragma unroll 8
+    for (int kk = 0; kk < kSkKC; ++kk) {
+      const double b = Bs[kk][tx];
+      const double2 a01 = *(const double2 *)&As[kk][4 * ty];
+      const double2 a23 = *(const double2 *)&As[kk][4 * ty + 2];
+      acc[0] = fma(a01.x, b, acc[0]);
+      acc[1] = fma(a01.y, b, acc[1]);
+      acc[2] = fma(a23.x, b, acc[2]);
+      acc[3] = fma(a23.y, b, acc[3]);
+    }
+  }
+  double *pp = part + (int64_t)blockIdx.z * M * N;
+#pragma unroll
+  for (int u = 0; u < 4; ++u) {
+    const int row = row0 + 4 * ty + u, col = col0 + tx;
+    if (row < M && col < N) pp[(int64_t)row * N + col] = acc[u];
+  }
+}
+
+// sym (square C only): C[i][j] (+)= (S[i][j] + S[j][i]) / 2 — the (A + A^T)/2 of reading R5 applied
+// to the increment (equal to symmetrizing the sum when C is symmetric).
+__global__ void k_reduce_sk(const double *__restrict__ part, int KS, int64_t n, int N, double *__restrict__ C, int acc,
+                            int sym) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double s = 0.0;
+  for (int k = 0; k < KS; ++k) s += part[k * n + i];
+  if (sym) {
+    const int64_t r = i / N, c = i % N;
+    double t = 0.0;
+    for (int k = 0; k < KS; ++k) t += part[k * n + c * N + r];
+    s = 0.5 * (s + t);
+  }
+  C[i] = acc ? C[i] + s : s;
+}
+
+size_t gemm_sk_ws_doubles(int M, int N, int64_t K) {
+  (void)K;
+  return (size_t)32 * M * N;   // up to 32 K-splits
+}
+
+int launch_gemm_sk(const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj, double *C,
+                   int M, int N, int64_t K, int acc, double *ws, cudaStream_t s, int sym) {
+  const int tiles = (int)(cdiv(M, 32) * cdiv(N, 32));
+  int KS = (int)std::min<int64_t>(32, std::max<int64_t>(1, std::min<int64_t>(cdiv(2 * 148, tiles), cdiv(K, 64))));
+  const int64_t kper = cdiv(cdiv(K, KS), kSkKC) * kSkKC;
+  KS = (int)cdiv(K, kper);
+  dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32), (unsigned)KS);
+  k_gemm_sk<<<grid, 256, 0, s>>>(A, sai, sak, B, sbk, sbj, M, N, K, kper, ws);
+  const int64_t n = (int64_t)M * N;
+  k_reduce_sk<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(ws, KS, n, N, C, acc, sym);
+  return 2;
+}
+
 // Dynamic shared-memory opt-ins, done once outside any stream capture.
 void prepare_kernel_attrs() {
   static bool done = false;

@@ -61,39 +61,6 @@ __global__ void k_gather_fibers(const T *__restrict__ X, const int32_t *__restri
   XS[e] = (double)X[off];
 }
 
-// C[M][N] (+)= sum_k A(i,k) B(k,j) with strided operands (fp64), 16x16 tiles.
-__global__ void k_gemm_strided(const double *__restrict__ A, int64_t sai, int64_t sak, const double *__restrict__ B,
-                               int64_t sbk, int64_t sbj, double *__restrict__ C, int M, int N, int64_t K,
-                               int accumulate) {
-  __shared__ double As[16][17], Bs[16][17];
-  int tx = threadIdx.x, ty = threadIdx.y;
-  int row = blockIdx.y * 16 + ty, col = blockIdx.x * 16 + tx;
-  double acc = 0.0;
-  for (int64_t k0 = 0; k0 < K; k0 += 16) {
-    As[ty][tx] = (row < M && k0 + tx < K) ? A[row * sai + (k0 + tx) * sak] : 0.0;
-    Bs[ty][tx] = (k0 + ty < K && col < N) ? B[(k0 + ty) * sbk + col * sbj] : 0.0;
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < 16; ++kk) acc = fma(As[ty][kk], Bs[kk][tx], acc);
-    __syncthreads();
-  }
-  if (row < M && col < N) {
-    double *c = C + (int64_t)row * N + col;
-    *c = accumulate ? *c + acc : acc;
-  }
-}
-
-// Symmetrize: Q = (Q + Q^T)/2 (reading R5).
-__global__ void k_symmetrize(double *Q, int S) {
-  int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= S * S) return;
-  int x = e / S, y = e % S;
-  if (y <= x) return;
-  double v = 0.5 * (Q[x * S + y] + Q[y * S + x]);
-  Q[x * S + y] = v;
-  Q[y * S + x] = v;
-}
-
 // p_i = (sum_c Y[i][c] G[i][c]) / rank   (leverage of row i, Def. 8 via g_i^T (G^T G)^{-1} g_i)
 __global__ void k_rowdot_scale(const double *__restrict__ Y, const double *__restrict__ G, int64_t I, int S,
                                double inv_rank, double *__restrict__ p) {
@@ -183,10 +150,9 @@ static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
 }
 
 static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj,
-                 double *C, int M, int N, int64_t K, int acc) {
-  dim3 blk(16, 16), grd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
-  k_gemm_strided<<<grd, blk, 0, h->st>>>(A, sai, sak, B, sbk, sbj, C, M, N, K, acc);
-  tl_mark(h, "k_gemm_strided");
+                 double *C, int M, int N, int64_t K, int acc, int sym = 0) {
+  const int nl = launch_gemm_sk(A, sai, sak, B, sbk, sbj, C, M, N, K, acc, (double *)h->sSk.p, h->st, sym);
+  tl_mark(h, "gemm_sk", nl);
 }
 
 // Core k's slices as G(2) rows: k < N -> current core; k == N -> temporal rows [t0, t0 + rows).
@@ -235,9 +201,12 @@ static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) 
     draw_weighted(h->seed, h->tau, k, h->N, p, h->m, ix);
   }
   int32_t *dix = (int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
-  RCU(cudaMemcpyAsync(dix, ix.data(), sizeof(int32_t) * h->m, cudaMemcpyHostToDevice, h->st));
-  // pageable source: make sure the copy has consumed `ix` before it can change
-  RCU(cudaStreamSynchronize(h->st));
+  // pinned staging slot per mode: wait only until the previous upload from this slot has run
+  int32_t *slot = h->idx_pinned + (int64_t)(k - 1) * h->m;
+  RCU(cudaEventSynchronize(h->idx_ev[k]));
+  std::copy(ix.begin(), ix.end(), slot);
+  RCU(cudaMemcpyAsync(dix, slot, sizeof(int32_t) * h->m, cudaMemcpyHostToDevice, h->st));
+  RCU(cudaEventRecord(h->idx_ev[k], h->st));
   ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
   double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
   k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
@@ -268,8 +237,16 @@ static str_status sampled_chain(str_state *h, int n, double *out) {
     f.stride = 1;
     fl.f[fl.n++] = f;
   }
-  launch_build_table(fl, h->m, out, h->st);
-  tl_mark(h, "build_table");
+  TableDesc td;
+  td.fl = fl;
+  td.Lk = h->m;
+  td.tk = 1;
+  td.Npad = 0;
+  if (launch_build_table2(td, out, nullptr, h->st) != 0) {
+    h->err = "sampled chain needs too much shared memory";
+    return STR_E_ARG;
+  }
+  tl_mark(h, "table_sampled");
   return STR_OK;
 }
 
@@ -296,6 +273,10 @@ static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, 
 }
 
 static str_status rstr_workspace(str_state *h, int64_t tn) {
+  if (!h->idx_pinned) {
+    RCU(cudaMallocHost(&h->idx_pinned, sizeof(int32_t) * h->N * h->m));
+    for (int k = 0; k <= h->N; ++k) RCU(cudaEventCreateWithFlags(&h->idx_ev[k], cudaEventDisableTiming));
+  }
   int64_t maxI = tn;
   int maxS = 0;
   for (auto &mb : h->md) {
@@ -308,6 +289,7 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
   RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS));
   RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS));   // G_S[2]
   RTRY(ensure_dev(h, h->sGram, sizeof(double) * maxS * maxS));
+  RTRY(ensure_dev(h, h->sSk, sizeof(double) * gemm_sk_ws_doubles((int)std::max<int64_t>(maxI, maxS), maxS, h->m)));
   RTRY(ensure_dev(h, h->Mt, sizeof(double) * std::max<int64_t>(maxI, tn) * maxS));
   for (auto &mb : h->md) RTRY(ensure_dev(h, mb.samp, sizeof(double) * h->m * mb.Ra * mb.Rb));
   return STR_OK;
@@ -323,9 +305,7 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   RTRY(sampled_chain(h, n, GS));
   RTRY(gather_fibers(h, X, n, tn, XS));
   gemm(h, XS, h->m, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, h->m, acc);
-  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, h->m, acc);
-  k_symmetrize<<<(unsigned)cdiv(S * S, 256), 256, 0, h->st>>>((double *)mb.Q.p, S);
-  tl_mark(h, "k_symmetrize");
+  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, h->m, acc, 1);   // Q_n += sym(G_S^T G_S)
   return STR_OK;
 }
 
@@ -359,9 +339,7 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
   RTRY(sampled_chain(h, N, GS));
   RTRY(gather_fibers(h, X, N, tn, XS));
   gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
-  gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0);
-  k_symmetrize<<<(unsigned)cdiv(SN * SN, 256), 256, 0, h->st>>>(K, SN);
-  tl_mark(h, "k_symmetrize");
+  gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
   double *GN_new = (double *)h->GN.p + h->T * SN;
   launch_chol_solve(K, SN, M, tn, GN_new, h->d_info, h->st);
   tl_mark(h, "chol_solve");

@@ -95,7 +95,9 @@ struct str_state {
   long long *tf_dbg = nullptr;      // device buffer for the contraction pipeline trace (diagnostic)
 
   // rSTR
-  DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev;
+  DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev, sSk;
+  int32_t *idx_pinned = nullptr;    // pinned index staging, one m-slot per mode
+  cudaEvent_t idx_ev[17] = {};       // last upload from each slot
   std::vector<int32_t> forced_idx[16];
   std::vector<int32_t> last_idx[16];
   int64_t tau = 0;
@@ -130,7 +132,11 @@ struct str_state {
     if (graph) cudaGraphDestroy(graph);
     gexec = nullptr;
     graph = nullptr;
-    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk);
+    if (idx_pinned) cudaFreeHost(idx_pinned);
+    idx_pinned = nullptr;
+    for (auto &e : idx_ev)
+      if (e) { cudaEventDestroy(e); e = nullptr; }
   }
 };
 
