@@ -356,10 +356,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       tc::tc_fence_before();
       if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 3] = clock64();
+      // conv[a] also certifies that this unit's table block has landed (the MMA waits only conv)
+      if (lane == 0) tc::mbar_wait(&bfull[sb], phb);
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&conv[a]);
       if (++s == SX) { s = 0; ph ^= 1; }
       if (++a == 2) { a = 0; pha ^= 1; }
+      if (++sb == SB) { sb = 0; phb ^= 1; }
     }
   } else if (warp >= 12) {
     // -------------------------------------------------------------- epilogue
@@ -519,7 +522,7 @@ static bool encode_x_map(str_state *h, CUtensorMap *tmap, const void *X, int pas
   return true;
 }
 
-str_status tf32_graph_update(str_state *h, cudaGraphExec_t exec, int pass, const void *X, int64_t tn) {
+str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn) {
   CUtensorMap tmap;
   if (!encode_x_map(h, &tmap, X, pass, tn)) return STR_E_CUDA;
   TcParams p;
@@ -532,7 +535,7 @@ str_status tf32_graph_update(str_state *h, cudaGraphExec_t exec, int pass, const
   kp.sharedMemBytes = (unsigned)h->tf_smem[pass - 1];
   kp.kernelParams = args;
   kp.extra = nullptr;
-  cudaError_t e = cudaGraphExecKernelNodeSetParams(exec, h->tf_node[pass - 1], &kp);
+  cudaError_t e = cudaGraphExecKernelNodeSetParams(h->gs[slot].exec, h->gs[slot].tf[pass - 1], &kp);
   if (e != cudaSuccess) {
     h->err = std::string("cudaGraphExecKernelNodeSetParams: ") + cudaGetErrorString(e);
     return STR_E_CUDA;
@@ -577,12 +580,7 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   cudaMemsetAsync(p.Y, 0, (size_t)M * W * sizeof(float), st);
   tl_mark(h, "memset", 0);
   const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + 1024 + 256;
-  cudaEvent_t e0 = nullptr, e1 = nullptr;
-  if (h->profiling) {
-    cudaEventCreate(&e0);
-    cudaEventCreate(&e1);
-    cudaEventRecord(e0, st);
-  }
+  prof_mark(h, 2 * (pass - 1));
   if (pass == 1)
     k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, p);
   else
@@ -596,16 +594,13 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
       h->err = "cannot locate the captured contraction node";
       return -1;
     }
-    h->tf_node[pass - 1] = deps[0];
+    h->gs[h->cur_slot].tf[pass - 1] = deps[0];
     static_assert(sizeof(TcParams) <= sizeof(h->tf_params[0]), "TcParams too large");
     memcpy(h->tf_params[pass - 1], &p, sizeof(TcParams));
     h->tf_grid[pass - 1] = grid;
     h->tf_smem[pass - 1] = smem;
   }
   tl_mark(h, pass == 1 ? "contract_tf32_p1" : "contract_tf32_p2");
-  if (h->profiling) {
-    cudaEventRecord(e1, st);
-    h->prof_events.push_back({pass, e0, e1});
-  }
+  prof_mark(h, 2 * (pass - 1) + 1);
   return 0;
 }

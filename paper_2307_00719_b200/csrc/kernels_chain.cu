@@ -569,25 +569,28 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
   const int64_t l1 = (l0 + 32 < td.Lk) ? l0 + 32 : td.Lk;
   const int64_t e_lo = l0 + td.Lk * tp, e_hi = l1 - 1 + td.Lk * tp;
   const FactorList &fl = td.fl;
-  // stage slices
-  double *base[kMaxFactors];
+  // stage slices (offsets into the shared array, so every later access is a shared-space load)
+  int boff[kMaxFactors];
   int64_t first[kMaxFactors];
   int cnt[kMaxFactors];
   {
-    double *p = tsm;
-    for (int f = 0; f < fl.n; ++f) {
-      const Factor &F = fl.f[f];
-      const int64_t q0 = e_lo / F.stride, q1 = e_hi / F.stride;
-      int c = (int)((q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I);
-      base[f] = p;
-      first[f] = q0;
-      cnt[f] = c;
-      const int AB = F.Ra * F.Rb;
-      for (int e = threadIdx.x; e < c * AB; e += blockDim.x) {
-        const int j = e / AB, w = e % AB;
-        cp_async8(p + e, F.G + ((q0 + j) % F.I) * AB + w);
+    int off = 0;
+#pragma unroll
+    for (int f = 0; f < kMaxFactors; ++f) {
+      if (f < fl.n) {
+        const Factor &F = fl.f[f];
+        const int64_t q0 = e_lo / F.stride, q1 = e_hi / F.stride;
+        const int c = (int)((q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I);
+        boff[f] = off;
+        first[f] = q0;
+        cnt[f] = c;
+        const int AB = F.Ra * F.Rb;
+        for (int e = threadIdx.x; e < c * AB; e += blockDim.x) {
+          const int j = e / AB, w = e % AB;
+          cp_async8(tsm + off + e, F.G + ((q0 + j) % F.I) * AB + w);
+        }
+        off += ((c * AB + 1) & ~1);
       }
-      p += ((c * AB + 1) & ~1);
     }
   }
   const int R0 = fl.f[0].Ra;
@@ -597,9 +600,11 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
   const int Np = td.Npad;
   if (tiles) {
     // tile staging area after the slices (float, 2 Np x 32)
-    double *p = tsm;
-    for (int f = 0; f < fl.n; ++f) p += ((cnt[f] * fl.f[f].Ra * fl.f[f].Rb + 1) & ~1);
-    tile = (float *)p;
+    int off = 0;
+#pragma unroll
+    for (int f = 0; f < kMaxFactors; ++f)
+      if (f < fl.n) off += ((cnt[f] * fl.f[f].Ra * fl.f[f].Rb + 1) & ~1);
+    tile = (float *)(tsm + off);
     for (int e = threadIdx.x; e < 2 * Np * 32; e += blockDim.x) tile[e] = 0.0f;
   }
   cp_async_wait_all();
@@ -612,7 +617,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
     {
       const Factor &F = fl.f[0];
       const int64_t q = e / F.stride;
-      const double *S = base[0] + ((q - first[0]) % cnt[0]) * (F.Ra * F.Rb);
+      const double *S = tsm + boff[0] + ((q - first[0]) % cnt[0]) * (F.Ra * F.Rb);
 #pragma unroll
       for (int b = 0; b < MR; ++b) v[b] = (b < F.Rb) ? S[pr + F.Ra * b] : 0.0;
     }
@@ -621,7 +626,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
       if (f < fl.n) {
         const Factor &F = fl.f[f];
         const int64_t q = e / F.stride;
-        const double *S = base[f] + ((q - first[f]) % cnt[f]) * (F.Ra * F.Rb);
+        const double *S = tsm + boff[f] + ((q - first[f]) % cnt[f]) * (F.Ra * F.Rb);
 #pragma unroll
         for (int b = 0; b < MR; ++b) {
           double acc = 0.0;

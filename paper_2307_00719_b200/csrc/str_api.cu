@@ -318,19 +318,11 @@ static str_status contract(str_state *h, const void *X, int pass, const double *
     double *tab = (double *)(pass == 1 ? h->TR.p : h->TL.p);
     TRY(build_table(h, td, tab, nullptr, pass == 1 ? "table_TR" : "table_TL"));
     double *out = (double *)(pass == 1 ? h->YL.p : h->YR.p);
-    cudaEvent_t e0 = nullptr, e1 = nullptr;
-    if (h->profiling) {
-      cudaEventCreate(&e0);
-      cudaEventCreate(&e1);
-      cudaEventRecord(e0, h->st);
-    }
+    prof_mark(h, 2 * (pass - 1));
     int nl = launch_contract_f64((const void *const *)h->dX.p, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn,
                                  out, (double *)h->ws.p, h->st);
     tl_mark(h, pass == 1 ? "contract_f64_p1" : "contract_f64_p2", nl);
-    if (h->profiling) {
-      cudaEventRecord(e1, h->st);
-      h->prof_events.push_back({pass, e0, e1});
-    }
+    prof_mark(h, 2 * (pass - 1) + 1);
     *Y = out;
     *y_f32 = false;
   }
@@ -375,12 +367,8 @@ str_status ensure_temporal_capacity(str_state *h, int64_t need) {
   cudaFree(h->GN.p);
   h->GN = nb;
   h->Tcap = cap;
-  if (h->gexec) {   // the captured append node points at the old buffer
-    cudaGraphExecDestroy(h->gexec);
-    cudaGraphDestroy(h->graph);
-    h->gexec = nullptr;
-    h->graph = nullptr;
-  }
+  h->gs[0].reset();   // the captured append nodes point at the old buffer
+  h->gs[1].reset();
   return STR_OK;
 }
 
@@ -395,7 +383,7 @@ static str_status set_x(str_state *h, const void *X) {
     size_t nd = 0;
     CU(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, nullptr, &deps, &nd));
     if (nd != 1) return fail(h, STR_E_CUDA, "cannot locate the captured set_x node");
-    h->g_setx = deps[0];
+    h->gs[h->cur_slot].setx = deps[0];
   }
   return check_launch(h, "set_x");
 }
@@ -577,60 +565,72 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
 }
 
 // One STR step: replays the captured graph of update_det_enqueue (capturing it on first use or
-// when t_new changes); eager when profiling / timeline diagnostics are on.
+// when t_new changes).  Profiling replays a second graph that also records events around the two
+// contraction passes (accumulated by str_profile); the timeline diagnostic runs eagerly.
 static str_status update_det(str_state *h, const void *X, int64_t tn) {
   TRY(ensure_workspace(h, tn));
   TRY(ensure_temporal_capacity(h, h->T + tn));
-  const bool graph = h->use_graph && !h->profiling && !h->timeline;
+  if (h->profiling && !h->pev[0]) {
+    for (auto &e : h->pev) CU(cudaEventCreate(&e));
+  }
+  const bool graph = h->use_graph && !h->timeline;
   if (!graph) {
     TRY(update_det_enqueue(h, X, tn));
   } else {
-    if (!h->gexec || h->g_tn != tn) {
-      if (h->gexec) {
-        cudaGraphExecDestroy(h->gexec);
-        cudaGraphDestroy(h->graph);
-        h->gexec = nullptr;
-        h->graph = nullptr;
-      }
+    const int slot = h->profiling ? 1 : 0;
+    str_state::GraphSlot &g = h->gs[slot];
+    if (!g.exec || g.tn != tn) {
+      g.reset();
       CU(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
       h->capturing = true;
+      h->cur_slot = slot;
       const int64_t l0 = h->launches;
       str_status st = update_det_enqueue(h, X, tn);
       h->capturing = false;
-      cudaGraph_t g = nullptr;
-      cudaError_t e = cudaStreamEndCapture(h->st, &g);
+      cudaGraph_t cg = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->st, &cg);
       if (st != STR_OK) {
-        if (g) cudaGraphDestroy(g);
+        if (cg) cudaGraphDestroy(cg);
         return st;
       }
       if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-      e = cudaGraphInstantiate(&h->gexec, g, 0);
+      e = cudaGraphInstantiate(&g.exec, cg, 0);
       if (e != cudaSuccess) {
-        cudaGraphDestroy(g);
+        cudaGraphDestroy(cg);
         return fail(h, STR_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
       }
-      h->graph = g;
-      h->g_tn = tn;
-      h->g_launches = h->launches - l0;
+      g.graph = cg;
+      g.tn = tn;
+      g.launches = h->launches - l0;
       h->launches = l0;
     } else {
       // point the replay at this batch
-      void *slot = h->dX.p;
+      void *slotp = h->dX.p;
       const void *xp = X;
-      void *args[2] = {&slot, &xp};
+      void *args[2] = {&slotp, &xp};
       cudaKernelNodeParams kp = {};
       kp.func = set_ptr_kernel();
       kp.gridDim = dim3(1);
       kp.blockDim = dim3(1);
       kp.kernelParams = args;
-      CU(cudaGraphExecKernelNodeSetParams(h->gexec, h->g_setx, &kp));
+      CU(cudaGraphExecKernelNodeSetParams(g.exec, g.setx, &kp));
       if (h->contract == STR_CONTRACT_3XTF32) {
-        TRY(tf32_graph_update(h, h->gexec, 1, X, tn));
-        TRY(tf32_graph_update(h, h->gexec, 2, X, tn));
+        TRY(tf32_graph_update(h, slot, 1, X, tn));
+        TRY(tf32_graph_update(h, slot, 2, X, tn));
       }
     }
-    CU(cudaGraphLaunch(h->gexec, h->st));
-    h->launches += h->g_launches;
+    CU(cudaGraphLaunch(g.exec, h->st));
+    h->launches += g.launches;
+  }
+  if (h->profiling) {   // pass times of this step (events on the library stream)
+    CU(cudaStreamSynchronize(h->st));
+    for (int ps = 0; ps < 2; ++ps) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, h->pev[2 * ps], h->pev[2 * ps + 1]) == cudaSuccess) {
+        h->prof_ms[ps] += ms;
+        h->prof_n[ps] += 1;
+      }
+    }
   }
   h->T += tn;
   return STR_OK;
@@ -1006,11 +1006,8 @@ extern "C" int64_t str_kernel_launches(const str_state *h) { return h ? h->launc
 extern "C" str_status str_set_profiling(str_state *h, int32_t enable) {
   if (!h) return STR_E_ARG;
   cudaStreamSynchronize(h->st);
-  for (auto &pe : h->prof_events) {
-    cudaEventDestroy(pe.e0);
-    cudaEventDestroy(pe.e1);
-  }
-  h->prof_events.clear();
+  h->prof_ms[0] = h->prof_ms[1] = 0.0;
+  h->prof_n[0] = h->prof_n[1] = 0;
   h->profiling = enable != 0;
   return STR_OK;
 }
@@ -1076,17 +1073,10 @@ extern "C" STR_API int64_t strdbg_timeline_dump(str_state *h, char *buf, int64_t
 extern "C" str_status str_profile(str_state *h, double *p1_ms, int64_t *p1_n, double *p2_ms, int64_t *p2_n) {
   if (!h) return STR_E_ARG;
   CU(cudaStreamSynchronize(h->st));
-  double a = 0, b = 0;
-  int64_t na = 0, nb = 0;
-  for (auto &pe : h->prof_events) {
-    float ms = 0;
-    cudaEventElapsedTime(&ms, pe.e0, pe.e1);
-    if (pe.pass == 1) { a += ms; na++; } else { b += ms; nb++; }
-  }
-  if (p1_ms) *p1_ms = a;
-  if (p1_n) *p1_n = na;
-  if (p2_ms) *p2_ms = b;
-  if (p2_n) *p2_n = nb;
+  if (p1_ms) *p1_ms = h->prof_ms[0];
+  if (p1_n) *p1_n = h->prof_n[0];
+  if (p2_ms) *p2_ms = h->prof_ms[1];
+  if (p2_n) *p2_n = h->prof_n[1];
   return STR_OK;
 }
 
@@ -1094,10 +1084,6 @@ extern "C" void str_destroy(str_state *h) {
   if (!h) return;
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
-  for (auto &pe : h->prof_events) {
-    cudaEventDestroy(pe.e0);
-    cudaEventDestroy(pe.e1);
-  }
   h->free_all();
   if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)h->comm);
   if (h->st2) {

@@ -28,11 +28,6 @@ struct ModeBuf {
   std::vector<int32_t> idx_host;
 };
 
-struct ProfEvent {
-  int pass;
-  cudaEvent_t e0, e1;
-};
-
 struct str_state {
   // configuration
   int N = 0;
@@ -82,12 +77,24 @@ struct str_state {
   // appended at the device-side row counter dT.
   DevBuf GNnew, dT, dX;
   bool use_graph = true;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  int64_t g_tn = 0;
-  int64_t g_launches = 0;
-  cudaGraphNode_t g_setx = nullptr;
-  cudaGraphNode_t tf_node[2] = {nullptr, nullptr};
+  struct GraphSlot {
+    cudaGraph_t graph = nullptr;
+    cudaGraphExec_t exec = nullptr;
+    int64_t tn = 0, launches = 0;
+    cudaGraphNode_t setx = nullptr, tf[2] = {nullptr, nullptr};
+    void reset() {
+      if (exec) cudaGraphExecDestroy(exec);
+      if (graph) cudaGraphDestroy(graph);
+      exec = nullptr;
+      graph = nullptr;
+      tn = 0;
+    }
+  };
+  GraphSlot gs[2];                  // [0] production replay, [1] profiling replay (events around the passes)
+  int cur_slot = 0;                 // slot being captured / replayed
+  cudaEvent_t pev[4] = {};          // profiling: pass-1 begin/end, pass-2 begin/end
+  double prof_ms[2] = {0.0, 0.0};
+  int64_t prof_n[2] = {0, 0};
   alignas(16) unsigned char tf_params[2][256];
   int tf_grid[2] = {0, 0};
   size_t tf_smem[2] = {0, 0};
@@ -106,7 +113,6 @@ struct str_state {
   int64_t launches = 0;
   int64_t collectives = 0;
   bool profiling = false;
-  std::vector<ProfEvent> prof_events;
   // launch timeline (diagnostic): an event after every launch, named by kernel
   bool timeline = false;
   std::vector<std::pair<const char *, cudaEvent_t>> tl;
@@ -128,10 +134,10 @@ struct str_state {
     fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
     fr(tab_split); fr(tf_part); fr(tf_part2);
     fr(GNnew); fr(dT); fr(dX);
-    if (gexec) cudaGraphExecDestroy(gexec);
-    if (graph) cudaGraphDestroy(graph);
-    gexec = nullptr;
-    graph = nullptr;
+    gs[0].reset();
+    gs[1].reset();
+    for (auto &e : pev)
+      if (e) { cudaEventDestroy(e); e = nullptr; }
     fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk);
     if (idx_pinned) cudaFreeHost(idx_pinned);
     idx_pinned = nullptr;
@@ -139,6 +145,13 @@ struct str_state {
       if (e) { cudaEventDestroy(e); e = nullptr; }
   }
 };
+
+// Profiling event i (pass-1 begin/end, pass-2 begin/end) on the library stream; inside a stream
+// capture it must be an external record node (a plain record there is only a capture dependency).
+inline void prof_mark(str_state *h, int i) {
+  if (!h->profiling) return;
+  cudaEventRecordWithFlags(h->pev[i], h->st, h->capturing ? cudaEventRecordExternal : cudaEventRecordDefault);
+}
 
 // Count a launch (n kernels) and, when the timeline is on, record a named event after it on the
 // handle's stream: consecutive events bracket each launch's in-stream time (incl. its gap).
@@ -167,4 +180,4 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn);
 int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y);
 int tf32_npad(int W);
 // Re-point captured contraction node `pass` of exec at new data X (3xTF32 path).
-str_status tf32_graph_update(str_state *h, cudaGraphExec_t exec, int pass, const void *X, int64_t tn);
+str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn);
