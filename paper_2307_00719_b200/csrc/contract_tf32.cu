@@ -12,7 +12,8 @@
 //
 // Structure (one CTA per SM, persistent "stream-K" over units (M-block of 256 rows, K-tile of 32)):
 //   warp 0       TMA producer: the two 128-row X tiles (cp.async.bulk.tensor, 128B swizzle, OOB
-//                zero-fill) and the pre-tiled hi/lo table block (cp.async.bulk) on one mbarrier
+//                zero-fill) into the X ring
+//   warp 3       table producer: the pre-tiled hi/lo table block (cp.async.bulk) into the table ring
 //   warp 1       UMMA issuer (one thread): per M-tile and k-step 3 x tcgen05.mma.kind::tf32 with A
 //                from TMEM (A_hi | A_lo) and B from shared memory (B_hi | B_lo); one B stage feeds
 //                both M-tiles, halving the table traffic per FLOP
@@ -42,17 +43,21 @@ constexpr int kBM = 128;       // UMMA M
 constexpr int kMT = 2;         // M-tiles per CTA (share every B stage)
 constexpr int kBK = 32;        // K per stage (one 128-byte swizzle row of fp32)
 constexpr int kABytes = kBM * kBK * 4;   // 16 KB per X tile
-constexpr uint32_t kAccCols = 256;       // accumulators at [0, 256): M-tile mt at mt * 128
 constexpr uint32_t kASlot0 = 256;        // A slots at [256, 512): slot a, M-tile mt at 256 + (2a + mt) * 64
+// epilogue staging: per lane quarter one dense [32 rows][W] fp32 box (W <= 128) -> one M-tile
+__host__ __device__ constexpr int ystage_box_bytes(int W) { return (32 * W * 4 + 1023) / 1024 * 1024; }
+__host__ __device__ constexpr int ystage_bytes(int W) { return 4 * ystage_box_bytes(W); }
 
 struct TcParams {
   int64_t L, Rr, tn;
   int W, Npad, stages, bstages;   // X ring / table ring depths
-  int mb_per_t;    // pass 1: ceil(L/256) M-blocks per t
+  int mt_per_t;    // 128-row M-tiles per t (pass 1: ceil(L/128)) or in all (pass 2: ceil(Rr/128))
+  int mtiles;      // M-tiles in all (pass 1: mt_per_t tn); an M-block pairs tiles 2b, 2b+1
   int nlb;         // pass 2: ceil(L/32) K-tiles per t
+  int yred;        // 1: epilogue by TMA reduce-add through a one-tile staging area (W % 4 == 0); 0: red.add
   int64_t KT, U, upc;
   const float *Btiles;   // [KT][2 Npad rows][32 k] fp32, 128B-swizzled K-major blocks
-  float *Y;              // fp32 output rows (zeroed), row stride W
+  float *Y;              // fp32 output rows (zeroed), row stride W (pass 1: row l + L t)
   long long *dbg;        // optional pipeline trace of CTA 0 (diagnostic; nullptr in production)
   int dbg_flags;         // diagnostic: bit0 skip table loads, bit1 skip X loads, bit2 skip TMEM stores, bit3 one commit per unit, bit4 spin waits, bit5 converters skip smem reads (wrong results)
 };
@@ -111,7 +116,8 @@ __device__ __forceinline__ long long gtimer() {
 
 template <int PASS>
 __global__ void __launch_bounds__(kTcThreads, 1)
-    k_contract_tf32(const __grid_constant__ CUtensorMap tmap, const TcParams p) {
+    k_contract_tf32(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap ymap,
+                    const TcParams p) {
   if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 0] = gtimer();
   extern __shared__ uint8_t smem_raw[];
   uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
@@ -122,15 +128,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int SX = p.stages, SB = p.bstages;
   uint8_t *xbuf = smem;
   uint8_t *bbuf = smem + (size_t)SX * XSTAGE;
-  uint64_t *xfull = (uint64_t *)(bbuf + (size_t)SB * BBYTES);
+  uint8_t *ystage = bbuf + (size_t)SB * BBYTES;   // one-tile epilogue staging ([q] dense [32][W] fp32 boxes)
+  uint64_t *xfull = (uint64_t *)(ystage + (p.yred ? ystage_bytes(p.W) : 0));
   uint64_t *xempty = xfull + SX;
   uint64_t *bfull = xempty + SX;
   uint64_t *bempty = bfull + SB;
   uint64_t *conv = bempty + SB;    // [2] A slot filled (converters -> MMA)
   uint64_t *aempty = conv + 2;     // [2] A slot free   (MMA -> converters)
   uint64_t *accf = aempty + 2;     // accumulators complete (MMA -> epilogue)
-  uint64_t *acce = accf + 1;       // accumulators drained  (epilogue -> MMA)
-  uint32_t *tslot = (uint32_t *)(acce + 1);
+  uint64_t *acce = accf + 1;       // [2] accumulator of M-tile mt drained (epilogue -> MMA)
+  uint32_t *tslot = (uint32_t *)(acce + 2);
 
   // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform and the
   // MMA warp keeps its descriptors / TMEM addresses in uniform registers (no per-MMA R2UR)
@@ -153,9 +160,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::mbar_init(&aempty[a], 1);
     }
     tc::mbar_init(accf, 1);
-    tc::mbar_init(acce, 4);          // one arrival per epilogue warp
+    tc::mbar_init(&acce[0], 4);      // one arrival per epilogue warp
+    tc::mbar_init(&acce[1], 4);
     tc::fence_barrier_init();
     tc::prefetch_tmap(&tmap);
+    if (p.yred) tc::prefetch_tmap(&ymap);
   }
   if (warp == 2) tc::tmem_alloc(tslot, 512);
   if (p.W < p.Npad) {   // table padding rows are never loaded: zero them once (read by the MMA)
@@ -179,30 +188,43 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   } else if (warp == 0) {
     if (lane == 0) {
       // ------------------------------------------------------------ TMA producer
-      int sx = 0, sb = 0;
-      uint32_t phx = 0, phb = 0;
+      int sx = 0;
+      uint32_t phx = 0;
+      const uint64_t pol = tc::policy_evict_first();   // X is read exactly once
       int mblk = (int)(u0 / p.KT), kt = (int)(u0 % p.KT);   // 32-bit, advanced incrementally
       for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0, ++mblk) : 0) {
+        const int nmt = (2 * mblk + 1 < p.mtiles) ? 2 : 1;   // the last M-block may hold one tile
         tc::mbar_wait(&xempty[sx], phx ^ 1);
         if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 0] = clock64();
         uint8_t *A = xbuf + (size_t)sx * XSTAGE;
         if (p.dbg_flags & 2) {
           tc::mbar_arrive(&xfull[sx]);
         } else {
-        tc::mbar_arrive_expect_tx(&xfull[sx], kMT * kABytes);
+        tc::mbar_arrive_expect_tx(&xfull[sx], nmt * kABytes);
         if (PASS == 1) {
-          const int t = mblk / p.mb_per_t, mb = mblk - t * p.mb_per_t;
-#pragma unroll
-          for (int mt = 0; mt < kMT; ++mt)
-            tc::tma_load_3d(A + mt * kABytes, &tmap, &xfull[sx], (mb * kMT + mt) * kBM, (int)kt * kBK, t);
+          // M-tile g = 2 mblk + mt covers rows l in [128 (g mod mt_per_t), +128) of slice t = g / mt_per_t
+          for (int mt = 0; mt < nmt; ++mt) {
+            const int g = 2 * mblk + mt, t = g / p.mt_per_t, lt = g - t * p.mt_per_t;
+            tc::tma_load_3d_hint(A + mt * kABytes, &tmap, &xfull[sx], lt * kBM, (int)kt * kBK, t, pol);
+          }
         } else {
           const int t = kt / p.nlb, lb = kt - t * p.nlb;
-#pragma unroll
-          for (int mt = 0; mt < kMT; ++mt)
-            tc::tma_load_3d(A + mt * kABytes, &tmap, &xfull[sx], lb * kBK, (int)(mblk * kMT + mt) * kBM, t);
+          for (int mt = 0; mt < nmt; ++mt)
+            tc::tma_load_3d_hint(A + mt * kABytes, &tmap, &xfull[sx], lb * kBK, (2 * mblk + mt) * kBM, t, pol);
         }
         }
         if (++sx == SX) { sx = 0; phx ^= 1; }
+      }
+    }
+  } else if (warp == 3) {
+    if (lane == 0) {
+      // ------------------------------------------------------------ table-block producer (own
+      // thread, so the table ring runs ahead independently of the X ring)
+      int sb = 0;
+      uint32_t phb = 0;
+      int kt = (int)(u0 % p.KT);
+      const uint64_t pol = tc::policy_evict_last();    // each table block is read by several CTAs
+      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0) : 0) {
         tc::mbar_wait(&bempty[sb], phb ^ 1);
         if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 8] = clock64();
         uint8_t *B = bbuf + (size_t)sb * BBYTES;
@@ -213,8 +235,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             tc::mbar_arrive(&bfull[sb]);
           } else {
             tc::mbar_arrive_expect_tx(&bfull[sb], 2 * rb);
-            tc::bulk_load(B, src, rb, &bfull[sb]);
-            tc::bulk_load(B + p.Npad * 128, src + p.Npad * 128, rb, &bfull[sb]);
+            tc::bulk_load_hint(B, src, rb, &bfull[sb], pol);
+            tc::bulk_load_hint(B + p.Npad * 128, src + p.Npad * 128, rb, &bfull[sb], pol);
           }
         }
         if (++sb == SB) { sb = 0; phb ^= 1; }
@@ -249,60 +271,63 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         tc::mbar_wait(accf, 0);
         if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2) p.dbg[63 * 16 + 0] = clock64() - t0;
       } else {
+      // Every value that reaches an MMA operand is re-broadcast from lane 0 each unit (shfl), so the
+      // compiler keeps the operands in uniform registers (no per-MMA R2UR after the barrier waits).
+      // The A-slot and table-slot commits of unit u follow its MMAs at once; the accumulator commit
+      // of a segment's last unit is deferred past the next unit's waits.
       int s = 0, a = 0;
-      uint32_t ph = 0, pha = 0, phe = 0;
-      int kt = (int)(u0 % p.KT);
-      // The commits of unit u are issued after the barrier waits of unit u+1 (deferred), so the
-      // waits do not queue behind the commit bookkeeping while unit u's MMAs still run.
-      int ps = -1, pa = 0;
-      bool plast = false;
-      auto flush = [&]() {
-        if (ps >= 0) {
-          mma_commit_elect(&bempty[ps]);
-          if (plast) mma_commit_elect(accf);
-          ps = -1;
-        }
-      };
-      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0) : 0) {   // s: table slot, a: TMEM A slot
+      uint32_t pha = 0, phe = 0;
+      int kt = (int)(u0 % p.KT), mblk = (int)(u0 / p.KT);
+      bool pend_accf = false;
+      const bool dbgcta = p.dbg != nullptr && blockIdx.x == gridDim.x / 2;
+      const uint64_t bdesc0 = tc::smem_desc_sw128(tc::smem_u32(bbuf), 16, 1024);
+      const uint32_t bstep = (uint32_t)(BBYTES >> 4), lostep = (uint32_t)((p.Npad * 128) >> 4);
+      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0, ++mblk) : 0) {   // s: table slot, a: TMEM A slot
+        const int nmt = (2 * mblk + 1 < p.mtiles) ? 2 : 1;
         const bool first = (u == u0) || (kt == 0);
         const bool last = (u == u1 - 1) || (kt == (int)p.KT - 1);
-        if (first) {
-          flush();                         // the previous segment's accf must go out first
-          tc::mbar_wait(acce, phe ^ 1);   // previous segment drained by the epilogue
-          phe ^= 1;
-          tc::tc_fence_after();
-        }
+        if (first && pend_accf) { mma_commit_elect(accf); pend_accf = false; }   // previous segment's accf first
         // (the table block of this unit has landed: the converters arrive on conv only after bfull)
-        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 4] = clock64();
-        if (p.dbg_flags & 128) {} else if (p.dbg_flags & 16) tc::mbar_spin(&conv[a], pha); else tc::mbar_wait(&conv[a], pha);
-        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 5] = clock64();
-        flush();
+        if (dbgcta && u - u0 < 64) p.dbg[(u - u0) * 16 + 4] = clock64();
+        if (!(p.dbg_flags & 128)) tc::mbar_wait(&conv[a], pha);
+        __syncwarp();
+        if (dbgcta && u - u0 < 64) p.dbg[(u - u0) * 16 + 5] = clock64();
+        if (pend_accf) { mma_commit_elect(accf); pend_accf = false; }
         tc::tc_fence_after();
-        const uint32_t b0 = tc::smem_u32(bbuf + (size_t)s * BBYTES);
+        const int su = __shfl_sync(0xffffffffu, s, 0), au = __shfl_sync(0xffffffffu, a, 0);
+        const int nmu = __shfl_sync(0xffffffffu, nmt, 0);
+        const uint32_t acc0 = __shfl_sync(0xffffffffu, first ? 0u : 1u, 0);
+        const uint64_t bd = bdesc0 + (uint64_t)(su * bstep);
+        const bool firstu = __shfl_sync(0xffffffffu, first ? 1 : 0, 0) != 0;
 #pragma unroll
         for (int mt = 0; mt < kMT; ++mt) {
+          if (mt >= nmu) break;
+          if (firstu) {   // the previous segment's accumulator of this tile has been drained
+            tc::mbar_wait(&acce[mt], phe ^ 1);
+            __syncwarp();
+            tc::tc_fence_after();
+          }
           const uint32_t d = tbase + (uint32_t)(mt * 128);
-          const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * a + mt) * 64);
+          const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * au + mt) * 64);
 #pragma unroll
           for (int ks = 0; ks < kBK / 8; ++ks) {
-            const uint64_t bhi = tc::smem_desc_sw128(b0 + ks * 32, 16, 1024);
-            const uint64_t blo = tc::smem_desc_sw128(b0 + p.Npad * 128 + ks * 32, 16, 1024);
-            mma_tf32_ts(d, ahi + ks * 8, bhi, idesc, (first && ks == 0) ? 0u : 1u);
+            const uint64_t bhi = bd + (uint64_t)(ks * 2), blo = bd + (uint64_t)(lostep + ks * 2);
+            mma_tf32_ts(d, ahi + ks * 8, bhi, idesc, ks == 0 ? acc0 : 1u);
             mma_tf32_ts(d, ahi + ks * 8, blo, idesc, 1u);
             mma_tf32_ts(d, ahi + 32 + ks * 8, bhi, idesc, 1u);
           }
         }
-        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 6] = clock64();
-        if (p.dbg && lane == 0 && u == u1 - 1) p.dbg[1024 + blockIdx.x * 4 + 2] = gtimer();
-        mma_commit_elect(&aempty[a]);    // the converters may refill this A slot as soon as possible
-        ps = s;
-        pa = a;
-        plast = last;
-        if (p.dbg && lane == 0 && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 7] = clock64();
-        if (++s == SB) { s = 0; ph ^= 1; }
+        if (dbgcta && u - u0 < 64) p.dbg[(u - u0) * 16 + 6] = clock64();
+        if (firstu) phe ^= 1;
+        mma_commit_elect(&aempty[au]);    // the converters may refill this A slot as soon as possible
+        mma_commit_elect(&bempty[su]);    // ... and the table producer this table slot
+        pend_accf = last;
+        if (dbgcta && u - u0 < 64) p.dbg[(u - u0) * 16 + 7] = clock64();
+        if (++s == SB) s = 0;
         if (++a == 2) { a = 0; pha ^= 1; }
       }
-      flush();
+      if (pend_accf) mma_commit_elect(accf);
+      if (p.dbg && lane == 0) p.dbg[1024 + blockIdx.x * 4 + 2] = gtimer();
       }
     }
   } else if (warp >= 4 && warp < 12) {
@@ -312,14 +337,16 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     const int m = q * 32 + lane;
     int s = 0, a = 0, sb = 0;
     uint32_t ph = 0, pha = 0, phb = 0;
-    for (int64_t u = u0; u < u1; ++u) {   // s: X ring slot, a: TMEM A slot, sb: table ring slot
+    int ckt = (int)(u0 % p.KT), cmb = (int)(u0 / p.KT);
+    for (int64_t u = u0; u < u1; ++u, (++ckt == (int)p.KT) ? (ckt = 0, ++cmb) : 0) {   // s: X ring slot, a: TMEM A slot, sb: table ring slot
+      const bool present = 2 * cmb + mt < p.mtiles;   // (an absent tile's MMAs are skipped)
       if (p.dbg_flags & 2048) tc::mbar_wait_sleep(&xfull[s], ph); else tc::mbar_wait(&xfull[s], ph);
       if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 1] = clock64();
       if (p.dbg_flags & 2048) tc::mbar_wait_sleep(&aempty[a], pha ^ 1); else tc::mbar_wait(&aempty[a], pha ^ 1);
       if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64 && threadIdx.x == 128) p.dbg[(u - u0) * 16 + 2] = clock64();
       const uint8_t *xt = xbuf + (size_t)s * XSTAGE + mt * kABytes;
       uint32_t hi[32], lo[32];
-      if (p.dbg_flags & 32) {
+      if ((p.dbg_flags & 32) || !present) {
 #pragma unroll
         for (int k = 0; k < 32; ++k) { hi[k] = 0; lo[k] = 0; }
       } else if (PASS == 2) {
@@ -349,7 +376,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&xempty[s]);   // the X slot is free once the tile sits in registers
       const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + kASlot0 + (uint32_t)((2 * a + mt) * 64);
-      if (!(p.dbg_flags & 4)) {
+      if (!(p.dbg_flags & 4) && present) {
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
         tmem_st_wait();
@@ -366,32 +393,66 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     }
   } else if (warp >= 12) {
     // -------------------------------------------------------------- epilogue
+    // Lane quarter q of both accumulators.  yred: tile by tile, TMEM -> a dense [32][W] box in the
+    // one-tile staging area -> release that tile's accumulator -> one TMA reduce-add (coalesced,
+    // clipped at the tensor edges); the next tile reuses the area once the reduce has read it.  In
+    // the CTA's last segment the second tile stages in the drained X ring instead (no wait).
+    // Otherwise (W % 4 != 0) per-lane red.add from registers.
     const int q = warp % 4;
     const int row = q * 32 + lane;
+    const int ybox = ystage_box_bytes(p.W);
+    bool pending = false;   // a reduce may still be reading the staging area
     uint32_t phf = 0;
     int64_t u = u0;
     while (u < u1) {
       const int64_t mblk = u / p.KT;
       const int64_t uend = ((mblk + 1) * p.KT < u1) ? (mblk + 1) * p.KT : u1;
+      const bool lastseg = uend == u1;
       if (p.dbg_flags & 1024) tc::mbar_wait_sleep(accf, phf); else tc::mbar_wait(accf, phf);
       phf ^= 1;
       tc::tc_fence_after();
 #pragma unroll
       for (int mt = 0; mt < kMT; ++mt) {
-        int64_t yrow;
-        bool valid;
+        const int g = 2 * (int)mblk + mt;
+        if (g >= p.mtiles) {
+          if (lane == 0) tc::mbar_arrive(&acce[mt]);   // absent tile: keep the phases in step
+          continue;
+        }
+        int t = 0, r0 = g * kBM;   // tile rows [r0, r0 + 128) of slice t
         if (PASS == 1) {
-          const int64_t t = mblk / p.mb_per_t, mb = mblk % p.mb_per_t;
-          const int64_t l = (mb * kMT + mt) * kBM + row;
-          valid = l < p.L;
-          yrow = l + p.L * t;
-        } else {
-          const int64_t r = (mblk * kMT + mt) * kBM + row;
-          valid = r < p.Rr;
-          yrow = r;
+          t = g / p.mt_per_t;
+          r0 = (g - t * p.mt_per_t) * kBM;
         }
         const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * 128);
-        float *yr = p.Y + yrow * p.W;
+        if (p.yred) {
+          uint8_t *box = (lastseg && mt == 1 ? xbuf : ystage) + q * ybox;
+          if (pending && box != xbuf + q * ybox) {
+            if (lane == 0) tc::bulk_wait_read<0>();
+            __syncwarp();
+          }
+          float *dst = (float *)box + lane * p.W;
+          for (int c0 = 0; c0 < p.W; c0 += 32) {
+            float v[32];
+            tmem_ld32(taddr + c0, v);   // columns >= Npad are never written by the MMA: not stored
+#pragma unroll
+            for (int i = 0; i < 32; i += 4)
+              if (c0 + i < p.W) *(float4 *)(dst + c0 + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+          }
+          tc::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) tc::mbar_arrive(&acce[mt]);   // the MMA may restart this tile now
+          tc::fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tc::tma_reduce_add_3d(&ymap, box, 0, r0 + q * 32, t);
+            tc::bulk_commit();
+          }
+          pending = true;
+          continue;
+        }
+        const int64_t rr = r0 + row;
+        const bool valid = rr < (PASS == 1 ? p.L : p.Rr);
+        float *yr = p.Y + (rr + (PASS == 1 ? p.L * t : 0)) * p.W;
         for (int c0 = 0; c0 < p.Npad; c0 += 32) {
           float v[32];
           if (c0 + 32 <= p.Npad) {
@@ -404,12 +465,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 #pragma unroll
             for (int i = 16; i < 32; ++i) v[i] = 0.0f;
           }
+          if (c0 + 32 >= p.Npad) {   // last TMEM load of this tile: release the accumulator
+            tc::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) tc::mbar_arrive(&acce[mt]);
+          }
           if (valid) {
-            if ((p.W & 3) == 0 && c0 + 32 <= p.W) {
-#pragma unroll
-              for (int i = 0; i < 32; i += 4)
-                atomicAdd((float4 *)(yr + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
-            } else if ((p.W & 3) == 0) {
+            if ((p.W & 3) == 0) {
 #pragma unroll
               for (int i = 0; i < 32; i += 4)
                 if (c0 + i < p.W) atomicAdd((float4 *)(yr + c0 + i), make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]));
@@ -421,11 +483,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           }
         }
       }
-      tc::tc_fence_before();
-      __syncwarp();
-      if (lane == 0) tc::mbar_arrive(acce);
       u = uend;
     }
+    if (p.yred && lane == 0) tc::bulk_wait_all();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -469,6 +529,8 @@ str_status tf32_prepare(str_state *h) {
   if (!attr) {
     cudaFuncSetAttribute(k_contract_tf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_contract_tf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+    prefer_max_smem(k_contract_tf32<1>);
+    prefer_max_smem(k_contract_tf32<2>);
     // (Npad <= 128 keeps 2 Npad x 128 B of table per stage; 3 stages fit)
     attr = true;
   }
@@ -476,7 +538,7 @@ str_status tf32_prepare(str_state *h) {
   return STR_OK;
 }
 
-static int npad_of(int W) { return (W + 15) / 16 * 16; }
+static int npad_of(int W) { return (W + 7) / 8 * 8; }   // UMMA N granularity 8 (cta_group::1, M = 128)
 
 str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
   const int N = h->N, k = h->k;
@@ -522,12 +584,30 @@ static bool encode_x_map(str_state *h, CUtensorMap *tmap, const void *X, int pas
   return true;
 }
 
+// Output map for the TMA reduce-add epilogue: Y as [t][rows][W] fp32 (pass 1: rows l < L, t < tn;
+// pass 2: rows r < Rr, one t), box [1][32][W], unswizzled (matches the dense staging boxes).
+static bool encode_y_map(str_state *h, CUtensorMap *ymap, float *Y, int pass, int W, int64_t tn) {
+  const int64_t rows = pass == 1 ? h->L : h->Rr, tt = pass == 1 ? tn : 1;
+  cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)tt};
+  cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)(rows * W * 4)};
+  cuuint32_t box[3] = {(cuuint32_t)W, 32, 1};
+  cuuint32_t es[3] = {1, 1, 1};
+  CUresult r = g_encode(ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    h->err = "cuTensorMapEncodeTiled (Y) failed (" + std::to_string((int)r) + ")";
+    return false;
+  }
+  return true;
+}
+
 str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn) {
-  CUtensorMap tmap;
+  CUtensorMap tmap, ymap;
   if (!encode_x_map(h, &tmap, X, pass, tn)) return STR_E_CUDA;
+  memcpy(&ymap, h->tf_ymap[pass - 1], sizeof(CUtensorMap));
   TcParams p;
   memcpy(&p, h->tf_params[pass - 1], sizeof(TcParams));
-  void *args[2] = {&tmap, &p};
+  void *args[3] = {&tmap, &ymap, &p};
   cudaKernelNodeParams kp = {};
   kp.func = pass == 1 ? (void *)k_contract_tf32<1> : (void *)k_contract_tf32<2>;
   kp.gridDim = dim3(h->tf_grid[pass - 1]);
@@ -558,33 +638,48 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.W = W;
   p.Npad = Np;
   const int bbytes = 2 * Np * 128;
-  p.bstages = 4;
-  p.stages = std::min(6, (int)((224 * 1024 - 1024 - 256 - p.bstages * bbytes) / (kMT * kABytes)));
-  p.mb_per_t = (int)cdiv(L, kMT * kBM);
+  p.yred = (W % 4 == 0 && W <= 128) ? 1 : 0;   // TMA needs 16-byte row strides; box width <= 256
+  const int ybytes = p.yred ? ystage_bytes(W) : 0;
+  p.bstages = 2;
+  if (const char *ev = getenv("STR_TF_BSTAGES")) p.bstages = std::max(2, atoi(ev));   // tuning knob
+  p.stages = std::min(6, (int)((227 * 1024 - 1024 - 256 - ybytes - p.bstages * bbytes) / (kMT * kABytes)));
+  if (p.stages < 2) {
+    h->err = "3xTF32 contraction: shared memory too small for the ring depths";
+    return -1;
+  }
+  if (p.yred && p.stages * kMT * kABytes < ystage_bytes(W)) p.yred = 0;   // (last-segment tile 1 uses the X ring)
+  p.mt_per_t = (int)cdiv(pass == 1 ? L : Rr, kBM);
+  p.mtiles = pass == 1 ? p.mt_per_t * (int)tn : p.mt_per_t;
   p.nlb = (int)cdiv(L, 32);
-  const int64_t tiles = pass == 1 ? (int64_t)p.mb_per_t * tn : cdiv(Rr, kMT * kBM);
+  const int64_t blocks = cdiv(p.mtiles, kMT);   // M-blocks (tile pairs; pass 1 pairs across t)
   p.KT = pass == 1 ? cdiv(Rr, kBK) : tn * p.nlb;
-  p.U = tiles * p.KT;
-  int grid = (int)std::min<int64_t>(148, p.U);
+  p.U = blocks * p.KT;
+  int maxg = 148;
+  if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(148, atoi(ev)));   // tuning knob
+  int grid = (int)std::min<int64_t>(maxg, p.U);
   p.upc = cdiv(p.U, grid);
   grid = (int)cdiv(p.U, p.upc);
   p.Btiles = (const float *)h->tab_split.p;
   p.Y = Y;
-  p.dbg = h->tf_dbg;
+  p.dbg = h->tf_dbg ? h->tf_dbg + (pass - 1) * str_state::kTfDbgWords : nullptr;
   p.dbg_flags = 0;
+  if (g_dbg_skip & 4) p.U = 0;   // what-if diagnostic: every CTA exits at once
   if (h->tf_dbg) {
     const char *ev = getenv("STR_TF_DBGFLAGS");
     if (ev) p.dbg_flags = atoi(ev);
   }
+  CUtensorMap ymap;
+  memset(&ymap, 0, sizeof(ymap));
+  if (p.yred && !encode_y_map(h, &ymap, Y, pass, W, tn)) return -1;
   const int64_t M = pass == 1 ? L * tn : Rr;
   cudaMemsetAsync(p.Y, 0, (size_t)M * W * sizeof(float), st);
   tl_mark(h, "memset", 0);
-  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + 1024 + 256;
+  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 256;
   prof_mark(h, 2 * (pass - 1));
   if (pass == 1)
-    k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, p);
+    k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, ymap, p);
   else
-    k_contract_tf32<2><<<grid, kTcThreads, smem, st>>>(tmap, p);
+    k_contract_tf32<2><<<grid, kTcThreads, smem, st>>>(tmap, ymap, p);
   if (h->capturing) {
     // remember the node so that graph replays can re-point it at new X (tf32_graph_update)
     cudaStreamCaptureStatus cs;
@@ -597,6 +692,7 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
     h->gs[h->cur_slot].tf[pass - 1] = deps[0];
     static_assert(sizeof(TcParams) <= sizeof(h->tf_params[0]), "TcParams too large");
     memcpy(h->tf_params[pass - 1], &p, sizeof(TcParams));
+    memcpy(h->tf_ymap[pass - 1], &ymap, sizeof(CUtensorMap));
     h->tf_grid[pass - 1] = grid;
     h->tf_smem[pass - 1] = smem;
   }

@@ -8,6 +8,12 @@
 
 namespace strb200 {
 
+// Diagnostic what-if knob (STR_DBG_SKIP, read at str_init; 0 in production): launchers whose bit
+// is set enqueue nothing, so a timing run shows how much of the step each kernel class holds.
+// Results are meaningless while it is non-zero.  1 spd_inv, 2 tables, 4 contraction, 8 absorbs,
+// 16 chain GEMMs, 32 row GEMMs, 64 Z Grams.
+extern int g_dbg_skip;
+
 // kernels_small.cu
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);
 void launch_absorb(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);
@@ -36,6 +42,14 @@ int launch_contract_f64(const void *const *X, bool x_is_f64, int pass, const dou
 void launch_set_ptr(const void **slot, const void *p, cudaStream_t s);
 void *set_ptr_kernel();
 void prepare_kernel_attrs();
+// Every kernel of the step prefers the maximum shared-memory carve-out, so the SMs never switch
+// their L1 / shared split between the 227 KB contraction and its neighbours (a switch drains the
+// SM and costs microseconds per launch).
+template <class F>
+inline void prefer_max_smem(F *f) {
+  cudaFuncSetAttribute((const void *)f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+}
+void prepare_f64_attrs();
 void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn, int SN, cudaStream_t s);
 size_t contract_f64_ws_doubles(int64_t M, int64_t K, int W);
 size_t fit_partials(int64_t L, int64_t Rr, int64_t tn);

@@ -16,6 +16,8 @@
 
 namespace strb200 {
 
+int g_dbg_skip = 0;
+
 void prepare_kernel_attrs();
 
 __device__ __forceinline__ void cp_async8(void *smem, const void *g) {
@@ -254,6 +256,7 @@ size_t spd_inv_smem(int S) {
 }
 
 void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {
+  if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
   if (S <= 104)
     k_spd_inv<5><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
@@ -318,12 +321,14 @@ __global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A
 }
 
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
+  if (g_dbg_skip & 16) return;
   prepare_kernel_attrs();
   dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32));
   k_chain_gemm<<<grid, 256, (size_t)2 * K * 32 * sizeof(double), s>>>(A, B, C, M, N, K, q);
 }
 
 void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s) {
+  if (g_dbg_skip & 32) return;
   if (I <= 0) return;
   launch_chain_gemm(P, B, out, (int)I, S, S, QEpi{nullptr, 0, 0, 0}, s);
 }
@@ -366,6 +371,7 @@ __global__ void __launch_bounds__(256) k_gram_z2(const double *__restrict__ G, i
 }
 
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s) {
+  if (g_dbg_skip & 64) return;
   const int n = Ra * Ra * Rb * Rb;
   k_gram_z2<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(G, I, Ra, Rb, Zm, accumulate);
 }
@@ -531,9 +537,18 @@ static void absorb_attrs() {
   cudaFuncSetAttribute(k_absorb4<TY, 10, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, STR_MAXR, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, STR_MAXR, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  prefer_max_smem(k_absorb4<TY, 4, true>);
+  prefer_max_smem(k_absorb4<TY, 4, false>);
+  prefer_max_smem(k_absorb4<TY, 8, true>);
+  prefer_max_smem(k_absorb4<TY, 8, false>);
+  prefer_max_smem(k_absorb4<TY, 10, true>);
+  prefer_max_smem(k_absorb4<TY, 10, false>);
+  prefer_max_smem(k_absorb4<TY, STR_MAXR, true>);
+  prefer_max_smem(k_absorb4<TY, STR_MAXR, false>);
 }
 
 void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s) {
+  if (g_dbg_skip & 8) return;
   prepare_kernel_attrs();
   int64_t rest = 1, before = 1;
   for (int j = 0; j < ad.nd; ++j)
@@ -560,34 +575,38 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 template <int MR>
 __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
+  // all index arithmetic in 32 bits (the host checks Lk * tk < 2^31): 64-bit division and modulo
+  // are emulated and used to dominate this kernel
   extern __shared__ __align__(16) double tsm[];
-  const int nlb = (int)cdiv(td.Lk, 32);
-  const int64_t unit = blockIdx.x;
-  const int64_t tp = unit / nlb;
-  const int lb = (int)(unit % nlb);
-  const int64_t l0 = (int64_t)lb * 32;
-  const int64_t l1 = (l0 + 32 < td.Lk) ? l0 + 32 : td.Lk;
-  const int64_t e_lo = l0 + td.Lk * tp, e_hi = l1 - 1 + td.Lk * tp;
+  const int Lk = (int)td.Lk;
+  const int nlb = (Lk + 31) / 32;
+  const int unit = blockIdx.x;
+  const int tp = unit / nlb;
+  const int lb = unit - tp * nlb;
+  const int l0 = lb * 32;
+  const int l1 = (l0 + 32 < Lk) ? l0 + 32 : Lk;
+  const int e_lo = l0 + Lk * tp, e_hi = l1 - 1 + Lk * tp;
   const FactorList &fl = td.fl;
   // stage slices (offsets into the shared array, so every later access is a shared-space load)
-  int boff[kMaxFactors];
-  int64_t first[kMaxFactors];
-  int cnt[kMaxFactors];
+  int boff[kMaxFactors], first[kMaxFactors], cnt[kMaxFactors];
   {
     int off = 0;
 #pragma unroll
     for (int f = 0; f < kMaxFactors; ++f) {
       if (f < fl.n) {
         const Factor &F = fl.f[f];
-        const int64_t q0 = e_lo / F.stride, q1 = e_hi / F.stride;
-        const int c = (int)((q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I);
+        const int st = (int)F.stride;
+        const int q0 = e_lo / st, q1 = e_hi / st;
+        const int c = (q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I;
         boff[f] = off;
         first[f] = q0;
         cnt[f] = c;
-        const int AB = F.Ra * F.Rb;
+        const int AB = F.Ra * F.Rb, span = F.I * AB;
+        const int s0 = (q0 % F.I) * AB;   // slices (q0 + j) mod I, j < c, wrap at most once
         for (int e = threadIdx.x; e < c * AB; e += blockDim.x) {
-          const int j = e / AB, w = e % AB;
-          cp_async8(tsm + off + e, F.G + ((q0 + j) % F.I) * AB + w);
+          int idx = s0 + e;
+          if (idx >= span) idx -= span;
+          cp_async8(tsm + off + e, F.G + idx);
         }
         off += ((c * AB + 1) & ~1);
       }
@@ -605,19 +624,24 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
     for (int f = 0; f < kMaxFactors; ++f)
       if (f < fl.n) off += ((cnt[f] * fl.f[f].Ra * fl.f[f].Rb + 1) & ~1);
     tile = (float *)(tsm + off);
-    for (int e = threadIdx.x; e < 2 * Np * 32; e += blockDim.x) tile[e] = 0.0f;
+    for (int e = threadIdx.x; e < 2 * Np * 8; e += blockDim.x) ((float4 *)tile)[e] = make_float4(0, 0, 0, 0);
   }
   cp_async_wait_all();
   __syncthreads();
-  const int el = threadIdx.x / R0, pr = threadIdx.x % R0;
-  const int64_t l = l0 + el;
+  const int el = threadIdx.x / R0, pr = threadIdx.x - (threadIdx.x / R0) * R0;
+  const int l = l0 + el;
   if (el < 32 && l < l1) {
-    const int64_t e = l + td.Lk * tp;
+    const int e = l + Lk * tp;
     double v[MR], w[MR];
+    auto slice = [&](int f) -> const double * {
+      const Factor &F = fl.f[f];
+      int j = e / (int)F.stride - first[f];
+      while (j >= cnt[f]) j -= cnt[f];   // only when the unit spans more than I slices
+      return tsm + boff[f] + j * (F.Ra * F.Rb);
+    };
     {
       const Factor &F = fl.f[0];
-      const int64_t q = e / F.stride;
-      const double *S = tsm + boff[0] + ((q - first[0]) % cnt[0]) * (F.Ra * F.Rb);
+      const double *S = slice(0);
 #pragma unroll
       for (int b = 0; b < MR; ++b) v[b] = (b < F.Rb) ? S[pr + F.Ra * b] : 0.0;
     }
@@ -625,8 +649,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
     for (int f = 1; f < kMaxFactors; ++f) {
       if (f < fl.n) {
         const Factor &F = fl.f[f];
-        const int64_t q = e / F.stride;
-        const double *S = tsm + boff[f] + ((q - first[f]) % cnt[f]) * (F.Ra * F.Rb);
+        const double *S = slice(f);
 #pragma unroll
         for (int b = 0; b < MR; ++b) {
           double acc = 0.0;
@@ -642,7 +665,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
       }
     }
     if (out64) {
-      double *o = out64 + e * (int64_t)W + (int64_t)pr * Rl;
+      double *o = out64 + (int64_t)e * W + pr * Rl;
 #pragma unroll
       for (int q = 0; q < MR; ++q)
         if (q < Rl) o[q] = v[q];
@@ -664,7 +687,7 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
   }
   if (tiles) {
     __syncthreads();
-    float4 *dst = (float4 *)(tiles + unit * (int64_t)(2 * Np * 32));
+    float4 *dst = (float4 *)(tiles + (int64_t)unit * (2 * Np * 32));
     const float4 *src = (const float4 *)tile;
     for (int e = threadIdx.x; e < 2 * Np * 8; e += blockDim.x) dst[e] = src[e];
   }
@@ -684,8 +707,10 @@ size_t table2_smem(const TableDesc &td) {
 }
 
 int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaStream_t s) {
+  if (g_dbg_skip & 2) return 0;
   const size_t smem = table2_smem(td);
   if (smem > 200 * 1024) return -1;
+  if (td.Lk * td.tk >= (int64_t)1 << 31) return -1;   // 32-bit entry indices
   prepare_kernel_attrs();
   const int64_t units = td.tk * cdiv(td.Lk, 32);
   const int threads = (int)cdiv(32 * td.fl.f[0].Ra, 32) * 32;
@@ -813,6 +838,19 @@ void prepare_kernel_attrs() {
   cudaFuncSetAttribute(k_build_table2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_build_table2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_build_table2<STR_MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  prefer_max_smem(k_spd_inv<5>);
+  prefer_max_smem(k_spd_inv<8>);
+  prefer_max_smem(k_chain_gemm);
+  prefer_max_smem(k_gram_z2);
+  prefer_max_smem(k_build_table2<4>);
+  prefer_max_smem(k_build_table2<8>);
+  prefer_max_smem(k_build_table2<10>);
+  prefer_max_smem(k_build_table2<STR_MAXR>);
+  prefer_max_smem(k_axpy_any<float>);
+  prefer_max_smem(k_axpy_any<double>);
+  prefer_max_smem(k_gemm_sk);
+  prefer_max_smem(k_reduce_sk);
+  prepare_f64_attrs();
   done = true;
 }
 

@@ -232,4 +232,22 @@ void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn
   k_append_rows<<<1, 512, 0, s>>>(GN, dT, GNnew, tn * SN, tn, SN);
 }
 
+void prepare_f64_attrs() {
+  prefer_max_smem(k_set_ptr);
+  prefer_max_smem(k_append_rows);
+  prefer_max_smem(k_reduce_splits);
+  prefer_max_smem(k_contract_f64<float, 1, 32>);
+  prefer_max_smem(k_contract_f64<float, 1, 64>);
+  prefer_max_smem(k_contract_f64<float, 1, 128>);
+  prefer_max_smem(k_contract_f64<float, 2, 32>);
+  prefer_max_smem(k_contract_f64<float, 2, 64>);
+  prefer_max_smem(k_contract_f64<float, 2, 128>);
+  prefer_max_smem(k_contract_f64<double, 1, 32>);
+  prefer_max_smem(k_contract_f64<double, 1, 64>);
+  prefer_max_smem(k_contract_f64<double, 1, 128>);
+  prefer_max_smem(k_contract_f64<double, 2, 32>);
+  prefer_max_smem(k_contract_f64<double, 2, 64>);
+  prefer_max_smem(k_contract_f64<double, 2, 128>);
+}
+
 }  // namespace strb200

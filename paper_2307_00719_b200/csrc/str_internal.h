@@ -96,10 +96,12 @@ struct str_state {
   double prof_ms[2] = {0.0, 0.0};
   int64_t prof_n[2] = {0, 0};
   alignas(16) unsigned char tf_params[2][256];
+  alignas(64) unsigned char tf_ymap[2][128];   // CUtensorMap of the pass outputs (TMA reduce epilogue)
   int tf_grid[2] = {0, 0};
   size_t tf_smem[2] = {0, 0};
   bool capturing = false;
   long long *tf_dbg = nullptr;      // device buffer for the contraction pipeline trace (diagnostic)
+  static constexpr int kTfDbgWords = 1024 + 4 * 160;   // per pass
 
   // rSTR
   DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev, sSk;

@@ -19,19 +19,23 @@ def main():
     pas = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     cfg = get_config(name)
     s = make_stream(cfg)
-    X = torch.from_numpy(s.batch(0)).cuda()
+    # distinct batches per run so that X streams from HBM as in the bench (82 MB each > L2 / 2)
+    Xs = [torch.from_numpy(s.batch(b % cfg.n_batches)).cuda() for b in range(4)]
     h = lib.str_init(cfg.N, cfg.dims, cfg.ranks, torch.from_numpy(s.init_slab()).cuda(), cfg.t_init, s.init_cores(),
                      dtype=cfg.dtype, contract="3xtf32", split_k=cfg.split_k)
     L = lib._lib.lib
     L.strdbg_tftrace.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_longlong)]
     L.strdbg_contract.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.POINTER(C.c_double)]
     out = np.zeros(20_000_000)
-    for it in range(3):
+    for it in range(4):
+        X = Xs[it]
         L.strdbg_tftrace(h.ptr, 1, None)
         L.strdbg_contract(h.ptr, C.c_void_p(X.data_ptr()), pas, min(cfg.t_new, cfg.t_init),
                           out.ctypes.data_as(C.POINTER(C.c_double)))
-        tr = np.zeros(1024 + 4 * 160, dtype=np.int64)
-        L.strdbg_tftrace(h.ptr, 0, tr.ctypes.data_as(C.POINTER(C.c_longlong)))
+        W = 1024 + 4 * 160
+        tr2 = np.zeros(2 * W, dtype=np.int64)
+        L.strdbg_tftrace(h.ptr, 0, tr2.ctypes.data_as(C.POINTER(C.c_longlong)))
+        tr = tr2[(pas - 1) * W:pas * W]
     g = tr[1024:].reshape(160, 4)
     g = g[g[:, 0] > 0]
     t00 = g[:, 0].min()
