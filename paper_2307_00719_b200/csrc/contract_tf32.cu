@@ -494,6 +494,13 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 3] = gtimer();
 }
 
+// Y = 0 before the stream-K reductions (a library kernel with the max-shared carve-out, so the SMs
+// keep their configuration between the table kernel, this and the contraction).
+__global__ void __launch_bounds__(256) k_zero_f32(float4 *__restrict__ y, int64_t n4) {
+  for (int64_t i = blockIdx.x * 256 + threadIdx.x; i < n4; i += (int64_t)gridDim.x * 256)
+    y[i] = make_float4(0.f, 0.f, 0.f, 0.f);
+}
+
 }  // namespace strb200
 
 // =============================================================================================
@@ -530,6 +537,7 @@ str_status tf32_prepare(str_state *h) {
     cudaFuncSetAttribute(k_contract_tf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_contract_tf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     prefer_max_smem(k_contract_tf32<1>);
+    prefer_max_smem(k_zero_f32);
     prefer_max_smem(k_contract_tf32<2>);
     // (Npad <= 128 keeps 2 Npad x 128 B of table per stage; 3 stages fit)
     attr = true;
@@ -547,7 +555,7 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
   const int64_t kt1 = cdiv(h->Rr, 32);
   const int64_t kt2 = tn * cdiv(h->L, 32);
   size_t tiles = (size_t)std::max(kt1, kt2) * 2 * Np * 32 * sizeof(float);
-  size_t yf = (size_t)std::max<int64_t>(h->L * tn, h->Rr) * W * sizeof(float);
+  size_t yf = ((size_t)std::max<int64_t>(h->L * tn, h->Rr) * W * sizeof(float) + 15) / 16 * 16;
   auto grow = [&](DevBuf &b, size_t bytes) -> bool {
     if (b.bytes >= bytes) return true;
     if (b.p) cudaFree(b.p);
@@ -672,8 +680,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   memset(&ymap, 0, sizeof(ymap));
   if (p.yred && !encode_y_map(h, &ymap, Y, pass, W, tn)) return -1;
   const int64_t M = pass == 1 ? L * tn : Rr;
-  cudaMemsetAsync(p.Y, 0, (size_t)M * W * sizeof(float), st);
-  tl_mark(h, "memset", 0);
+  {
+    const int64_t n = M * W;   // floats; the buffer is allocated in whole float4s
+    const int64_t n4 = (n + 3) / 4;
+    k_zero_f32<<<(unsigned)std::min<int64_t>(296, (n4 + 255) / 256), 256, 0, st>>>((float4 *)p.Y, n4);
+  }
+  tl_mark(h, "zero_y");
   const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 256;
   prof_mark(h, 2 * (pass - 1));
   if (pass == 1)

@@ -100,138 +100,159 @@ __device__ __forceinline__ bool warp_sweep8(double (&d)[2], int g, int tg) {
 }
 
 // SLOTS = off-diagonal tiles per warp: ceil(nt(nt-1)/2 / (32 - nt)) = 5 for nt <= 13, 8 for nt <= 16
+// The step loop runs from kb = -1 (the prologue: publish V_0, invert tile (0,0)) so that the pivot
+// sweep is instantiated once; tile coordinates come from a shared table (no register arrays).
+// Row stride of the V / W panels is kVS doubles (12: the 8-byte fragment loads of a half-warp hit
+// 32 distinct banks).
+constexpr int kVS = 12;
 template <int kInvMaxSlots>
 __global__ void __launch_bounds__(kInvThreads, 1) k_spd_inv(const double *__restrict__ Q, int S,
                                                               double *__restrict__ Qinv, int *info) {
   extern __shared__ __align__(16) double ism[];
   double *Qs = ism;                                   // S x S staging (in and out)
-  double *Vs0 = Qs + ((S * S + 1) & ~1);              // [2][128*8] pivot column blocks V[i][m]
-  double *Ws = Vs0 + 2 * STR_MAXW * 8;                // [128*8] W = V D
-  double *Ds0 = Ws + STR_MAXW * 8;                    // [2][64] D = A_PP^{-1}
+  double *Vs0 = Qs + ((S * S + 1) & ~1);              // [2][128][kVS] pivot column blocks V[i][m]
+  double *Ws = Vs0 + 2 * STR_MAXW * kVS;              // [128][kVS] W = V D
+  double *Ds0 = Ws + STR_MAXW * kVS;                  // [2][64] D = A_PP^{-1}
   __shared__ int s_bad;
+  __shared__ short s_tile[kInvMaxSlots][32][2];       // (I, J) of slot sl of warp w; I = -1: none
   const int nt = (S + 7) >> 3, Sp = nt * 8;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int g = lane >> 2, tg = lane & 3;
   const int noff = nt * (nt - 1) / 2, nwoff = 32 - nt;
   if (threadIdx.x == 0) s_bad = 0;
-#ifdef INV_PROBE
-  long long tp0 = clock64();
-#endif
-  for (int e = threadIdx.x; e < S * S; e += kInvThreads) cp_async8(Qs + e, Q + e);
-  cp_async_wait_all();
-  __syncthreads();
-  // ---- owned tiles: diagonal warps hold (w, w); the others hold off-diagonal slots
-  const bool diag = warp < nt;
-  double c[kInvMaxSlots][2];
-  int TI[kInvMaxSlots], TJ[kInvMaxSlots];
-#pragma unroll
-  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+  if (threadIdx.x < kInvMaxSlots * 32) {
+    const int sl = threadIdx.x / 32, w = threadIdx.x % 32;
     int I = -1, J = 0;
-    if (diag) {
-      if (sl == 0) I = J = warp;
+    if (w < nt) {
+      if (sl == 0) I = J = w;
     } else {
-      const int tt = (warp - nt) + nwoff * sl;      // off-diagonal tiles, row-major (I > J)
+      const int tt = (w - nt) + nwoff * sl;          // off-diagonal tiles, row-major (I > J)
       if (tt < noff) {
         I = 1;
         while (I * (I + 1) / 2 <= tt) ++I;
         J = tt - I * (I - 1) / 2;
       }
     }
-    TI[sl] = I;
-    TJ[sl] = J;
+    s_tile[sl][w][0] = (short)I;
+    s_tile[sl][w][1] = (short)J;
+  }
+#ifdef INV_PROBE
+  long long tp0 = clock64();
+#endif
+  for (int e = threadIdx.x; e < S * S; e += kInvThreads) cp_async8(Qs + e, Q + e);
+  cp_async_wait_all();
+  __syncthreads();
+  // ---- owned tiles in registers (accumulator layout), symmetrized on load
+  double c[kInvMaxSlots][2];
+#pragma unroll
+  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+    const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
       c[sl][e] = (I >= 0 && i < S && j < S) ? 0.5 * (Qs[i * S + j] + Qs[j * S + i]) : (i == j ? 1.0 : 0.0);
     }
   }
-  // ---- prologue: V_0 = A[:, 0], D_0 by warp 0, W_0 = V_0 D_0
-#pragma unroll
-  for (int sl = 0; sl < kInvMaxSlots; ++sl)
-    if (TI[sl] >= 0 && TJ[sl] == 0) {
-      Vs0[(8 * TI[sl] + g) * 8 + 2 * tg] = c[sl][0];
-      Vs0[(8 * TI[sl] + g) * 8 + 2 * tg + 1] = c[sl][1];
-    }
-  if (warp == 0) {
-    double d[2] = {c[0][0], c[0][1]};
-    if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
-    Ds0[g * 8 + 2 * tg] = -d[0];
-    Ds0[g * 8 + 2 * tg + 1] = -d[1];
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < Sp * 8; e += kInvThreads) {
-    const int i = e >> 3, m = e & 7;
-    double acc = 0.0;
-#pragma unroll
-    for (int l = 0; l < 8; ++l) acc = fma(Vs0[i * 8 + l], Ds0[l * 8 + m], acc);
-    Ws[e] = acc;
-  }
-  __syncthreads();
 #ifdef INV_PROBE
   long long tp1 = clock64();
+  long long pa = 0, pb = 0, pc = 0, pd = 0;
 #endif
-  for (int kb = 0; kb < nt; ++kb) {
-    const int cur = kb & 1, nxt = cur ^ 1;
-    const double *V = Vs0 + cur * STR_MAXW * 8;
-    double *Vn = Vs0 + nxt * STR_MAXW * 8;
+  const bool diag = warp < nt;
+  for (int kb = -1; kb < nt; ++kb) {
+#ifdef INV_PROBE
+    long long q0 = clock64();
+#endif
+    const int cur = (kb + 2) & 1, nxt = cur ^ 1;
+    const double *V = Vs0 + cur * STR_MAXW * kVS;
+    double *Vn = Vs0 + nxt * STR_MAXW * kVS;
     const double *D = Ds0 + cur * 64;
     double *Dn = Ds0 + nxt * 64;
     const int kn = kb + 1;
-#pragma unroll
-    for (int sl = 0; sl < kInvMaxSlots; ++sl) {
-      const int I = TI[sl], J = TJ[sl];
-      if (I < 0) continue;
-      if (I != kb && J != kb) {
-        const double a0 = Ws[(8 * I + g) * 8 + tg], b0 = V[(8 * J + g) * 8 + tg];
-        const double a1 = Ws[(8 * I + g) * 8 + 4 + tg], b1 = V[(8 * J + g) * 8 + 4 + tg];
-        dmma884(c[sl][0], c[sl][1], -a0, b0);
-        dmma884(c[sl][0], c[sl][1], -a1, b1);
-      } else if (I != kb) {          // J == kb: A_RP = W_R
-        c[sl][0] = Ws[(8 * I + g) * 8 + 2 * tg];
-        c[sl][1] = Ws[(8 * I + g) * 8 + 2 * tg + 1];
-      } else if (J != kb) {          // I == kb: A_PR = W_R^T
-        c[sl][0] = Ws[(8 * J + 2 * tg) * 8 + g];
-        c[sl][1] = Ws[(8 * J + 2 * tg + 1) * 8 + g];
-      } else {                        // pivot block: -D
-        c[sl][0] = -D[g * 8 + 2 * tg];
-        c[sl][1] = -D[g * 8 + 2 * tg + 1];
+    if (diag && warp == kn) {
+      // look-ahead warp: bring its tile (kn, kn) up to date, publish it, invert it at once
+      if (kb >= 0) {
+        const double a0 = Ws[(8 * kn + g) * kVS + tg], b0 = V[(8 * kn + g) * kVS + tg];
+        const double a1 = Ws[(8 * kn + g) * kVS + 4 + tg], b1 = V[(8 * kn + g) * kVS + 4 + tg];
+        dmma884(c[0][0], c[0][1], -a0, b0);
+        dmma884(c[0][0], c[0][1], -a1, b1);
       }
-      if (kn < nt) {
-        if (J == kn) {
-          Vn[(8 * I + g) * 8 + 2 * tg] = c[sl][0];
-          Vn[(8 * I + g) * 8 + 2 * tg + 1] = c[sl][1];
-          if (I == kn) {              // look-ahead: invert the next pivot block right away
-            double d[2] = {c[sl][0], c[sl][1]};
-            if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
-            Dn[g * 8 + 2 * tg] = -d[0];
-            Dn[g * 8 + 2 * tg + 1] = -d[1];
+      Vn[(8 * kn + g) * kVS + 2 * tg] = c[0][0];
+      Vn[(8 * kn + g) * kVS + 2 * tg + 1] = c[0][1];
+      double d[2] = {c[0][0], c[0][1]};
+      if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
+      Dn[g * 8 + 2 * tg] = -d[0];
+      Dn[g * 8 + 2 * tg + 1] = -d[1];
+    } else {
+#pragma unroll
+      for (int sl = 0; sl < kInvMaxSlots; ++sl) {
+        const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
+        if (I < 0) continue;
+        if (kb >= 0) {
+          if (I != kb && J != kb) {
+            const double a0 = Ws[(8 * I + g) * kVS + tg], b0 = V[(8 * J + g) * kVS + tg];
+            const double a1 = Ws[(8 * I + g) * kVS + 4 + tg], b1 = V[(8 * J + g) * kVS + 4 + tg];
+            dmma884(c[sl][0], c[sl][1], -a0, b0);
+            dmma884(c[sl][0], c[sl][1], -a1, b1);
+          } else if (I != kb) {          // J == kb: A_RP = W_R
+            c[sl][0] = Ws[(8 * I + g) * kVS + 2 * tg];
+            c[sl][1] = Ws[(8 * I + g) * kVS + 2 * tg + 1];
+          } else if (J != kb) {          // I == kb: A_PR = W_R^T
+            c[sl][0] = Ws[(8 * J + 2 * tg) * kVS + g];
+            c[sl][1] = Ws[(8 * J + 2 * tg + 1) * kVS + g];
+          } else {                        // pivot block: -D
+            c[sl][0] = -D[g * 8 + 2 * tg];
+            c[sl][1] = -D[g * 8 + 2 * tg + 1];
           }
-        } else if (I == kn) {        // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
-          Vn[(8 * J + 2 * tg) * 8 + g] = c[sl][0];
-          Vn[(8 * J + 2 * tg + 1) * 8 + g] = c[sl][1];
+        }
+        if (kn < nt) {
+          if (J == kn) {                 // (I == kn == J is the look-ahead warp's tile)
+            Vn[(8 * I + g) * kVS + 2 * tg] = c[sl][0];
+            Vn[(8 * I + g) * kVS + 2 * tg + 1] = c[sl][1];
+          } else if (I == kn) {          // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
+            Vn[(8 * J + 2 * tg) * kVS + g] = c[sl][0];
+            Vn[(8 * J + 2 * tg + 1) * kVS + g] = c[sl][1];
+          }
         }
       }
     }
+#ifdef INV_PROBE
+    long long q1 = clock64();
+#endif
     __syncthreads();
+#ifdef INV_PROBE
+    long long q2 = clock64();
+#endif
     if (kn < nt) {
-      for (int e = threadIdx.x; e < Sp * 8; e += kInvThreads) {
-        const int i = e >> 3, m = e & 7;
+      if (threadIdx.x < Sp * 8) {
+        const int e = threadIdx.x, i = e >> 3, m = e & 7;
         double acc = 0.0;
 #pragma unroll
-        for (int l = 0; l < 8; ++l) acc = fma(Vn[i * 8 + l], Dn[l * 8 + m], acc);
-        Ws[e] = acc;
+        for (int l = 0; l < 8; ++l) acc = fma(Vn[i * kVS + l], Dn[l * 8 + m], acc);
+        Ws[i * kVS + m] = acc;
       }
+#ifdef INV_PROBE
+      pc += clock64() - q2;
+#endif
       __syncthreads();
     }
+#ifdef INV_PROBE
+    pa += q1 - q0;
+    pb += q2 - q1;
+    pd += clock64() - q0;
+    if (warp == (kn < nt ? kn : 0) && lane == 0) {   // the look-ahead warp of this step
+      atomicAdd((unsigned long long *)&g_inv_probe[4], (unsigned long long)(q1 - q0));
+    }
+#endif
   }
 #ifdef INV_PROBE
+  if (threadIdx.x == 32 * 20) { g_inv_probe[3] = pa; g_inv_probe[5] = pb; g_inv_probe[6] = pc; g_inv_probe[7] = pd; }
   long long tp2 = clock64();
 #endif
   if (threadIdx.x == 0 && s_bad && info) atomicExch(info, 1);
   // ---- -A -> Qinv through shared memory (both triangles), coalesced store
 #pragma unroll
   for (int sl = 0; sl < kInvMaxSlots; ++sl) {
-    const int I = TI[sl], J = TJ[sl];
+    const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
     if (I < 0) continue;
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
@@ -252,7 +273,7 @@ __global__ void __launch_bounds__(kInvThreads, 1) k_spd_inv(const double *__rest
 }
 
 size_t spd_inv_smem(int S) {
-  return sizeof(double) * ((size_t)((S * S + 1) & ~1) + 3 * STR_MAXW * 8 + 2 * 64);
+  return sizeof(double) * ((size_t)((S * S + 1) & ~1) + 3 * STR_MAXW * kVS + 2 * 64);
 }
 
 void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {

@@ -1121,3 +1121,33 @@ extern "C" STR_API str_status strdbg_contract(str_state *h, const void *X, int32
   }
   return STR_OK;
 }
+
+// Launch-cost probe (diagnostic, not in include/str.h): builds the pass's table once, then times
+// `reps` back-to-back launches of only the contraction (memset + kernel) between two events on the
+// library stream; returns the average milliseconds per launch in *ms.
+extern "C" STR_API str_status strdbg_contract_repeat(str_state *h, const void *X, int32_t pass, int64_t tn, int32_t reps,
+                                                     double *ms) {
+  if (!h || !X || !ms || (pass != 1 && pass != 2) || tn < 1 || tn > h->T || reps < 1) return STR_E_ARG;
+  if (h->contract != STR_CONTRACT_3XTF32) return STR_E_ARG;
+  TRY(ensure_workspace(h, tn));
+  const int W = RR(h, h->k + 1) * RR(h, h->N);
+  const void *Y;
+  bool y32;
+  TRY(set_x(h, X));
+  TRY(contract(h, X, pass, (const double *)h->GN.p, tn, &Y, &y32));
+  cudaEvent_t e0, e1;
+  CU(cudaEventCreate(&e0));
+  CU(cudaEventCreate(&e1));
+  float *out = (float *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
+  CU(cudaEventRecord(e0, h->st));
+  for (int i = 0; i < reps; ++i)
+    if (launch_contract_tf32(h, X, pass, W, tn, out) != 0) return fail(h, STR_E_CUDA, h->err);
+  CU(cudaEventRecord(e1, h->st));
+  CU(cudaEventSynchronize(e1));
+  float t = 0.0f;
+  CU(cudaEventElapsedTime(&t, e0, e1));
+  *ms = t / reps;
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  return STR_OK;
+}

@@ -26,9 +26,15 @@ def main():
     L = lib._lib.lib
     L.strdbg_tftrace.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_longlong)]
     L.strdbg_tftrace(h.ptr, 1, None)
+    prof = "--prof" in sys.argv
+    if prof:
+        lib.str_set_profiling(h, True)
     for i in range(12):
         lib.str_update_batch(h, xs[i % 6], cfg.t_new)
     lib.str_sync(h)
+    if prof:
+        p1, n1, p2, n2 = lib.str_profile(h)
+        print(f"events (profiling graph): pass 1 {1e3 * p1 / max(n1, 1):.2f} us, pass 2 {1e3 * p2 / max(n2, 1):.2f} us")
     W = 1024 + 4 * 160
     tr = np.zeros(2 * W, dtype=np.int64)
     L.strdbg_tftrace(h.ptr, 0, tr.ctypes.data_as(C.POINTER(C.c_longlong)))

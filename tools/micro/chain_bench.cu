@@ -7,6 +7,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <vector>
+namespace strb200 { void prepare_f64_attrs() {} }
 using namespace strb200;
 
 template <typename F>
@@ -200,8 +201,17 @@ int main(int argc, char **argv) {
   printf("S=%d I=%d  empty %.2f us | spd_inv %.2f us | rows_mm %.2f us | chain_gemm %.2f us | gram %.2f us\n", S, I,
          t_empty, t_inv, t_rows, t_gemm, t_gram);
   long long pr[8];
+  {
+    long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    cudaMemcpyToSymbol(g_inv_probe, z, sizeof(z));
+    launch_spd_inv(dQ, S, dQi, info, 0);
+    cudaDeviceSynchronize();
+  }
   cudaMemcpyFromSymbol(pr, g_inv_probe, sizeof(pr));
   printf("spd_inv cycles: load %lld  sweep %lld (%.0f/block step)  store %lld\n", pr[0], pr[1], pr[1] / (double)((S + 7) / 8), pr[2]);
+  const int nt = (S + 7) / 8;
+  printf("  per step (warp 20): slots %.0f  sync1 %.0f  W %.0f  total %.0f | look-ahead warps' slot+sweep %.0f (summed over %d launches)\n",
+         pr[3] / (double)nt, pr[5] / (double)nt, pr[6] / (double)nt, pr[7] / (double)nt, pr[4] / (double)nt, 1);
 
   printf("residual ||G Q - P||/||P|| = %.2e  info=%d  err=%s\n", sqrt(err / nrm), hinfo,
          cudaGetErrorString(cudaGetLastError()));
