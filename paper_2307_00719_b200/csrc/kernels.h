@@ -13,6 +13,7 @@ namespace strb200 {
 // Results are meaningless while it is non-zero.  1 spd_inv, 2 tables, 4 contraction, 8 absorbs,
 // 16 chain GEMMs, 32 row GEMMs, 64 Z Grams.
 extern int g_dbg_skip;
+extern int g_gemm_stage;
 
 // kernels_small.cu
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);

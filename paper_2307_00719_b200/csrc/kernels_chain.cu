@@ -13,10 +13,12 @@
 
 #include "common.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace strb200 {
 
 int g_dbg_skip = 0;
+int g_gemm_stage = -1;   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
 
 void prepare_kernel_attrs();
 
@@ -295,36 +297,91 @@ void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_
 // (Def. 1 P:126 applied to the chain result).  Q is left unsymmetrized; k_spd_inv symmetrizes.
 // Used for the Gram-chain links and for G = P Q^{-1} (M = I rows).
 
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
+               : "memory");
+}
+
+// STAGE 0: 8-byte cp.async; 1: 16-byte cp.async (16-byte aligned rows); 2: cp.async.bulk row copies
+template <int STAGE>
 __global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A, const double *__restrict__ B,
                                                     double *__restrict__ C, int M, int N, int K, QEpi q) {
   extern __shared__ __align__(16) double gsm[];
-  double *AsT = gsm;            // [K][32]  (k-major A block)
-  double *Bs = gsm + K * 32;    // [K][32]
+  // BULK: A rows [32][K] and B rows [K][32] arrive by cp.async.bulk row copies (16-byte aligned rows);
+  // otherwise by 8-byte cp.async.  A is read row-major (4 broadcast loads per k), B per lane.
+  double *As = gsm;             // [32][K]
+  double *Bs = gsm + 32 * K;    // [K][32]
+  __shared__ __align__(8) uint64_t bar;
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
-  for (int e = threadIdx.x; e < 32 * K; e += 256) {
-    const int r = e / K, k = e % K;          // A row-major: consecutive threads read consecutive k
-    if (row0 + r < M) cp_async8(AsT + k * 32 + r, A + (int64_t)(row0 + r) * K + k);
-    else AsT[k * 32 + r] = 0.0;
+  const int mr = min(32, M - row0), nc = min(32, N - col0);
+  if (STAGE == 2) {
+    if (threadIdx.x == 0) {
+      tc::mbar_init(&bar, 1);
+      tc::fence_barrier_init();
+    }
+    // zero what no copy writes (rows of A beyond M, columns of B beyond N)
+    for (int e = threadIdx.x; e < (32 - mr) * K; e += 256) As[mr * K + e] = 0.0;
+    if (nc < 32)
+      for (int e = threadIdx.x; e < K * (32 - nc); e += 256) Bs[(e / (32 - nc)) * 32 + nc + e % (32 - nc)] = 0.0;
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&bar, (uint32_t)((mr * K + K * nc) * 8));
+      __syncwarp();
+      for (int r = threadIdx.x; r < mr; r += 32)
+        tc::bulk_load(As + r * K, A + (int64_t)(row0 + r) * K, (uint32_t)(K * 8), &bar);
+      for (int k = threadIdx.x; k < K; k += 32)
+        tc::bulk_load(Bs + k * 32, B + (int64_t)k * N + col0, (uint32_t)(nc * 8), &bar);
+    }
+    tc::mbar_wait(&bar, 0);
+  } else if (STAGE == 1) {
+    const int K2 = K >> 1;   // 16-byte chunks per A row
+    for (int e = threadIdx.x; e < 32 * K2; e += 256) {
+      const int r = e / K2;
+      if (r < mr) cp_async16(As + 2 * e, A + (int64_t)row0 * K + 2 * e);
+      else *(double2 *)(As + 2 * e) = make_double2(0.0, 0.0);
+    }
+    for (int e = threadIdx.x; e < 16 * K; e += 256) {
+      const int kk = e >> 4, c = 2 * (e & 15);
+      if (c < nc) cp_async16(Bs + kk * 32 + c, B + (int64_t)kk * N + col0 + c);
+      else *(double2 *)(Bs + kk * 32 + c) = make_double2(0.0, 0.0);
+    }
+    cp_async_wait_all();
+    __syncthreads();
+  } else {
+    for (int e = threadIdx.x; e < 32 * K; e += 256) {
+      const int r = e / K;
+      if (r < mr) cp_async8(As + e, A + (int64_t)row0 * K + e);
+      else As[e] = 0.0;
+    }
+    for (int e = threadIdx.x; e < 32 * K; e += 256) {
+      const int k = e >> 5, c = e & 31;
+      if (c < nc) cp_async8(Bs + k * 32 + c, B + (int64_t)k * N + col0 + c);
+      else Bs[k * 32 + c] = 0.0;
+    }
+    cp_async_wait_all();
+    __syncthreads();
   }
-  for (int e = threadIdx.x; e < 32 * K; e += 256) {
-    const int k = e >> 5, c = e & 31;
-    if (col0 + c < N) cp_async8(Bs + k * 32 + c, B + (int64_t)k * N + col0 + c);
-    else Bs[k * 32 + c] = 0.0;
+  // two interleaved k-halves (even / odd k): eight independent FMA chains of length K/2
+  double acc[4] = {0.0, 0.0, 0.0, 0.0}, acd[4] = {0.0, 0.0, 0.0, 0.0};
+  const double *a0 = As + (4 * ty) * K;
+  int k = 0;
+#pragma unroll 2
+  for (; k + 1 < K; k += 2) {
+    const double b = Bs[k * 32 + tx], b1 = Bs[(k + 1) * 32 + tx];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      acc[u] = fma(a0[u * K + k], b, acc[u]);
+      acd[u] = fma(a0[u * K + k + 1], b1, acd[u]);
+    }
   }
-  cp_async_wait_all();
-  __syncthreads();
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-#pragma unroll 4
-  for (int k = 0; k < K; ++k) {
+  if (k < K) {
     const double b = Bs[k * 32 + tx];
-    const double2 a01 = *(const double2 *)(AsT + k * 32 + 4 * ty);
-    const double2 a23 = *(const double2 *)(AsT + k * 32 + 4 * ty + 2);
-    acc[0] = fma(a01.x, b, acc[0]);
-    acc[1] = fma(a01.y, b, acc[1]);
-    acc[2] = fma(a23.x, b, acc[2]);
-    acc[3] = fma(a23.y, b, acc[3]);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = fma(a0[u * K + k], b, acc[u]);
   }
+#pragma unroll
+  for (int u = 0; u < 4; ++u) acc[u] += acd[u];
 #pragma unroll
   for (int u = 0; u < 4; ++u) {
     const int row = row0 + 4 * ty + u, col = col0 + tx;
@@ -341,11 +398,113 @@ __global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A
   }
 }
 
+// C = A B (fp64, row-major) on the FP64 tensor-core fragments (mma.sync m8n8k4): one 16 x 16
+// output tile per CTA (2 x 2 DMMA tiles), 8 warps = 4 tiles x 2 halves of K, so each warp runs one
+// accumulator chain over ceil(K/8) k-steps and the halves meet in shared memory.  A rows (stride
+// Ka = K rounded to 4 mod 16) and B rows (stride 20) make the fragment loads of a half-warp hit 32
+// distinct banks.  Epilogue as k_chain_gemm (q.mode).
+constexpr int kGbS = 20;   // B row stride (doubles)
+__host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
+template <bool AL16>
+__global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restrict__ A, const double *__restrict__ B,
+                                                         double *__restrict__ C, int M, int N, int K, QEpi q) {
+  extern __shared__ __align__(16) double gsm[];
+  const int Ka = gemm_ka(K), K4 = (K + 3) / 4 * 4;
+  double *As = gsm;                 // [16][Ka]
+  double *Bs = gsm + 16 * Ka;       // [K4][kGbS]
+  double *Rs = Bs + K4 * kGbS;      // [4 tiles][32 lanes][2] partials of the upper K half
+  const int row0 = blockIdx.y * 16, col0 = blockIdx.x * 16;
+  const int mr = min(16, M - row0), nc = min(16, N - col0);
+  // zero-fill: A rows >= mr and k >= K; B rows k >= K and columns >= nc
+  for (int e = threadIdx.x; e < 16 * (K4 - K); e += 256) As[(e / (K4 - K)) * Ka + K + e % (K4 - K)] = 0.0;
+  for (int e = threadIdx.x; e < (16 - mr) * K; e += 256) As[(mr + e / K) * Ka + e % K] = 0.0;
+  for (int e = threadIdx.x; e < (K4 - K) * 16; e += 256) Bs[(K + e / 16) * kGbS + e % 16] = 0.0;
+  if (nc < 16)
+    for (int e = threadIdx.x; e < K * (16 - nc); e += 256) Bs[(e / (16 - nc)) * kGbS + nc + e % (16 - nc)] = 0.0;
+  if (AL16) {
+    const int K2 = K >> 1, n2 = nc >> 1;
+    for (int e = threadIdx.x; e < mr * K2; e += 256) {
+      const int r = e / K2, c = 2 * (e - r * K2);
+      cp_async16(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+    }
+    for (int e = threadIdx.x; e < K * n2; e += 256) {
+      const int k = e / n2, c = 2 * (e - k * n2);
+      cp_async16(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
+    }
+  } else {
+    for (int e = threadIdx.x; e < mr * K; e += 256) {
+      const int r = e / K, c = e - r * K;
+      cp_async8(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+    }
+    for (int e = threadIdx.x; e < K * nc; e += 256) {
+      const int k = e / nc, c = e - k * nc;
+      cp_async8(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
+    }
+  }
+  cp_async_wait_all();
+  __syncthreads();
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int tile = warp & 3, half = warp >> 2, ti = tile >> 1, tj = tile & 1;
+  const int nks = K4 / 4, ks0 = half ? (nks + 1) / 2 : 0, ks1 = half ? nks : (nks + 1) / 2;
+  double c0 = 0.0, c1 = 0.0;
+  const double *ap = As + (8 * ti + g) * Ka + tg;
+  const double *bp = Bs + tg * kGbS + 8 * tj + g;
+#pragma unroll 4
+  for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks], bp[4 * ks * kGbS]);
+  if (half) {
+    Rs[(tile * 32 + lane) * 2] = c0;
+    Rs[(tile * 32 + lane) * 2 + 1] = c1;
+  }
+  __syncthreads();
+  if (half) return;
+  c0 += Rs[(tile * 32 + lane) * 2];
+  c1 += Rs[(tile * 32 + lane) * 2 + 1];
+  const int row = row0 + 8 * ti + g;
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int col = col0 + 8 * tj + 2 * tg + e;
+    const double v = e ? c1 : c0;
+    if (row < M && col < N) {
+      if (q.mode == 0) {
+        C[(int64_t)row * N + col] = v;
+      } else {
+        const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
+        const int S = q.Rn * q.Rn1;
+        double *dst = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
+        *dst = (q.mode == 1) ? v : *dst + v;
+      }
+    }
+  }
+}
+
+static size_t gemm_dmma_smem(int K) {
+  return sizeof(double) * ((size_t)16 * gemm_ka(K) + (size_t)(K + 3) / 4 * 4 * kGbS + 4 * 32 * 2);
+}
+
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
   if (g_dbg_skip & 16) return;
   prepare_kernel_attrs();
   dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32));
-  k_chain_gemm<<<grid, 256, (size_t)2 * K * 32 * sizeof(double), s>>>(A, B, C, M, N, K, q);
+  const bool al16 = (K % 2 == 0) && (N % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  if (g_gemm_stage < 0 || g_gemm_stage == 3) {   // default: FP64 tensor-core fragments
+    dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
+    const size_t smd = gemm_dmma_smem(K);
+    if (al16)
+      k_chain_gemm_dmma<true><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+    else
+      k_chain_gemm_dmma<false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+    return;
+  }
+  const size_t sm = (size_t)2 * K * 32 * sizeof(double);
+  int mode = al16 ? 1 : 0;
+  if (g_gemm_stage >= 0 && (al16 || g_gemm_stage == 0)) mode = g_gemm_stage;
+  if (mode == 2)
+    k_chain_gemm<2><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
+  else if (mode == 1)
+    k_chain_gemm<1><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
+  else
+    k_chain_gemm<0><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
 }
 
 void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s) {
@@ -852,7 +1011,13 @@ void prepare_kernel_attrs() {
   if (done) return;
   cudaFuncSetAttribute(k_spd_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
   cudaFuncSetAttribute(k_spd_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
-  cudaFuncSetAttribute(k_chain_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
+  cudaFuncSetAttribute(k_chain_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
+  cudaFuncSetAttribute(k_chain_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
+  cudaFuncSetAttribute(k_chain_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
+  cudaFuncSetAttribute(k_chain_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
+  cudaFuncSetAttribute(k_chain_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
+  prefer_max_smem(k_chain_gemm_dmma<true>);
+  prefer_max_smem(k_chain_gemm_dmma<false>);
   absorb_attrs<float>();
   absorb_attrs<double>();
   cudaFuncSetAttribute(k_build_table2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
@@ -861,7 +1026,9 @@ void prepare_kernel_attrs() {
   cudaFuncSetAttribute(k_build_table2<STR_MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   prefer_max_smem(k_spd_inv<5>);
   prefer_max_smem(k_spd_inv<8>);
-  prefer_max_smem(k_chain_gemm);
+  prefer_max_smem(k_chain_gemm<0>);
+  prefer_max_smem(k_chain_gemm<1>);
+  prefer_max_smem(k_chain_gemm<2>);
   prefer_max_smem(k_gram_z2);
   prefer_max_smem(k_build_table2<4>);
   prefer_max_smem(k_build_table2<8>);

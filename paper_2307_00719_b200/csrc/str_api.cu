@@ -507,18 +507,54 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   TRY(check_launch(h, "temporal solve"));
   launch_gram_z2(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);  // Z_N^new
   tl_mark(h, "gram_z");
-  // modes 1..N-1 in order (Gauss-Seidel)
-  bool Lp_id = true;
-  int lp_cur = 0;
+  // modes 1..N-1 in order (Gauss-Seidel).  Gram chain of mode j (Prop. 1 with the new Z's before
+  // j and the old ones after): H_j = Lp_j Z_N^new Sf_j, Lp_j = Z_{j-1} ... Z_1.  Carried as
+  // T1_j = Lp_j Z_N^new (T1_1 = Z_N^new, T1_{j+1} = Z_j T1_j) and B_{j+1} = T1_j Sf_{j+1}, both
+  // formed on the main stream while mode j's inverse runs, so that once Z_j is known the critical
+  // path to Q_{j+1} is the single product H_{j+1} = Z_j B_{j+1}.
+  const double *T1cur = (const double *)h->ZmN.p;   // T1_j (R_j^2 x R_N^2)
+  int t1buf = 0;
+  const double *Bj = nullptr;                       // B_j (R_{j-1}^2 x R_{j+1}^2), j >= 2
   const void *YR = nullptr;
   bool yr32 = false;
   for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
-    // side: Q_j += H^{≠j}_new (l.15-16), Q_j^{-1}
+    // side: Q_j += H_j<2> (l.15-16), Q_j^{-1}
     TRY(fork(h));
-    TRY(q_update(h, j, (const double *)h->Lp[lp_cur].p, Lp_id, (const double *)h->ZmN.p, 1, (double *)m.Q.p));
+    {
+      const QEpi q{(double *)m.Q.p, RR(h, j), RR(h, j + 1), 2};
+      if (j == 1) {   // H_1 = Z_N^new Sf_1  (R_1^2 x R_N^2 . R_N^2 x R_2^2)
+        if (N - 1 == 1) return fail(h, STR_E_ARG, "order N >= 3 required");
+        launch_chain_gemm((const double *)h->ZmN.p, (const double *)h->Sf[1].p, nullptr, RR(h, 1) * RR(h, 1),
+                          RR(h, 2) * RR(h, 2), RR(h, N) * RR(h, N), q, h->st);
+      } else {        // H_j = Z_{j-1} B_j  (R_j^2 x R_{j-1}^2 . R_{j-1}^2 x R_{j+1}^2)
+        launch_chain_gemm((const double *)h->md[j - 2].Zm.p, Bj, nullptr, RR(h, j) * RR(h, j),
+                          RR(h, j + 1) * RR(h, j + 1), RR(h, j - 1) * RR(h, j - 1), q, h->st);
+      }
+      tl_mark(h, "chain_gemm_q");
+      TRY(check_launch(h, "chain_gemm_q"));
+    }
     TRY(invert_mode(h, j));
     main_again(h);
+    // main: T1_j and B_{j+1} for the next mode (off the critical path)
+    if (j + 1 <= N - 1) {
+      if (j >= 2) {   // T1_j = Z_{j-1} T1_{j-1}
+        double *t1n = (double *)h->Lp[t1buf].p;
+        TRY(chain_mul(h, (const double *)h->md[j - 2].Zm.p, false, T1cur, false, t1n, RR(h, j) * RR(h, j),
+                      RR(h, N) * RR(h, N), RR(h, j - 1) * RR(h, j - 1)));
+        T1cur = t1n;
+        t1buf ^= 1;
+      }
+      if (j + 1 == N - 1) {
+        Bj = T1cur;   // Sf_{N-1} = I
+      } else {        // B_{j+1} = T1_j Sf_{j+1}  (R_j^2 x R_N^2 . R_N^2 x R_{j+2}^2)
+        // (ping-pong: the side stream may still be reading B_j while B_{j+1} is formed)
+        double *bn = (double *)((j & 1) ? h->T1.p : h->H.p);
+        TRY(chain_mul(h, T1cur, false, (const double *)h->Sf[j + 1].p, false, bn, RR(h, j) * RR(h, j),
+                      RR(h, j + 2) * RR(h, j + 2), RR(h, N) * RR(h, N)));
+        Bj = bn;
+      }
+    }
     // main: P_j += X_new[j] G^{≠j}_new (l.13-14)
     if (j <= k) {
       left_modes(h, modes, dims);
@@ -550,13 +586,6 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     }
     TRY(join(h));
     TRY(finish_mode(h, j));
-    if (j < N - 1) {   // Lp_{j+1} = Zm_j * Lp_j
-      int M = RR(h, j + 1) * RR(h, j + 1), K = RR(h, j) * RR(h, j), Nc = RR(h, 1) * RR(h, 1);
-      TRY(chain_mul(h, (const double *)m.Zm.p, false, (const double *)h->Lp[lp_cur].p, Lp_id,
-                    (double *)h->Lp[1 - lp_cur].p, M, Nc, K));
-      lp_cur = 1 - lp_cur;
-      Lp_id = false;
-    }
   }
   // l.10: append the new temporal rows
   launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, h->SN, h->st);

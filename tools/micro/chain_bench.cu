@@ -154,6 +154,25 @@ int main(int argc, char **argv) {
   float t_ginv = time_us([&] { cudaGraphLaunch(ge, st); }, 10) / 10.f;
   cudaStreamSynchronize(st);
   printf("graph: %.2f us per empty node, %.2f us per spd_inv node\n", t_graph, t_ginv);
+  // graph-node cost of the chain GEMM (S x S x S and I x S x S) per staging mode
+  for (int mode = 0; mode < 4; ++mode) {
+    g_gemm_stage = mode;
+    float tg[2];
+    for (int w = 0; w < 2; ++w) {
+      cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal);
+      for (int i = 0; i < 20; ++i) {
+        if (w == 0) launch_chain_gemm(dA, dB, dC, S, S, S, QEpi{nullptr, 0, 0, 0}, st);
+        else launch_rows_mm(dP, dQi, S, I, dG, st);
+      }
+      cudaStreamEndCapture(st, &g);
+      cudaGraphInstantiate(&ge, g, 0);
+      tg[w] = time_us([&] { cudaGraphLaunch(ge, st); }, 10) / 20.f;
+      cudaStreamSynchronize(st);
+    }
+    printf("graph: chain_gemm stage %d: %.2f us per %dx%dx%d node, %.2f us per rows_mm (%d rows) node\n", mode, tg[0], S, S,
+           S, tg[1], I);
+  }
+  g_gemm_stage = -1;
   {
     // C5-shaped absorbs: Y_L (i1, i2, t) 40 x 40 x 8 entries 10x10 (fp32), contract i2 with G_2 slices
     float *Yf; double *Ad, *Od, *Wd;
