@@ -14,6 +14,8 @@ namespace strb200 {
 // 16 chain GEMMs, 32 row GEMMs, 64 Z Grams.
 extern int g_dbg_skip;
 extern int g_gemm_stage;
+extern int g_absorb_v5;
+extern int g_table_v3;
 
 // kernels_small.cu
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);

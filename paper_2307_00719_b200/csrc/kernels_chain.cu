@@ -18,7 +18,9 @@
 namespace strb200 {
 
 int g_dbg_skip = 0;
-int g_gemm_stage = -1;   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
+int g_gemm_stage = -1;
+int g_table_v3 = 1;       // diagnostic switch: 0 keeps the generic table kernel
+int g_absorb_v5 = 1;      // diagnostic switch: 1 k_absorb6 (tensor-core fragments), 2 k_absorb5, 0 k_absorb4   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
 
 void prepare_kernel_attrs();
 
@@ -405,36 +407,59 @@ __global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A
 // distinct banks.  Epilogue as k_chain_gemm (q.mode).
 constexpr int kGbS = 20;   // B row stride (doubles)
 __host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
-template <bool AL16>
+// TA: A is given transposed (K x M row-major, A_eff[m][k] = A[k M + m]) and staged like B.
+// q.mode 3: Gram-chain epilogue, C = G^T G -> Z[(a + Rb c)][(b + Ra d)] = C[b + Ra a][d + Ra c]
+// (Ra = q.Rn, Rb = q.Rn1; the layout of k_gram_z2).
+template <bool AL16, bool TA>
 __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restrict__ A, const double *__restrict__ B,
                                                          double *__restrict__ C, int M, int N, int K, QEpi q) {
   extern __shared__ __align__(16) double gsm[];
-  const int Ka = gemm_ka(K), K4 = (K + 3) / 4 * 4;
-  double *As = gsm;                 // [16][Ka]
-  double *Bs = gsm + 16 * Ka;       // [K4][kGbS]
+  const int Ka = TA ? 0 : gemm_ka(K), K4 = (K + 3) / 4 * 4;
+  double *As = gsm;                 // [16][Ka], or TA: [K4][kGbS]
+  double *Bs = gsm + (TA ? K4 * kGbS : 16 * Ka);   // [K4][kGbS]
   double *Rs = Bs + K4 * kGbS;      // [4 tiles][32 lanes][2] partials of the upper K half
   const int row0 = blockIdx.y * 16, col0 = blockIdx.x * 16;
   const int mr = min(16, M - row0), nc = min(16, N - col0);
   // zero-fill: A rows >= mr and k >= K; B rows k >= K and columns >= nc
-  for (int e = threadIdx.x; e < 16 * (K4 - K); e += 256) As[(e / (K4 - K)) * Ka + K + e % (K4 - K)] = 0.0;
-  for (int e = threadIdx.x; e < (16 - mr) * K; e += 256) As[(mr + e / K) * Ka + e % K] = 0.0;
+  if (TA) {
+    for (int e = threadIdx.x; e < (K4 - K) * 16; e += 256) As[(K + e / 16) * kGbS + e % 16] = 0.0;
+    if (mr < 16)
+      for (int e = threadIdx.x; e < K * (16 - mr); e += 256) As[(e / (16 - mr)) * kGbS + mr + e % (16 - mr)] = 0.0;
+  } else {
+    for (int e = threadIdx.x; e < 16 * (K4 - K); e += 256) As[(e / (K4 - K)) * Ka + K + e % (K4 - K)] = 0.0;
+    for (int e = threadIdx.x; e < (16 - mr) * K; e += 256) As[(mr + e / K) * Ka + e % K] = 0.0;
+  }
   for (int e = threadIdx.x; e < (K4 - K) * 16; e += 256) Bs[(K + e / 16) * kGbS + e % 16] = 0.0;
   if (nc < 16)
     for (int e = threadIdx.x; e < K * (16 - nc); e += 256) Bs[(e / (16 - nc)) * kGbS + nc + e % (16 - nc)] = 0.0;
   if (AL16) {
-    const int K2 = K >> 1, n2 = nc >> 1;
-    for (int e = threadIdx.x; e < mr * K2; e += 256) {
-      const int r = e / K2, c = 2 * (e - r * K2);
-      cp_async16(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+    const int K2 = K >> 1, n2 = nc >> 1, m2 = mr >> 1;
+    if (TA) {
+      for (int e = threadIdx.x; e < K * m2; e += 256) {
+        const int k = e / m2, c = 2 * (e - k * m2);
+        cp_async16(As + k * kGbS + c, A + (int64_t)k * M + row0 + c);
+      }
+    } else {
+      for (int e = threadIdx.x; e < mr * K2; e += 256) {
+        const int r = e / K2, c = 2 * (e - r * K2);
+        cp_async16(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+      }
     }
     for (int e = threadIdx.x; e < K * n2; e += 256) {
       const int k = e / n2, c = 2 * (e - k * n2);
       cp_async16(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
     }
   } else {
-    for (int e = threadIdx.x; e < mr * K; e += 256) {
-      const int r = e / K, c = e - r * K;
-      cp_async8(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+    if (TA) {
+      for (int e = threadIdx.x; e < K * mr; e += 256) {
+        const int k = e / mr, c = e - k * mr;
+        cp_async8(As + k * kGbS + c, A + (int64_t)k * M + row0 + c);
+      }
+    } else {
+      for (int e = threadIdx.x; e < mr * K; e += 256) {
+        const int r = e / K, c = e - r * K;
+        cp_async8(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
+      }
     }
     for (int e = threadIdx.x; e < K * nc; e += 256) {
       const int k = e / nc, c = e - k * nc;
@@ -448,10 +473,16 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
   const int tile = warp & 3, half = warp >> 2, ti = tile >> 1, tj = tile & 1;
   const int nks = K4 / 4, ks0 = half ? (nks + 1) / 2 : 0, ks1 = half ? nks : (nks + 1) / 2;
   double c0 = 0.0, c1 = 0.0;
-  const double *ap = As + (8 * ti + g) * Ka + tg;
   const double *bp = Bs + tg * kGbS + 8 * tj + g;
+  if (TA) {
+    const double *ap = As + tg * kGbS + 8 * ti + g;
 #pragma unroll 4
-  for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks], bp[4 * ks * kGbS]);
+    for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks * kGbS], bp[4 * ks * kGbS]);
+  } else {
+    const double *ap = As + (8 * ti + g) * Ka + tg;
+#pragma unroll 4
+    for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks], bp[4 * ks * kGbS]);
+  }
   if (half) {
     Rs[(tile * 32 + lane) * 2] = c0;
     Rs[(tile * 32 + lane) * 2 + 1] = c1;
@@ -468,6 +499,10 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
     if (row < M && col < N) {
       if (q.mode == 0) {
         C[(int64_t)row * N + col] = v;
+      } else if (q.mode == 3) {
+        const int Ra = q.Rn, Rb = q.Rn1;
+        const int a = row / Ra, b = row - a * Ra, c = col / Ra, d = col - c * Ra;
+        q.Q[(int64_t)(a + Rb * c) * (Ra * Ra) + (b + Ra * d)] = v;
       } else {
         const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
         const int S = q.Rn * q.Rn1;
@@ -479,7 +514,8 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
 }
 
 static size_t gemm_dmma_smem(int K) {
-  return sizeof(double) * ((size_t)16 * gemm_ka(K) + (size_t)(K + 3) / 4 * 4 * kGbS + 4 * 32 * 2);
+  const size_t k4 = (size_t)(K + 3) / 4 * 4;
+  return sizeof(double) * (std::max((size_t)16 * gemm_ka(K), k4 * kGbS) + k4 * kGbS + 4 * 32 * 2);
 }
 
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
@@ -491,9 +527,9 @@ void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N
     dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
     const size_t smd = gemm_dmma_smem(K);
     if (al16)
-      k_chain_gemm_dmma<true><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+      k_chain_gemm_dmma<true, false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
     else
-      k_chain_gemm_dmma<false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+      k_chain_gemm_dmma<false, false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
     return;
   }
   const size_t sm = (size_t)2 * K * 32 * sizeof(double);
@@ -552,6 +588,18 @@ __global__ void __launch_bounds__(256) k_gram_z2(const double *__restrict__ G, i
 
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s) {
   if (g_dbg_skip & 64) return;
+  const int S = Ra * Rb;
+  const size_t smd = gemm_dmma_smem((int)I);
+  if (!accumulate && I > 0 && smd <= 160 * 1024) {   // G^T G on the FP64 tensor-core fragments
+    prepare_kernel_attrs();
+    dim3 gd((unsigned)cdiv(S, 16), (unsigned)cdiv(S, 16));
+    const QEpi q{Zm, Ra, Rb, 3};
+    if (S % 2 == 0 && (uintptr_t)G % 16 == 0)
+      k_chain_gemm_dmma<true, true><<<gd, 256, smd, s>>>(G, G, nullptr, S, S, (int)I, q);
+    else
+      k_chain_gemm_dmma<false, true><<<gd, 256, smd, s>>>(G, G, nullptr, S, S, (int)I, q);
+    return;
+  }
   const int n = Ra * Ra * Rb * Rb;
   k_gram_z2<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(G, I, Ra, Rb, Zm, accumulate);
 }
@@ -665,6 +713,254 @@ __global__ void __launch_bounds__(256) k_absorb4(AbsorbDesc ad, const TY *__rest
   }
 }
 
+// Absorb, one thread per output element: CTA = RB consecutive rests x O = Po Qo outputs each.
+// The Y blocks (rest, i) of the CTA (contiguous P x Q entries each) and the slices A(i) are staged in
+// shared memory in chunks of ic contracted indices; every thread runs four interleaved FMA chains
+// over (i, contracted rank).  left: out[u][q] = sum_i sum_p A(i)[u][p] Y(i)[p][q] (A(i)[u][p] at
+// u + Ra p); right: out[p][v] = sum_i sum_q Y(i)[p][q] A(i)[q][v] (A(i)[q][v] at q + Ra v).
+template <typename TY, bool LEFT>
+__global__ void __launch_bounds__(256) k_absorb5(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
+                                                 int accumulate, int before, int I, int nrest, int RB, int ic) {
+  extern __shared__ __align__(16) double asm5[];
+  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
+  const int Po = LEFT ? ad.Ra : ad.P, Qo = LEFT ? ad.Q : ad.Rb, O = Po * Qo;
+  const int C = LEFT ? ad.P : ad.Q;   // contracted rank
+  double *As = asm5;                                       // [ic][AB]
+  TY *Ys = (TY *)(asm5 + ((ic * AB + 1) & ~1));            // [RB][ic][PQ]
+  const int rest0 = blockIdx.x * RB;
+  const int rl = threadIdx.x / O, o = threadIdx.x - rl * O;
+  const int rest = rest0 + rl;
+  const bool act = rl < RB && rest < nrest;
+  const int x = o / Qo, y = o - x * Qo;   // left: (u, q); right: (p, v)
+  double acc[4] = {0.0, 0.0, 0.0, 0.0};
+  __shared__ __align__(8) uint64_t bar;
+  const bool bulk = ((PQ * (int)sizeof(TY)) % 16 == 0) && ((AB * 8) % 16 == 0) && ((uintptr_t)Y % 16 == 0) &&
+                    ((uintptr_t)ad.A % 16 == 0);
+  if (bulk && threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+  }
+  uint32_t ph = 0;
+  const int nr = min(RB, nrest - rest0);
+  for (int i0 = 0; i0 < I; i0 += ic) {
+    const int icn = min(ic, I - i0);
+    __syncthreads();
+    if (bulk) {
+      // one copy for the A chunk, one per (rest, i) block of P x Q entries
+      if (threadIdx.x < 32) {
+        if (threadIdx.x == 0)
+          tc::mbar_arrive_expect_tx(&bar, (uint32_t)(icn * AB * 8 + nr * icn * PQ * (int)sizeof(TY)));
+        __syncwarp();
+        if (threadIdx.x == 0) tc::bulk_load(As, ad.A + (int64_t)i0 * AB, (uint32_t)(icn * AB * 8), &bar);
+        for (int e = threadIdx.x; e < nr * icn; e += 32) {
+          const int r = e / icn, ii = e - r * icn, rr = rest0 + r;
+          const int b0 = rr % before, a0 = rr / before;
+          tc::bulk_load(Ys + (r * ic + ii) * PQ, Y + ((int64_t)b0 + (int64_t)before * (i0 + ii + (int64_t)I * a0)) * PQ,
+                        (uint32_t)(PQ * sizeof(TY)), &bar);
+        }
+      }
+      tc::mbar_wait(&bar, ph);
+      ph ^= 1;
+    } else {
+      for (int e = threadIdx.x; e < icn * AB; e += blockDim.x) cp_async8(As + e, ad.A + (int64_t)i0 * AB + e);
+      for (int e = threadIdx.x; e < nr * icn * PQ; e += blockDim.x) {
+        const int r = e / (icn * PQ), w = e - r * (icn * PQ), ii = w / PQ, el = w - ii * PQ;
+        const int rr = rest0 + r;
+        const int b0 = rr % before, a0 = rr / before;
+        cp_async_el(Ys + (r * ic + ii) * PQ + el, Y + ((int64_t)b0 + (int64_t)before * (i0 + ii + (int64_t)I * a0)) * PQ + el);
+      }
+      cp_async_wait_all();
+      __syncthreads();
+    }
+    if (act) {
+      const TY *yb = Ys + rl * ic * PQ;
+      for (int ii = 0; ii < icn; ++ii) {
+        const double *Ai = As + ii * AB;
+        const TY *Yi = yb + ii * PQ;
+        if (LEFT) {
+#pragma unroll 4
+          for (int c = 0; c < C; ++c) acc[c & 3] = fma(Ai[x + ad.Ra * c], (double)Yi[c * ad.Q + y], acc[c & 3]);
+        } else {
+#pragma unroll 4
+          for (int c = 0; c < C; ++c) acc[c & 3] = fma((double)Yi[x * ad.Q + c], Ai[c + ad.Ra * y], acc[c & 3]);
+        }
+      }
+    }
+  }
+  if (!act) return;
+  const double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
+  double *dst = out + (int64_t)rest * O + o;
+  *dst = accumulate ? *dst + v : v;
+}
+
+// Absorb on the FP64 tensor-core fragments (mma.sync m8n8k4).  For a CTA of RB rests the absorb is
+// a GEMM whose large dimension stacks (rest, free rank) and whose small dimension is the new rank:
+//   left:  D[u][(r, q)] = sum_{(i, p)} A(i)[u][p] Y(r, i)[p][q]     (M = Ra small, N = RB Q)
+//   right: D[(r, p)][v] = sum_{(i, q)} Y(r, i)[p][q] A(i)[q][v]     (M = RB P, N = Rb small)
+// K runs over (i, c) with the contracted rank c padded to a multiple of 4 (zero fragments), split
+// over KW warp groups that meet in shared memory.  Y blocks and A chunks arrive by bulk copies.
+template <typename TY, bool LEFT>
+__global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
+                                                 int accumulate, int before, int I, int nrest, int RB, int ic, int KW) {
+  extern __shared__ __align__(16) double asm6[];
+  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
+  const int Cb = LEFT ? ad.Q : ad.P;        // free rank carried along the large dimension
+  const int Sm = LEFT ? ad.Ra : ad.Rb;      // new rank (small dimension, <= 16)
+  const int C = LEFT ? ad.P : ad.Q;         // contracted rank
+  const int O = LEFT ? ad.Ra * ad.Q : ad.P * ad.Rb;
+  const int nc4 = (C + 3) >> 2;
+  double *As = asm6;                                              // [ic][AB]
+  TY *Ys = (TY *)(asm6 + ((ic * AB + 1) & ~1));                   // [RB][ic][PQ]
+  double *Rd = (double *)(Ys + ((RB * ic * PQ * (int)sizeof(TY) + 15) / 16) * (16 / (int)sizeof(TY)));
+  __shared__ __align__(8) uint64_t bar;
+  const int rest0 = blockIdx.x * RB;
+  const int nr = min(RB, nrest - rest0);
+  const int NB = RB * Cb, nbt = (NB + 7) >> 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int bt = warp % nbt, kw = warp / nbt;
+  const bool wact = kw < KW;
+  // this lane's large-dimension index (fragment row/col g of big tile bt)
+  const int nb = 8 * bt + g;
+  const int rb = nb / Cb, cb = nb - rb * Cb;
+  const bool nbv = rb < nr;
+  double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+  if (threadIdx.x == 0) {
+    tc::mbar_init(&bar, 1);
+    tc::fence_barrier_init();
+  }
+  uint32_t ph = 0;
+  for (int i0 = 0; i0 < I; i0 += ic) {
+    const int icn = min(ic, I - i0);
+    __syncthreads();
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0)
+        tc::mbar_arrive_expect_tx(&bar, (uint32_t)(icn * AB * 8 + nr * icn * PQ * (int)sizeof(TY)));
+      __syncwarp();
+      if (threadIdx.x == 0) tc::bulk_load(As, ad.A + (int64_t)i0 * AB, (uint32_t)(icn * AB * 8), &bar);
+      for (int e = threadIdx.x; e < nr * icn; e += 32) {
+        const int r = e / icn, ii = e - r * icn, rr = rest0 + r;
+        const int b0 = rr % before, a0 = rr / before;
+        tc::bulk_load(Ys + (r * ic + ii) * PQ, Y + ((int64_t)b0 + (int64_t)before * (i0 + ii + (int64_t)I * a0)) * PQ,
+                      (uint32_t)(PQ * sizeof(TY)), &bar);
+      }
+    }
+    tc::mbar_wait(&bar, ph);
+    ph ^= 1;
+    if (wact) {
+      const int nsteps = icn * nc4;
+      const TY *yrow = Ys + (size_t)rb * ic * PQ + (LEFT ? cb : cb * ad.Q);   // + i PQ + (LEFT ? c Q : c)
+      for (int st = kw; st < nsteps; st += KW) {
+        const int i = st / nc4, cc = ((st - i * nc4) << 2) + tg;
+        const bool cv = cc < C;
+        const double yv = (nbv && cv) ? (double)yrow[i * PQ + (LEFT ? cc * ad.Q : cc)] : 0.0;
+        const double *Ai = As + i * AB;
+#pragma unroll
+        for (int s2 = 0; s2 < 2; ++s2) {
+          const int sm = 8 * s2 + g;   // small-dimension index held by this lane's fragment
+          if (8 * s2 < Sm) {
+            const double av = (sm < Sm && cv) ? (LEFT ? Ai[sm + ad.Ra * cc] : Ai[cc + ad.Ra * sm]) : 0.0;
+            if (LEFT)
+              dmma884(c[s2][0], c[s2][1], av, yv);   // A = A(i) (small x K), B = Y (K x large)
+            else
+              dmma884(c[s2][0], c[s2][1], yv, av);   // A = Y (large x K), B = A(i) (K x small)
+          }
+        }
+      }
+    }
+  }
+  if (KW > 1) {
+    if (wact && kw > 0) {
+      double *rp = Rd + ((size_t)((kw - 1) * nbt + bt) * 32 + lane) * 4;
+      rp[0] = c[0][0];
+      rp[1] = c[0][1];
+      rp[2] = c[1][0];
+      rp[3] = c[1][1];
+    }
+    __syncthreads();
+    if (!wact || kw > 0) return;
+    for (int k2 = 1; k2 < KW; ++k2) {
+      const double *rp = Rd + ((size_t)((k2 - 1) * nbt + bt) * 32 + lane) * 4;
+      c[0][0] += rp[0];
+      c[0][1] += rp[1];
+      c[1][0] += rp[2];
+      c[1][1] += rp[3];
+    }
+  } else if (!wact) {
+    return;
+  }
+  // accumulator fragment: row g, columns 2 tg + e of the 8 x 8 tile
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      int rest, idx;
+      if (LEFT) {   // D[u][n]: u = 8 s2 + g, n = 8 bt + 2 tg + e
+        const int u = 8 * s2 + g, n = 8 * bt + 2 * tg + e, r = n / Cb, q = n - r * Cb;
+        if (u >= Sm || r >= nr) continue;
+        rest = rest0 + r;
+        idx = u * ad.Q + q;
+      } else {      // D[m][v]: m = 8 bt + g, v = 8 s2 + 2 tg + e
+        const int v = 8 * s2 + 2 * tg + e;
+        if (v >= Sm || !nbv) continue;
+        rest = rest0 + rb;
+        idx = cb * ad.Rb + v;
+      }
+      double *dst = out + (int64_t)rest * O + idx;
+      const double val = c[s2][e];
+      *dst = accumulate ? *dst + val : val;
+    }
+  }
+}
+
+template <typename TY>
+static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest, int64_t before,
+                           int64_t I, cudaStream_t s) {
+  const bool left = ad.left != 0;
+  const int Sm = left ? ad.Ra : ad.Rb, Cb = left ? ad.Q : ad.P;
+  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
+  if (Sm > 16 || nrest >= ((int64_t)1 << 31) || before * I * nrest >= ((int64_t)1 << 40)) return false;
+  if ((PQ * (int)sizeof(TY)) % 16 != 0 || (AB * 8) % 16 != 0 || (uintptr_t)Y % 16 != 0 || (uintptr_t)ad.A % 16 != 0)
+    return false;
+  // rests per CTA: enough CTAs to cover the GPU, at most 8 big tiles (one warp each)
+  int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / 148, 64 / std::max(1, Cb)));
+  const int nbt = (RB * Cb + 7) / 8;
+  const int KW = std::max(1, std::min(8 / nbt, (int)(I * ((std::max(left ? ad.P : ad.Q, 1) + 3) / 4) / 8)));
+  const int threads = std::max(32, std::min(256, nbt * KW * 32));
+  const size_t per_i = 8 * (size_t)AB + sizeof(TY) * (size_t)RB * PQ;
+  const int ic = (int)std::min<int64_t>(I, std::max<int64_t>(1, (96 * 1024) / (int64_t)per_i));
+  const size_t ybytes = ((size_t)RB * ic * PQ * sizeof(TY) + 15) / 16 * 16;
+  const size_t smem = sizeof(double) * (((size_t)ic * AB + 1) & ~1) + ybytes + sizeof(double) * (size_t)(KW - 1) * nbt * 32 * 4;
+  if (smem > 160 * 1024) return false;
+  const unsigned grid = (unsigned)cdiv(nrest, RB);
+  if (left)
+    k_absorb6<TY, true><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic, KW);
+  else
+    k_absorb6<TY, false><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic, KW);
+  return true;
+}
+
+template <typename TY>
+static bool absorb5_launch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest, int64_t before,
+                           int64_t I, cudaStream_t s) {
+  const bool left = ad.left != 0;
+  const int O = (left ? ad.Ra : ad.P) * (left ? ad.Q : ad.Rb);
+  if (O > 256 || nrest >= ((int64_t)1 << 31) || before * I * nrest >= ((int64_t)1 << 40)) return false;
+  const int RB = std::max(1, 256 / O);
+  const int threads = (int)std::min<int64_t>(256, cdiv((int64_t)RB * O, 32) * 32);
+  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
+  const size_t per_i = sizeof(double) * AB + sizeof(TY) * (size_t)RB * PQ;
+  int ic = (int)std::min<int64_t>(I, std::max<int64_t>(1, (96 * 1024) / (int64_t)per_i));
+  const size_t smem = sizeof(double) * (((size_t)ic * AB + 1) & ~1) + sizeof(TY) * (size_t)RB * ic * PQ;
+  if (smem > 160 * 1024) return false;
+  const unsigned grid = (unsigned)cdiv(nrest, RB);
+  if (left)
+    k_absorb5<TY, true><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic);
+  else
+    k_absorb5<TY, false><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic);
+  return true;
+}
+
 template <typename TY, int MR>
 static void absorb_launch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest,
                           int64_t before, int64_t I, cudaStream_t s) {
@@ -694,6 +990,8 @@ static void absorb_launch(const AbsorbDesc &ad, const TY *Y, double *out, int ac
 template <typename TY>
 static void absorb_dispatch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest,
                             int64_t before, int64_t I, cudaStream_t s) {
+  if (g_absorb_v5 == 1 && absorb6_launch<TY>(ad, Y, out, accumulate, nrest, before, I, s)) return;
+  if (g_absorb_v5 == 2 && absorb5_launch<TY>(ad, Y, out, accumulate, nrest, before, I, s)) return;
   // MR bounds both the accumulator length (Ra | Rb) and the contracted rank (P | Q)
   const int L = std::max(ad.left ? ad.Ra : ad.Rb, ad.left ? ad.P : ad.Q);
   if (L <= 4)
@@ -709,6 +1007,14 @@ static void absorb_dispatch(const AbsorbDesc &ad, const TY *Y, double *out, int 
 template <typename TY>
 static void absorb_attrs() {
   const int mx = 160 * 1024;
+  cudaFuncSetAttribute(k_absorb6<TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb6<TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  prefer_max_smem(k_absorb6<TY, true>);
+  prefer_max_smem(k_absorb6<TY, false>);
+  cudaFuncSetAttribute(k_absorb5<TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  cudaFuncSetAttribute(k_absorb5<TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
+  prefer_max_smem(k_absorb5<TY, true>);
+  prefer_max_smem(k_absorb5<TY, false>);
   cudaFuncSetAttribute(k_absorb4<TY, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -873,6 +1179,125 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
   }
 }
 
+// Uniform-rank variant (every factor R x R, R even): two output rows per thread (R/2 threads per
+// entry), slice columns read as 16-byte pairs, compile-time strides.  Same staging and outputs as
+// k_build_table2.
+template <int R>
+__global__ void __launch_bounds__(256) k_build_table3(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
+  extern __shared__ __align__(16) double tsm[];
+  constexpr int AB = R * R, H = R / 2;
+  const int Lk = (int)td.Lk;
+  const int nlb = (Lk + 31) / 32;
+  const int unit = blockIdx.x;
+  const int tp = unit / nlb;
+  const int lb = unit - tp * nlb;
+  const int l0 = lb * 32;
+  const int l1 = (l0 + 32 < Lk) ? l0 + 32 : Lk;
+  const int e_lo = l0 + Lk * tp, e_hi = l1 - 1 + Lk * tp;
+  const FactorList &fl = td.fl;
+  int boff[kMaxFactors], first[kMaxFactors], cnt[kMaxFactors];
+  int off = 0;
+#pragma unroll
+  for (int f = 0; f < kMaxFactors; ++f) {
+    if (f < fl.n) {
+      const Factor &F = fl.f[f];
+      const int st = (int)F.stride;
+      const int q0 = e_lo / st, q1 = e_hi / st;
+      const int c = (q1 - q0 + 1) < F.I ? (q1 - q0 + 1) : F.I;
+      boff[f] = off;
+      first[f] = q0;
+      cnt[f] = c;
+      const int span = F.I * AB, s0 = (q0 % F.I) * AB;
+      for (int e = threadIdx.x; e < c * (AB / 2); e += blockDim.x) {   // 16-byte chunks (AB even)
+        int idx = s0 + 2 * e;
+        if (idx >= span) idx -= span;
+        cp_async16(tsm + off + 2 * e, F.G + idx);
+      }
+      off += c * AB;
+    }
+  }
+  const int Np = td.Npad;
+  float *tile = (float *)(tsm + off);
+  if (tiles)
+    for (int e = threadIdx.x; e < 2 * Np * 8; e += blockDim.x) ((float4 *)tile)[e] = make_float4(0, 0, 0, 0);
+  cp_async_wait_all();
+  __syncthreads();
+  const int el = threadIdx.x / H, pr = 2 * (threadIdx.x - el * H);
+  const int l = l0 + el;
+  if (el < 32 && l < l1) {
+    const int e = l + Lk * tp;
+    auto slice = [&](int f) -> const double * {
+      int j = e / (int)fl.f[f].stride - first[f];
+      while (j >= cnt[f]) j -= cnt[f];
+      return tsm + boff[f] + j * AB;
+    };
+    double v[2][R];
+    {
+      const double *S = slice(0);
+#pragma unroll
+      for (int b = 0; b < R; ++b) {
+        v[0][b] = S[pr + R * b];
+        v[1][b] = S[pr + 1 + R * b];
+      }
+    }
+#pragma unroll
+    for (int f = 1; f < kMaxFactors; ++f) {
+      if (f < fl.n) {
+        const double *S = slice(f);
+        double w[2][R];
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+          for (int a = 0; a < R; a += 2) {
+            const double2 col = *(const double2 *)(S + a + R * b);
+            a0 = fma(v[0][a], col.x, a0);
+            a1 = fma(v[1][a], col.x, a1);
+            a0 = fma(v[0][a + 1], col.y, a0);
+            a1 = fma(v[1][a + 1], col.y, a1);
+          }
+          w[0][b] = a0;
+          w[1][b] = a1;
+        }
+#pragma unroll
+        for (int b = 0; b < R; ++b) {
+          v[0][b] = w[0][b];
+          v[1][b] = w[1][b];
+        }
+      }
+    }
+    if (out64) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        double *o = out64 + (int64_t)e * AB + (pr + r) * R;
+#pragma unroll
+        for (int q = 0; q < R; ++q) o[q] = v[r][q];
+      }
+    }
+    if (tiles) {
+      const int kk = el, chunk = kk >> 2, within = kk & 3;
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+#pragma unroll
+        for (int q = 0; q < R; ++q) {
+          const int n = (pr + r) * R + q;
+          const float hi = tf32_rna((float)v[r][q]);
+          const float lo = tf32_rna((float)(v[r][q] - (double)hi));
+          tile[n * 32 + ((chunk ^ (n & 7)) << 2) + within] = hi;
+          const int n2 = Np + n;
+          tile[n2 * 32 + ((chunk ^ (n2 & 7)) << 2) + within] = lo;
+        }
+      }
+    }
+  }
+  if (tiles) {
+    __syncthreads();
+    float4 *dst = (float4 *)(tiles + (int64_t)unit * (2 * Np * 32));
+    const float4 *src = (const float4 *)tile;
+    for (int e = threadIdx.x; e < 2 * Np * 8; e += blockDim.x) dst[e] = src[e];
+  }
+}
+
 size_t table2_smem(const TableDesc &td) {
   size_t n = 0;
   for (int f = 0; f < td.fl.n; ++f) {
@@ -893,6 +1318,20 @@ int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaSt
   if (td.Lk * td.tk >= (int64_t)1 << 31) return -1;   // 32-bit entry indices
   prepare_kernel_attrs();
   const int64_t units = td.tk * cdiv(td.Lk, 32);
+  {   // uniform rank R (all factors R x R) with 16-byte aligned slices: the specialized kernel
+    const int R = td.fl.f[0].Ra;
+    bool uni = (R == 4 || R == 8 || R == 10 || R == 16);
+    for (int f = 0; f < td.fl.n && uni; ++f)
+      uni = td.fl.f[f].Ra == R && td.fl.f[f].Rb == R && (uintptr_t)td.fl.f[f].G % 16 == 0;
+    if (uni && g_table_v3) {
+      const int th = (int)cdiv(16 * R, 32) * 32;
+      if (R == 4) k_build_table3<4><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
+      else if (R == 8) k_build_table3<8><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
+      else if (R == 10) k_build_table3<10><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
+      else k_build_table3<16><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
+      return 0;
+    }
+  }
   const int threads = (int)cdiv(32 * td.fl.f[0].Ra, 32) * 32;
   int mr = 0;
   for (int f = 0; f < td.fl.n; ++f) mr = std::max(mr, std::max(td.fl.f[f].Ra, td.fl.f[f].Rb));
@@ -1014,16 +1453,28 @@ void prepare_kernel_attrs() {
   cudaFuncSetAttribute(k_chain_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
   cudaFuncSetAttribute(k_chain_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
   cudaFuncSetAttribute(k_chain_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
-  cudaFuncSetAttribute(k_chain_gemm_dmma<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
-  cudaFuncSetAttribute(k_chain_gemm_dmma<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
-  prefer_max_smem(k_chain_gemm_dmma<true>);
-  prefer_max_smem(k_chain_gemm_dmma<false>);
+  cudaFuncSetAttribute(k_chain_gemm_dmma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
+  cudaFuncSetAttribute(k_chain_gemm_dmma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
+  cudaFuncSetAttribute(k_chain_gemm_dmma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  cudaFuncSetAttribute(k_chain_gemm_dmma<false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+  prefer_max_smem(k_chain_gemm_dmma<true, false>);
+  prefer_max_smem(k_chain_gemm_dmma<false, false>);
+  prefer_max_smem(k_chain_gemm_dmma<true, true>);
+  prefer_max_smem(k_chain_gemm_dmma<false, true>);
   absorb_attrs<float>();
   absorb_attrs<double>();
   cudaFuncSetAttribute(k_build_table2<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_build_table2<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_build_table2<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
   cudaFuncSetAttribute(k_build_table2<STR_MAXR>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table3<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table3<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table3<10>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  cudaFuncSetAttribute(k_build_table3<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+  prefer_max_smem(k_build_table3<4>);
+  prefer_max_smem(k_build_table3<8>);
+  prefer_max_smem(k_build_table3<10>);
+  prefer_max_smem(k_build_table3<16>);
   prefer_max_smem(k_spd_inv<5>);
   prefer_max_smem(k_spd_inv<8>);
   prefer_max_smem(k_chain_gemm<0>);
