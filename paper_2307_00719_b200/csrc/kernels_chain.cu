@@ -848,22 +848,25 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
     tc::mbar_wait(&bar, ph);
     ph ^= 1;
     if (wact) {
-      const int nsteps = icn * nc4;
+      // K = (i, c): warp group kw takes i = kw, kw + KW, ...; per i ceil(C/4) k-steps of 4 ranks
       const TY *yrow = Ys + (size_t)rb * ic * PQ + (LEFT ? cb : cb * ad.Q);   // + i PQ + (LEFT ? c Q : c)
-      for (int st = kw; st < nsteps; st += KW) {
-        const int i = st / nc4, cc = ((st - i * nc4) << 2) + tg;
-        const bool cv = cc < C;
-        const double yv = (nbv && cv) ? (double)yrow[i * PQ + (LEFT ? cc * ad.Q : cc)] : 0.0;
+      const int ystep = LEFT ? 4 * ad.Q : 4, yoff = LEFT ? tg * ad.Q : tg;
+      const int sm0 = g, sm1 = 8 + g;
+      const int aoff0 = LEFT ? sm0 + ad.Ra * tg : tg + ad.Ra * sm0;
+      const int aoff1 = LEFT ? sm1 + ad.Ra * tg : tg + ad.Ra * sm1;
+      const int astep = LEFT ? 4 * ad.Ra : 4;
+      const bool two = Sm > 8;
+      for (int i = kw; i < icn; i += KW) {
+        const TY *yi = yrow + i * PQ + yoff;
         const double *Ai = As + i * AB;
-#pragma unroll
-        for (int s2 = 0; s2 < 2; ++s2) {
-          const int sm = 8 * s2 + g;   // small-dimension index held by this lane's fragment
-          if (8 * s2 < Sm) {
-            const double av = (sm < Sm && cv) ? (LEFT ? Ai[sm + ad.Ra * cc] : Ai[cc + ad.Ra * sm]) : 0.0;
-            if (LEFT)
-              dmma884(c[s2][0], c[s2][1], av, yv);   // A = A(i) (small x K), B = Y (K x large)
-            else
-              dmma884(c[s2][0], c[s2][1], yv, av);   // A = Y (large x K), B = A(i) (K x small)
+        for (int j = 0; j < nc4; ++j) {
+          const bool cv = 4 * j + tg < C;
+          const double yv = (nbv && cv) ? (double)yi[j * ystep] : 0.0;
+          const double av0 = (sm0 < Sm && cv) ? Ai[aoff0 + j * astep] : 0.0;
+          if (LEFT) dmma884(c[0][0], c[0][1], av0, yv); else dmma884(c[0][0], c[0][1], yv, av0);
+          if (two) {
+            const double av1 = (sm1 < Sm && cv) ? Ai[aoff1 + j * astep] : 0.0;
+            if (LEFT) dmma884(c[1][0], c[1][1], av1, yv); else dmma884(c[1][0], c[1][1], yv, av1);
           }
         }
       }
@@ -925,7 +928,7 @@ static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int a
   // rests per CTA: enough CTAs to cover the GPU, at most 8 big tiles (one warp each)
   int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / 148, 64 / std::max(1, Cb)));
   const int nbt = (RB * Cb + 7) / 8;
-  const int KW = std::max(1, std::min(8 / nbt, (int)(I * ((std::max(left ? ad.P : ad.Q, 1) + 3) / 4) / 8)));
+  const int KW = (int)std::max<int64_t>(1, std::min<int64_t>(8 / nbt, I));
   const int threads = std::max(32, std::min(256, nbt * KW * 32));
   const size_t per_i = 8 * (size_t)AB + sizeof(TY) * (size_t)RB * PQ;
   const int ic = (int)std::min<int64_t>(I, std::max<int64_t>(1, (96 * 1024) / (int64_t)per_i));
