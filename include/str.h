@@ -118,6 +118,19 @@ STR_API str_status str_get_temporal_rows(str_state *h, int64_t t0, int64_t t, do
  * when world_size > 1.  ||X|| = 0 gives STR_E_ARG. Waits for the stream. */
 STR_API str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t, double *rel_err);
 
+/* Batch TR-ALS on the GPU (Alg. 1; initialization protocol P:734; SURVEY
+ * §8(f) NEXT-1).  Re-fits every core to X (t temporal slices, DEVICE pointer to this rank's shard,
+ * element type cfg.dtype, paper linearization, caller-owned, read during the call) by `sweeps`
+ * ALS sweeps starting from the cores the handle holds, then rebuilds the streaming state of Alg. 4
+ * l.1-5 (Z_n, P_n, Q_n) from X and the fitted cores, as if X had been X_init: the stream
+ * continues from there.  A sweep updates the modes in the cyclic order N, 1, ..., N-1 (Alg. 1's
+ * order 1..N started one mode earlier), each mode by the exact LS solution of Eq. (tr_als)
+ * P:160-164 formed through Prop. 1 (normal equations, Q = H^{≠n}_<2>), so one sweep is one
+ * empty-history STR step over X.  The processed count becomes t.  rel_err (optional, host) gets
+ * ||X - TR(G)||_F / ||X||_F after the last sweep (str_fit over X).  STR variant only
+ * (STR_E_ARG for rSTR handles); collective when world_size > 1.  Waits for the stream. */
+STR_API str_status str_tr_als(str_state *h, const void *X, int64_t t, int32_t sweeps, double *rel_err);
+
 /* Waits for all enqueued work; reports deferred numerical failures. */
 STR_API str_status str_sync(str_state *h);
 

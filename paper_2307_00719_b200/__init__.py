@@ -23,7 +23,8 @@ from ._lib import (STR_CONTRACT_3XTF32, STR_CONTRACT_F64, STR_DET, STR_F32, STR_
 
 __all__ = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",
            "str_fit", "str_sync", "str_processed", "str_error_string", "str_destroy", "str_kernel_launches",
-           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "Handle", "StrError",
+           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "str_tr_als", "Handle",
+           "StrError",
            "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
@@ -151,6 +152,16 @@ def str_fit(h: Handle, X, t0: int, t: int) -> float:
     ptr = _dev_ptr(X, h.local_slice * int(t), h.dtype)
     v = C.c_double()
     _check(h, _lib.lib.str_fit(h.ptr, C.c_void_p(ptr), int(t0), int(t), C.byref(v)))
+    return v.value
+
+
+def str_tr_als(h: Handle, X, t: int, sweeps: int) -> float:
+    """Batch TR-ALS on the GPU (Alg. 1): `sweeps` sweeps in mode order N, 1..N-1 from the cores the
+    handle holds, then the streaming state rebuilt from X (device, t slices).  Returns the fit
+    ||X - TR(G)|| / ||X|| after the last sweep."""
+    ptr = _dev_ptr(X, h.local_slice * int(t), h.dtype)
+    v = C.c_double()
+    _check(h, _lib.lib.str_tr_als(h.ptr, C.c_void_p(ptr), int(t), int(sweeps), C.byref(v)))
     return v.value
 
 

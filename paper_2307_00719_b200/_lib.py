@@ -21,7 +21,7 @@ STR_DET, STR_SAMPLE_UNIFORM, STR_SAMPLE_LEVERAGE = 0, 1, 2
 # Every symbol include/str.h declares (checked by tests/test_abi.py without a GPU).
 EXPORTS = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",
            "str_fit", "str_sync", "str_processed", "str_error_string", "str_destroy", "str_kernel_launches",
-           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table"]
+           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "str_tr_als"]
 
 
 class str_config(C.Structure):
@@ -65,6 +65,7 @@ def _load():
         "str_get_cores": (C.c_int, [P, C.c_int32, C.POINTER(C.c_double), C.c_int64]),
         "str_get_temporal_rows": (C.c_int, [P, C.c_int64, C.c_int64, C.POINTER(C.c_double)]),
         "str_fit": (C.c_int, [P, P, C.c_int64, C.c_int64, C.POINTER(C.c_double)]),
+        "str_tr_als": (C.c_int, [P, P, C.c_int64, C.c_int32, C.POINTER(C.c_double)]),
         "str_sync": (C.c_int, [P]),
         "str_processed": (C.c_int64, [P]),
         "str_error_string": (C.c_char_p, [P]),

@@ -940,6 +940,41 @@ extern "C" str_status str_update_batch_host(str_state *h, const void *X_host, in
   return str_update_batch(h, h->Xstage.p, t_new);
 }
 
+// Batch TR-ALS (include/str.h): each sweep is update_det over X with the history cleared
+// (P_n = Q_n = 0, no temporal rows), i.e. Alg. 1 in the mode order N, 1..N-1; then Alg. 4's init.
+extern "C" str_status str_tr_als(str_state *h, const void *X, int64_t t, int32_t sweeps, double *rel_err) {
+  if (!h) return STR_E_ARG;
+  if (h->poisoned) return STR_E_POISONED;
+  if (!X || t < 1 || sweeps < 0) return fail(h, STR_E_ARG, "X must be non-NULL, t >= 1, sweeps >= 0");
+  if (h->variant != STR_DET) return fail(h, STR_E_ARG, "str_tr_als needs an STR (deterministic) handle");
+  cudaSetDevice(h->device);
+  TRY(deferred_check(h));
+  TRY(ensure_temporal_capacity(h, t));
+  for (int s = 0; s < sweeps; ++s) {
+    for (auto &m : h->md) {
+      CU(cudaMemsetAsync(m.P.p, 0, sizeof(double) * m.I * m.Ra * m.Rb, h->st));
+      CU(cudaMemsetAsync(m.Q.p, 0, sizeof(double) * (size_t)m.Ra * m.Rb * m.Ra * m.Rb, h->st));
+    }
+    const int64_t zero = 0;
+    CU(cudaMemcpyAsync(h->dT.p, &zero, sizeof(zero), cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));   // (the host value of zero must outlive the copy)
+    h->T = 0;
+    TRY(update_det(h, X, t));            // h->T = t afterwards
+    TRY(deferred_check(h));
+  }
+  // Alg. 4 l.1-5 from the fitted cores: Z_N over all t rows, P_n, Q_n, Z_n
+  h->T = t;
+  {
+    const int64_t tt = t;
+    CU(cudaMemcpyAsync(h->dT.p, &tt, sizeof(tt), cudaMemcpyHostToDevice, h->st));
+    CU(cudaStreamSynchronize(h->st));
+  }
+  TRY(init_det(h, X, t));   // (eager; not part of the step graph)
+  TRY(deferred_check(h));
+  if (rel_err) TRY(str_fit(h, X, 0, t, rel_err));
+  return STR_OK;
+}
+
 extern "C" str_status str_sync(str_state *h) {
   if (!h) return STR_E_ARG;
   return deferred_check(h);
