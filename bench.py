@@ -20,6 +20,7 @@ passes) with CUDA events on the library's stream.  `cpu_baseline` times the fp64
 from __future__ import annotations
 
 import argparse
+import ctypes
 import json
 import os
 import subprocess
@@ -180,13 +181,28 @@ def bench_ours(args):
     global_entries = cfg.batch_entries
     value = args.steps * global_entries / (ms / 1e3)
 
-    # ---- roofline of the dominant kernels (contraction passes), events on the library stream
+    # ---- roofline of the dominant kernels (contraction passes), events on the library stream;
+    # the kernels also stamp %globaltimer per CTA (diagnostic trace) for their in-kernel span
+    Ld = lib._lib.lib
+    span = None
+    if hasattr(Ld, "strdbg_tftrace") and contract == "3xtf32":
+        Ld.strdbg_tftrace.argtypes = [ctypes.c_void_p, ctypes.c_int32, ctypes.POINTER(ctypes.c_longlong)]
+        Ld.strdbg_tftrace(h.ptr, 1, None)
     lib.str_set_profiling(h, True)
     kp = min(args.steps, 10)
     for _ in range(kp):
         one_step()
     p1_ms, p1_n, p2_ms, p2_n = lib.str_profile(h)
     lib.str_set_profiling(h, False)
+    if hasattr(Ld, "strdbg_tftrace") and contract == "3xtf32":
+        Wd = 1024 + 4 * 160
+        tr = np.zeros(2 * Wd, dtype=np.int64)
+        Ld.strdbg_tftrace(h.ptr, 0, tr.ctypes.data_as(ctypes.POINTER(ctypes.c_longlong)))
+        span = []
+        for pas in (0, 1):
+            g = tr[pas * Wd + 1024:(pas + 1) * Wd].reshape(160, 4)
+            g = g[g[:, 0] > 0]
+            span.append(float(g[:, 3].max() - g[:, 0].min()) / 1e3 if len(g) else None)
     peaks, peaks_src = load_peaks()
     R2 = cfg.ranks[0] * cfg.ranks[-1]
     local_entries = global_entries // world
@@ -227,6 +243,15 @@ def bench_ours(args):
                 "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
                 "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
                 "peak_basis": basis}
+    if span and all(x for x in span):
+        # in-kernel span (first CTA start to last CTA end, %globaltimer) of the last profiled step;
+        # the event pair above also holds the graph node's launch latency (~6 us measured with an
+        # empty kernel in the same position)
+        sp = 0.5 * (span[0] + span[1])
+        ach_sp = (flops_per_pass if unit == "TFLOP/s" else bytes_per_pass) / (sp / 1e6) / (1e12 if unit == "TFLOP/s" else 1e9)
+        roofline["kernel_span_us"] = {"pass1": round(span[0], 2), "pass2": round(span[1], 2)}
+        roofline["achieved_kernel_span"] = round(ach_sp, 3)
+        roofline["frac_kernel_span"] = round(ach_sp / peak, 4)
 
     # ---- e2e: public host-buffer API, pinned H2D + D2H of the step's result every step
     pinned = [torch.from_numpy(x).pin_memory() for x in host[:min(nd, 4)]]
@@ -248,6 +273,20 @@ def bench_ours(args):
     e2e = {"value": args.e2e_steps * global_entries / (e2e_ms / 1e3), "unit": UNIT,
            "h2d_bytes_per_step": int(pinned[0].numel() * pinned[0].element_size()),
            "d2h_bytes_per_step": int(res.size * 8), "steps": args.e2e_steps}
+    # ---- batch TR-ALS on the init slab (Alg. 1, the initialization stage; not part of the step)
+    tr_als = None
+    if world == 1:
+        Xi_d = torch.from_numpy(Xi).to(dev)
+        torch.cuda.synchronize(dev)
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        sw = 2
+        lib.str_tr_als(h, Xi_d, cfg.t_init, 1)   # warm-up (captures the sweep graph)
+        a0.record(stream)
+        fit = lib.str_tr_als(h, Xi_d, cfg.t_init, sw)
+        a1.record(stream)
+        torch.cuda.synchronize(dev)
+        tr_als = {"sweeps": sw, "t": cfg.t_init, "ms_per_sweep": round(a0.elapsed_time(a1) / sw, 4),
+                  "note": "includes the rebuild of the streaming state and one fit evaluation", "fit": fit}
     lib.str_destroy(h)
 
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
@@ -261,6 +300,8 @@ def bench_ours(args):
                        "l2": f"rotating {nd} distinct device-resident batches ({nd * global_entries * 4 / 1e9:.2f} GB)"
                              " > 126 MB L2"},
             "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline}
+    if tr_als:
+        line["tr_als_init"] = tr_als
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg)
     if world > 1:

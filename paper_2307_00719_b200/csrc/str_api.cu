@@ -1092,6 +1092,8 @@ extern "C" STR_API str_status strdbg_tftrace(str_state *h, int32_t enable, long 
     if (host_out) CU(cudaMemcpy(host_out, h->tf_dbg, 2 * str_state::kTfDbgWords * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(h->tf_dbg);
     h->tf_dbg = nullptr;
+    h->gs[0].reset();   // captured contraction nodes may point at the freed trace buffer
+    h->gs[1].reset();
   }
   return STR_OK;
 }
