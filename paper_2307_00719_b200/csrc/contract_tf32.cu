@@ -662,8 +662,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   const int64_t blocks = cdiv(p.mtiles, kMT);   // M-blocks (tile pairs; pass 1 pairs across t)
   p.KT = pass == 1 ? cdiv(Rr, kBK) : tn * p.nlb;
   p.U = blocks * p.KT;
-  int maxg = 148;
-  if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(148, atoi(ev)));   // tuning knob
+  // persistent grid: every SM but the kInvNC that the side stream's cluster inverse occupies while
+  // a pass runs (a pass CTA waiting for such an SM would hold the whole pass back)
+  static int nsm = 0;
+  if (!nsm && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) nsm = 148;
+  int maxg = std::max(1, nsm - (g_inv_cluster ? kInvClusterCTAs : 0));
+  if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(nsm, atoi(ev)));   // tuning knob
   int grid = (int)std::min<int64_t>(maxg, p.U);
   p.upc = cdiv(p.U, grid);
   grid = (int)cdiv(p.U, p.upc);

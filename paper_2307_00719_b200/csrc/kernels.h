@@ -16,6 +16,8 @@ extern int g_dbg_skip;
 extern int g_gemm_stage;
 extern int g_absorb_v5;
 extern int g_table_v3;
+extern int g_inv_cluster;
+constexpr int kInvClusterCTAs = 4;   // CTAs of the cluster inverse (k_spd_inv_cl)
 
 // kernels_small.cu
 void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);

@@ -11,6 +11,8 @@
 //                  pre-tiled 3xTF32 hi/lo operand blocks of the tensor-core contraction.
 #include <algorithm>
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
@@ -19,7 +21,8 @@ namespace strb200 {
 
 int g_dbg_skip = 0;
 int g_gemm_stage = -1;
-int g_table_v3 = 1;       // diagnostic switch: 0 keeps the generic table kernel
+int g_table_v3 = 1;
+int g_inv_cluster = 1;    // diagnostic switch: 0 keeps the single-CTA inverse       // diagnostic switch: 0 keeps the generic table kernel
 int g_absorb_v5 = 1;      // diagnostic switch: 1 k_absorb6 (tensor-core fragments), 2 k_absorb5, 0 k_absorb4   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
 
 void prepare_kernel_attrs();
@@ -280,9 +283,169 @@ size_t spd_inv_smem(int S) {
   return sizeof(double) * ((size_t)((S * S + 1) & ~1) + 3 * STR_MAXW * kVS + 2 * 64);
 }
 
+// ------------------------------------------------------------------------------------------
+// Q^{-1} by the same blocked symmetric sweep, spread over a cluster of kInvNC CTAs (distributed
+// shared memory).  CTA c owns the lower-triangle tile rows I = c (mod kInvNC) in registers (warp 0:
+// its diagonal tiles; warps 1-7: its off-diagonal tiles).  Step kb: every CTA forms W = V D for all
+// row blocks from its local copy of the pivot panel V and pivot inverse D, updates its tiles,
+// and the owners of the next pivot column write their tiles (the next panel V') into EVERY CTA's
+// shared memory; the owner of the next pivot block updates it first, inverts it (8-pivot sweep)
+// and broadcasts D'.  One cluster barrier (release / acquire) ends the step.  The FP64 update
+// work per step is split four ways, and the pivot sweep runs on an SM whose pipe carries only a
+// quarter of the trailing update.
+constexpr int kInvNC = kInvClusterCTAs;   // CTAs per cluster
+constexpr int kInvCThreads = 256;  // 8 warps
+constexpr int kInvCSlots = 6;      // off-diagonal tiles per warp (nt <= 16: <= 36 per CTA over 7 warps)
+constexpr int kInvCDiag = 4;       // diagonal tiles of warp 0 (nt <= 16)
+
+__global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1)
+    k_spd_inv_cl(const double *__restrict__ Q, int S, double *__restrict__ Qinv, int *info) {
+  namespace cg = cooperative_groups;
+  cg::cluster_group cl = cg::this_cluster();
+  __shared__ __align__(16) double Vb[2][STR_MAXW * kVS];   // pivot panels V (double-buffered)
+  __shared__ __align__(16) double Wb[STR_MAXW * kVS];      // W = V D
+  __shared__ __align__(16) double Db[2][64];               // pivot inverses D
+  __shared__ short s_off[7][kInvCSlots][2];                // off-diagonal tiles of warps 1-7
+  const int c = (int)cl.block_rank();
+  const int nt = (S + 7) >> 3;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  if (threadIdx.x == 0) {
+    int t = 0;
+    for (int w = 0; w < 7; ++w)
+      for (int sl = 0; sl < kInvCSlots; ++sl) s_off[w][sl][0] = -1;
+    for (int I = c; I < nt; I += kInvNC)
+      for (int J = 0; J < I; ++J, ++t) {
+        s_off[t % 7][t / 7][0] = (short)I;
+        s_off[t % 7][t / 7][1] = (short)J;
+      }
+  }
+  __syncthreads();
+  // owned tiles -> registers (symmetrized, identity padding beyond S)
+  constexpr int NSL = kInvCSlots > kInvCDiag ? kInvCSlots : kInvCDiag;
+  int TI[NSL], TJ[NSL];
+  double cc[NSL][2];
+#pragma unroll
+  for (int sl = 0; sl < NSL; ++sl) {
+    int I = -1, J = -1;
+    if (warp == 0) {
+      if (sl < kInvCDiag && c + kInvNC * sl < nt) I = J = c + kInvNC * sl;
+    } else if (sl < kInvCSlots) {
+      I = s_off[warp - 1][sl][0];
+      J = s_off[warp - 1][sl][1];
+    }
+    TI[sl] = __shfl_sync(0xffffffffu, I, 0);
+    TJ[sl] = __shfl_sync(0xffffffffu, J, 0);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * TI[sl] + g, j = 8 * TJ[sl] + 2 * tg + e;
+      cc[sl][e] = (TI[sl] >= 0 && i < S && j < S) ? 0.5 * (Q[(int64_t)i * S + j] + Q[(int64_t)j * S + i])
+                                                 : (i == j ? 1.0 : 0.0);
+    }
+  }
+  // broadcast helpers: write 2 doubles of a panel / D entry into every CTA of the cluster
+  auto put2 = [&](double *local, int idx, double v0, double v1) {
+#pragma unroll
+    for (int r = 0; r < kInvNC; ++r) {
+      double *rem = cl.map_shared_rank(local, r);
+      rem[idx] = v0;
+      rem[idx + 1] = v1;
+    }
+  };
+  auto put1 = [&](double *local, int idx, double v) {
+#pragma unroll
+    for (int r = 0; r < kInvNC; ++r) cl.map_shared_rank(local, r)[idx] = v;
+  };
+  bool bad = false;
+  cl.sync();   // every CTA's shared memory exists before the first remote store
+  for (int kb = -1; kb < nt; ++kb) {
+    const int cur = (kb + 2) & 1, nxt = cur ^ 1, kn = kb + 1;
+    const double *V = Vb[cur];
+    double *Vn = Vb[nxt];
+    const double *D = Db[cur];
+    double *Dn = Db[nxt];
+    if (kb >= 0) {
+      // W = V D for every row block (DMMA: A = V block rows, B = D)
+      for (int I = warp; I < nt; I += kInvCThreads / 32) {
+        double w0 = 0.0, w1 = 0.0;
+        dmma884(w0, w1, V[(8 * I + g) * kVS + tg], D[tg * 8 + g]);
+        dmma884(w0, w1, V[(8 * I + g) * kVS + 4 + tg], D[(4 + tg) * 8 + g]);
+        Wb[(8 * I + g) * kVS + 2 * tg] = w0;
+        Wb[(8 * I + g) * kVS + 2 * tg + 1] = w1;
+      }
+      __syncthreads();
+    }
+    // one tile: step-kb update, then its share of the next panel
+    auto tile = [&](double (&t)[2], int I, int J) {
+      if (kb >= 0) {
+        if (I != kb && J != kb) {
+          const double *wp = Wb + (8 * I + g) * kVS + tg, *vp = V + (8 * J + g) * kVS + tg;
+          dmma884(t[0], t[1], -wp[0], vp[0]);
+          dmma884(t[0], t[1], -wp[4], vp[4]);
+        } else if (I != kb) {   // J == kb: A_RP = W_R
+          t[0] = Wb[(8 * I + g) * kVS + 2 * tg];
+          t[1] = Wb[(8 * I + g) * kVS + 2 * tg + 1];
+        } else if (J != kb) {   // I == kb: A_PR = W_R^T
+          t[0] = Wb[(8 * J + 2 * tg) * kVS + g];
+          t[1] = Wb[(8 * J + 2 * tg + 1) * kVS + g];
+        } else {                // pivot block: -D
+          t[0] = -D[g * 8 + 2 * tg];
+          t[1] = -D[g * 8 + 2 * tg + 1];
+        }
+      }
+      if (kn < nt) {
+        if (J == kn) {
+          put2(Vn, (8 * I + g) * kVS + 2 * tg, t[0], t[1]);
+        } else if (I == kn) {   // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
+          put1(Vn, (8 * J + 2 * tg) * kVS + g, t[0]);
+          put1(Vn, (8 * J + 2 * tg + 1) * kVS + g, t[1]);
+        }
+      }
+    };
+    if (warp == 0) {
+      // the next pivot block first (if it lives here): update, publish, invert, broadcast
+#pragma unroll
+      for (int sl = 0; sl < kInvCDiag; ++sl)
+        if (TI[sl] == kn) {
+          tile(cc[sl], kn, kn);
+          double d[2] = {cc[sl][0], cc[sl][1]};
+          bad = warp_sweep8(d, g, tg) || bad;
+          put2(Dn, g * 8 + 2 * tg, -d[0], -d[1]);
+        }
+#pragma unroll
+      for (int sl = 0; sl < kInvCDiag; ++sl)
+        if (TI[sl] >= 0 && TI[sl] != kn) tile(cc[sl], TI[sl], TI[sl]);
+    } else {
+#pragma unroll
+      for (int sl = 0; sl < kInvCSlots; ++sl)
+        if (TI[sl] >= 0) tile(cc[sl], TI[sl], TJ[sl]);
+    }
+    cl.sync();
+  }
+  if (bad && lane == 0 && info) atomicExch(info, 1);
+  // -A = Q^{-1}: both triangles straight to global memory
+#pragma unroll
+  for (int sl = 0; sl < NSL; ++sl) {
+    const int I = TI[sl], J = TJ[sl];
+    if (I < 0) continue;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
+      if (i < S && j < S && (I != J || j <= i)) {
+        Qinv[(int64_t)i * S + j] = -cc[sl][e];
+        Qinv[(int64_t)j * S + i] = -cc[sl][e];
+      }
+    }
+  }
+}
+
 void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {
   if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
+  if (g_inv_cluster && S <= STR_MAXW && S > 8) {
+    k_spd_inv_cl<<<kInvNC, kInvCThreads, 0, s>>>(Q, S, Qinv, info);
+    return;
+  }
   if (S <= 104)
     k_spd_inv<5><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
   else
