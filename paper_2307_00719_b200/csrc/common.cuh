@@ -51,6 +51,8 @@ struct TableDesc {
   FactorList fl;
   int64_t Lk, tk;
   int32_t Npad;
+  float4 *zero = nullptr;   // optional: zeroed by the table kernel (the next contraction's output)
+  int64_t zero_n4 = 0;      // float4s to zero
 };
 
 // Epilogue of k_chain_gemm: mode 0 = store C; 1 = Q = H_<2>; 2 = Q += H_<2> (Rn = R_n, Rn1 = R_{n+1}).

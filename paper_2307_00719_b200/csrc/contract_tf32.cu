@@ -631,7 +631,7 @@ str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, in
   return STR_OK;
 }
 
-int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y) {
+int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y, bool y_zeroed) {
   cudaStream_t st = h->st;
   const int Np = npad_of(W);
   const int64_t L = h->L, Rr = h->Rr;
@@ -684,12 +684,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   memset(&ymap, 0, sizeof(ymap));
   if (p.yred && !encode_y_map(h, &ymap, Y, pass, W, tn)) return -1;
   const int64_t M = pass == 1 ? L * tn : Rr;
-  {
+  if (!y_zeroed) {
     const int64_t n = M * W;   // floats; the buffer is allocated in whole float4s
     const int64_t n4 = (n + 3) / 4;
     k_zero_f32<<<(unsigned)std::min<int64_t>(296, (n4 + 255) / 256), 256, 0, st>>>((float4 *)p.Y, n4);
+    tl_mark(h, "zero_y");
   }
-  tl_mark(h, "zero_y");
   const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 256;
   prof_mark(h, 2 * (pass - 1));
   if (pass == 1)

@@ -1227,6 +1227,9 @@ __device__ __forceinline__ float tf32_rna(float x) {
 
 template <int MR>
 __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
+  if (td.zero)   // the next contraction's output (one node fewer per pass)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < td.zero_n4; i += (int64_t)gridDim.x * blockDim.x)
+      td.zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   // all index arithmetic in 32 bits (the host checks Lk * tk < 2^31): 64-bit division and modulo
   // are emulated and used to dominate this kernel
   extern __shared__ __align__(16) double tsm[];
@@ -1350,6 +1353,9 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
 // k_build_table2.
 template <int R>
 __global__ void __launch_bounds__(256) k_build_table3(TableDesc td, double *__restrict__ out64, float *__restrict__ tiles) {
+  if (td.zero)   // the next contraction's output (one node fewer per pass)
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < td.zero_n4; i += (int64_t)gridDim.x * blockDim.x)
+      td.zero[i] = make_float4(0.f, 0.f, 0.f, 0.f);
   extern __shared__ __align__(16) double tsm[];
   constexpr int AB = R * R, H = R / 2;
   const int Lk = (int)td.Lk;

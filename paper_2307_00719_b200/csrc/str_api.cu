@@ -308,9 +308,11 @@ static str_status contract(str_state *h, const void *X, int pass, const double *
   TableDesc td = pass == 1 ? desc_TR(h) : desc_TL_at(h, trows, tn);
   if (h->contract == STR_CONTRACT_3XTF32) {
     td.Npad = tf32_npad(W);
-    TRY(build_table(h, td, nullptr, (float *)h->tab_split.p, pass == 1 ? "table_TR" : "table_TL"));
     float *out = (float *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
-    if (launch_contract_tf32(h, X, pass, W, tn, out) != 0)
+    td.zero = (float4 *)out;   // the table kernel clears the pass output
+    td.zero_n4 = ((pass == 1 ? h->L * tn : h->Rr) * W + 3) / 4;
+    TRY(build_table(h, td, nullptr, (float *)h->tab_split.p, pass == 1 ? "table_TR" : "table_TL"));
+    if (launch_contract_tf32(h, X, pass, W, tn, out, true) != 0)
       return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
     *Y = out;
     *y_f32 = true;
@@ -1207,7 +1209,7 @@ extern "C" STR_API str_status strdbg_contract_repeat(str_state *h, const void *X
   float *out = (float *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
   CU(cudaEventRecord(e0, h->st));
   for (int i = 0; i < reps; ++i)
-    if (launch_contract_tf32(h, X, pass, W, tn, out) != 0) return fail(h, STR_E_CUDA, h->err);
+    if (launch_contract_tf32(h, X, pass, W, tn, out, false) != 0) return fail(h, STR_E_CUDA, h->err);
   CU(cudaEventRecord(e1, h->st));
   CU(cudaEventSynchronize(e1));
   float t = 0.0f;

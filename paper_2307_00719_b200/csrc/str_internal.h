@@ -178,8 +178,8 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn);
 str_status tf32_prepare(str_state *h);
 str_status tf32_ensure_workspace(str_state *h, int64_t tn);
 // Tensor-core pass over X with the pre-tiled table operand already in h->tab_split; fp32 output Y
-// (zeroed and accumulated here).  Returns 0, or -1 with h->err set.
-int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y);
+// (zeroed here unless y_zeroed, then accumulated).  Returns 0, or -1 with h->err set.
+int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y, bool y_zeroed);
 int tf32_npad(int W);
 // Re-point captured contraction node `pass` of exec at new data X (3xTF32 path).
 str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn);
