@@ -15,6 +15,7 @@ namespace strb200 {
 extern int g_dbg_skip;
 extern int g_gemm_stage;
 extern int g_absorb_v5;
+extern int g_absorb_cps;
 extern int g_table_v3;
 extern int g_inv_cluster;
 constexpr int kInvClusterCTAs = 4;   // CTAs of the cluster inverse (k_spd_inv_cl)

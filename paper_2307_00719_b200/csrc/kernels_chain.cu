@@ -23,7 +23,8 @@ int g_dbg_skip = 0;
 int g_gemm_stage = -1;
 int g_table_v3 = 1;
 int g_inv_cluster = 1;    // diagnostic switch: 0 keeps the single-CTA inverse       // diagnostic switch: 0 keeps the generic table kernel
-int g_absorb_v5 = 1;      // diagnostic switch: 1 k_absorb6 (tensor-core fragments), 2 k_absorb5, 0 k_absorb4   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
+int g_absorb_v5 = 1;
+int g_absorb_cps = 3;     // target absorb CTAs per SM (several CTAs overlap staging with compute)      // diagnostic switch: 1 k_absorb6 (tensor-core fragments), 2 k_absorb5, 0 k_absorb4   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
 
 void prepare_kernel_attrs();
 
@@ -1089,7 +1090,7 @@ static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int a
   if ((PQ * (int)sizeof(TY)) % 16 != 0 || (AB * 8) % 16 != 0 || (uintptr_t)Y % 16 != 0 || (uintptr_t)ad.A % 16 != 0)
     return false;
   // rests per CTA: enough CTAs to cover the GPU, at most 8 big tiles (one warp each)
-  int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / 148, 64 / std::max(1, Cb)));
+  int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / (148 * g_absorb_cps), 64 / std::max(1, Cb)));
   const int nbt = (RB * Cb + 7) / 8;
   const int KW = (int)std::max<int64_t>(1, std::min<int64_t>(8 / nbt, I));
   const int threads = std::max(32, std::min(256, nbt * KW * 32));

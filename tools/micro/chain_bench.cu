@@ -201,6 +201,16 @@ int main(int argc, char **argv) {
     td.Lk = 1600; td.tk = 8; td.Npad = 112;
     float *tiles; cudaMalloc(&tiles, sizeof(float) * 400 * 2 * 112 * 32);
     float t4 = time_us([&] { launch_build_table2(td, nullptr, tiles, 0); });
+    for (int cps : {1, 2, 3, 4}) {
+      g_absorb_cps = cps;
+      ad.pos = 1; ad.left = 1;
+      float u1 = time_us([&] { launch_absorb2(ad, Yf, true, Od, 0, 0); });
+      ad.pos = 2; ad.left = 0;
+      float u2 = time_us([&] { launch_absorb2(ad, Yf, true, Od, 0, 0); });
+      float u3 = time_us([&] { launch_absorb2(am, Wd, false, Od, 1, 0); });
+      printf("absorb CTAs/SM target %d: %.2f | %.2f | %.2f us\n", cps, u1, u2, u3);
+    }
+    g_absorb_cps = 3;
     printf("absorb Y_L->mode2 (320 rest) %.2f us | absorb W over t (1600 rest) %.2f us | mode absorb (40 rest) %.2f us | table T_L %.2f us\n",
            t1, t2, t3, t4);
   }
