@@ -19,9 +19,11 @@ def test_parity_f64_small(name):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name,contract", [("P2", "f64"), ("P3", "f64"), ("P5", "f64"), ("P2", "3xtf32"), ("P5", "3xtf32")])
+@pytest.mark.parametrize("name,contract", [("P2", "f64"), ("P3", "f64"), ("P5", "f64"), ("P6", "f64"), ("P2", "3xtf32"),
+                                           ("P5", "3xtf32"), ("P6", "3xtf32")])
 def test_parity_multi_tile(name, contract):
-    """Sizes spanning several 64/128-row tiles with ragged tails, unequal ranks."""
+    """Sizes spanning several 64/128-row tiles with ragged tails, unequal ranks; P6 has
+    R_nR_{n+1} up to 120 (the inverse's largest tile grids) and rank 12."""
     for b, errs, fo, fg, h, orc in gpu_stream(name, contract=contract):
         assert max(errs) <= TOL[contract], (b, errs)
         assert abs(fg - fo) <= TOL[contract] * fo, (b, fo, fg)

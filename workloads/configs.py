@@ -98,6 +98,10 @@ CONFIGS.update({
                        core_scale=0.5, noise_abs=1e-2, seed=51, split_k=2),
     "P1": StreamConfig("P1", (20, 20), (3, 3, 3), 10, 2, 10, "f64", "f64",
                        core_scale=1.0, noise_abs=1e-3, seed=111),
+    # Large ranks (R_nR_{n+1} up to 120 = 15 pivot blocks of the inverse, rank 12 > 10 in the
+    # table / absorb kernels), ragged dims.
+    "P6": StreamConfig("P6", (36, 29, 23), (12, 10, 11, 9), 10, 4, 3, "f32", "3xtf32",
+                       core_scale=12 ** -0.5, noise_abs=1e-2, seed=61),
     # rSTR parity: I_k > R_kR_{k+1} so leverage scores are non-uniform; m >= max R_nR_{n+1}.
     "R4": StreamConfig("R4", (30, 25, 20), (2, 3, 2, 3), 6, 4, 3, "f32", "f64",
                        core_scale=0.7, noise_abs=1e-2, seed=41, sketch_rows=200),
