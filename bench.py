@@ -139,9 +139,12 @@ def bench_ours(args):
     total_steps = args.warmup + args.steps
     cap = cfg.t_init + cfg.t_new * (2 * total_steps + 2 * args.e2e_steps + 64)
     with torch.cuda.stream(stream):
+        vkw = {}
+        if args.variant != "det":   # rSTR-U / rSTR-L (Alg. 7 / 8) with the config's sketch size
+            vkw = dict(variant=args.variant, sketch_rows=cfg.sketch_rows or 2000, seed=cfg.seed)
         h = lib.str_init(cfg.N, cfg.dims, cfg.ranks, torch.from_numpy(Xi).to(dev), cfg.t_init, init, dtype=cfg.dtype,
                          contract=contract, split_k=cfg.split_k, t_capacity=cap, world_size=world, rank=rank,
-                         nccl_id=nccl_id, device=local, stream=stream.cuda_stream)
+                         nccl_id=nccl_id, device=local, stream=stream.cuda_stream, **vkw)
     lib.str_sync(h)
 
     def barrier():
@@ -220,6 +223,8 @@ def bench_ours(args):
         peak_tf = 148 * 64 * 2 * 1.965e9 / 1e12       # FP64 FMA lanes x clock
         bound, unit = "alu", "TFLOP/s"
         basis = "FP64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz"
+    if avg_pass <= 0:   # rSTR: no dense contraction pass on the path (sampled GEMMs only)
+        avg_pass = float("nan")
     achieved = flops_per_pass / (avg_pass / 1e3) / 1e12
     t_hbm = bytes_per_pass / (peaks["hbm_gbs"] * 1e9) * 1e3
     t_cmp = flops_per_pass / (peak_tf * 1e12) * 1e3
@@ -237,13 +242,16 @@ def bench_ours(args):
             traffic = json.load(open(tpath)).get(f"{args.config}:{contract}")
         except Exception:
             traffic = None
-    roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
-                "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "contraction pass (avg of pass 1/2)",
-                "pass1_us": round(avg_p1 * 1e3, 2), "pass2_us": round(avg_p2 * 1e3, 2),
-                "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
-                "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
-                "peak_basis": basis}
-    if span and all(x for x in span):
+    if args.variant != "det":
+        roofline = {"kernel": "n/a: rSTR has no dense contraction pass (the step is sampled GEMMs and solves)"}
+    else:
+      roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
+                  "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "contraction pass (avg of pass 1/2)",
+                  "pass1_us": round(avg_p1 * 1e3, 2), "pass2_us": round(avg_p2 * 1e3, 2),
+                  "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
+                  "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
+                  "peak_basis": basis}
+    if args.variant == "det" and span and all(x for x in span):
         # in-kernel span (first CTA start to last CTA end, %globaltimer) of the last profiled step;
         # the event pair above also holds the graph node's launch latency (~6 us measured with an
         # empty kernel in the same position)
@@ -275,7 +283,7 @@ def bench_ours(args):
            "d2h_bytes_per_step": int(res.size * 8), "steps": args.e2e_steps}
     # ---- batch TR-ALS on the init slab (Alg. 1, the initialization stage; not part of the step)
     tr_als = None
-    if world == 1:
+    if world == 1 and args.variant == "det":
         Xi_d = torch.from_numpy(Xi).to(dev)
         torch.cuda.synchronize(dev)
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -294,7 +302,10 @@ def bench_ours(args):
             "vs_baseline": None, "dtype": "3xtf32+f64" if contract == "3xtf32" else "f64",
             "data": "synthetic (seeded TR stream, SURVEY.md §8(d).1)",
             "config": {"workload": f"{cfg.name}: order-{cfg.N} {'x'.join(map(str, cfg.dims))} x t_new={cfg.t_new} "
-                                   f"{cfg.dtype}, TR ranks {cfg.ranks[0]}, STR (Alg. 4), X_new sharded on mode 1",
+                                   f"{cfg.dtype}, TR ranks {cfg.ranks[0]}, "
+                                   + ("STR (Alg. 4)" if args.variant == "det" else
+                                      f"rSTR-{'U' if args.variant == 'uniform' else 'L'} (Alg. {7 if args.variant == 'uniform' else 8}), "
+                                      f"m = {cfg.sketch_rows or 2000}") + ", X_new sharded on mode 1",
                        "global_batch_entries": global_entries, "contract": contract, "split_k": cfg.split_k,
                        "parallelism": f"mode-1 shard x{world}",
                        "l2": f"rotating {nd} distinct device-resident batches ({nd * global_entries * 4 / 1e9:.2f} GB)"
@@ -372,6 +383,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--contract", default=None, choices=[None, "3xtf32", "f64"])
+    ap.add_argument("--variant", default="det", choices=["det", "uniform", "leverage"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-budget", type=float, default=60.0)

@@ -4,7 +4,7 @@
 // Per draw (mode k, time step tau) the host draws m indices with replacement from a SplitMix64
 // stream keyed by (seed, tau, k) (reading R11; the oracle re-implements the same
 // generator independently).  Leverage probabilities p_k(i) = l_i(G_k(2)) / rank (Lemma 1,
-// P:567) are computed on the device (Gram + Cholesky: l_i = g_i^T (G^T G)^{-1} g_i when
+// P:567) are computed on the device (Gram + SPD inverse: l_i = g_i^T (G^T G)^{-1} g_i when
 // I_k > R_kR_{k+1}; uniform when I_k <= R_kR_{k+1}, reading R10) and copied to the host for the
 // inverse-CDF draw.  Everything else runs in device kernels:
 //   * sampled slices (G_k)_S = G_k(:, idxs(:,k), :)                       (Alg. 7 l.4)
@@ -149,6 +149,15 @@ static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
   return STR_OK;
 }
 
+// out = B A^{-1} for SPD A (S x S) and `rows` rows of B: the cluster inverse, then a row GEMM on the
+// FP64 tensor-core fragments (the "†" of reading R3/R4 on the device).  Ai: S x S scratch.
+static void solve_right(str_state *h, const double *A, int S, double *Ai, const double *B, int64_t rows, double *out) {
+  launch_spd_inv(A, S, Ai, h->d_info, h->st);
+  tl_mark(h, "spd_inv");
+  launch_rows_mm(B, Ai, S, rows, out, h->st);
+  tl_mark(h, "rows_mm");
+}
+
 static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj,
                  double *C, int M, int N, int64_t K, int acc, int sym = 0) {
   const int nl = launch_gemm_sk(A, sai, sak, B, sbk, sbj, C, M, N, K, acc, (double *)h->sSk.p, h->st, sym);
@@ -171,8 +180,7 @@ static str_status leverage_probs(str_state *h, const double *G, int64_t I, int S
   double *Y = (double *)h->sTmp.p;
   double *pd = Y + I * S;
   gemm(h, G, 1, S, G, S, 1, K, S, S, I, 0);                         // K = G^T G
-  launch_chol_solve(K, S, G, I, Y, h->d_info, h->st);                // Y = G K^{-1}
-  tl_mark(h, "chol_solve");
+  solve_right(h, K, S, (double *)h->Hq.p, G, I, Y);                 // Y = G K^{-1}
   k_rowdot_scale<<<(unsigned)cdiv(I, 128), 128, 0, h->st>>>(Y, G, I, S, 1.0 / (double)S, pd);
   tl_mark(h, "k_rowdot_scale");
   RCU(cudaMemcpyAsync(p.data(), pd, sizeof(double) * I, cudaMemcpyDeviceToHost, h->st));
@@ -341,16 +349,14 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
   gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
   double *GN_new = (double *)h->GN.p + h->T * SN;
-  launch_chol_solve(K, SN, M, tn, GN_new, h->d_info, h->st);
-  tl_mark(h, "chol_solve");
+  solve_right(h, K, SN, (double *)h->Hi.p, M, tn, GN_new);
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
   RTRY(draw_mode(h, N, GN_new, tn));
   for (int n = 1; n < N; ++n) {
     ModeBuf &mb = h->md[n - 1];
     RTRY(sampled_normal_eq(h, X, n, tn, 1));
-    launch_chol_solve((const double *)mb.Q.p, mb.Ra * mb.Rb, (const double *)mb.P.p, mb.I, (double *)mb.G.p,
-                      h->d_info, h->st);
-    tl_mark(h, "chol_solve");
+    solve_right(h, (const double *)mb.Q.p, mb.Ra * mb.Rb, (double *)mb.Qi.p, (const double *)mb.P.p, mb.I,
+                (double *)mb.G.p);
     RTRY(draw_mode(h, n, (const double *)mb.G.p, mb.I));
   }
   h->T += tn;
