@@ -45,10 +45,11 @@ struct GatherDesc {
 };
 
 template <typename T>
-__global__ void k_gather_fibers(const T *__restrict__ X, const int32_t *__restrict__ idx, GatherDesc gd,
+__global__ void k_gather_fibers(const void *const *__restrict__ Xp, const int32_t *__restrict__ idx, GatherDesc gd,
                                 double *__restrict__ XS) {
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= gd.In * gd.m) return;
+  const T *__restrict__ X = (const T *)*Xp;   // the batch, through the device slot set_x fills
   int64_t s = e % gd.m, i = e / gd.m;
   int64_t off = 0;
 #pragma unroll
@@ -59,6 +60,59 @@ __global__ void k_gather_fibers(const T *__restrict__ X, const int32_t *__restri
     }
   }
   XS[e] = (double)X[off];
+}
+
+// Device SplitMix64 draws, bit-identical to the host sampler below (and to the oracle's): output j
+// of the stream keyed by (seed, tau, k) is mix(key + (j + 1) GOLDEN), so every draw is independent
+// (counter-based) and one thread makes one draw.  tau lives on the device so that a captured step
+// graph advances it itself.
+__device__ __forceinline__ uint64_t splitmix_at(uint64_t key, uint64_t j) {
+  uint64_t z = key + (j + 1) * 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ uint64_t draw_key(uint64_t seed, int64_t tau, int k, int N) {
+  return seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(1 + tau * (N + 1) + k));
+}
+
+__global__ void k_tau_advance(int64_t *tau) { *tau += 1; }
+
+// uniform on [I): (u * I) >> 64
+__global__ void k_draw_uniform(uint64_t seed, const int64_t *__restrict__ tau, int k, int N, int64_t I, int64_t m,
+                               int32_t *__restrict__ out) {
+  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (j >= m) return;
+  const uint64_t u = splitmix_at(draw_key(seed, *tau, k, N), (uint64_t)j);
+  out[j] = (int32_t)__umul64hi(u, (uint64_t)I);
+}
+
+// weighted by p (nullptr: 1/I each): one CTA; the CDF is summed by one thread in index order (as the
+// host does), then each thread inverts it for its draws: first i with cdf[i] > (u >> 11) 2^-53 cdf[I-1]
+__global__ void k_draw_weighted(const double *__restrict__ p, int64_t I, uint64_t seed, const int64_t *__restrict__ tau,
+                                int k, int N, int64_t m, int32_t *__restrict__ out) {
+  extern __shared__ double cdf[];
+  if (threadIdx.x == 0) {
+    double acc = 0.0;
+    const double pu = 1.0 / (double)I;
+    for (int64_t i = 0; i < I; ++i) {
+      acc = acc + (p ? p[i] : pu);
+      cdf[i] = acc;
+    }
+  }
+  __syncthreads();
+  const uint64_t key = draw_key(seed, *tau, k, N);
+  const double total = cdf[I - 1];
+  for (int64_t j = threadIdx.x; j < m; j += blockDim.x) {
+    const uint64_t u = splitmix_at(key, (uint64_t)j);
+    const double target = (double)(u >> 11) * 0x1.0p-53 * total;
+    int64_t lo = 0, hi = I;   // upper_bound
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (cdf[mid] <= target) lo = mid + 1; else hi = mid;
+    }
+    out[j] = (int32_t)(lo < I - 1 ? lo : I - 1);
+  }
 }
 
 // p_i = (sum_c Y[i][c] G[i][c]) / rank   (leverage of row i, Def. 8 via g_i^T (G^T G)^{-1} g_i)
@@ -170,6 +224,24 @@ static const double *core_rows(const str_state *h, int k, int64_t t0) {
   return (const double *)h->md[k - 1].G.p;
 }
 
+// Leverage probabilities of an I x S matrix G (device rows), left on the device: returns the
+// pointer, or nullptr when I <= S (every score is 1: the uniform distribution, reading R10).
+static str_status leverage_probs_dev(str_state *h, const double *G, int64_t I, int S, const double **pout) {
+  *pout = nullptr;
+  if (I <= S) return STR_OK;
+  RTRY(ensure_dev(h, h->sGram, sizeof(double) * S * S));
+  RTRY(ensure_dev(h, h->sTmp, sizeof(double) * (I * S + I)));
+  double *K = (double *)h->sGram.p;
+  double *Y = (double *)h->sTmp.p;
+  double *pd = Y + I * S;
+  gemm(h, G, 1, S, G, S, 1, K, S, S, I, 0);                         // K = G^T G
+  solve_right(h, K, S, (double *)h->Hq.p, G, I, Y);                 // Y = G K^{-1}
+  k_rowdot_scale<<<(unsigned)cdiv(I, 128), 128, 0, h->st>>>(Y, G, I, S, 1.0 / (double)S, pd);
+  tl_mark(h, "k_rowdot_scale");
+  *pout = pd;
+  return STR_OK;
+}
+
 // Leverage probabilities of an I x S matrix G (device rows) -> host vector p.
 static str_status leverage_probs(str_state *h, const double *G, int64_t I, int S, std::vector<double> &p) {
   p.assign(I, 1.0 / (double)I);
@@ -195,9 +267,36 @@ static str_status leverage_probs(str_state *h, const double *G, int64_t I, int S
   return STR_OK;
 }
 
+constexpr int64_t kDevCdfMax = 24576;   // leverage CDF in shared memory (192 KB)
+
+// idxs(:,k) <- Randsample(I_k, m[, p_k]) on the device (no host round trip; capturable)
+static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t I) {
+  const int S = RRr(h, k) * RRr(h, k + 1);
+  int32_t *dix = (int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
+  const int64_t *tau = (const int64_t *)h->dTau.p;
+  if (h->variant == STR_SAMPLE_UNIFORM) {
+    k_draw_uniform<<<(unsigned)cdiv(h->m, 256), 256, 0, h->st>>>(h->seed, tau, k, h->N, I, h->m, dix);
+    tl_mark(h, "draw_uniform");
+  } else {
+    const double *pd = nullptr;
+    RTRY(leverage_probs_dev(h, rows, I, S, &pd));
+    k_draw_weighted<<<1, 1024, sizeof(double) * I, h->st>>>(pd, I, h->seed, tau, k, h->N, h->m, dix);
+    tl_mark(h, "draw_weighted");
+  }
+  h->idx_dev[k] = true;
+  ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
+  double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
+  k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
+  tl_mark(h, "k_gather_rows");
+  return STR_OK;
+}
+
 // idxs(:,k) <- Randsample(I_k, m[, p_k]); (G_k)_S <- G_k(:, idxs(:,k), :)
 static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) {
   const int S = RRr(h, k) * RRr(h, k + 1);
+  if (h->forced_idx[k].empty() && h->rstr_dev && (h->variant == STR_SAMPLE_UNIFORM || I <= kDevCdfMax))
+    return draw_mode_dev(h, k, rows, I);
+  h->idx_dev[k] = false;
   std::vector<int32_t> &ix = h->last_idx[k];
   if (!h->forced_idx[k].empty()) {
     ix = h->forced_idx[k];
@@ -273,14 +372,19 @@ static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, 
   gd.m = h->m;
   const unsigned grid = (unsigned)cdiv(gd.In * gd.m, 256);
   if (h->dtype == STR_F64)
-    k_gather_fibers<double><<<grid, 256, 0, h->st>>>((const double *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
+    k_gather_fibers<double><<<grid, 256, 0, h->st>>>((const void *const *)h->dX.p, (const int32_t *)h->sIdxDev.p, gd, XS);
   else
-    k_gather_fibers<float><<<grid, 256, 0, h->st>>>((const float *)X, (const int32_t *)h->sIdxDev.p, gd, XS);
+    k_gather_fibers<float><<<grid, 256, 0, h->st>>>((const void *const *)h->dX.p, (const int32_t *)h->sIdxDev.p, gd, XS);
   tl_mark(h, "gather_fibers");
   return STR_OK;
 }
 
 static str_status rstr_workspace(str_state *h, int64_t tn) {
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_draw_weighted, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kDevCdfMax * 8));
+    attr = true;
+  }
   if (!h->idx_pinned) {
     RCU(cudaMallocHost(&h->idx_pinned, sizeof(int32_t) * h->N * h->m));
     for (int k = 0; k <= h->N; ++k) RCU(cudaEventCreateWithFlags(&h->idx_ev[k], cudaEventDisableTiming));
@@ -293,6 +397,11 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
   }
   maxS = std::max(maxS, h->SN);
   RTRY(ensure_dev(h, h->sIdxDev, sizeof(int32_t) * h->N * h->m));
+  RTRY(ensure_dev(h, h->GNnew, sizeof(double) * tn * h->SN));
+  if (!h->dTau.p) {
+    RTRY(ensure_dev(h, h->dTau, sizeof(int64_t)));
+    RCU(cudaMemsetAsync(h->dTau.p, 0, sizeof(int64_t), h->st));
+  }
   RTRY(ensure_dev(h, h->sX, sizeof(double) * maxI * h->m));
   RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS));
   RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS));   // G_S[2]
@@ -320,6 +429,9 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
 str_status rstr_init(str_state *h, const void *X, int64_t tn) {
   RTRY(rstr_workspace(h, tn));
   h->tau = 0;
+  RCU(cudaMemsetAsync(h->dTau.p, 0, sizeof(int64_t), h->st));
+  launch_set_ptr((const void **)h->dX.p, X, h->st);
+  tl_mark(h, "set_x");
   const int N = h->N;
   // Alg. 7 l.2-5 / Alg. 8 l.2-6: draws for k = 1..N (I_N = t_init)
   for (int k = 1; k <= N; ++k) RTRY(draw_mode(h, k, core_rows(h, k, 0), k == N ? tn : h->md[k - 1].I));
@@ -333,22 +445,38 @@ str_status rstr_init(str_state *h, const void *X, int64_t tn) {
   return STR_OK;
 }
 
-str_status rstr_update(str_state *h, const void *X, int64_t tn) {
-  RTRY(rstr_workspace(h, tn));
+// One rSTR step enqueued without host synchronization (Alg. 7 l.6-38 / Alg. 8): the batch enters
+// through the device slot, tau advances on the device, the new temporal rows go to the scratch
+// GNnew and are appended at the device row counter (as in the STR step), so the whole step can be
+// captured as a graph when every draw runs on the device.
+static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   const int N = h->N;
-  h->tau++;
-  RTRY(ensure_temporal_capacity(h, h->T + tn));
+  launch_set_ptr((const void **)h->dX.p, X, h->st);
+  tl_mark(h, "set_x");
+  if (h->capturing) {
+    cudaStreamCaptureStatus cs;
+    const cudaGraphNode_t *deps = nullptr;
+    size_t nd = 0;
+    RCU(cudaStreamGetCaptureInfo(h->st, &cs, nullptr, nullptr, &deps, &nd));
+    if (nd != 1) {
+      h->err = "cannot locate the captured set_x node";
+      return STR_E_CUDA;
+    }
+    h->gs[0].setx = deps[0];
+  }
+  k_tau_advance<<<1, 1, 0, h->st>>>((int64_t *)h->dTau.p);
+  tl_mark(h, "tau");
   // temporal: G_N^new = X_S[N] G_S (G_S^T G_S)^{-1}  (Alg. 7 l.17-23, reading R4)
   const int SN = h->SN;
   double *GS = (double *)h->sidx.p;
   double *XS = (double *)h->sX.p;
   double *K = (double *)h->sGram.p;
   double *M = (double *)h->Mt.p;
+  double *GN_new = (double *)h->GNnew.p;
   RTRY(sampled_chain(h, N, GS));
   RTRY(gather_fibers(h, X, N, tn, XS));
   gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
-  double *GN_new = (double *)h->GN.p + h->T * SN;
   solve_right(h, K, SN, (double *)h->Hi.p, M, tn, GN_new);
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
   RTRY(draw_mode(h, N, GN_new, tn));
@@ -358,6 +486,71 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
     solve_right(h, (const double *)mb.Q.p, mb.Ra * mb.Rb, (double *)mb.Qi.p, (const double *)mb.P.p, mb.I,
                 (double *)mb.G.p);
     RTRY(draw_mode(h, n, (const double *)mb.G.p, mb.I));
+  }
+  launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, SN, h->st);
+  tl_mark(h, "append");
+  return STR_OK;
+}
+
+str_status rstr_update(str_state *h, const void *X, int64_t tn) {
+  RTRY(rstr_workspace(h, tn));
+  const int N = h->N;
+  h->tau++;   // host mirror of the device counter (host-side draws use it)
+  RTRY(ensure_temporal_capacity(h, h->T + tn));
+  bool forced = false;
+  for (int k = 1; k <= N; ++k) forced = forced || !h->forced_idx[k].empty();
+  bool dev_ok = h->variant == STR_SAMPLE_UNIFORM;
+  if (!dev_ok) {   // weighted draws on the device need each I_k in the shared-memory CDF
+    dev_ok = tn <= kDevCdfMax;
+    for (auto &mb : h->md) dev_ok = dev_ok && mb.I <= kDevCdfMax;
+  }
+  const bool graph = h->use_graph && !h->timeline && h->rstr_dev && dev_ok && !forced;
+  if (!graph) {
+    RTRY(rstr_enqueue(h, X, tn));
+  } else {
+    str_state::GraphSlot &g = h->gs[0];
+    if (!g.exec || g.tn != tn) {
+      g.reset();
+      RCU(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
+      h->capturing = true;
+      h->cur_slot = 0;
+      const int64_t l0 = h->launches;
+      str_status st = rstr_enqueue(h, X, tn);
+      h->capturing = false;
+      cudaGraph_t cg = nullptr;
+      cudaError_t e = cudaStreamEndCapture(h->st, &cg);
+      if (st != STR_OK) {
+        if (cg) cudaGraphDestroy(cg);
+        return st;
+      }
+      if (e != cudaSuccess) {
+        h->err = std::string("rSTR graph capture: ") + cudaGetErrorString(e);
+        return STR_E_CUDA;
+      }
+      e = cudaGraphInstantiate(&g.exec, cg, 0);
+      if (e != cudaSuccess) {
+        cudaGraphDestroy(cg);
+        h->err = std::string("rSTR graph instantiate: ") + cudaGetErrorString(e);
+        return STR_E_CUDA;
+      }
+      g.graph = cg;
+      g.tn = tn;
+      g.launches = h->launches - l0;
+      h->launches = l0;
+    } else {
+      void *slotp = h->dX.p;
+      const void *xp = X;
+      void *args[2] = {&slotp, &xp};
+      cudaKernelNodeParams kp = {};
+      kp.func = set_ptr_kernel();
+      kp.gridDim = dim3(1);
+      kp.blockDim = dim3(1);
+      kp.kernelParams = args;
+      RCU(cudaGraphExecKernelNodeSetParams(g.exec, g.setx, &kp));
+    }
+    RCU(cudaGraphLaunch(g.exec, h->st));
+    h->launches += g.launches;
+    for (int k = 1; k <= N; ++k) h->idx_dev[k] = true;
   }
   h->T += tn;
   cudaError_t e = cudaGetLastError();
@@ -371,6 +564,12 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
 
 extern "C" STR_API str_status str_get_index_table(str_state *h, int32_t mode, int32_t *idx, int64_t m) {
   if (!h || !idx) return STR_E_ARG;
+  if (h->variant != STR_DET && mode >= 1 && mode <= h->N && m == h->m && h->idx_dev[mode]) {
+    RCU(cudaStreamSynchronize(h->st));   // the table was drawn on the device
+    h->last_idx[mode].resize(m);
+    RCU(cudaMemcpy(h->last_idx[mode].data(), (const int32_t *)h->sIdxDev.p + (int64_t)(mode - 1) * m,
+                   sizeof(int32_t) * m, cudaMemcpyDeviceToHost));
+  }
   if (h->variant == STR_DET || mode < 1 || mode > h->N || m != h->m || h->last_idx[mode].empty()) {
     h->err = "no index table for this mode";
     return STR_E_ARG;

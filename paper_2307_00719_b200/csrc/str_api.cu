@@ -886,6 +886,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   {
     const char *ev = getenv("STR_NO_GRAPH");
     h->use_graph = !(ev && ev[0] == '1');
+    const char *hd = getenv("STR_RSTR_HOST_DRAWS");   // diagnostic: the host sampler for rSTR draws
+    h->rstr_dev = !(hd && hd[0] == '1');
   }
 
   // upload init cores: paper layout (a, i, b) at a + Ra*(i + I*b) -> G(2) rows [i][a + Ra*b]

@@ -110,6 +110,9 @@ struct str_state {
   std::vector<int32_t> forced_idx[16];
   std::vector<int32_t> last_idx[16];
   int64_t tau = 0;
+  DevBuf dTau;                      // device copy of tau (advanced by the step itself)
+  bool rstr_dev = true;             // draws on the device (STR_RSTR_HOST_DRAWS=1: host sampler)
+  bool idx_dev[17] = {};            // index table k was drawn on the device (copy back on request)
 
   // bookkeeping
   int64_t launches = 0;
@@ -140,7 +143,7 @@ struct str_state {
     gs[1].reset();
     for (auto &e : pev)
       if (e) { cudaEventDestroy(e); e = nullptr; }
-    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau);
     if (idx_pinned) cudaFreeHost(idx_pinned);
     idx_pinned = nullptr;
     for (auto &e : idx_ev)
