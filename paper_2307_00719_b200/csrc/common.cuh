@@ -60,6 +60,12 @@ struct QEpi {
   double *Q;
   int32_t Rn, Rn1;
   int32_t mode;
+  // mode 4 (fit epilogue of str_fit): C[row][col] = X^hat at (l, r, t) with row = l + L t, col = r;
+  // per-CTA partial sums (sum (x - x^hat)^2, sum x^2) of the tile go to part[CTA]
+  const void *X = nullptr;
+  int64_t L = 0, Rr = 0;
+  int32_t xf64 = 0;
+  double2 *part = nullptr;
 };
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }

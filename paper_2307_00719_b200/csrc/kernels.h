@@ -56,6 +56,10 @@ inline void prefer_max_smem(F *f) {
   cudaFuncSetAttribute((const void *)f, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
 }
 void prepare_f64_attrs();
+int launch_fit_gemm(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,
+                    int64_t Rr, int64_t tn, double *TRp, double2 *partials, double *acc2, cudaStream_t s);
+size_t fit_gemm_partials(int64_t L, int64_t Rr, int64_t tn);
+void launch_fit_reduce(const double2 *partials, int64_t n, double *acc2, cudaStream_t s);
 void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn, int SN, cudaStream_t s);
 size_t contract_f64_ws_doubles(int64_t M, int64_t K, int W);
 size_t fit_partials(int64_t L, int64_t Rr, int64_t tn);

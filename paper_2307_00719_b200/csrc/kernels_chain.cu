@@ -656,6 +656,34 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
   c0 += Rs[(tile * 32 + lane) * 2];
   c1 += Rs[(tile * 32 + lane) * 2 + 1];
   const int row = row0 + 8 * ti + g;
+  if (q.mode == 4) {   // fit: residual and norm sums of this tile (warps 0-3), fixed-order partials
+    double d2 = 0.0, x2 = 0.0;
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = col0 + 8 * tj + 2 * tg + e;
+      if (row < M && col < N) {
+        const int64_t l = row % q.L, t = row / q.L;
+        const int64_t off = l + q.L * col + q.L * q.Rr * t;
+        const double x = q.xf64 ? ((const double *)q.X)[off] : (double)((const float *)q.X)[off];
+        const double dv = x - (e ? c1 : c0);
+        d2 = fma(dv, dv, d2);
+        x2 = fma(x, x, x2);
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      d2 += __shfl_xor_sync(0xffffffffu, d2, o);
+      x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+    }
+    if (lane == 0) {
+      Rs[256 + 2 * warp] = d2;
+      Rs[256 + 2 * warp + 1] = x2;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");   // the four epilogue warps
+    if (threadIdx.x == 0)
+      q.part[blockIdx.x + (int64_t)gridDim.x * blockIdx.y] =
+          make_double2((Rs[256] + Rs[258]) + (Rs[260] + Rs[262]), (Rs[257] + Rs[259]) + (Rs[261] + Rs[263]));
+    return;
+  }
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int col = col0 + 8 * tj + 2 * tg + e;
@@ -679,8 +707,43 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
 
 static size_t gemm_dmma_smem(int K) {
   const size_t k4 = (size_t)(K + 3) / 4 * 4;
-  return sizeof(double) * (std::max((size_t)16 * gemm_ka(K), k4 * kGbS) + k4 * kGbS + 4 * 32 * 2);
+  return sizeof(double) * (std::max((size_t)16 * gemm_ka(K), k4 * kGbS) + k4 * kGbS + 4 * 32 * 2 + 8);
 }
+
+// TRp[p Rb + q][r] = TR[r][q Ra + p]: T_R rows as the K x N operand of the fit GEMM
+__global__ void k_fit_perm_tr(const double *__restrict__ TR, int Ra, int Rb, int64_t Rr, double *__restrict__ TRp) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int W = Ra * Rb;
+  if (e >= (int64_t)W * Rr) return;
+  const int64_t w = e / Rr, r = e - w * Rr;
+  const int p = (int)(w / Rb), qq = (int)(w - (int64_t)p * Rb);
+  TRp[e] = TR[r * W + qq * Ra + p];
+}
+
+// ||X - TL TR^T||^2 and ||X||^2 of tn slices on the fragment GEMM with the fit epilogue.
+int launch_fit_gemm(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,
+                    int64_t Rr, int64_t tn, double *TRp, double2 *partials, double *acc2, cudaStream_t s) {
+  prepare_kernel_attrs();
+  const int W = Ra * Rb;
+  k_fit_perm_tr<<<(unsigned)cdiv((int64_t)W * Rr, 256), 256, 0, s>>>(TR, Ra, Rb, Rr, TRp);
+  const int M = (int)(L * tn), N = (int)Rr;
+  dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
+  QEpi q{nullptr, 0, 0, 4};
+  q.X = X;
+  q.L = L;
+  q.Rr = Rr;
+  q.xf64 = x_is_f64 ? 1 : 0;
+  q.part = partials;
+  const size_t smd = gemm_dmma_smem(W);
+  const bool al16 = (W % 2 == 0) && (N % 2 == 0);
+  if (al16)
+    k_chain_gemm_dmma<true, false><<<gd, 256, smd, s>>>(TLf, TRp, nullptr, M, N, W, q);
+  else
+    k_chain_gemm_dmma<false, false><<<gd, 256, smd, s>>>(TLf, TRp, nullptr, M, N, W, q);
+  launch_fit_reduce(partials, (int64_t)gd.x * gd.y, acc2, s);
+  return 3;
+}
+size_t fit_gemm_partials(int64_t L, int64_t Rr, int64_t tn) { return (size_t)cdiv(Rr, 16) * cdiv(L * tn, 16); }
 
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
   if (g_dbg_skip & 16) return;

@@ -232,6 +232,10 @@ void launch_append_rows(double *GN, int64_t *dT, const double *GNnew, int64_t tn
   k_append_rows<<<1, 512, 0, s>>>(GN, dT, GNnew, tn * SN, tn, SN);
 }
 
+void launch_fit_reduce(const double2 *partials, int64_t n, double *acc2, cudaStream_t s) {
+  k_fit_reduce<<<1, 256, 0, s>>>(partials, n, acc2);
+}
+
 void prepare_f64_attrs() {
   prefer_max_smem(k_set_ptr);
   prefer_max_smem(k_append_rows);

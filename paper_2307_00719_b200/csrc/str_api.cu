@@ -1039,19 +1039,25 @@ extern "C" str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t
   const int N = h->N, k = h->k;
   const int Ra = RR(h, N), Rb = RR(h, k + 1);
   const int64_t chunk = 16;
-  DevBuf tr, tl, parts, acc;
+  DevBuf tr, tl, parts, acc, trp;
   TRY(ensure(h, tr, sizeof(double) * h->Rr * Ra * Rb));
+  TRY(ensure(h, trp, sizeof(double) * h->Rr * Ra * Rb));
   TRY(build_table(h, desc_TR(h), (double *)tr.p, nullptr, "table_TR"));
   TRY(ensure(h, tl, sizeof(double) * h->L * chunk * Ra * Rb));
-  TRY(ensure(h, parts, sizeof(double2) * fit_partials(h->L, h->Rr, chunk)));
+  TRY(ensure(h, parts, sizeof(double2) * std::max(fit_partials(h->L, h->Rr, chunk), fit_gemm_partials(h->L, h->Rr, chunk))));
   TRY(ensure(h, acc, sizeof(double) * 2));
   CU(cudaMemsetAsync(acc.p, 0, sizeof(double) * 2, h->st));
   for (int64_t c0 = 0; c0 < t; c0 += chunk) {
     int64_t tn = std::min(chunk, t - c0);
     TRY(build_table(h, desc_TL(h, t0 + c0, tn), (double *)tl.p, nullptr, "table_TL"));
     const char *xp = (const char *)X + (size_t)h->L * h->Rr * c0 * h->xbytes;
-    int nf = launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
-                              h->Rr, tn, (double2 *)parts.p, (double *)acc.p, h->st);
+    // X^hat = T_L T_R^T on the FP64 tensor-core fragments, residual sums in the epilogue (the row
+    // GEMM needs L tn and R_r below 2^31 and the ranks' W <= 256)
+    const bool fg = h->L * tn < ((int64_t)1 << 31) && h->Rr < ((int64_t)1 << 31) && Ra * Rb <= 256;
+    int nf = fg ? launch_fit_gemm(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
+                                  h->Rr, tn, (double *)trp.p, (double2 *)parts.p, (double *)acc.p, h->st)
+                : launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
+                             h->Rr, tn, (double2 *)parts.p, (double *)acc.p, h->st);
     tl_mark(h, "fit", nf);
     TRY(check_launch(h, "fit"));
   }
@@ -1060,6 +1066,7 @@ extern "C" str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t
   CU(cudaMemcpyAsync(sums, acc.p, sizeof(sums), cudaMemcpyDeviceToHost, h->st));
   CU(cudaStreamSynchronize(h->st));
   cudaFree(tr.p);
+  cudaFree(trp.p);
   cudaFree(tl.p);
   cudaFree(parts.p);
   cudaFree(acc.p);

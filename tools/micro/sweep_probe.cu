@@ -2,7 +2,10 @@
 // building blocks on sm_100a (diagnostic only).
 #include "../../paper_2307_00719_b200/csrc/kernels_chain.cu"
 #include <cstdio>
-namespace strb200 { void prepare_f64_attrs() {} }
+namespace strb200 {
+void prepare_f64_attrs() {}
+void launch_fit_reduce(const double2 *, int64_t, double *, cudaStream_t) {}
+}  // namespace strb200
 using namespace strb200;
 
 __global__ void k_sweep_lat(double *out, long long *cyc, int iters) {
