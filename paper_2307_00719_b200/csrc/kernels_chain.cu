@@ -359,23 +359,36 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
   };
   bool bad = false;
   cl.sync();   // every CTA's shared memory exists before the first remote store
+#ifdef INV_PROBE
+  long long pw = 0, pu = 0, pb = 0, ps = 0;
+#endif
   for (int kb = -1; kb < nt; ++kb) {
+#ifdef INV_PROBE
+    const long long q0 = clock64();
+#endif
     const int cur = (kb + 2) & 1, nxt = cur ^ 1, kn = kb + 1;
     const double *V = Vb[cur];
     double *Vn = Vb[nxt];
     const double *D = Db[cur];
     double *Dn = Db[nxt];
-    if (kb >= 0) {
-      // W = V D for every row block (DMMA: A = V block rows, B = D)
-      for (int I = warp; I < nt; I += kInvCThreads / 32) {
-        double w0 = 0.0, w1 = 0.0;
-        dmma884(w0, w1, V[(8 * I + g) * kVS + tg], D[tg * 8 + g]);
-        dmma884(w0, w1, V[(8 * I + g) * kVS + 4 + tg], D[(4 + tg) * 8 + g]);
-        Wb[(8 * I + g) * kVS + 2 * tg] = w0;
-        Wb[(8 * I + g) * kVS + 2 * tg + 1] = w1;
-      }
-      __syncthreads();
+    // W = V D for a row block (DMMA: A = V block rows, B = D) into Wb
+    auto wrow = [&](int I) {
+      double w0 = 0.0, w1 = 0.0;
+      dmma884(w0, w1, V[(8 * I + g) * kVS + tg], D[tg * 8 + g]);
+      dmma884(w0, w1, V[(8 * I + g) * kVS + 4 + tg], D[(4 + tg) * 8 + g]);
+      Wb[(8 * I + g) * kVS + 2 * tg] = w0;
+      Wb[(8 * I + g) * kVS + 2 * tg + 1] = w1;
+    };
+    if (kb >= 0 && warp > 0) {
+      // warps 1-7: every row block (the pivot-row / pivot-column cases read other rows), then a
+      // named barrier among these 224 threads only: warp 0 (the diagonal tiles, the look-ahead
+      // sweep) forms the rows it needs itself and never waits for this phase
+      for (int I = warp - 1; I < nt; I += kInvCThreads / 32 - 1) wrow(I);
+      asm volatile("bar.sync 1, %0;" ::"n"(kInvCThreads - 32) : "memory");
     }
+#ifdef INV_PROBE
+    const long long q1 = clock64();
+#endif
     // one tile: step-kb update, then its share of the next panel
     auto tile = [&](double (&t)[2], int I, int J) {
       if (kb >= 0) {
@@ -404,25 +417,61 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
       }
     };
     if (warp == 0) {
-      // the next pivot block first (if it lives here): update, publish, invert, broadcast
+      // the next pivot block first (if it lives here): its W row, update, publish, invert, broadcast
 #pragma unroll
       for (int sl = 0; sl < kInvCDiag; ++sl)
         if (TI[sl] == kn) {
+          if (kb >= 0) {
+            wrow(kn);
+            __syncwarp();
+          }
           tile(cc[sl], kn, kn);
+#ifdef INV_PROBE
+          const long long qs = clock64();
+#endif
           double d[2] = {cc[sl][0], cc[sl][1]};
           bad = warp_sweep8(d, g, tg) || bad;
           put2(Dn, g * 8 + 2 * tg, -d[0], -d[1]);
+#ifdef INV_PROBE
+          ps += clock64() - qs;
+#endif
         }
 #pragma unroll
       for (int sl = 0; sl < kInvCDiag; ++sl)
-        if (TI[sl] >= 0 && TI[sl] != kn) tile(cc[sl], TI[sl], TI[sl]);
+        if (TI[sl] >= 0 && TI[sl] != kn) {
+          if (kb >= 0 && TI[sl] != kb) {   // the diagonal update needs only its own W row
+            wrow(TI[sl]);
+            __syncwarp();
+          }
+          tile(cc[sl], TI[sl], TI[sl]);
+        }
     } else {
 #pragma unroll
       for (int sl = 0; sl < kInvCSlots; ++sl)
         if (TI[sl] >= 0) tile(cc[sl], TI[sl], TJ[sl]);
     }
+#ifdef INV_PROBE
+    const long long q2 = clock64();
+#endif
     cl.sync();
+#ifdef INV_PROBE
+    const long long q3 = clock64();
+    pw += q1 - q0;
+    pu += q2 - q1;
+    pb += q3 - q2;
+#endif
   }
+#ifdef INV_PROBE
+  // per-CTA totals of warp 0 (W phase, updates incl. look-ahead sweep, cluster barrier) and the
+  // look-ahead sweeps this CTA ran
+  if (threadIdx.x == 0) {
+    g_inv_probe[0 + 0] = 0;
+    atomicAdd((unsigned long long *)&g_inv_probe[1], (unsigned long long)pw);
+    atomicAdd((unsigned long long *)&g_inv_probe[2], (unsigned long long)pu);
+    atomicAdd((unsigned long long *)&g_inv_probe[3], (unsigned long long)pb);
+    atomicAdd((unsigned long long *)&g_inv_probe[4], (unsigned long long)ps);
+  }
+#endif
   if (bad && lane == 0 && info) atomicExch(info, 1);
   // -A = Q^{-1}: both triangles straight to global memory
 #pragma unroll

@@ -240,10 +240,13 @@ int main(int argc, char **argv) {
     cudaDeviceSynchronize();
   }
   cudaMemcpyFromSymbol(pr, g_inv_probe, sizeof(pr));
-  printf("spd_inv cycles: load %lld  sweep %lld (%.0f/block step)  store %lld\n", pr[0], pr[1], pr[1] / (double)((S + 7) / 8), pr[2]);
-  const int nt = (S + 7) / 8;
-  printf("  per step (warp 20): slots %.0f  sync1 %.0f  W %.0f  total %.0f | look-ahead warps' slot+sweep %.0f (summed over %d launches)\n",
-         pr[3] / (double)nt, pr[5] / (double)nt, pr[6] / (double)nt, pr[7] / (double)nt, pr[4] / (double)nt, 1);
+  {
+    const int nt = (S + 7) / 8;
+    printf("cluster inverse, per step (mean over the 4 CTAs, warp 0): W %.0f  updates %.0f  barrier %.0f cycles; "
+           "pivot sweeps %.0f cycles each\n", pr[1] / 4.0 / (nt + 1), pr[2] / 4.0 / (nt + 1), pr[3] / 4.0 / (nt + 1),
+           pr[4] / (double)nt);
+  }
+
 
   printf("residual ||G Q - P||/||P|| = %.2e  info=%d  err=%s\n", sqrt(err / nrm), hinfo,
          cudaGetErrorString(cudaGetLastError()));
