@@ -14,6 +14,7 @@ Modules
   stream   STR (Alg. 4)
   sampler  SplitMix64 index draws, uniform / leverage distributions (ledger #11)
   rstream  rSTR-U / rSTR-L (Alg. 7, Alg. 8)
+  ksrft    rSTR-K: KSRFT mixing (Def. 10, Alg. 5), Alg. 9
   fit      relative error
 
 Parity status: every function is pinned by a -m "not gpu"
