@@ -140,7 +140,7 @@ def bench_ours(args):
     cap = cfg.t_init + cfg.t_new * (2 * total_steps + 2 * args.e2e_steps + 64)
     with torch.cuda.stream(stream):
         vkw = {}
-        if args.variant != "det":   # rSTR-U / rSTR-L (Alg. 7 / 8) with the config's sketch size
+        if args.variant != "det":   # rSTR-U / -L / -K (Alg. 7 / 8 / 9) with the config's sketch size
             vkw = dict(variant=args.variant, sketch_rows=cfg.sketch_rows or 2000, seed=cfg.seed)
         h = lib.str_init(cfg.N, cfg.dims, cfg.ranks, torch.from_numpy(Xi).to(dev), cfg.t_init, init, dtype=cfg.dtype,
                          contract=contract, split_k=cfg.split_k, t_capacity=cap, world_size=world, rank=rank,
@@ -304,7 +304,8 @@ def bench_ours(args):
             "config": {"workload": f"{cfg.name}: order-{cfg.N} {'x'.join(map(str, cfg.dims))} x t_new={cfg.t_new} "
                                    f"{cfg.dtype}, TR ranks {cfg.ranks[0]}, "
                                    + ("STR (Alg. 4)" if args.variant == "det" else
-                                      f"rSTR-{'U' if args.variant == 'uniform' else 'L'} (Alg. {7 if args.variant == 'uniform' else 8}), "
+                                      f"rSTR-{ {'uniform': 'U', 'leverage': 'L', 'ksrft': 'K'}[args.variant]} "
+                                      f"(Alg. { {'uniform': 7, 'leverage': 8, 'ksrft': 9}[args.variant]}), "
                                       f"m = {cfg.sketch_rows or 2000}") + ", X_new sharded on mode 1",
                        "global_batch_entries": global_entries, "contract": contract, "split_k": cfg.split_k,
                        "parallelism": f"mode-1 shard x{world}",
@@ -383,7 +384,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="C5")
     ap.add_argument("--contract", default=None, choices=[None, "3xtf32", "f64"])
-    ap.add_argument("--variant", default="det", choices=["det", "uniform", "leverage"])
+    ap.add_argument("--variant", default="det", choices=["det", "uniform", "leverage", "ksrft"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-budget", type=float, default=60.0)

@@ -65,7 +65,9 @@ typedef enum {
 
 typedef enum { STR_F32 = 0, STR_F64 = 1 } str_dtype;
 typedef enum { STR_CONTRACT_3XTF32 = 0, STR_CONTRACT_F64 = 1 } str_contract;
-typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2 } str_variant;
+/* STR (Alg. 4); rSTR-U (Alg. 7), rSTR-L (Alg. 8); rSTR-K: KSRFT mixing + uniform rows (Def. 10
+   P:614-627, Alg. 9; readings R12-R17) */
+typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2, STR_SAMPLE_KSRFT = 3 } str_variant;
 
 typedef struct {
   int32_t order;          /* N >= 3 */
@@ -73,7 +75,7 @@ typedef struct {
   const int32_t *ranks;   /* R_1 .. R_N, each in [1, 16]; R_n R_{n+1} <= 128 */
   str_dtype dtype;        /* element type of every X passed in */
   str_contract contract;  /* precision of the X contractions (state is always fp64) */
-  str_variant variant;    /* STR (Alg. 4) or rSTR with uniform (Alg. 7) / leverage (Alg. 8) rows */
+  str_variant variant;    /* STR (Alg. 4) or rSTR-U / rSTR-L / rSTR-K (Alg. 7 / 8 / 9) */
   int64_t sketch_rows;    /* rSTR m; must be >= max_n R_n R_{n+1} */
   uint64_t seed;          /* rSTR sampler seed (reading R11) */
   int64_t t_capacity;     /* initial capacity of temporal rows kept on the device (0 = 4096);

@@ -18,8 +18,8 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 from . import _lib
-from ._lib import (STR_CONTRACT_3XTF32, STR_CONTRACT_F64, STR_DET, STR_F32, STR_F64, STR_SAMPLE_LEVERAGE,
-                   STR_SAMPLE_UNIFORM, StrError, str_config)
+from ._lib import (STR_CONTRACT_3XTF32, STR_CONTRACT_F64, STR_DET, STR_F32, STR_F64, STR_SAMPLE_KSRFT,
+                   STR_SAMPLE_LEVERAGE, STR_SAMPLE_UNIFORM, StrError, str_config)
 
 __all__ = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",
            "str_fit", "str_sync", "str_processed", "str_error_string", "str_destroy", "str_kernel_launches",
@@ -28,7 +28,7 @@ __all__ = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cor
            "LIB_PATH"]
 
 LIB_PATH = _lib.LIB_PATH
-_VARIANTS = {"det": STR_DET, "uniform": STR_SAMPLE_UNIFORM, "leverage": STR_SAMPLE_LEVERAGE}
+_VARIANTS = {"det": STR_DET, "uniform": STR_SAMPLE_UNIFORM, "leverage": STR_SAMPLE_LEVERAGE, "ksrft": STR_SAMPLE_KSRFT}
 _CONTRACTS = {"3xtf32": STR_CONTRACT_3XTF32, "f64": STR_CONTRACT_F64}
 _DTYPES = {"f32": STR_F32, "f64": STR_F64}
 

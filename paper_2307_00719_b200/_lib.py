@@ -16,7 +16,7 @@ STATUS_NAMES = ["STR_OK", "STR_E_ARG", "STR_E_SHAPE", "STR_E_PRECOND", "STR_E_NU
                 "STR_E_OOM", "STR_E_POISONED"]
 STR_F32, STR_F64 = 0, 1
 STR_CONTRACT_3XTF32, STR_CONTRACT_F64 = 0, 1
-STR_DET, STR_SAMPLE_UNIFORM, STR_SAMPLE_LEVERAGE = 0, 1, 2
+STR_DET, STR_SAMPLE_UNIFORM, STR_SAMPLE_LEVERAGE, STR_SAMPLE_KSRFT = 0, 1, 2, 3
 
 # Every symbol include/str.h declares (checked by tests/test_abi.py without a GPU).
 EXPORTS = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",

@@ -12,6 +12,11 @@
 //   * zipped fibers X_S[n] (I_n x m) gathered from X                      (reading R7)
 //   * P_n += X_S[n] G_S[2], Q_n += G_S[2]^T G_S[2], G_n = P_n Q_n^{-1}     (Alg. 7 l.36-38)
 //   * temporal rows G_N^new = X_S[N] G_S (G_S^T G_S)^{-1}                (reading R4)
+// rSTR-K (Alg. 9) runs the same schedule on KSRFT-mixed data (ksrft.cu): every step
+// draws sign flips and mixes the batch, the sampled slices are rows of the mixed cores, the chain
+// is complex and written as the stacked real [Re; Im] matrix (2m rows), the fibers are unmixed on
+// their own mode, so the same real GEMMs with K = 2m give Re(X~ conj G^) and Re(G^T conj G^); the
+// temporal solve takes the real halves (K = m; readings R12-R17).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -224,6 +229,51 @@ static const double *core_rows(const str_state *h, int k, int64_t t0) {
   return (const double *)h->md[k - 1].G.p;
 }
 
+// ---- rSTR-K helpers
+static bool ks_f64(const str_state *h) { return h->contract == STR_CONTRACT_F64; }
+
+// dims of the batch being mixed: I_1..I_{N-1}, tn
+static void ks_dims(const str_state *h, int64_t tn, int64_t *dims) {
+  for (int j = 0; j < h->N - 1; ++j) dims[j] = h->md[j].I;
+  dims[h->N - 1] = tn;
+}
+
+// Sign flips of this step (tau on the device) and X^ = X x_1 (F_1 D_1) ... x_N (F_N D_N) (Alg. 9
+// l.21-22 P:1224-1225; Alg. 5 l.3 P:651).  The batch enters through the device slot dX.
+static str_status ks_mix(str_state *h, int64_t tn) {
+  int64_t dims[16];
+  ks_dims(h, tn, dims);
+  int64_t off = 0;
+  for (int j = 0; j < h->N; ++j) {
+    h->ks_off[j] = off;
+    off += dims[j];
+  }
+  launch_draw_signs(h->seed, (const int64_t *)h->dTau.p, h->N, off, (double *)h->ksSign.p, h->st);
+  tl_mark(h, "draw_signs");
+  for (int j = 0; j < h->N; ++j) {
+    if (launch_mix_mode((const void *const *)h->dX.p, h->dtype == STR_F64, h->ksXh.p, ks_f64(h), dims, h->N, j,
+                        (const double *)h->ksSign.p + h->ks_off[j], h->st) != 0) {
+      h->err = "KSRFT mixing: mode too long for the shared-memory DFT";
+      return STR_E_ARG;
+    }
+    tl_mark(h, "mix_mode");
+  }
+  return STR_OK;
+}
+
+// (G^_k)_S = (G_k x_2 F_k D_k)(:, idxs(:,k), :) for the rows of G_k (I rows), into dst (m x S complex)
+static str_status ks_sample(str_state *h, int k, const double *rows, int64_t I, double *dst) {
+  const int S = RRr(h, k) * RRr(h, k + 1);
+  const int32_t *dix = (const int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
+  if (launch_mix_sample(rows, I, S, dix, h->m, (const double *)h->ksSign.p + h->ks_off[k - 1], (double2 *)dst,
+                        h->st) != 0) {
+    h->err = "KSRFT: mode too long for the sampled mixing kernel";
+    return STR_E_ARG;
+  }
+  tl_mark(h, "mix_sample");
+  return STR_OK;
+}
+
 // Leverage probabilities of an I x S matrix G (device rows), left on the device: returns the
 // pointer, or nullptr when I <= S (every score is 1: the uniform distribution, reading R10).
 static str_status leverage_probs_dev(str_state *h, const double *G, int64_t I, int S, const double **pout) {
@@ -274,7 +324,7 @@ static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t
   const int S = RRr(h, k) * RRr(h, k + 1);
   int32_t *dix = (int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
   const int64_t *tau = (const int64_t *)h->dTau.p;
-  if (h->variant == STR_SAMPLE_UNIFORM) {
+  if (h->variant != STR_SAMPLE_LEVERAGE) {
     k_draw_uniform<<<(unsigned)cdiv(h->m, 256), 256, 0, h->st>>>(h->seed, tau, k, h->N, I, h->m, dix);
     tl_mark(h, "draw_uniform");
   } else {
@@ -286,6 +336,7 @@ static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t
   h->idx_dev[k] = true;
   ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
   double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
+  if (h->ksrft()) return ks_sample(h, k, rows, I, dst);
   k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
   tl_mark(h, "k_gather_rows");
   return STR_OK;
@@ -294,13 +345,13 @@ static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t
 // idxs(:,k) <- Randsample(I_k, m[, p_k]); (G_k)_S <- G_k(:, idxs(:,k), :)
 static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) {
   const int S = RRr(h, k) * RRr(h, k + 1);
-  if (h->forced_idx[k].empty() && h->rstr_dev && (h->variant == STR_SAMPLE_UNIFORM || I <= kDevCdfMax))
+  if (h->forced_idx[k].empty() && h->rstr_dev && (h->variant != STR_SAMPLE_LEVERAGE || I <= kDevCdfMax))
     return draw_mode_dev(h, k, rows, I);
   h->idx_dev[k] = false;
   std::vector<int32_t> &ix = h->last_idx[k];
   if (!h->forced_idx[k].empty()) {
     ix = h->forced_idx[k];
-  } else if (h->variant == STR_SAMPLE_UNIFORM) {
+  } else if (h->variant != STR_SAMPLE_LEVERAGE) {
     draw_uniform(h->seed, h->tau, k, h->N, I, h->m, ix);
   } else {
     std::vector<double> p;
@@ -316,6 +367,7 @@ static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) 
   RCU(cudaEventRecord(h->idx_ev[k], h->st));
   ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
   double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
+  if (h->ksrft()) return ks_sample(h, k, rows, I, dst);
   k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
   tl_mark(h, "k_gather_rows");
   return STR_OK;
@@ -323,6 +375,25 @@ static str_status draw_mode(str_state *h, int k, const double *rows, int64_t I) 
 
 // G_S[2] (m x R_nR_{n+1}) = ⊡₂ chain of sampled slices in order n+1..N, 1..n-1 (identity start).
 static str_status sampled_chain(str_state *h, int n, double *out) {
+  if (h->ksrft()) {   // complex slices -> stacked [Re; Im] (2m x S)
+    const double2 *G[kMaxFactors];
+    int Ra[kMaxFactors], Rb[kMaxFactors], nf = 0;
+    const int N = h->N;
+    auto add = [&](int k) {
+      G[nf] = (const double2 *)((k == N) ? h->sG.p : h->md[k - 1].samp.p);
+      Ra[nf] = RRr(h, k);
+      Rb[nf] = RRr(h, k + 1);
+      ++nf;
+    };
+    for (int k = n + 1; k <= N; ++k) add(k);
+    for (int k = 1; k < n; ++k) add(k);
+    if (launch_chain_complex(G, Ra, Rb, nf, h->m, out, h->st) != 0) {
+      h->err = "complex sampled chain: bad factor list";
+      return STR_E_ARG;
+    }
+    tl_mark(h, "chain_complex");
+    return STR_OK;
+  }
   FactorList fl;
   fl.n = 0;
   const int N = h->N;
@@ -358,6 +429,17 @@ static str_status sampled_chain(str_state *h, int n, double *out) {
 }
 
 static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, double *XS) {
+  if (h->ksrft()) {   // X~_S[n] = D_n F_n^* X^_S[n], stacked [Re | Im] (I_n x 2m)
+    int64_t dims[16];
+    ks_dims(h, tn, dims);
+    if (launch_gather_unmix(h->ksXh.p, ks_f64(h), dims, h->N, n, (const int32_t *)h->sIdxDev.p, h->m,
+                            (const double *)h->ksSign.p + h->ks_off[n - 1], XS, h->st) != 0) {
+      h->err = "KSRFT: fiber too long for the unmixing kernel";
+      return STR_E_ARG;
+    }
+    tl_mark(h, "gather_unmix");
+    return STR_OK;
+  }
   GatherDesc gd;
   gd.N = h->N;
   gd.n = n;
@@ -402,13 +484,24 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
     RTRY(ensure_dev(h, h->dTau, sizeof(int64_t)));
     RCU(cudaMemsetAsync(h->dTau.p, 0, sizeof(int64_t), h->st));
   }
-  RTRY(ensure_dev(h, h->sX, sizeof(double) * maxI * h->m));
-  RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS));
-  RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS));   // G_S[2]
+  const int64_t cw = h->ksrft() ? 2 : 1;   // rSTR-K: complex slices, stacked [Re; Im] rows
+  RTRY(ensure_dev(h, h->sX, sizeof(double) * maxI * h->m * cw));
+  RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS * cw));
+  RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS * cw));   // G_S[2]
   RTRY(ensure_dev(h, h->sGram, sizeof(double) * maxS * maxS));
-  RTRY(ensure_dev(h, h->sSk, sizeof(double) * gemm_sk_ws_doubles((int)std::max<int64_t>(maxI, maxS), maxS, h->m)));
+  RTRY(ensure_dev(h, h->sSk,
+                  sizeof(double) * gemm_sk_ws_doubles((int)std::max<int64_t>(maxI, maxS), maxS, h->m * cw)));
   RTRY(ensure_dev(h, h->Mt, sizeof(double) * std::max<int64_t>(maxI, tn) * maxS));
-  for (auto &mb : h->md) RTRY(ensure_dev(h, mb.samp, sizeof(double) * h->m * mb.Ra * mb.Rb));
+  for (auto &mb : h->md) RTRY(ensure_dev(h, mb.samp, sizeof(double) * h->m * mb.Ra * mb.Rb * cw));
+  if (h->ksrft()) {
+    int64_t slice = 1, sumI = tn;
+    for (auto &mb : h->md) {
+      slice *= mb.I;
+      sumI += mb.I;
+    }
+    RTRY(ensure_dev(h, h->ksXh, (ks_f64(h) ? sizeof(double2) : sizeof(float2)) * slice * tn));
+    RTRY(ensure_dev(h, h->ksSign, sizeof(double) * sumI));
+  }
   return STR_OK;
 }
 
@@ -419,10 +512,11 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   const int S = mb.Ra * mb.Rb;
   double *GS = (double *)h->sidx.p;
   double *XS = (double *)h->sX.p;
+  const int64_t K = h->ksrft() ? 2 * h->m : h->m;   // rSTR-K: [Re X~, Im X~][Re G^; Im G^] (reading R16)
   RTRY(sampled_chain(h, n, GS));
   RTRY(gather_fibers(h, X, n, tn, XS));
-  gemm(h, XS, h->m, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, h->m, acc);
-  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, h->m, acc, 1);   // Q_n += sym(G_S^T G_S)
+  gemm(h, XS, K, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, K, acc);
+  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1);   // Q_n += sym(G_S^T G_S)
   return STR_OK;
 }
 
@@ -433,7 +527,8 @@ str_status rstr_init(str_state *h, const void *X, int64_t tn) {
   launch_set_ptr((const void **)h->dX.p, X, h->st);
   tl_mark(h, "set_x");
   const int N = h->N;
-  // Alg. 7 l.2-5 / Alg. 8 l.2-6: draws for k = 1..N (I_N = t_init)
+  if (h->ksrft()) RTRY(ks_mix(h, tn));   // Alg. 9 l.2-4
+  // Alg. 7 l.2-5 / Alg. 8 l.2-6 / Alg. 9 l.5-8: draws for k = 1..N (I_N = t_init)
   for (int k = 1; k <= N; ++k) RTRY(draw_mode(h, k, core_rows(h, k, 0), k == N ? tn : h->md[k - 1].I));
   for (int n = 1; n < N; ++n) RTRY(sampled_normal_eq(h, X, n, tn, 0));
   cudaError_t e = cudaGetLastError();
@@ -466,6 +561,11 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   }
   k_tau_advance<<<1, 1, 0, h->st>>>((int64_t *)h->dTau.p);
   tl_mark(h, "tau");
+  if (h->ksrft()) {   // Alg. 9 l.21-23: new D_j, mixed batch, sampled rows of the re-mixed cores (R14)
+    RTRY(ks_mix(h, tn));
+    for (int k = 1; k < N; ++k)
+      RTRY(ks_sample(h, k, (const double *)h->md[k - 1].G.p, h->md[k - 1].I, (double *)h->md[k - 1].samp.p));
+  }
   // temporal: G_N^new = X_S[N] G_S (G_S^T G_S)^{-1}  (Alg. 7 l.17-23, reading R4)
   const int SN = h->SN;
   double *GS = (double *)h->sidx.p;
@@ -475,7 +575,8 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   double *GN_new = (double *)h->GNnew.p;
   RTRY(sampled_chain(h, N, GS));
   RTRY(gather_fibers(h, X, N, tn, XS));
-  gemm(h, XS, h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
+  // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R17)
+  gemm(h, XS, h->ksrft() ? 2 * h->m : h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
   solve_right(h, K, SN, (double *)h->Hi.p, M, tn, GN_new);
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)

@@ -770,6 +770,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   if (cfg->dims[0] % p != 0) return STR_E_PRECOND;
   if (cfg->split_k < 0 || cfg->split_k > N - 2) return STR_E_ARG;
   if (cfg->dtype != STR_F32 && cfg->dtype != STR_F64) return STR_E_ARG;
+  if (cfg->variant < STR_DET || cfg->variant > STR_SAMPLE_KSRFT) return STR_E_ARG;
   if (cfg->variant != STR_DET && p > 1) return STR_E_PRECOND;   // rSTR runs as replicas only
   if (cfg->variant != STR_DET) {
     int64_t need = 0;
@@ -879,7 +880,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     h->d_info = (int *)info.p;
     CU(cudaMemsetAsync(h->d_info, 0, sizeof(int), h->st));
   }
-  if (h->contract == STR_CONTRACT_3XTF32) TRY(tf32_prepare(h));
+  if (h->contract == STR_CONTRACT_3XTF32 && h->variant == STR_DET) TRY(tf32_prepare(h));   // rSTR has no dense pass
   TRY(ensure(h, h->dT, sizeof(int64_t)));
   TRY(ensure(h, h->dX, sizeof(void *)));
   prepare_kernel_attrs();

@@ -113,6 +113,11 @@ struct str_state {
   DevBuf dTau;                      // device copy of tau (advanced by the step itself)
   bool rstr_dev = true;             // draws on the device (STR_RSTR_HOST_DRAWS=1: host sampler)
   bool idx_dev[17] = {};            // index table k was drawn on the device (copy back on request)
+  // rSTR-K (KSRFT): mixed batch X^ (complex, fp32 pairs or fp64 pairs per `contract`), the step's
+  // sign flips D_1..D_N (mode j at ks_off[j-1]; D_N has t_new entries)
+  DevBuf ksXh, ksSign;
+  int64_t ks_off[17] = {};
+  bool ksrft() const { return variant == STR_SAMPLE_KSRFT; }
 
   // bookkeeping
   int64_t launches = 0;
@@ -143,7 +148,7 @@ struct str_state {
     gs[1].reset();
     for (auto &e : pev)
       if (e) { cudaEventDestroy(e); e = nullptr; }
-    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau); fr(ksXh); fr(ksSign);
     if (idx_pinned) cudaFreeHost(idx_pinned);
     idx_pinned = nullptr;
     for (auto &e : idx_ev)
