@@ -1657,7 +1657,7 @@ constexpr int kSkKC = 32;
 __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, int64_t sai, int64_t sak,
                                                  const double *__restrict__ B, int64_t sbk, int64_t sbj, int M, int N,
                                                  int64_t K, int64_t kper, double *__restrict__ part) {
-  __shared__ __align__(16) double As[kSkKC][32], Bs[kSkKC][32];
+  __shared__ __align__(16) double As[kSkKC][34], Bs[kSkKC][32];   // As row padded (transposed loads)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
   const int64_t k0 = (int64_t)blockIdx.z * kper;
@@ -1666,12 +1666,15 @@ __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, i
   for (int64_t kc = k0; kc < k1; kc += kSkKC) {
     __syncthreads();
     for (int e = threadIdx.x; e < 32 * kSkKC; e += 256) {
-      const int kk = e >> 5, r = e & 31;
+      // A: consecutive threads along whichever of (row, k) is contiguous in memory
+      const int kk = (sak == 1) ? (e & 31) : (e >> 5), r = (sak == 1) ? (e >> 5) : (e & 31);
       const int64_t k = kc + kk;
       if (k < k1 && row0 + r < M) cp_async8(&As[kk][r], A + (int64_t)(row0 + r) * sai + k * sak);
       else As[kk][r] = 0.0;
-      if (k < k1 && col0 + r < N) cp_async8(&Bs[kk][r], B + k * sbk + (int64_t)(col0 + r) * sbj);
-      else Bs[kk][r] = 0.0;
+      const int kb = e >> 5, cb = e & 31;
+      const int64_t kq = kc + kb;
+      if (kq < k1 && col0 + cb < N) cp_async8(&Bs[kb][cb], B + kq * sbk + (int64_t)(col0 + cb) * sbj);
+      else Bs[kb][cb] = 0.0;
     }
     cp_async_wait_all();
     __syncthreads();

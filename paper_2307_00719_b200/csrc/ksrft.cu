@@ -243,8 +243,8 @@ __global__ void __launch_bounds__(256) k_mix_mode(const void *const *__restrict_
 
 // Compile-time p x q variant (the fp32 mixing path): the sub-DFT twiddles are the p-th / q-th roots
 // of unity, held in registers and indexed by compile-time (n1 k1 mod p), (n2 k2 mod q), so every
-// complex MAC is 4 FMAs (products with w^0 = 1 folded away).  Same tile walk and layout as
-// k_mix_mode.
+// complex MAC is 2 packed FFMA2 (products with w^0 = 1 folded away).  Same tile layout as k_mix_mode,
+// with direct address walks for the two common tile shapes.
 template <int P, int Q, typename TIn, bool FIRST>
 __global__ void __launch_bounds__(256) k_mix_pq(const void *const *__restrict__ xslot, float2 *__restrict__ Y, MixDesc md) {
   constexpr int I = P * Q;
@@ -263,91 +263,138 @@ __global__ void __launch_bounds__(256) k_mix_pq(const void *const *__restrict__ 
     ds[k] = (float)(md.d[k] * scale);
   }
   __syncthreads();
-  float2 wp[P], wq[Q];                                   // w_P^j = w^{Q j}, w_Q^j = w^{P j}
-#pragma unroll
-  for (int j = 0; j < P; ++j) wp[j] = tw[Q * j];
-#pragma unroll
-  for (int j = 0; j < Q; ++j) wq[j] = tw[P * j];
   const int64_t tile = blockIdx.x;
   const int64_t a0 = (tile % md.nA) * md.WA, b0 = (tile / md.nA) * md.WB;
   const int n_el = WF * I;
   const int64_t A = md.A;
   const int aval = (int)(A - a0 < md.WA ? A - a0 : md.WA), bval = (int)(md.B - b0 < md.WB ? md.B - b0 : md.WB);
   const int64_t base = a0 + A * (int64_t)I * b0;
-  {
+  // tile shapes: (a) WA = 32, WB = 1: lane = fa, rows i = warp + 8 k (offset += 8 A);
+  //              (b) A = 1: the tile is one contiguous run of WB fibers (offset = e);  (c) general walk
+  const bool shape_a = (md.WA == 32 && md.WB == 1), shape_b = (A == 1);
+  auto load_el = [&](int64_t off, int i) -> float2 {
+    const float sc = ds[i];
+    if (FIRST) return make_float2((float)((const TIn *)*xslot)[off] * sc, 0.f);
+    float2 v = Y[off];
+    return make_float2(v.x * sc, v.y * sc);
+  };
+  if (shape_a) {
+    const int fa = threadIdx.x & 31;
+    const bool ok = fa < aval;
+    for (int i = threadIdx.x >> 5; i < I; i += 8)
+      xs[i * ld + fa] = ok ? load_el(base + fa + A * i, i) : make_float2(0.f, 0.f);
+  } else if (shape_b) {
+    const int lim = bval * I;
+    int i = threadIdx.x % I, fb = threadIdx.x / I;
+    const int di = 256 % I, dfb = 256 / I;
+    for (int e = threadIdx.x; e < n_el; e += 256) {
+      xs[i * ld + fb] = e < lim ? load_el(base + e, i) : make_float2(0.f, 0.f);
+      i += di;
+      fb += dfb;
+      if (i >= I) { i -= I; ++fb; }
+    }
+  } else {
     TileWalk w;
     w.init(threadIdx.x, md);
     for (int e = threadIdx.x; e < n_el; e += 256, w.step(md)) {
-      float2 v = make_float2(0.f, 0.f);
-      if (w.fa < aval && w.fb < bval) {
-        const int64_t off = base + w.fa + A * (w.i + (int64_t)I * w.fb);
-        const float sc = ds[w.i];
-        if (FIRST) {
-          v.x = (float)((const TIn *)*xslot)[off] * sc;
-        } else {
-          v = Y[off];
-          v.x *= sc;
-          v.y *= sc;
-        }
-      }
-      xs[w.i * ld + w.fa + md.WA * w.fb] = v;
+      const bool ok = w.fa < aval && w.fb < bval;
+      xs[w.i * ld + w.fa + md.WA * w.fb] =
+          ok ? load_el(base + w.fa + A * (w.i + (int64_t)I * w.fb), w.i) : make_float2(0.f, 0.f);
     }
   }
   __syncthreads();
-  for (int it = threadIdx.x; it < WF * Q; it += 256) {   // stage 1, item (f, n2)
-    const int f = it % WF, n2 = it / WF;
-    float2 x[P];
+  // complex MAC on packed fp32 pairs: acc += x w = x (w.x, w.x) + (-x.y, x.x) (w.y, w.y)  (2 FFMA2)
+  {
+    float2 wxx[P], wyy[P];                               // w_P^j = w^{Q j}
 #pragma unroll
-    for (int n1 = 0; n1 < P; ++n1) x[n1] = xs[(Q * n1 + n2) * ld + f];
-#pragma unroll
-    for (int k1 = 0; k1 < P; ++k1) {
-      float ax = x[0].x, ay = x[0].y;
-#pragma unroll
-      for (int n1 = 1; n1 < P; ++n1) {
-        const int j = (n1 * k1) % P;
-        if (j == 0) {
-          ax += x[n1].x;
-          ay += x[n1].y;
-        } else {
-          ax = fmaf(x[n1].x, wp[j].x, fmaf(-x[n1].y, wp[j].y, ax));
-          ay = fmaf(x[n1].x, wp[j].y, fmaf(x[n1].y, wp[j].x, ay));
-        }
-      }
-      float2 t;
-      if (k1 == 0) {
-        t = make_float2(ax, ay);
-      } else {
-        const float2 w = tw[n2 * k1];                    // w^{n2 k1}, n2 k1 < I
-        t = make_float2(ax * w.x - ay * w.y, ax * w.y + ay * w.x);
-      }
-      ts[(k1 * Q + n2) * ld + f] = t;
+    for (int j = 0; j < P; ++j) {
+      const float2 w = tw[Q * j];
+      wxx[j] = make_float2(w.x, w.x);
+      wyy[j] = make_float2(w.y, w.y);
     }
-  }
-  __syncthreads();
-  for (int it = threadIdx.x; it < WF * P; it += 256) {   // stage 2, item (f, k1)
-    const int f = it % WF, k1 = it / WF;
-    float2 t[Q];
+    for (int it = threadIdx.x; it < WF * Q; it += 256) {   // stage 1, item (f, n2)
+      const int f = it % WF, n2 = it / WF;
+      float2 x[P], xr[P];
 #pragma unroll
-    for (int n2 = 0; n2 < Q; ++n2) t[n2] = ts[(k1 * Q + n2) * ld + f];
-#pragma unroll
-    for (int k2 = 0; k2 < Q; ++k2) {
-      float ax = t[0].x, ay = t[0].y;
-#pragma unroll
-      for (int n2 = 1; n2 < Q; ++n2) {
-        const int j = (n2 * k2) % Q;
-        if (j == 0) {
-          ax += t[n2].x;
-          ay += t[n2].y;
-        } else {
-          ax = fmaf(t[n2].x, wq[j].x, fmaf(-t[n2].y, wq[j].y, ax));
-          ay = fmaf(t[n2].x, wq[j].y, fmaf(t[n2].y, wq[j].x, ay));
-        }
+      for (int n1 = 0; n1 < P; ++n1) {
+        x[n1] = xs[(Q * n1 + n2) * ld + f];
+        xr[n1] = make_float2(-x[n1].y, x[n1].x);
       }
-      xs[(k1 + P * k2) * ld + f] = make_float2(ax, ay);
+#pragma unroll
+      for (int k1 = 0; k1 < P; ++k1) {
+        float2 acc = x[0];
+#pragma unroll
+        for (int n1 = 1; n1 < P; ++n1) {
+          const int j = (n1 * k1) % P;
+          if (j == 0) {
+            acc.x += x[n1].x;
+            acc.y += x[n1].y;
+          } else {
+            acc = __ffma2_rn(x[n1], wxx[j], acc);
+            acc = __ffma2_rn(xr[n1], wyy[j], acc);
+          }
+        }
+        float2 t = acc;
+        if (k1 != 0) {
+          const float2 w = tw[n2 * k1];                  // w^{n2 k1}, n2 k1 < I
+          t = __fmul2_rn(acc, make_float2(w.x, w.x));
+          t = __ffma2_rn(make_float2(-acc.y, acc.x), make_float2(w.y, w.y), t);
+        }
+        ts[(k1 * Q + n2) * ld + f] = t;
+      }
     }
   }
   __syncthreads();
   {
+    float2 wxx[Q], wyy[Q];                               // w_Q^j = w^{P j}
+#pragma unroll
+    for (int j = 0; j < Q; ++j) {
+      const float2 w = tw[P * j];
+      wxx[j] = make_float2(w.x, w.x);
+      wyy[j] = make_float2(w.y, w.y);
+    }
+    for (int it = threadIdx.x; it < WF * P; it += 256) {   // stage 2, item (f, k1)
+      const int f = it % WF, k1 = it / WF;
+      float2 t[Q], tr[Q];
+#pragma unroll
+      for (int n2 = 0; n2 < Q; ++n2) {
+        t[n2] = ts[(k1 * Q + n2) * ld + f];
+        tr[n2] = make_float2(-t[n2].y, t[n2].x);
+      }
+#pragma unroll
+      for (int k2 = 0; k2 < Q; ++k2) {
+        float2 acc = t[0];
+#pragma unroll
+        for (int n2 = 1; n2 < Q; ++n2) {
+          const int j = (n2 * k2) % Q;
+          if (j == 0) {
+            acc.x += t[n2].x;
+            acc.y += t[n2].y;
+          } else {
+            acc = __ffma2_rn(t[n2], wxx[j], acc);
+            acc = __ffma2_rn(tr[n2], wyy[j], acc);
+          }
+        }
+        xs[(k1 + P * k2) * ld + f] = acc;
+      }
+    }
+  }
+  __syncthreads();
+  if (shape_a) {
+    const int fa = threadIdx.x & 31;
+    if (fa < aval)
+      for (int i = threadIdx.x >> 5; i < I; i += 8) Y[base + fa + A * i] = xs[i * ld + fa];
+  } else if (shape_b) {
+    const int lim = bval * I;
+    int i = threadIdx.x % I, fb = threadIdx.x / I;
+    const int di = 256 % I, dfb = 256 / I;
+    for (int e = threadIdx.x; e < lim; e += 256) {
+      Y[base + e] = xs[i * ld + fb];
+      i += di;
+      fb += dfb;
+      if (i >= I) { i -= I; ++fb; }
+    }
+  } else {
     TileWalk w;
     w.init(threadIdx.x, md);
     for (int e = threadIdx.x; e < n_el; e += 256, w.step(md))
@@ -397,6 +444,42 @@ __global__ void k_mix_sample(const double *__restrict__ G, int64_t I, int S, con
   }
   const double sc = rsqrt((double)I);
   out[e] = make_double2(ax * sc, ay * sc);
+}
+
+// Whole mixed core G^(a, c) = sum_i w^{a i} d_i / sqrt(I) G(i, c) for every a < I (I x S complex),
+// then the sampled rows are gathered: I^2 S MACs instead of m I S when I < m.
+__global__ void k_mix_core(const double *__restrict__ G, int I, int S, const double *__restrict__ d,
+                           double2 *__restrict__ out) {
+  extern __shared__ double2 tws[];
+  for (int k = threadIdx.x; k < I; k += blockDim.x) {
+    double s, c;
+    sincospi(-2.0 * (double)k / (double)I, &s, &c);
+    tws[k] = make_double2(c, s);
+  }
+  __syncthreads();
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= I * S) return;
+  const int a = e / S, c = e % S;
+  double ax = 0.0, ay = 0.0;
+  int widx = 0;
+  for (int i = 0; i < I; ++i) {
+    const double g = d[i] * G[i * S + c];
+    const double2 w = tws[widx];
+    ax = fma(g, w.x, ax);
+    ay = fma(g, w.y, ay);
+    widx += a;
+    if (widx >= I) widx -= I;
+  }
+  const double sc = rsqrt((double)I);
+  out[e] = make_double2(ax * sc, ay * sc);
+}
+
+__global__ void k_gather_crows(const double2 *__restrict__ Gh, int S, const int32_t *__restrict__ idx, int64_t m,
+                               double2 *__restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * S) return;
+  const int64_t s = e / S;
+  out[e] = Gh[(int64_t)idx[s] * S + (e - s * S)];
 }
 
 // One thread per (sample s, row a of the chain product): row a of F_1(s) F_2(s) ... F_L(s), each F
@@ -464,53 +547,57 @@ struct UnmixDesc {
   const double *d;             // D_n
 };
 
+constexpr int kUnmixSB = 2;   // samples per CTA (m / 2 CTAs: the whole GPU busy at m = 2000)
+
 template <typename TC>
 __global__ void __launch_bounds__(128) k_gather_unmix(const typename C2<TC>::t *__restrict__ Xh, UnmixDesc ud,
                                                       double *__restrict__ out) {
-  constexpr int SB = 8;                                  // samples per CTA
-  extern __shared__ double2 us[];                        // [SB][I] fibers, then w^k
-  double2 *tw = us + SB * ud.I;
-  const int64_t s0 = (int64_t)blockIdx.x * SB;
-  for (int64_t k = threadIdx.x; k < ud.I; k += blockDim.x) {
+  extern __shared__ double2 us[];                        // [SB][I] fibers, then w^{-k}
+  const int I = (int)ud.I;
+  double2 *tw = us + kUnmixSB * I;
+  const int64_t s0 = (int64_t)blockIdx.x * kUnmixSB;
+  for (int k = threadIdx.x; k < I; k += blockDim.x) {
     double s, c;
-    sincospi(2.0 * (double)k / (double)ud.I, &s, &c);   // w^{-k}
+    sincospi(2.0 * (double)k / (double)I, &s, &c);
     tw[k] = make_double2(c, s);
   }
-  for (int64_t e = threadIdx.x; e < SB * ud.I; e += blockDim.x) {
-    const int sl = (int)(e / ud.I);
-    const int64_t k = e % ud.I;
+  for (int sl = 0; sl < kUnmixSB; ++sl) {
     const int64_t s = s0 + sl;
-    double2 v = make_double2(0.0, 0.0);
+    int64_t base = 0;
     if (s < ud.m) {
-      int64_t off = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j)
-        if (j < ud.N) off += ((j == ud.n - 1) ? k : (int64_t)ud.idx[j * ud.m + s]) * ud.stride[j];
-      const typename C2<TC>::t x = Xh[off];
-      v = make_double2((double)x.x, (double)x.y);
+        if (j < ud.N && j != ud.n - 1) base += (int64_t)ud.idx[j * ud.m + s] * ud.stride[j];
     }
-    us[sl * ud.I + k] = v;
+    const int64_t sn = ud.stride[ud.n - 1];
+    for (int k = threadIdx.x; k < I; k += blockDim.x) {
+      double2 v = make_double2(0.0, 0.0);
+      if (s < ud.m) {
+        const typename C2<TC>::t x = Xh[base + k * sn];
+        v = make_double2((double)x.x, (double)x.y);
+      }
+      us[sl * I + k] = v;
+    }
   }
   __syncthreads();
-  const double sc = rsqrt((double)ud.I);
-  for (int64_t o = threadIdx.x; o < SB * ud.I; o += blockDim.x) {
-    const int sl = (int)(o % SB);
-    const int64_t i = o / SB;
+  const double sc = rsqrt((double)I);
+  for (int o = threadIdx.x; o < kUnmixSB * I; o += blockDim.x) {
+    const int sl = o % kUnmixSB, i = o / kUnmixSB;
     const int64_t s = s0 + sl;
     if (s >= ud.m) continue;
     double ax = 0.0, ay = 0.0;
-    int64_t widx = 0;
-    const double2 *x = us + sl * ud.I;
-    for (int64_t k = 0; k < ud.I; ++k) {
+    int widx = 0;
+    const double2 *x = us + sl * I;
+    for (int k = 0; k < I; ++k) {
       const double2 v = x[k], w = tw[widx];
       ax = fma(v.x, w.x, fma(-v.y, w.y, ax));
       ay = fma(v.x, w.y, fma(v.y, w.x, ay));
       widx += i;
-      if (widx >= ud.I) widx -= ud.I;
+      if (widx >= I) widx -= I;
     }
     const double di = ud.d[i] * sc;
-    out[i * 2 * ud.m + s] = ax * di;
-    out[i * 2 * ud.m + ud.m + s] = ay * di;
+    out[(int64_t)i * 2 * ud.m + s] = ax * di;
+    out[(int64_t)i * 2 * ud.m + ud.m + s] = ay * di;
   }
 }
 
@@ -606,16 +693,22 @@ int launch_mix_mode(const void *const *xslot, bool x_f64, void *Xh, bool f64, co
 }
 
 int launch_mix_sample(const double *G, int64_t I, int S, const int32_t *idx, int64_t m, const double *d, double2 *out,
-                      cudaStream_t st) {
+                      double2 *core_ws, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (size_t)I;
   if (smem > 200 * 1024) return -1;
   static bool attr = false;
   if (!attr) {
     cudaFuncSetAttribute(k_mix_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(k_mix_core, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+  if (core_ws && I <= m) {
+    k_mix_core<<<(unsigned)cdiv(I * S, 128), 128, smem, st>>>(G, (int)I, S, d, core_ws);
+    k_gather_crows<<<(unsigned)cdiv(m * S, 256), 256, 0, st>>>(core_ws, S, idx, m, out);
+    return 2;
+  }
   k_mix_sample<<<(unsigned)cdiv(m * S, 256), 256, smem, st>>>(G, I, S, idx, m, d, out);
-  return 0;
+  return 1;
 }
 
 int launch_chain_complex(const double2 *const *G, const int *Ra, const int *Rb, int nf, int64_t m, double *out,
@@ -647,7 +740,7 @@ int launch_gather_unmix(const void *Xh, bool f64, const int64_t *dims, int N, in
   ud.m = m;
   ud.idx = idx;
   ud.d = d;
-  const size_t smem = sizeof(double2) * (size_t)(8 + 1) * ud.I;
+  const size_t smem = sizeof(double2) * (size_t)(kUnmixSB + 1) * ud.I;
   if (smem > 200 * 1024) return -1;
   static bool attr = false;
   if (!attr) {
@@ -655,7 +748,7 @@ int launch_gather_unmix(const void *Xh, bool f64, const int64_t *dims, int N, in
     cudaFuncSetAttribute(k_gather_unmix<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
-  const unsigned grid = (unsigned)cdiv(m, 8);
+  const unsigned grid = (unsigned)cdiv(m, kUnmixSB);
   if (f64) k_gather_unmix<double><<<grid, 128, smem, st>>>((const double2 *)Xh, ud, out);
   else k_gather_unmix<float><<<grid, 128, smem, st>>>((const float2 *)Xh, ud, out);
   return 0;

@@ -265,12 +265,13 @@ static str_status ks_mix(str_state *h, int64_t tn) {
 static str_status ks_sample(str_state *h, int k, const double *rows, int64_t I, double *dst) {
   const int S = RRr(h, k) * RRr(h, k + 1);
   const int32_t *dix = (const int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
-  if (launch_mix_sample(rows, I, S, dix, h->m, (const double *)h->ksSign.p + h->ks_off[k - 1], (double2 *)dst,
-                        h->st) != 0) {
+  const int nl = launch_mix_sample(rows, I, S, dix, h->m, (const double *)h->ksSign.p + h->ks_off[k - 1],
+                                   (double2 *)dst, (double2 *)h->ksCore.p, h->st);
+  if (nl < 0) {
     h->err = "KSRFT: mode too long for the sampled mixing kernel";
     return STR_E_ARG;
   }
-  tl_mark(h, "mix_sample");
+  tl_mark(h, "mix_sample", nl);
   return STR_OK;
 }
 
@@ -501,6 +502,7 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
     }
     RTRY(ensure_dev(h, h->ksXh, (ks_f64(h) ? sizeof(double2) : sizeof(float2)) * slice * tn));
     RTRY(ensure_dev(h, h->ksSign, sizeof(double) * sumI));
+    RTRY(ensure_dev(h, h->ksCore, sizeof(double2) * maxI * maxS));   // whole mixed core (k_mix_core)
   }
   return STR_OK;
 }

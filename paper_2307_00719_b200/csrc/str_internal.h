@@ -115,7 +115,7 @@ struct str_state {
   bool idx_dev[17] = {};            // index table k was drawn on the device (copy back on request)
   // rSTR-K (KSRFT): mixed batch X^ (complex, fp32 pairs or fp64 pairs per `contract`), the step's
   // sign flips D_1..D_N (mode j at ks_off[j-1]; D_N has t_new entries)
-  DevBuf ksXh, ksSign;
+  DevBuf ksXh, ksSign, ksCore;
   int64_t ks_off[17] = {};
   bool ksrft() const { return variant == STR_SAMPLE_KSRFT; }
 
@@ -148,7 +148,7 @@ struct str_state {
     gs[1].reset();
     for (auto &e : pev)
       if (e) { cudaEventDestroy(e); e = nullptr; }
-    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau); fr(ksXh); fr(ksSign);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau); fr(ksXh); fr(ksSign); fr(ksCore);
     if (idx_pinned) cudaFreeHost(idx_pinned);
     idx_pinned = nullptr;
     for (auto &e : idx_ev)

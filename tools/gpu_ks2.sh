@@ -1,2 +1,5 @@
 python paper_2307_00719_b200/build.py 2>&1 | tail -1
-python tools/ks_probe.py C4 2 && ncu --clock-control none -k regex:k_mix_mode --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum,launch__grid_size,launch__occupancy_limit_shared_mem,sm__warps_active.avg.pct_of_peak_sustained_active,smsp__inst_executed.sum,l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum,smsp__sass_inst_executed_op_shared_ld.sum --csv python tools/ks_probe.py C4 1 > gpurun_out/ks_ncu.csv 2>&1
+timeout 900 python -m pytest tests/test_gpu_ksrft.py -x -q 2>&1 | tail -2
+timeout 300 python bench.py --config C4 --variant ksrft --steps 10 --warmup 3 --no-cpu-baseline --e2e-steps 2 > gpurun_out/ks_bench.log 2>&1; python -c "
+import json;d=json.loads(open('gpurun_out/ks_bench.log').read().strip().splitlines()[-1]);print('ksrft C4 ms/step',d['ms_per_step'])"
+python tools/ks_probe.py C4 1 && ncu --clock-control none -k regex:k_mix_pq --metrics gpu__time_duration.sum,smsp__inst_executed.sum,smsp__issue_active.avg.pct_of_peak_sustained_active,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,sm__warps_active.avg.pct_of_peak_sustained_active --csv python tools/ks_probe.py C4 1 > gpurun_out/ks_ncu.csv 2>&1
