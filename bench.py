@@ -242,7 +242,21 @@ def bench_ours(args):
             traffic = json.load(open(tpath)).get(f"{args.config}:{contract}")
         except Exception:
             traffic = None
-    if args.variant != "det":
+    if args.variant == "ksrft":
+        # rSTR-K: the dominant kernels are the N KSRFT mixing passes over the batch (HBM-bound):
+        # algorithmic bytes = |X| (in + 8 B complex out) for mode 1 + 16 B per entry for modes 2..N
+        mix_ms = p1_ms / max(p1_n, 1)
+        xb = 4 if cfg.dtype == "f32" else 8
+        cb = 8 if contract == "3xtf32" else 16
+        mix_bytes = local_entries * ((xb + cb) + 2 * cb * (cfg.N - 1))
+        ach = mix_bytes / (mix_ms / 1e3) / 1e9
+        roofline = {"bound": "hbm", "achieved": round(ach, 3), "peak": round(peaks["hbm_gbs"], 3), "unit": "GB/s",
+                    "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+                    "kernel": f"KSRFT mixing ({cfg.N} passes, events around the span)",
+                    "mix_us": round(mix_ms * 1e3, 2),
+                    "mix_share_of_step": round(mix_ms / (ms / args.steps), 4),
+                    "algorithmic_per_launch": {"bytes": mix_bytes}, "peak_basis": f"{peaks_src} HBM copy bandwidth"}
+    elif args.variant != "det":
         roofline = {"kernel": "n/a: rSTR has no dense contraction pass (the step is sampled GEMMs and solves)"}
     else:
       roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
@@ -315,21 +329,35 @@ def bench_ours(args):
     if tr_als:
         line["tr_als_init"] = tr_als
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        line["cpu_baseline"] = cpu_baseline(cfg)
+        line["cpu_baseline"] = cpu_baseline(cfg, variant=args.variant)
     if world > 1:
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
 
 
-def cpu_baseline(cfg, budget_s=20.0):
+def oracle_stream(cfg, variant, s):
+    """The oracle of the benched variant: STR (Alg. 4), rSTR-U / -L (Alg. 7 / 8), rSTR-K (Alg. 9)."""
+    from workloads.gen import paper_view
+    Xi = paper_view(s.init_slab())
+    m = cfg.sketch_rows or 2000
+    if variant == "det":
+        from oracle.stream import StreamingTR
+        return StreamingTR(Xi, s.init_cores())
+    if variant == "ksrft":
+        from oracle.ksrft import KSRFTStreamingTR
+        return KSRFTStreamingTR(Xi, s.init_cores(), m, cfg.seed)
+    from oracle.rstream import RandomizedStreamingTR
+    return RandomizedStreamingTR(Xi, s.init_cores(), m, variant, cfg.seed)
+
+
+def cpu_baseline(cfg, budget_s=20.0, variant="det"):
     """The oracle as it stands (fp64 numpy) on this host's cores: init + update steps on the
     same workload until ~budget_s of update time; value = entries / update seconds."""
-    from oracle.stream import StreamingTR
     from workloads import make_stream
     from workloads.gen import paper_view
     s = make_stream(cfg)
-    st = StreamingTR(paper_view(s.init_slab()), s.init_cores())
+    st = oracle_stream(cfg, variant, s)
     t_used, steps = 0.0, 0
     while t_used < budget_s and steps < cfg.n_batches:
         Xb = paper_view(s.batch(steps))
@@ -338,7 +366,7 @@ def cpu_baseline(cfg, budget_s=20.0):
         t_used += time.perf_counter() - t
         steps += 1
     return {"value": steps * cfg.batch_entries / t_used, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
-            "sample": f"{cfg.name}: oracle init + {steps} full update steps ({t_used:.1f} s of update time; "
+            "sample": f"{cfg.name} ({variant}): oracle init + {steps} full update steps ({t_used:.1f} s of update time; "
                       f"numpy BLAS threads = all {os.cpu_count()} host cores)"}
 
 
@@ -348,12 +376,11 @@ def bench_reference(args):
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    from oracle.stream import StreamingTR
     from workloads import get_config, make_stream
     from workloads.gen import paper_view
     cfg = get_config(args.config)
     s = make_stream(cfg)
-    st = StreamingTR(paper_view(s.init_slab()), s.init_cores())
+    st = oracle_stream(cfg, args.variant, s)
     nd = min(N_DISTINCT, cfg.n_batches)
     for w in range(min(args.warmup, 1)):
         st.update(paper_view(s.batch(w % nd)))
@@ -371,7 +398,8 @@ def bench_reference(args):
             "steps": steps, "warmup": min(args.warmup, 1), "ms_per_step": 1e3 * t_used / steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic (seeded TR stream, SURVEY.md §8(d).1)",
-            "config": {"workload": f"{cfg.name} (same as ours)", "global_batch_entries": cfg.batch_entries},
+            "config": {"workload": f"{cfg.name} (same as ours), variant {args.variant}",
+                       "global_batch_entries": cfg.batch_entries},
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)

@@ -143,9 +143,10 @@ STR_API void str_destroy(str_state *h);                     /* idempotent on NUL
 /* Number of CUDA kernels this library has launched on the handle's stream so far. */
 STR_API int64_t str_kernel_launches(const str_state *h);
 
-/* Profiling: when enabled, CUDA events bracket the dominant contraction kernels on the
- * handle's stream; str_profile returns accumulated milliseconds and launch counts of the
- * pass-1 and pass-2 contractions since the last reset (waits for the stream). */
+/* Profiling: when enabled, CUDA events bracket the dominant kernels on the handle's stream;
+ * str_profile returns accumulated milliseconds and step counts since the last reset (waits for
+ * the stream): STR — the pass-1 and pass-2 contractions; rSTR-K — the span of the N KSRFT mixing
+ * passes in the pass-1 slot (pass-2 slot unused); rSTR-U/L — nothing is bracketed. */
 STR_API str_status str_set_profiling(str_state *h, int32_t enable);
 STR_API str_status str_profile(str_state *h, double *pass1_ms, int64_t *pass1_launches, double *pass2_ms,
                        int64_t *pass2_launches);

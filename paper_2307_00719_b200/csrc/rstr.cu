@@ -250,6 +250,7 @@ static str_status ks_mix(str_state *h, int64_t tn) {
   }
   launch_draw_signs(h->seed, (const int64_t *)h->dTau.p, h->N, off, (double *)h->ksSign.p, h->st);
   tl_mark(h, "draw_signs");
+  prof_mark(h, 0);   // profiling replay: events around the N mixing passes (bench roofline)
   for (int j = 0; j < h->N; ++j) {
     if (launch_mix_mode((const void *const *)h->dX.p, h->dtype == STR_F64, h->ksXh.p, ks_f64(h), dims, h->N, j,
                         (const double *)h->ksSign.p + h->ks_off[j], h->st) != 0) {
@@ -258,6 +259,7 @@ static str_status ks_mix(str_state *h, int64_t tn) {
     }
     tl_mark(h, "mix_mode");
   }
+  prof_mark(h, 1);
   return STR_OK;
 }
 
@@ -559,7 +561,7 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
       h->err = "cannot locate the captured set_x node";
       return STR_E_CUDA;
     }
-    h->gs[0].setx = deps[0];
+    h->gs[h->cur_slot].setx = deps[0];
   }
   k_tau_advance<<<1, 1, 0, h->st>>>((int64_t *)h->dTau.p);
   tl_mark(h, "tau");
@@ -608,15 +610,21 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
     for (auto &mb : h->md) dev_ok = dev_ok && mb.I <= kDevCdfMax;
   }
   const bool graph = h->use_graph && !h->timeline && h->rstr_dev && dev_ok && !forced;
+  if (h->profiling && !h->pev[0]) {
+    for (auto &e : h->pev) RCU(cudaEventCreate(&e));
+  }
+  const bool prof = h->profiling && h->ksrft();   // rSTR-K: time the mixing passes
   if (!graph) {
+    h->cur_slot = 0;
     RTRY(rstr_enqueue(h, X, tn));
   } else {
-    str_state::GraphSlot &g = h->gs[0];
+    const int slot = prof ? 1 : 0;
+    str_state::GraphSlot &g = h->gs[slot];
     if (!g.exec || g.tn != tn) {
       g.reset();
       RCU(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeThreadLocal));
       h->capturing = true;
-      h->cur_slot = 0;
+      h->cur_slot = slot;
       const int64_t l0 = h->launches;
       str_status st = rstr_enqueue(h, X, tn);
       h->capturing = false;
@@ -654,6 +662,14 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
     RCU(cudaGraphLaunch(g.exec, h->st));
     h->launches += g.launches;
     for (int k = 1; k <= N; ++k) h->idx_dev[k] = true;
+  }
+  if (prof) {
+    RCU(cudaStreamSynchronize(h->st));
+    float ms = 0.0f;
+    if (cudaEventElapsedTime(&ms, h->pev[0], h->pev[1]) == cudaSuccess) {
+      h->prof_ms[0] += ms;
+      h->prof_n[0] += 1;
+    }
   }
   h->T += tn;
   cudaError_t e = cudaGetLastError();
