@@ -249,9 +249,15 @@ def bench_ours(args):
         xb = 4 if cfg.dtype == "f32" else 8
         cb = 8 if contract == "3xtf32" else 16
         mix_bytes = local_entries * ((xb + cb) + 2 * cb * (cfg.N - 1))
+        ksrft_traffic = None   # DRAM bytes of the N passes from one ncu --set full capture (tools/save_profiles.py)
+        if os.path.exists(tpath):
+            try:
+                ksrft_traffic = json.load(open(tpath)).get(f"{cfg.name}:ksrft")
+            except Exception:
+                ksrft_traffic = None
         ach = mix_bytes / (mix_ms / 1e3) / 1e9
         roofline = {"bound": "hbm", "achieved": round(ach, 3), "peak": round(peaks["hbm_gbs"], 3), "unit": "GB/s",
-                    "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": None,
+                    "frac": round(ach / peaks["hbm_gbs"], 4), "traffic": ksrft_traffic,
                     "kernel": f"KSRFT mixing ({cfg.N} passes, events around the span)",
                     "mix_us": round(mix_ms * 1e3, 2),
                     "mix_share_of_step": round(mix_ms / (ms / args.steps), 4),

@@ -66,7 +66,7 @@ typedef enum {
 typedef enum { STR_F32 = 0, STR_F64 = 1 } str_dtype;
 typedef enum { STR_CONTRACT_3XTF32 = 0, STR_CONTRACT_F64 = 1 } str_contract;
 /* STR (Alg. 4); rSTR-U (Alg. 7), rSTR-L (Alg. 8); rSTR-K: KSRFT mixing + uniform rows (Def. 10
-   P:614-627, Alg. 9; readings R12-R17) */
+   P:614-627, Alg. 9; readings R17-R22) */
 typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2, STR_SAMPLE_KSRFT = 3 } str_variant;
 
 typedef struct {

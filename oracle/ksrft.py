@@ -2,23 +2,23 @@
 (KSRFT, Def. 10; Alg. 5; update rules P:629-641; Alg. 9
 P:1194-1258), step by step.
 
-Test infrastructure only (see oracle/__init__.py).  Readings (R12-R17):
-  R12 F_j is the unitary DFT, F_j(a, b) = exp(-2 pi i a b / I_j) / sqrt(I_j).
-  R13 sign flips D_j come from the SplitMix64 stream of reading R11 with k = 0 (a slot the
+Test infrastructure only (see oracle/__init__.py).  Readings (R17-R22):
+  R17 F_j is the unitary DFT, F_j(a, b) = exp(-2 pi i a b / I_j) / sqrt(I_j).
+  R18 sign flips D_j come from the SplitMix64 stream of reading R11 with k = 0 (a slot the
       index draws never use): per step tau one stream of sum_j I_j draws, mode j's entries at
       offsets sum_{l<j} I_l .. (I_N = t_init at tau = 0, t_new afterwards); d = +1 when the top bit
       of the draw is 0, else -1.  Redrawn every step (Alg. 9 l.21 P:1224).
-  R14 the sampled mixed slices (G^_k)_S are always taken from G_k mixed with the CURRENT step's
+  R19 the sampled mixed slices (G^_k)_S are always taken from G_k mixed with the CURRENT step's
       D_k (Alg. 9 l.22-23 re-mix the cores every step; X^new is mixed with the same D), at the
       index table idxs(:,k) drawn when G_k last changed.
-  R15 garbles of ledger #19: P_n <- P_n^old + X^_S conj(G^_S) (the extra "+P_n" of P:635 dropped);
+  R20 garbles of ledger #19: P_n <- P_n^old + X^_S conj(G^_S) (the extra "+P_n" of P:635 dropped);
       Q_n <- Q_n + G^_S^T conj(G^_S) with the conjugate of Alg. 9 l.1250 (P:637 omits it; without it
       Re(Q) is not the Gram of the real-constrained problem); the unhatted X, G of P:1249-1250 and
       the "init" superscripts of P:1232, P:1248 read as the hatted, new-data quantities; the init
       stage uses the same conjugated forms.
-  R16 only Re(P_n), Re(Q_n) are ever read (Alg. 9 l.1251), so the state keeps the real
+  R21 only Re(P_n), Re(Q_n) are ever read (Alg. 9 l.1251), so the state keeps the real
       parts: Re(A conj B) = Re A Re B + Im A Im B.
-  R17 the temporal solve is the literal G_N^new = Re(X~_S[N]) (Re(G^_S[2]^T))^dagger (P:632,
+  R22 the temporal solve is the literal G_N^new = Re(X~_S[N]) (Re(G^_S[2]^T))^dagger (P:632,
       Alg. 9 l.1233), evaluated with an SVD pseudo-inverse (as reading R4).
 Index draws are uniform with replacement (S in Def. 10) with the rSTR-U streams (R11).
 """
@@ -34,13 +34,13 @@ from .tralg import core_fold, solve_right, symmetrize, unfold2
 
 
 def dft_unitary(I: int) -> np.ndarray:
-    """F (I x I): F(a, b) = exp(-2 pi i a b / I) / sqrt(I) (Def. 10; reading R12)."""
+    """F (I x I): F(a, b) = exp(-2 pi i a b / I) / sqrt(I) (Def. 10; reading R17)."""
     a = np.arange(I)
     return np.exp(-2j * np.pi * np.outer(a, a) / I) / np.sqrt(I)
 
 
 def sign_flips(seed: int, tau: int, N: int, dims: Sequence[int]) -> List[np.ndarray]:
-    """D_1..D_N diagonals in {+1, -1} for step tau (Def. 10; reading R13)."""
+    """D_1..D_N diagonals in {+1, -1} for step tau (Def. 10; reading R18)."""
     total = int(sum(dims))
     u, _ = splitmix64(stream_key(seed, tau, 0, N) & MASK, total)
     out, off = [], 0
@@ -103,7 +103,7 @@ class KSRFTStreamingTR:
             self._draw(k, X_init.shape[k - 1])
         self.P: List[np.ndarray] = []
         self.Q: List[np.ndarray] = []
-        for n in range(1, N):                               # l.9-20 (reading R15, R16)
+        for n in range(1, N):                               # l.9-20 (reading R20, R21)
             GS2 = unfold2(sampled_subchain(self._sampled(), N, n))
             XS = unmix_fibers(sampled_fibers(Xh, self.idxs, n), self.W[n - 1])
             self.P.append(np.real(XS @ GS2.conj()))
@@ -116,7 +116,7 @@ class KSRFTStreamingTR:
         return mixing_matrices(d)
 
     def _sampled(self) -> List[np.ndarray]:
-        """(G^_k)_S = (G_k x_2 W_k)(:, idxs(:,k), :) with the current W_k (reading R14).  The
+        """(G^_k)_S = (G_k x_2 W_k)(:, idxs(:,k), :) with the current W_k (reading R19).  The
         temporal core contributes only its rows of the current step (G_N^new)."""
         out = []
         for k in range(1, self.N + 1):
@@ -146,14 +146,14 @@ class KSRFTStreamingTR:
         X_new = np.asarray(X_new, dtype=np.float64)
         self.tau += 1
         tn = X_new.shape[-1]
-        # l.22-24: redefine D_j, mix X^new and the cores (R13, R14)
+        # l.22-24: redefine D_j, mix X^new and the cores (R18, R19)
         self.W = self._mixers(X_new.shape)
         Xh = mix_tensor(X_new, self.W)
         # temporal mode, l.26-34: chain of (G^_k)_S, k = 1..N-1
         samp = self._sampled()
         GS2 = unfold2(sampled_subchain(samp, N, N))                         # m x R_N R_1 (complex)
         XS = unmix_fibers(sampled_fibers(Xh, self.idxs, N), self.W[N - 1])  # t_new x m
-        GN_new2 = np.real(XS) @ np.linalg.pinv(np.real(GS2.T), rcond=1e-12)  # reading R17
+        GN_new2 = np.real(XS) @ np.linalg.pinv(np.real(GS2.T), rcond=1e-12)  # reading R22
         RN, R1 = self.cores[-1].shape[0], self.cores[-1].shape[2]
         self.cores[-1] = np.concatenate([self.cores[-1], core_fold(GN_new2, RN, R1)], axis=1)
         # l.35-37: G^_N^new, idxs(:,N) over [t_new], (G^_N^new)_S
@@ -161,7 +161,7 @@ class KSRFTStreamingTR:
         for n in range(1, N):                                                # l.39-55
             GS2 = unfold2(sampled_subchain(self._sampled(), N, n))          # m x R_nR_{n+1}
             XS = unmix_fibers(sampled_fibers(Xh, self.idxs, n), self.W[n - 1])
-            self.P[n - 1] = self.P[n - 1] + np.real(XS @ GS2.conj())        # R15, R16
+            self.P[n - 1] = self.P[n - 1] + np.real(XS @ GS2.conj())        # R20, R21
             self.Q[n - 1] = symmetrize(self.Q[n - 1] + np.real(GS2.T @ GS2.conj()))
             G = self.cores[n - 1]
             self.cores[n - 1] = core_fold(solve_right(self.P[n - 1], self.Q[n - 1]), G.shape[0], G.shape[2])

@@ -1,18 +1,18 @@
 // ksrft.cu — the KSRFT kernels of rSTR-K (Def. 10; Alg. 5 P:643-661;
-// Alg. 9).  DESIGN.md readings R12-R17; the host orchestration is in rstr.cu.
+// Alg. 9).  DESIGN.md readings R17-R22; the host orchestration is in rstr.cu.
 //
-//   k_draw_signs     D_1..D_N for the step (SplitMix64 stream k = 0 of reading R11; R13)
+//   k_draw_signs     D_1..D_N for the step (SplitMix64 stream k = 0 of reading R11; R18)
 //   k_mix_mode       X^ <- X^ x_j (F_j D_j), one mode per launch, complex in place (the first
 //                    mode reads the real batch through the device slot).  HBM-bound: each launch
 //                    streams the tensor once.  The length-I DFT of every fiber runs in shared
 //                    memory as two passes of a p x q factorization (I = p q, Cooley-Tukey without
 //                    recursion), p + q complex MACs per output instead of I.
 //   k_mix_sample     (G^_k)_S(s, :) = sum_i (F_k D_k)(idxs(s,k), i) G_k(i, :)  (only the sampled
-//                    rows of the mixed core are formed; reading R14)
+//                    rows of the mixed core are formed; reading R19)
 //   k_chain_complex  the ⊡₂ chain of complex sampled slices, written as the stacked real matrix
 //                    [Re G^_S[2]; Im G^_S[2]] (2m x R_nR_{n+1}) so that the real GEMMs of rSTR give
 //                    Re(X~ conj G^) = [Re X~, Im X~][Re G^; Im G^] and Re(G^T conj G^) = stacked Gram
-//                    (reading R16)
+//                    (reading R21)
 //   k_gather_unmix   X~_S[n] = D_n F_n^* X^_S[n] on the zipped fibers, stacked [Re | Im] (I_n x 2m)
 #include <cuda_runtime.h>
 
@@ -34,7 +34,7 @@ __device__ __forceinline__ uint64_t ks_splitmix_at(uint64_t key, uint64_t j) {
   return z ^ (z >> 31);
 }
 
-// d[j] = +1 / -1 from the top bit of draw j of the stream (seed, tau, k = 0)  (reading R13)
+// d[j] = +1 / -1 from the top bit of draw j of the stream (seed, tau, k = 0)  (reading R18)
 __global__ void k_draw_signs(uint64_t seed, const int64_t *__restrict__ tau, int N, int64_t total, double *__restrict__ d) {
   const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (j >= total) return;

@@ -16,7 +16,7 @@
 // draws sign flips and mixes the batch, the sampled slices are rows of the mixed cores, the chain
 // is complex and written as the stacked real [Re; Im] matrix (2m rows), the fibers are unmixed on
 // their own mode, so the same real GEMMs with K = 2m give Re(X~ conj G^) and Re(G^T conj G^); the
-// temporal solve takes the real halves (K = m; readings R12-R17).
+// temporal solve takes the real halves (K = m; readings R17-R22).
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -516,7 +516,7 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   const int S = mb.Ra * mb.Rb;
   double *GS = (double *)h->sidx.p;
   double *XS = (double *)h->sX.p;
-  const int64_t K = h->ksrft() ? 2 * h->m : h->m;   // rSTR-K: [Re X~, Im X~][Re G^; Im G^] (reading R16)
+  const int64_t K = h->ksrft() ? 2 * h->m : h->m;   // rSTR-K: [Re X~, Im X~][Re G^; Im G^] (reading R21)
   RTRY(sampled_chain(h, n, GS));
   RTRY(gather_fibers(h, X, n, tn, XS));
   gemm(h, XS, K, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, K, acc);
@@ -565,7 +565,7 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   }
   k_tau_advance<<<1, 1, 0, h->st>>>((int64_t *)h->dTau.p);
   tl_mark(h, "tau");
-  if (h->ksrft()) {   // Alg. 9 l.21-23: new D_j, mixed batch, sampled rows of the re-mixed cores (R14)
+  if (h->ksrft()) {   // Alg. 9 l.21-23: new D_j, mixed batch, sampled rows of the re-mixed cores (R19)
     RTRY(ks_mix(h, tn));
     for (int k = 1; k < N; ++k)
       RTRY(ks_sample(h, k, (const double *)h->md[k - 1].G.p, h->md[k - 1].I, (double *)h->md[k - 1].samp.p));
@@ -579,7 +579,7 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   double *GN_new = (double *)h->GNnew.p;
   RTRY(sampled_chain(h, N, GS));
   RTRY(gather_fibers(h, X, N, tn, XS));
-  // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R17)
+  // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R22)
   gemm(h, XS, h->ksrft() ? 2 * h->m : h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
   solve_right(h, K, SN, (double *)h->Hi.p, M, tn, GN_new);

@@ -1,6 +1,6 @@
-"""GPU parity for rSTR-K (KSRFT, Alg. 9; readings R12-R17) against oracle/ksrft.py.
+"""GPU parity for rSTR-K (KSRFT, Alg. 9; readings R17-R22) against oracle/ksrft.py.
 
-Index draws and sign flips are integer work on SplitMix64 streams (reading R11/R13): the library's
+Index draws and sign flips are integer work on SplitMix64 streams (reading R11/R18): the library's
 index tables must be bit-identical to the oracle's own draws.  Cores after every batch: <= 1e-9
 relative with the fp64 mixing (contract "f64"), <= 1e-4 with the fp32 mixing that goes with the
 3xTF32 contract (BASELINE.json north_star tolerance for the fp32 paths)."""

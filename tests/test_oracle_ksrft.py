@@ -129,7 +129,7 @@ def test_exhaustive_sketch_is_exact_normal_equations():
 
 def test_exact_stream_fixed_point():
     """Noise-free exact TR stream from the true cores: every sketched LS problem is consistent,
-    so rSTR-K keeps the true cores (Alg. 9 on exact data; reading R17's Re-LS included)."""
+    so rSTR-K keeps the true cores (Alg. 9 on exact data; reading R22's Re-LS included)."""
     rng = np.random.default_rng(7)
     dims, ranks, t0, tn = (5, 6, 4), (2, 3, 2, 2), 4, 3
     N = 4

@@ -8,6 +8,8 @@ timeout 600 python bench.py --config C3 --no-cpu-baseline > gpurun_out/bench_c3.
 timeout 600 python bench.py --config C4 --no-cpu-baseline > gpurun_out/bench_c4.log 2>&1
 timeout 600 python bench.py --config C4 --variant uniform --no-cpu-baseline > gpurun_out/bench_rstr_u.log 2>&1
 timeout 600 python bench.py --config C4 --variant leverage --no-cpu-baseline > gpurun_out/bench_rstr_l.log 2>&1
+timeout 600 python bench.py --config C4 --variant ksrft > gpurun_out/bench_rstr_k.log 2>&1
+timeout 600 ncu --set full --clock-control none --import-source on -k "regex:k_mix_(pq|mode)" -s 4 -c 4 -o gpurun_out/prof_ksrft_mix python tools/ks_probe.py C4 2 > gpurun_out/ncu3.log 2>&1
 timeout 600 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref.log 2>&1
 CMD="python bench.py --steps 3 --warmup 3 --no-cpu-baseline --e2e-steps 2"
 timeout 300 $CMD > gpurun_out/plain.log 2>&1 && \

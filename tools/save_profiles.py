@@ -36,7 +36,7 @@ def to_bytes(v, unit):
 
 def main():
     tag = sys.argv[1] if len(sys.argv) > 1 else "r01"
-    for name in ("default", "f64", "c2", "c3", "c4", "ref", "rstr_u", "rstr_l"):
+    for name in ("default", "f64", "c2", "c3", "c4", "ref", "rstr_u", "rstr_l", "rstr_k"):
         p = os.path.join(OUT, f"bench_{name}.log")
         if not os.path.exists(p):
             continue
@@ -76,6 +76,30 @@ def main():
             cur["C5:3xtf32"] = round(sum(traffic) / len(traffic))
             json.dump(cur, open(tp, "w"), indent=1)
             print("traffic", cur)
+    # rSTR-K: the N mixing passes of one C4 step (--set full) -> per-step DRAM traffic
+    rep = os.path.join(OUT, "prof_ksrft_mix.ncu-rep")
+    if os.path.exists(rep):
+        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+        rows = list(csv.reader(io.StringIO(raw)))
+        hdr, units = rows[0], rows[1]
+        lines, tot = [], 0.0
+        for r in rows[2:]:
+            lines.append(r[hdr.index("Kernel Name")])
+            for m in METRICS + ["smsp__issue_active.avg.pct_of_peak_sustained_active",
+                                "sm__warps_active.avg.pct_of_peak_sustained_active", "smsp__inst_executed.sum"]:
+                if m in hdr:
+                    i = hdr.index(m)
+                    lines.append(f"  {m} = {r[i]} {units[i]}")
+            rd = to_bytes(r[hdr.index("dram__bytes_read.sum")], units[hdr.index("dram__bytes_read.sum")])
+            wr = to_bytes(r[hdr.index("dram__bytes_write.sum")], units[hdr.index("dram__bytes_write.sum")])
+            tot += rd + wr
+        lines.append(f"dram read+write over the {len(rows) - 2} passes of one step = {tot:.0f} B")
+        open(os.path.join(PROF, f"{tag}_ncu_ksrft_mix.txt"), "w").write("\n".join(lines) + "\n")
+        tp = os.path.join(PROF, "traffic_latest.json")
+        cur = json.load(open(tp)) if os.path.exists(tp) else {}
+        cur["C4:ksrft"] = round(tot)
+        json.dump(cur, open(tp, "w"), indent=1)
+        print("ksrft traffic", cur["C4:ksrft"])
 
 
 if __name__ == "__main__":
