@@ -85,3 +85,82 @@ def test_rstrk_graph_replay_is_deterministic():
         lib.str_destroy(h)
     for a, b in zip(*out):
         np.testing.assert_array_equal(a, b)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("contract,tol", [("f64", 1e-9), ("3xtf32", 1e-4)])
+def test_rstrk_varying_t_new_and_single_slice(contract, tol):
+    """t_new = 3, 1, 4, 1, 2 (F_N of size 1 is the identity up to the sign flip; every new t_new
+    re-captures the step graph; the sign stream length changes with t_new)."""
+    import torch
+    import paper_2307_00719_b200 as lib
+    s = make_stream("R5")
+    cfg = s.cfg
+    m, N, seed = cfg.sketch_rows, cfg.N, 5
+    h = lib.str_init(N, cfg.dims, cfg.ranks, torch.from_numpy(s.init_slab()).cuda(), cfg.t_init, s.init_cores(),
+                     dtype=cfg.dtype, contract=contract, variant="ksrft", sketch_rows=m, seed=seed, t_capacity=64)
+    orc = KSRFTStreamingTR(paper_view(s.init_slab()), s.init_cores(), m, seed)
+    t0 = cfg.t_init
+    for tn in (3, 1, 4, 1, 2):
+        slab = np.ascontiguousarray(s.slab(t0, tn))
+        t0 += tn
+        lib.str_update_batch(h, torch.from_numpy(slab).cuda(), tn)
+        orc.update(paper_view(slab))
+        np.testing.assert_array_equal(lib.str_get_index_table(h, N, m), orc.draws[(orc.tau, N)])
+        for n in range(1, N + 1):
+            g, o = lib.str_get_cores(h, n), orc.cores[n - 1]
+            assert np.linalg.norm(g - o) / np.linalg.norm(o) <= tol, (tn, n)
+    lib.str_destroy(h)
+
+
+@pytest.mark.gpu
+def test_rstrk_host_draws_and_replayed_tables(monkeypatch):
+    """The host sampler (STR_RSTR_HOST_DRAWS=1: host index draws, eager steps) gives the same
+    tables and cores as the oracle; the sign flips stay on the device."""
+    import torch
+    import paper_2307_00719_b200 as lib
+    monkeypatch.setenv("STR_RSTR_HOST_DRAWS", "1")
+    s = make_stream("R4")
+    cfg = s.cfg
+    m, N = cfg.sketch_rows, cfg.N
+    h = lib.str_init(N, cfg.dims, cfg.ranks, torch.from_numpy(s.init_slab()).cuda(), cfg.t_init, s.init_cores(),
+                     dtype=cfg.dtype, contract="f64", variant="ksrft", sketch_rows=m, seed=9)
+    orc = KSRFTStreamingTR(paper_view(s.init_slab()), s.init_cores(), m, 9)
+    for b in range(2):
+        lib.str_update_batch(h, torch.from_numpy(s.batch(b)).cuda(), cfg.t_new)
+        orc.update(paper_view(s.batch(b)))
+    errs = [np.linalg.norm(lib.str_get_cores(h, n) - orc.cores[n - 1]) / np.linalg.norm(orc.cores[n - 1])
+            for n in range(1, N + 1)]
+    assert max(errs) <= 1e-9, errs
+    lib.str_destroy(h)
+
+
+@pytest.mark.gpu
+def test_rstrk_forced_index_tables():
+    """Index tables forced through str_set_index_table (for every draw of each mode) against the
+    oracle with the same tables injected by its draw hook; sign flips still from the seed."""
+    import torch
+    import paper_2307_00719_b200 as lib
+    s = make_stream("R4")
+    cfg = s.cfg
+    m, N = cfg.sketch_rows, cfg.N
+    rng = np.random.default_rng(12)
+    lim = list(cfg.dims) + [min(cfg.t_init, cfg.t_new)]
+    tables = {k: rng.integers(0, lim[k - 1], m).astype(np.int32) for k in range(1, N + 1)}
+    # the init draws come from the seed (str_init draws before a table can be set); updates are forced
+    h = lib.str_init(N, cfg.dims, cfg.ranks, torch.from_numpy(s.init_slab()).cuda(), cfg.t_init, s.init_cores(),
+                     dtype=cfg.dtype, contract="f64", variant="ksrft", sketch_rows=m, seed=4)
+    init_tabs = {k: lib.str_get_index_table(h, k, m).astype(np.int64) for k in range(1, N + 1)}
+    for k in range(1, N + 1):
+        lib.str_set_index_table(h, k, tables[k])
+    orc = KSRFTStreamingTR(paper_view(s.init_slab()), s.init_cores(), m, 4,
+                           draw_hook=lambda tau, k, I, p: init_tabs[k] if tau == 0 else tables[k])
+    for b in range(2):
+        lib.str_update_batch(h, torch.from_numpy(s.batch(b)).cuda(), cfg.t_new)
+        orc.update(paper_view(s.batch(b)))
+        for k in range(1, N + 1):
+            np.testing.assert_array_equal(lib.str_get_index_table(h, k, m), tables[k])
+    errs = [np.linalg.norm(lib.str_get_cores(h, n) - orc.cores[n - 1]) / np.linalg.norm(orc.cores[n - 1])
+            for n in range(1, N + 1)]
+    assert max(errs) <= 1e-9, errs
+    lib.str_destroy(h)
