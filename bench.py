@@ -184,6 +184,25 @@ def bench_ours(args):
     global_entries = cfg.batch_entries
     value = args.steps * global_entries / (ms / 1e3)
 
+    # ---- per-batch latency: an event pair around each of K further steps (after
+    # the timed region, so the throughput above carries no per-step events); median, p90 and the
+    # trend against the processed length T (the step must not grow with the history)
+    lat = []
+    for _ in range(args.steps):
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        one_step()
+        a1.record(stream)
+        lat.append((a0, a1))
+    torch.cuda.synchronize(dev)
+    lat_ms = np.array([maxall(a.elapsed_time(b)) for a, b in lat])
+    slope = float(np.polyfit(np.arange(len(lat_ms)) * cfg.t_new, lat_ms * 1e3, 1)[0]) if len(lat_ms) > 2 else None
+    latency = {"median_ms": round(float(np.median(lat_ms)), 5), "p90_ms": round(float(np.percentile(lat_ms, 90)), 5),
+               "min_ms": round(float(lat_ms.min()), 5), "max_ms": round(float(lat_ms.max()), 5),
+               "slope_us_per_slice": round(slope, 5) if slope is not None else None,
+               "T_range": [int(lib.str_processed(h) - len(lat_ms) * cfg.t_new), int(lib.str_processed(h))],
+               "note": "events around each step (adds the event overhead per step)"}
+
     # ---- roofline of the dominant kernels (contraction passes), events on the library stream;
     # the kernels also stamp %globaltimer per CTA (diagnostic trace) for their in-kernel span
     Ld = lib._lib.lib
@@ -270,7 +289,12 @@ def bench_ours(args):
                   "pass1_us": round(avg_p1 * 1e3, 2), "pass2_us": round(avg_p2 * 1e3, 2),
                   "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
                   "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
-                  "peak_basis": basis}
+                  "peak_basis": basis,
+                  # the paper's mode-by-mode work F_paper = N 2|X|R^2 per step vs the
+                  # two-pass F_min = 2 passes x 2|X|R^2, both over the measured step time
+                  "per_step": {"F_min": 2 * flops_per_pass, "F_paper": cfg.N * flops_per_pass,
+                               "F_min_tflops_over_step": round(2 * flops_per_pass / (ms / args.steps / 1e3) / 1e12, 3),
+                               "F_paper_tflops_over_step": round(cfg.N * flops_per_pass / (ms / args.steps / 1e3) / 1e12, 3)}}
     if args.variant == "det" and span and all(x for x in span):
         # in-kernel span (first CTA start to last CTA end, %globaltimer) of the last profiled step;
         # the event pair above also holds the graph node's launch latency (~6 us measured with an
@@ -331,7 +355,8 @@ def bench_ours(args):
                        "parallelism": f"mode-1 shard x{world}",
                        "l2": f"rotating {nd} distinct device-resident batches ({nd * global_entries * 4 / 1e9:.2f} GB)"
                              " > 126 MB L2"},
-            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline}
+            "gpu_launches": int(launches), "clocks": clk.summary(), "e2e": e2e, "roofline": roofline,
+            "latency": latency}
     if tr_als:
         line["tr_als_init"] = tr_als
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -26,7 +26,8 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "sm__pipe_tc_cycles_active.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed", "lts__t_bytes.sum",
            "l1tex__data_pipe_tc_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
-           "launch__grid_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic"]
+           "launch__grid_size", "launch__registers_per_thread", "launch__shared_mem_per_block_dynamic",
+           "lts__t_sector_hit_rate.pct", "lts__t_sector_op_read_hit_rate.pct"]
 
 
 def to_bytes(v, unit):
