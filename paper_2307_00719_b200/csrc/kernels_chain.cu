@@ -1657,37 +1657,48 @@ constexpr int kSkKC = 32;
 __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, int64_t sai, int64_t sak,
                                                  const double *__restrict__ B, int64_t sbk, int64_t sbj, int M, int N,
                                                  int64_t K, int64_t kper, double *__restrict__ part) {
-  __shared__ __align__(16) double As[kSkKC][34], Bs[kSkKC][32];   // As row padded (transposed loads)
+  // two chunk buffers: the cp.async of chunk c+1 is in flight while chunk c is multiplied
+  __shared__ __align__(16) double As[2][kSkKC][34], Bs[2][kSkKC][32];   // As rows padded (transposed loads)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
   const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
   const int64_t k0 = (int64_t)blockIdx.z * kper;
   const int64_t k1 = (k0 + kper < K) ? k0 + kper : K;
   double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  for (int64_t kc = k0; kc < k1; kc += kSkKC) {
-    __syncthreads();
+  auto load = [&](int buf, int64_t kc) {
     for (int e = threadIdx.x; e < 32 * kSkKC; e += 256) {
       // A: consecutive threads along whichever of (row, k) is contiguous in memory
       const int kk = (sak == 1) ? (e & 31) : (e >> 5), r = (sak == 1) ? (e >> 5) : (e & 31);
       const int64_t k = kc + kk;
-      if (k < k1 && row0 + r < M) cp_async8(&As[kk][r], A + (int64_t)(row0 + r) * sai + k * sak);
-      else As[kk][r] = 0.0;
+      if (k < k1 && row0 + r < M) cp_async8(&As[buf][kk][r], A + (int64_t)(row0 + r) * sai + k * sak);
+      else As[buf][kk][r] = 0.0;
       const int kb = e >> 5, cb = e & 31;
       const int64_t kq = kc + kb;
-      if (kq < k1 && col0 + cb < N) cp_async8(&Bs[kb][cb], B + kq * sbk + (int64_t)(col0 + cb) * sbj);
-      else Bs[kb][cb] = 0.0;
+      if (kq < k1 && col0 + cb < N) cp_async8(&Bs[buf][kb][cb], B + kq * sbk + (int64_t)(col0 + cb) * sbj);
+      else Bs[buf][kb][cb] = 0.0;
     }
-    cp_async_wait_all();
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  int buf = 0;
+  if (k0 < k1) load(0, k0);
+  for (int64_t kc = k0; kc < k1; kc += kSkKC, buf ^= 1) {
+    if (kc + kSkKC < k1) {
+      load(buf ^ 1, kc + kSkKC);
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;" ::: "memory");
+    }
     __syncthreads();
 #pragma unroll 8
     for (int kk = 0; kk < kSkKC; ++kk) {
-      const double b = Bs[kk][tx];
-      const double2 a01 = *(const double2 *)&As[kk][4 * ty];
-      const double2 a23 = *(const double2 *)&As[kk][4 * ty + 2];
+      const double b = Bs[buf][kk][tx];
+      const double2 a01 = *(const double2 *)&As[buf][kk][4 * ty];
+      const double2 a23 = *(const double2 *)&As[buf][kk][4 * ty + 2];
       acc[0] = fma(a01.x, b, acc[0]);
       acc[1] = fma(a01.y, b, acc[1]);
       acc[2] = fma(a23.x, b, acc[2]);
       acc[3] = fma(a23.y, b, acc[3]);
     }
+    __syncthreads();   // buf is refilled two chunks later
   }
   double *pp = part + (int64_t)blockIdx.z * M * N;
 #pragma unroll
@@ -1703,12 +1714,22 @@ __global__ void k_reduce_sk(const double *__restrict__ part, int KS, int64_t n, 
                             int sym) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  // all partials are loaded before the (fixed-order) sums, so the loads overlap
+  double v[32], w[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) v[k] = k < KS ? part[k * n + i] : 0.0;
   double s = 0.0;
-  for (int k = 0; k < KS; ++k) s += part[k * n + i];
+#pragma unroll
+  for (int k = 0; k < 32; ++k)
+    if (k < KS) s += v[k];
   if (sym) {
     const int64_t r = i / N, c = i % N;
+#pragma unroll
+    for (int k = 0; k < 32; ++k) w[k] = k < KS ? part[k * n + c * N + r] : 0.0;
     double t = 0.0;
-    for (int k = 0; k < KS; ++k) t += part[k * n + c * N + r];
+#pragma unroll
+    for (int k = 0; k < 32; ++k)
+      if (k < KS) t += w[k];
     s = 0.5 * (s + t);
   }
   C[i] = acc ? C[i] + s : s;

@@ -218,9 +218,28 @@ static void solve_right(str_state *h, const double *A, int S, double *Ai, const 
 }
 
 static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj,
-                 double *C, int M, int N, int64_t K, int acc, int sym = 0) {
-  const int nl = launch_gemm_sk(A, sai, sak, B, sbk, sbj, C, M, N, K, acc, (double *)h->sSk.p, h->st, sym);
+                 double *C, int M, int N, int64_t K, int acc, int sym = 0, bool side_ws = false) {
+  const int nl = launch_gemm_sk(A, sai, sak, B, sbk, sbj, C, M, N, K, acc,
+                                (double *)(side_ws ? h->sSk2.p : h->sSk.p), h->st, sym);
   tl_mark(h, "gemm_sk", nl);
+}
+
+// Fork / join of the side stream inside one rSTR step (graph branches when capturing): the Gram
+// G_S^T G_S and its inverse run beside X_S G_S; the diagnostic timeline keeps one stream.
+static str_status rs_fork(str_state *h) {
+  h->st_main = h->st;
+  if (h->timeline) return STR_OK;
+  RCU(cudaEventRecord(h->ev_fork, h->st));
+  RCU(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
+  h->st = h->st2;
+  return STR_OK;
+}
+static void rs_main(str_state *h) { h->st = h->st_main; }
+static str_status rs_join(str_state *h) {
+  if (h->timeline) return STR_OK;
+  RCU(cudaEventRecord(h->ev_join, h->st2));
+  RCU(cudaStreamWaitEvent(h->st, h->ev_join, 0));
+  return STR_OK;
 }
 
 // Core k's slices as G(2) rows: k < N -> current core; k == N -> temporal rows [t0, t0 + rows).
@@ -494,6 +513,7 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
   RTRY(ensure_dev(h, h->sGram, sizeof(double) * maxS * maxS));
   RTRY(ensure_dev(h, h->sSk,
                   sizeof(double) * gemm_sk_ws_doubles((int)std::max<int64_t>(maxI, maxS), maxS, h->m * cw)));
+  RTRY(ensure_dev(h, h->sSk2, sizeof(double) * gemm_sk_ws_doubles(maxS, maxS, h->m * cw)));
   RTRY(ensure_dev(h, h->Mt, sizeof(double) * std::max<int64_t>(maxI, tn) * maxS));
   for (auto &mb : h->md) RTRY(ensure_dev(h, mb.samp, sizeof(double) * h->m * mb.Ra * mb.Rb * cw));
   if (h->ksrft()) {
@@ -510,8 +530,9 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
 }
 
 // Accumulate the sampled normal equations of mode n (1..N-1) from X (tn slices): P_n (+)= X_S G_S,
-// Q_n (+)= G_S^T G_S (Alg. 7 l.15-16 / l.36-37).
-static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t tn, int acc) {
+// Q_n (+)= G_S^T G_S (Alg. 7 l.15-16 / l.36-37); with `solve`, then G_n = P_n Q_n^{-1} (l.38).  The
+// Gram and the inverse run on the side stream beside X_S G_S.
+static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t tn, int acc, bool solve) {
   ModeBuf &mb = h->md[n - 1];
   const int S = mb.Ra * mb.Rb;
   double *GS = (double *)h->sidx.p;
@@ -519,8 +540,19 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   const int64_t K = h->ksrft() ? 2 * h->m : h->m;   // rSTR-K: [Re X~, Im X~][Re G^; Im G^] (reading R21)
   RTRY(sampled_chain(h, n, GS));
   RTRY(gather_fibers(h, X, n, tn, XS));
+  RTRY(rs_fork(h));
+  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1, true);   // Q_n += sym(G_S^T G_S)
+  if (solve) {
+    launch_spd_inv((const double *)mb.Q.p, S, (double *)mb.Qi.p, h->d_info, h->st);
+    tl_mark(h, "spd_inv");
+  }
+  rs_main(h);
   gemm(h, XS, K, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, K, acc);
-  gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1);   // Q_n += sym(G_S^T G_S)
+  RTRY(rs_join(h));
+  if (solve) {
+    launch_rows_mm((const double *)mb.P.p, (const double *)mb.Qi.p, S, mb.I, (double *)mb.G.p, h->st);
+    tl_mark(h, "rows_mm");
+  }
   return STR_OK;
 }
 
@@ -534,7 +566,7 @@ str_status rstr_init(str_state *h, const void *X, int64_t tn) {
   if (h->ksrft()) RTRY(ks_mix(h, tn));   // Alg. 9 l.2-4
   // Alg. 7 l.2-5 / Alg. 8 l.2-6 / Alg. 9 l.5-8: draws for k = 1..N (I_N = t_init)
   for (int k = 1; k <= N; ++k) RTRY(draw_mode(h, k, core_rows(h, k, 0), k == N ? tn : h->md[k - 1].I));
-  for (int n = 1; n < N; ++n) RTRY(sampled_normal_eq(h, X, n, tn, 0));
+  for (int n = 1; n < N; ++n) RTRY(sampled_normal_eq(h, X, n, tn, 0, false));
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) {
     h->err = std::string("rstr_init: ") + cudaGetErrorString(e);
@@ -580,16 +612,20 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   RTRY(sampled_chain(h, N, GS));
   RTRY(gather_fibers(h, X, N, tn, XS));
   // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R22)
+  RTRY(rs_fork(h));   // the Gram and its inverse beside X_S G_S
+  gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1, true);
+  launch_spd_inv(K, SN, (double *)h->Hi.p, h->d_info, h->st);
+  tl_mark(h, "spd_inv");
+  rs_main(h);
   gemm(h, XS, h->ksrft() ? 2 * h->m : h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
-  gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1);
-  solve_right(h, K, SN, (double *)h->Hi.p, M, tn, GN_new);
+  RTRY(rs_join(h));
+  launch_rows_mm(M, (const double *)h->Hi.p, SN, tn, GN_new, h->st);
+  tl_mark(h, "rows_mm");
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
   RTRY(draw_mode(h, N, GN_new, tn));
   for (int n = 1; n < N; ++n) {
     ModeBuf &mb = h->md[n - 1];
-    RTRY(sampled_normal_eq(h, X, n, tn, 1));
-    solve_right(h, (const double *)mb.Q.p, mb.Ra * mb.Rb, (double *)mb.Qi.p, (const double *)mb.P.p, mb.I,
-                (double *)mb.G.p);
+    RTRY(sampled_normal_eq(h, X, n, tn, 1, true));
     RTRY(draw_mode(h, n, (const double *)mb.G.p, mb.I));
   }
   launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, SN, h->st);

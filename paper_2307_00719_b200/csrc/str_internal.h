@@ -104,7 +104,7 @@ struct str_state {
   static constexpr int kTfDbgWords = 1024 + 4 * 160;   // per pass
 
   // rSTR
-  DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev, sSk;
+  DevBuf sidx, sX, sG, sGram, sTmp, sIdxDev, sSk, sSk2;   // sSk2: split-K workspace of the side branch
   int32_t *idx_pinned = nullptr;    // pinned index staging, one m-slot per mode
   cudaEvent_t idx_ev[17] = {};       // last upload from each slot
   std::vector<int32_t> forced_idx[16];
@@ -148,7 +148,7 @@ struct str_state {
     gs[1].reset();
     for (auto &e : pev)
       if (e) { cudaEventDestroy(e); e = nullptr; }
-    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(dTau); fr(ksXh); fr(ksSign); fr(ksCore);
+    fr(sidx); fr(sX); fr(sG); fr(sGram); fr(sTmp); fr(sIdxDev); fr(sSk); fr(sSk2); fr(dTau); fr(ksXh); fr(ksSign); fr(ksCore);
     if (idx_pinned) cudaFreeHost(idx_pinned);
     idx_pinned = nullptr;
     for (auto &e : idx_ev)
