@@ -26,7 +26,6 @@ void launch_absorb(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out,
 void launch_gram_z(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
 void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, cudaStream_t s);
 void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate, cudaStream_t s);
-void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s);
 void launch_axpy(const double *x, double *y, int64_t n, cudaStream_t s);
 void launch_set_identity(double *A, int n, cudaStream_t s);
 

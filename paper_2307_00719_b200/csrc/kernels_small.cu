@@ -245,234 +245,6 @@ void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate
 }
 
 // ------------------------------------------------------------------------------------------
-// G = P Q^{-1} for SPD Q (S x S, S <= 128) and I right-hand-side rows P (I x S), row-major.
-// Blocked right-looking Cholesky (block 8) on the shared-memory copy of Q, written as compact
-// loops (the code must stay small: the kernel runs one CTA and is latency/I-cache bound):
-//   B-phase: one thread per row i >= kb factors the 8x8 diagonal block in registers
-//            (rsqrt pivots), solves its row of the panel and (rows in the block) emits one
-//            column of the inverted diagonal block;
-//   C-phase: warps own rows, lanes own columns: the panel is finalized and the trailing
-//            entries take the rank-8 update.
-// Forward / backward substitution then use the inverted diagonal blocks.  Each CTA factors Q
-// (cheap, redundant) and solves a chunk of <= 16 RHS rows.  A non-positive pivot sets *info.
-constexpr int kNB = 8, kNT = 512, kSolveChunk = 4;    // RHS rows per CTA (the factorization is repeated per CTA)
-#ifdef STR_CHOL_PROBE
-__device__ long long *g_probe = nullptr;
-#endif
-
-__global__ void __launch_bounds__(kNT, 1) k_chol_solve(const double *__restrict__ Q, int S,
-                                                        const double *__restrict__ P, int64_t I,
-                                                        double *__restrict__ Gout, int *info) {
-  extern __shared__ double sm[];
-  const int LD = S + 1;                      // padded row stride of A
-  const int nblk = (S + kNB - 1) / kNB;
-  double *A = sm;                            // S x LD
-  double *Bm = A + ((S * LD + 3) & ~3);      // kSolveChunk x LD (RHS rows)
-  double *LnT = Bm + ((kSolveChunk * LD + 3) & ~3);   // 8 x S panel of L, m-major
-  double *Ln = LnT + ((kNB * S + 3) & ~3);            // S x 8 panel of L, row-major
-  double *Di = Ln + kNB * S;                          // nblk x 64 inverted diagonal blocks (zero padded)
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = kNT / 32;
-  const int64_t row0 = (int64_t)blockIdx.x * kSolveChunk;
-  const int rows = (int)((I - row0) < kSolveChunk ? (I - row0) : kSolveChunk);
-#ifdef STR_CHOL_PROBE
-  long long t_start = clock64();
-#endif
-  for (int e = tid; e < S * S; e += kNT) A[(e / S) * LD + e % S] = Q[e];
-  for (int e = tid; e < rows * S; e += kNT) Bm[(e / S) * LD + e % S] = P[(row0 + e / S) * S + e % S];
-  for (int e = tid; e < nblk * kNB * kNB; e += kNT) Di[e] = 0.0;
-  __syncthreads();
-#ifdef STR_CHOL_PROBE
-  long long t_loaded = clock64();
-  long long tB = 0, tC = 0;
-#endif
-  bool bad = false;
-  for (int kb = 0; kb < S; kb += kNB) {
-    const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
-#ifdef STR_CHOL_PROBE
-    long long t0 = clock64();
-#endif
-    if (tid < S - kb) {
-      const int i = kb + tid;
-      double Ld[kNB][kNB], rd[kNB], l[kNB];
-#pragma unroll
-      for (int a = 0; a < kNB; ++a)
-#pragma unroll
-        for (int b = 0; b <= a; ++b) Ld[a][b] = (a < nbk) ? A[(kb + a) * LD + kb + b] : 0.0;
-#pragma unroll
-      for (int c = 0; c < kNB; ++c) {
-        double d = Ld[c][c], r = 0.0;
-        if (c < nbk) {
-          if (!(d > 0.0)) bad = true;
-          r = rsqrt(d);
-          Ld[c][c] = d * r;
-        }
-        rd[c] = r;
-#pragma unroll
-        for (int a = c + 1; a < kNB; ++a) Ld[a][c] *= r;
-#pragma unroll
-        for (int a = c + 1; a < kNB; ++a)
-#pragma unroll
-          for (int b = c + 1; b <= a; ++b) Ld[a][b] = fma(-Ld[a][c], Ld[b][c], Ld[a][b]);
-      }
-      const int c = i - kb;                    // < nbk for rows inside the diagonal block
-#pragma unroll
-      for (int m = 0; m < kNB; ++m) {
-        double a = (m < nbk && m <= c) ? A[i * LD + kb + m] : 0.0;
-#pragma unroll
-        for (int q = 0; q < m; ++q) a = fma(-l[q], Ld[m][q], a);
-        l[m] = (m <= c) ? a * rd[m] : 0.0;
-      }
-#pragma unroll
-      for (int m = 0; m < kNB; ++m) LnT[m * S + i] = l[m];
-      double4 *lr = (double4 *)(Ln + i * kNB);
-      lr[0] = make_double4(l[0], l[1], l[2], l[3]);
-      lr[1] = make_double4(l[4], l[5], l[6], l[7]);
-      if (c < nbk) {
-        double x[kNB];
-#pragma unroll
-        for (int a = 0; a < kNB; ++a) {
-          double v = (a == c) ? 1.0 : 0.0;
-#pragma unroll
-          for (int q = 0; q < a; ++q) v = fma(-Ld[a][q], x[q], v);
-          x[a] = v * rd[a];
-        }
-        double *D = Di + (kb / kNB) * kNB * kNB;
-#pragma unroll
-        for (int a = 0; a < kNB; ++a) D[a * kNB + c] = x[a];
-      }
-    }
-    __syncthreads();
-#ifdef STR_CHOL_PROBE
-    long long t1 = clock64();
-    tB += t1 - t0;
-#endif
-    // panel write-back, then rank-8 update of the trailing lower triangle: a warp task is a strip
-    // of up to 8 rows x 32 columns; lane j keeps y = L[j][kb..kb+7] in registers and reads the
-    // row values x = L[i][kb..kb+7] as broadcasts from the row-major copy Ln.
-    for (int e = tid; e < (S - kb) * nbk; e += kNT) {
-      const int i = kb + e / nbk, m = e % nbk;
-      A[i * LD + kb + m] = LnT[m * S + i];
-    }
-    {
-      const int j0 = kb + nbk;
-      const int nch = (S - j0 + 31) / 32;
-      const int nrg = (S - j0 + 7) / 8;
-      for (int task = warp; task < nch * nrg; task += nw) {
-        const int ch = task % nch, rg = task / nch;
-        const int j = j0 + ch * 32 + lane;
-        const int ib = j0 + rg * 8;
-        if (ib + 7 < j0 + ch * 32) continue;               // strip entirely above the diagonal
-        double y[kNB];
-#pragma unroll
-        for (int m = 0; m < kNB; ++m) y[m] = (j < S && m < nbk) ? LnT[m * S + j] : 0.0;
-        // two groups of 4 rows: all shared loads of a group are issued before its stores
-#pragma unroll
-        for (int g4 = 0; g4 < 8; g4 += 4) {
-          double4 xa[4][2];
-          double av[4];
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int i = ib + g4 + a;
-            const bool ok = i < S;
-            const double4 *xr = (const double4 *)(Ln + (ok ? i : kb) * kNB);
-            xa[a][0] = xr[0];
-            xa[a][1] = xr[1];
-            av[a] = (ok && j <= i) ? A[i * LD + j] : 0.0;
-          }
-#pragma unroll
-          for (int a = 0; a < 4; ++a) {
-            const int i = ib + g4 + a;
-            double acc0 = av[a], acc1 = 0.0;
-            acc0 = fma(-xa[a][0].x, y[0], acc0);
-            acc1 = fma(-xa[a][0].y, y[1], acc1);
-            acc0 = fma(-xa[a][0].z, y[2], acc0);
-            acc1 = fma(-xa[a][0].w, y[3], acc1);
-            acc0 = fma(-xa[a][1].x, y[4], acc0);
-            acc1 = fma(-xa[a][1].y, y[5], acc1);
-            acc0 = fma(-xa[a][1].z, y[6], acc0);
-            acc1 = fma(-xa[a][1].w, y[7], acc1);
-            if (i < S && j <= i) A[i * LD + j] = acc0 + acc1;
-          }
-        }
-      }
-    }
-    __syncthreads();
-#ifdef STR_CHOL_PROBE
-    tC += clock64() - t1;
-#endif
-  }
-  if (bad && info) atomicExch(info, 1);
-#ifdef STR_CHOL_PROBE
-  long long t_fact = clock64();
-#endif
-  // forward substitution L y = b (rows of Bm hold b^T), then backward L^T x = y, block by block:
-  // (1) threads (r, m) form y_blk = Dinv b_blk, (2) store, (3) threads (i, r) take the rank-8 update.
-  const int ti = tid & 127, tr = tid >> 7;
-  for (int pass = 0; pass < 2; ++pass) {
-    for (int bb = 0; bb < nblk; ++bb) {
-      const int bi = pass == 0 ? bb : nblk - 1 - bb;
-      const int kb = bi * kNB;
-      const int nbk = (S - kb) < kNB ? (S - kb) : kNB;
-      const double *D = Di + bi * kNB * kNB;
-      const int r1 = tid >> 3, m1 = tid & 7;
-      const bool act = (r1 < rows) && (m1 < nbk);
-      double v0 = 0.0, v1 = 0.0;
-      if (act) {
-#pragma unroll
-        for (int q = 0; q < kNB; q += 2) {
-          const double d0 = pass == 0 ? D[m1 * kNB + q] : D[q * kNB + m1];
-          const double d1 = pass == 0 ? D[m1 * kNB + q + 1] : D[(q + 1) * kNB + m1];
-          v0 = fma(d0, (q < nbk) ? Bm[r1 * LD + kb + q] : 0.0, v0);
-          v1 = fma(d1, (q + 1 < nbk) ? Bm[r1 * LD + kb + q + 1] : 0.0, v1);
-        }
-      }
-      __syncthreads();
-      if (act) Bm[r1 * LD + kb + m1] = v0 + v1;
-      __syncthreads();
-      const bool upd = ti < S && (pass == 0 ? (ti >= kb + nbk) : (ti < kb));
-      if (upd) {
-        double lv[kNB];
-#pragma unroll
-        for (int m = 0; m < kNB; ++m)
-          lv[m] = (m < nbk) ? (pass == 0 ? A[ti * LD + kb + m] : A[(kb + m) * LD + ti]) : 0.0;
-        for (int r = tr; r < rows; r += kNT / 128) {
-          const double *yb = Bm + r * LD + kb;
-          double acc0 = Bm[r * LD + ti], acc1 = 0.0;
-#pragma unroll
-          for (int m = 0; m < kNB; m += 2) {
-            acc0 = fma(-lv[m], (m < nbk) ? yb[m] : 0.0, acc0);
-            acc1 = fma(-lv[m + 1], (m + 1 < nbk) ? yb[m + 1] : 0.0, acc1);
-          }
-          Bm[r * LD + ti] = acc0 + acc1;
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (int e = tid; e < rows * S; e += kNT) Gout[(row0 + e / S) * S + e % S] = Bm[(e / S) * LD + e % S];
-#ifdef STR_CHOL_PROBE
-  if (tid == 0 && blockIdx.x == 0 && g_probe) {
-    g_probe[0] = t_loaded - t_start; g_probe[1] = tB; g_probe[2] = tC; g_probe[3] = clock64() - t_fact;
-  }
-#endif
-}
-
-size_t chol_solve_smem(int S) {
-  const int nblk = (S + kNB - 1) / kNB;
-  return sizeof(double) * ((size_t)((S * (S + 1) + 3) & ~3) + (size_t)((kSolveChunk * (S + 1) + 3) & ~3) +
-                           (size_t)((S * kNB + 3) & ~3) + (size_t)S * kNB + (size_t)nblk * kNB * kNB);
-}
-
-void launch_chol_solve(const double *Q, int S, const double *P, int64_t I, double *Gout, int *info, cudaStream_t s) {
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    attr_set = true;
-  }
-  k_chol_solve<<<(unsigned)cdiv(I, kSolveChunk), kNT, chol_solve_smem(S), s>>>(Q, S, P, I, Gout, info);
-}
-
-// ------------------------------------------------------------------------------------------
 __global__ void k_axpy(const double *__restrict__ x, double *__restrict__ y, int64_t n) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i < n) y[i] += x[i];
