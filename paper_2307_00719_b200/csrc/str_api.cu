@@ -793,7 +793,12 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   h->k = cfg->split_k ? cfg->split_k : auto_split(h->dims_g, N);
   h->xbytes = cfg->dtype == STR_F64 ? 8 : 4;
 
-  if (const char *sk = getenv("STR_DBG_SKIP")) g_dbg_skip = atoi(sk);
+  if (const char *sk = getenv("STR_DBG_SKIP")) {   // what-if timing diagnostic (tools/gpu_whatif.sh)
+    g_dbg_skip = atoi(sk);
+    if (g_dbg_skip)
+      fprintf(stderr, "libstr: STR_DBG_SKIP=%d skips kernel classes: results are WRONG (what-if timing only)\n",
+              g_dbg_skip);
+  }
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) {
     delete h;
