@@ -16,6 +16,9 @@ def main():
     h = lib.str_init(cfg.N, cfg.dims, cfg.ranks, torch.from_numpy(s.init_slab()).cuda(), cfg.t_init, s.init_cores(),
                      dtype=cfg.dtype, contract="3xtf32", split_k=cfg.split_k)
     L = lib._lib.lib
+    if os.environ.get("STR_TF_DBGFLAGS"):   # the diagnostic flags act only while the pipeline trace is on
+        L.strdbg_tftrace.argtypes = [C.c_void_p, C.c_int32, C.POINTER(C.c_longlong)]
+        L.strdbg_tftrace(h.ptr, 1, None)
     L.strdbg_contract_repeat.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int64, C.c_int32, C.POINTER(C.c_double)]
     for pas in (1, 2):
         for reps in (1, 5, 20):
