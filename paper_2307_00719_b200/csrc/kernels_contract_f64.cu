@@ -85,6 +85,111 @@ __global__ void __launch_bounds__(256) k_contract_f64(const void *const *Xp, con
   }
 }
 
+// FP64 tensor-core (DMMA m8n8k4) version: CTA tile 64 (M) x 128 (N = W padded), 8 warps as
+// 2 (M) x 4 (N), each warp 32 x 32 = 4 x 4 fragments.  Fragment layouts (m8n8k4, f64): A (8 x 4,
+// row) lane holds A[lane/4][lane%4]; B (4 x 8, col) lane holds B[lane%4][lane/4]; C (8 x 8) lane
+// holds C[lane/4][2 (lane%4) + {0,1}].  Shared tiles As[m][k], Bs[n][k] with row stride 20 doubles:
+// the 32 fragment reads of a warp hit every 8-byte slot of two wavefronts exactly once.  The X
+// offsets of the rows (pass 1) / columns (pass 2) a thread loads are formed once per tile, not per
+// element.
+constexpr int DBM = 64, DBN = 128, DBK = 16, DLD = DBK + 4;
+
+__device__ __forceinline__ void dmma884_f(double &c0, double &c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+template <typename T, int PASS>
+__global__ void __launch_bounds__(256) k_contract_f64_dmma(const void *const *Xp, const double *__restrict__ Btab, int W,
+                                                           int64_t L, int64_t Rr, int64_t M, int64_t K, int64_t kchunk,
+                                                           double *__restrict__ part) {
+  const T *__restrict__ X = (const T *)*Xp;
+  __shared__ __align__(16) double As[DBM][DLD];
+  __shared__ __align__(16) double Bs[DBN][DLD];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp >> 2, wn = warp & 3;                 // warp tile rows wm*32.., cols wn*32..
+  const int64_t m0 = (int64_t)blockIdx.x * DBM;
+  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
+  const int64_t k1 = min(K, k0 + kchunk);
+  const int64_t LRr = L * Rr;
+  double acc[4][4][2];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+  // A-tile load mapping (DBM x DBK = 1024 elements, 4 per thread):
+  //   pass 1: element (mm, kk), mm = tid % 64 (contiguous l), kk = tid / 64 + 4 q; X offset of row m
+  //           = l + LRr t (m = l + L t), formed once; + L k per k.
+  //   pass 2: element (mm, kk), kk = tid % 16 (contiguous l), mm = tid / 16 + 16 q; X offset of
+  //           column k = l + LRr t (k = l + L t), advanced per chunk; + L m per row.
+  int64_t rowoff = 0;
+  bool rowok = true;
+  int amm = 0, akk = 0;
+  if (PASS == 1) {
+    amm = tid % DBM;
+    akk = tid / DBM;
+    const int64_t m = m0 + amm;
+    rowok = m < M;
+    if (rowok) rowoff = (m % L) + LRr * (m / L);
+  } else {
+    akk = tid % DBK;
+    amm = tid / DBK;
+  }
+  for (int64_t kb = k0; kb < k1; kb += DBK) {
+    if (PASS == 1) {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int kk = akk + 4 * q;
+        const int64_t k = kb + kk;
+        As[amm][kk] = (rowok && k < k1) ? (double)X[rowoff + L * k] : 0.0;
+      }
+    } else {
+      const int64_t k = kb + akk;
+      const bool kok = k < k1;
+      const int64_t coloff = kok ? (k % L) + LRr * (k / L) : 0;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int mm = amm + 16 * q;
+        const int64_t m = m0 + mm;
+        As[mm][akk] = (kok && m < M) ? (double)X[coloff + L * m] : 0.0;
+      }
+    }
+    // B tile: Btab[k][w] (K x W row-major) -> Bs[w][k]; consecutive threads along w
+    for (int e = tid; e < DBK * DBN; e += 256) {
+      const int kk = e / DBN, w = e % DBN;
+      const int64_t k = kb + kk;
+      Bs[w][kk] = (k < k1 && w < W) ? Btab[k * W + w] : 0.0;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int ks = 0; ks < DBK / 4; ++ks) {
+      double a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[wm * 32 + i * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[wn * 32 + j * 8 + (lane >> 2)][ks * 4 + (lane & 3)];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) dmma884_f(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+    }
+    __syncthreads();
+  }
+  double *o = part + (int64_t)blockIdx.y * M * W;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int64_t m = m0 + wm * 32 + i * 8 + (lane >> 2);
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int w = wn * 32 + j * 8 + 2 * (lane & 3);
+      if (w < W) o[m * W + w] = acc[i][j][0];
+      if (w + 1 < W) o[m * W + w + 1] = acc[i][j][1];
+    }
+  }
+}
+
 __global__ void k_reduce_splits(const double *__restrict__ part, int splits, int64_t n, double *__restrict__ out) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -96,6 +201,11 @@ __global__ void k_reduce_splits(const double *__restrict__ part, int splits, int
 template <typename T, int PASS>
 static void dispatch_w(const void *const *X, const double *B, int W, int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
                        int64_t kchunk, int splits, double *part, cudaStream_t s) {
+  if (W <= DBN) {   // FP64 tensor cores
+    dim3 g((unsigned)cdiv(M, DBM), (unsigned)splits);
+    k_contract_f64_dmma<T, PASS><<<g, 256, 0, s>>>(X, B, W, L, Rr, M, K, kchunk, part);
+    return;
+  }
   dim3 grid((unsigned)cdiv(M, BM), (unsigned)splits);
   if (W <= 32)
     k_contract_f64<T, PASS, 32><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
