@@ -126,9 +126,9 @@ __global__ void __launch_bounds__(256) k_contract_f64_dmma(const void *const *Xp
   int64_t rowoff = 0;
   bool rowok = true;
   int amm = 0, akk = 0;
-  if (PASS == 1) {
-    amm = tid % DBM;
-    akk = tid / DBM;
+  if (PASS == 1) {   // a warp stores 8 consecutive rows x 4 k: all 16 8-byte slots of 2 wavefronts
+    amm = 8 * warp + (lane & 7);
+    akk = lane >> 3;
     const int64_t m = m0 + amm;
     rowok = m < M;
     if (rowok) rowoff = (m % L) + LRr * (m / L);
@@ -136,13 +136,15 @@ __global__ void __launch_bounds__(256) k_contract_f64_dmma(const void *const *Xp
     akk = tid % DBK;
     amm = tid / DBK;
   }
-  for (int64_t kb = k0; kb < k1; kb += DBK) {
+  // software pipeline: the global values of tile kb + DBK are loaded into registers while the
+  // fragments of tile kb are multiplied, then stored to shared memory
+  double ra[4], rb[8];
+  auto gload = [&](int64_t kb) {
     if (PASS == 1) {
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int kk = akk + 4 * q;
-        const int64_t k = kb + kk;
-        As[amm][kk] = (rowok && k < k1) ? (double)X[rowoff + L * k] : 0.0;
+        const int64_t k = kb + akk + 4 * q;
+        ra[q] = (rowok && k < k1) ? (double)X[rowoff + L * k] : 0.0;
       }
     } else {
       const int64_t k = kb + akk;
@@ -150,18 +152,31 @@ __global__ void __launch_bounds__(256) k_contract_f64_dmma(const void *const *Xp
       const int64_t coloff = kok ? (k % L) + LRr * (k / L) : 0;
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        const int mm = amm + 16 * q;
-        const int64_t m = m0 + mm;
-        As[mm][akk] = (kok && m < M) ? (double)X[coloff + L * m] : 0.0;
+        const int64_t m = m0 + amm + 16 * q;
+        ra[q] = (kok && m < M) ? (double)X[coloff + L * m] : 0.0;
       }
     }
-    // B tile: Btab[k][w] (K x W row-major) -> Bs[w][k]; consecutive threads along w
-    for (int e = tid; e < DBK * DBN; e += 256) {
-      const int kk = e / DBN, w = e % DBN;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {   // B: w = 8 (warp + 8 (q / 4)) + lane % 8, kk = lane / 8 + 4 (q % 4)
+      const int w = 8 * (warp + 8 * (q >> 2)) + (lane & 7), kk = (lane >> 3) + 4 * (q & 3);
       const int64_t k = kb + kk;
-      Bs[w][kk] = (k < k1 && w < W) ? Btab[k * W + w] : 0.0;
+      rb[q] = (k < k1 && w < W) ? Btab[k * W + w] : 0.0;
     }
+  };
+  auto sstore = [&]() {
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      if (PASS == 1) As[amm][akk + 4 * q] = ra[q];
+      else As[amm + 16 * q][akk] = ra[q];
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q) Bs[8 * (warp + 8 * (q >> 2)) + (lane & 7)][(lane >> 3) + 4 * (q & 3)] = rb[q];
+  };
+  if (k0 < k1) gload(k0);
+  for (int64_t kb = k0; kb < k1; kb += DBK) {
+    sstore();
     __syncthreads();
+    if (kb + DBK < k1) gload(kb + DBK);
 #pragma unroll
     for (int ks = 0; ks < DBK / 4; ++ks) {
       double a[4], b[4];
