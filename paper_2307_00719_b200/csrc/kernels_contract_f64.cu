@@ -233,7 +233,7 @@ static void dispatch_w(const void *const *X, const double *B, int W, int64_t L, 
 int contract_f64_splits(int64_t M, int64_t K) {
   int64_t mt = cdiv(M, BM);
   int64_t want = cdiv(2 * 148, mt);
-  int64_t maxs = cdiv(K, 4 * BK);
+  int64_t maxs = cdiv(K, 2 * BK);
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;
   if (s > 64) s = 64;
