@@ -72,7 +72,8 @@ typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2, STR
 typedef struct {
   int32_t order;          /* N >= 3 */
   const int64_t *dims;    /* I_1 .. I_{N-1}: GLOBAL sizes of the non-temporal modes */
-  const int32_t *ranks;   /* R_1 .. R_N, each in [1, 16]; R_n R_{n+1} <= 128 */
+  const int32_t *ranks;   /* R_1 .. R_N, each in [1, 16]; R_n R_{n+1} <= 128; STR also needs
+                             R_{k+1} R_N <= 128 for the two-pass split k (STR_E_ARG otherwise) */
   str_dtype dtype;        /* element type of every X passed in */
   str_contract contract;  /* precision of the X contractions (state is always fp64) */
   str_variant variant;    /* STR (Alg. 4) or rSTR-U / rSTR-L / rSTR-K (Alg. 7 / 8 / 9) */

@@ -6,84 +6,14 @@
 //   pass 2: Y_R[r][w]     = sum_{l,t} X[l + L r + L Rr t] T_L[l + L t][w]  (M = Rr, K = L*t)
 // where l runs over the left modes (1..k), r over the right modes (k+1..N-1), and the tables
 // hold products of TR-core lateral slices (Def. 3).  This file is the FP64 path
-// (DFMA, fp64 accumulation; used where cond(Q_n) demands it and as the reference-precision
-// GPU path).  Split-K partials are reduced in a fixed order, so results are deterministic.
+// (FP64 tensor cores, fp64 accumulation; used where cond(Q_n) demands it and as the reference-
+// precision GPU path).  Split-K partials are reduced in a fixed order, so results are deterministic.
 #include "common.cuh"
 #include "kernels.h"
 
 namespace strb200 {
 
-constexpr int BM = 64, BK = 16;
-
-template <typename T, int PASS, int WT>
-__global__ void __launch_bounds__(256) k_contract_f64(const void *const *Xp, const double *__restrict__ Btab, int W,
-                                                      int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
-                                                      int64_t kchunk, double *__restrict__ part) {
-  // X is read through a device-side pointer slot so that a captured CUDA graph replays on new data
-  const T *__restrict__ X = (const T *)*Xp;
-  __shared__ double As[BK][BM + 1];
-  __shared__ double Bs[BK][WT];
-  const int tid = threadIdx.x;
-  const int tx = tid % 16, ty = tid / 16;
-  const int64_t m0 = (int64_t)blockIdx.x * BM;
-  const int64_t k0 = (int64_t)blockIdx.y * kchunk;
-  const int64_t k1 = min(K, k0 + kchunk);
-  const int64_t LRr = L * Rr;
-  constexpr int NJ = WT / 16;
-  double acc[4][NJ];
-#pragma unroll
-  for (int i = 0; i < 4; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j] = 0.0;
-
-  for (int64_t kb = k0; kb < k1; kb += BK) {
-    // A tile: BM x BK
-    for (int e = tid; e < BM * BK; e += 256) {
-      int mm, kk;
-      if (PASS == 1) { mm = e % BM; kk = e / BM; }   // m (l) contiguous
-      else           { kk = e % BK; mm = e / BK; }   // k (l) contiguous
-      int64_t m = m0 + mm, k = kb + kk;
-      double v = 0.0;
-      if (m < M && k < k1) {
-        int64_t off;
-        if (PASS == 1) { int64_t l = m % L, t = m / L; off = l + L * k + LRr * t; }
-        else           { int64_t l = k % L, t = k / L; off = l + L * m + LRr * t; }
-        v = (double)X[off];
-      }
-      As[kk][mm] = v;
-    }
-    for (int e = tid; e < BK * WT; e += 256) {
-      int kk = e / WT, w = e % WT;
-      int64_t k = kb + kk;
-      Bs[kk][w] = (k < k1 && w < W) ? Btab[k * W + w] : 0.0;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < BK; ++kk) {
-      double a[4], b[NJ];
-#pragma unroll
-      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
-#pragma unroll
-      for (int j = 0; j < NJ; ++j) b[j] = Bs[kk][tx + 16 * j];
-#pragma unroll
-      for (int i = 0; i < 4; ++i)
-#pragma unroll
-        for (int j = 0; j < NJ; ++j) acc[i][j] = fma(a[i], b[j], acc[i][j]);
-    }
-    __syncthreads();
-  }
-  double *o = part + (int64_t)blockIdx.y * M * W;
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    int64_t m = m0 + ty * 4 + i;
-    if (m >= M) continue;
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) {
-      int w = tx + 16 * j;
-      if (w < W) o[m * W + w] = acc[i][j];
-    }
-  }
-}
+constexpr int BM = 64, BK = 16;   // M tile and K granule of the split-K partition
 
 // FP64 tensor-core (DMMA m8n8k4) version: CTA tile 64 (M) x 128 (N = W padded), 8 warps as
 // 2 (M) x 4 (N), each warp 32 x 32 = 4 x 4 fragments.  Fragment layouts (m8n8k4, f64): A (8 x 4,
@@ -216,18 +146,9 @@ __global__ void k_reduce_splits(const double *__restrict__ part, int splits, int
 template <typename T, int PASS>
 static void dispatch_w(const void *const *X, const double *B, int W, int64_t L, int64_t Rr, int64_t tn, int64_t M, int64_t K,
                        int64_t kchunk, int splits, double *part, cudaStream_t s) {
-  if (W <= DBN) {   // FP64 tensor cores
-    dim3 g((unsigned)cdiv(M, DBM), (unsigned)splits);
-    k_contract_f64_dmma<T, PASS><<<g, 256, 0, s>>>(X, B, W, L, Rr, M, K, kchunk, part);
-    return;
-  }
-  dim3 grid((unsigned)cdiv(M, BM), (unsigned)splits);
-  if (W <= 32)
-    k_contract_f64<T, PASS, 32><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
-  else if (W <= 64)
-    k_contract_f64<T, PASS, 64><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
-  else
-    k_contract_f64<T, PASS, 128><<<grid, 256, 0, s>>>(X, B, W, L, Rr, tn, M, K, kchunk, part);
+  (void)tn;
+  dim3 g((unsigned)cdiv(M, DBM), (unsigned)splits);   // W <= 128 (str_init)
+  k_contract_f64_dmma<T, PASS><<<g, 256, 0, s>>>(X, B, W, L, Rr, M, K, kchunk, part);
 }
 
 int contract_f64_splits(int64_t M, int64_t K) {
@@ -365,18 +286,10 @@ void prepare_f64_attrs() {
   prefer_max_smem(k_set_ptr);
   prefer_max_smem(k_append_rows);
   prefer_max_smem(k_reduce_splits);
-  prefer_max_smem(k_contract_f64<float, 1, 32>);
-  prefer_max_smem(k_contract_f64<float, 1, 64>);
-  prefer_max_smem(k_contract_f64<float, 1, 128>);
-  prefer_max_smem(k_contract_f64<float, 2, 32>);
-  prefer_max_smem(k_contract_f64<float, 2, 64>);
-  prefer_max_smem(k_contract_f64<float, 2, 128>);
-  prefer_max_smem(k_contract_f64<double, 1, 32>);
-  prefer_max_smem(k_contract_f64<double, 1, 64>);
-  prefer_max_smem(k_contract_f64<double, 1, 128>);
-  prefer_max_smem(k_contract_f64<double, 2, 32>);
-  prefer_max_smem(k_contract_f64<double, 2, 64>);
-  prefer_max_smem(k_contract_f64<double, 2, 128>);
+  prefer_max_smem(k_contract_f64_dmma<float, 1>);
+  prefer_max_smem(k_contract_f64_dmma<float, 2>);
+  prefer_max_smem(k_contract_f64_dmma<double, 1>);
+  prefer_max_smem(k_contract_f64_dmma<double, 2>);
 }
 
 }  // namespace strb200

@@ -791,6 +791,12 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   h->rank = cfg->rank;
   h->device = cfg->device;
   h->k = cfg->split_k ? cfg->split_k : auto_split(h->dims_g, N);
+  if (h->variant == STR_DET && cfg->ranks[h->k] * cfg->ranks[N - 1] > STR_MAXW) {
+    // the two-pass outputs carry R_{k+1} R_N columns: one tensor-core N tile / one
+    // 128-wide DMMA tile
+    delete h;
+    return STR_E_ARG;
+  }
   h->xbytes = cfg->dtype == STR_F64 ? 8 : 4;
 
   if (const char *sk = getenv("STR_DBG_SKIP")) {   // what-if timing diagnostic (tools/gpu_whatif.sh)

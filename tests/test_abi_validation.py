@@ -36,6 +36,7 @@ def _init(cfg, t_init=3):
     (dict(ranks=(2, 17, 2, 2)), 3, L.STR_E_ARG),
     (dict(ranks=(2, 12, 12, 2)), 3, L.STR_E_ARG),                               # R_n R_{n+1} <= 128
     (dict(split_k=3), 3, L.STR_E_ARG),                                          # split in [0, N-2]
+    (dict(ranks=(1, 12, 8, 12), split_k=1), 3, L.STR_E_ARG),                    # STR: R_{k+1} R_N <= 128
     (dict(dtype=7), 3, L.STR_E_ARG),
     (dict(variant=9), 3, L.STR_E_ARG),
     (dict(world=2, rank=2), 3, L.STR_E_ARG),                                    # rank < world
