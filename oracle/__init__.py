@@ -20,5 +20,8 @@ Modules
 Parity status: every function is pinned by a -m "not gpu"
 test except the noisy whole-trajectory results, which are pinned only through invariants
 (the paper prints no numbers for them) and rSTR at m=2000 ("parity unpinned" vs theory;
-pinned only by the exhaustive-enumeration degeneracy rSTR == STR).
+pinned only by the exhaustive-enumeration degeneracy rSTR == STR).  rSTR-K (ksrft) likewise:
+its mixing is pinned by numpy's FFT and brute force, its sketched normal equations by the
+exhaustive-sketch identity and the exact-stream fixed point; at m=2000 it is "parity unpinned"
+against Theorem 3.
 """
