@@ -97,8 +97,9 @@ def run_workload(label, dims, IN, t_new, R, methods, seed, max_steps, contract="
            "methods": {}}
     for meth in methods:
         kw = {}
-        if meth in ("rSTR-U", "rSTR-L"):
-            kw = dict(variant="uniform" if meth == "rSTR-U" else "leverage", sketch_rows=1000, seed=seed)
+        if meth in ("rSTR-U", "rSTR-L", "rSTR-K"):
+            kw = dict(variant={"rSTR-U": "uniform", "rSTR-L": "leverage", "rSTR-K": "ksrft"}[meth], sketch_rows=1000,
+                      seed=seed)
         h = lib.str_init(N, dims, ranks, hist[:t_init * slice_n], t_init, init_cores, dtype="f32", contract=contract,
                          t_capacity=T_total + 8, **kw)
         times, errs = [], []
@@ -107,7 +108,7 @@ def run_workload(label, dims, IN, t_new, R, methods, seed, max_steps, contract="
         for b in range(n_batches):
             a = T * slice_n
             T += t_new
-            if meth in ("STR", "rSTR-U", "rSTR-L"):
+            if meth in ("STR", "rSTR-U", "rSTR-L", "rSTR-K"):
                 ms, _ = ev_time(lambda: (lib.str_update_batch(h, hist[a:a + t_new * slice_n], t_new),
                                          lib.str_sync(h)))
                 err = lib.str_fit(h, hist[:T * slice_n], 0, T)
@@ -140,7 +141,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--set", default="order", choices=["order", "length", "slice", "rank", "all"])
     ap.add_argument("--quick", action="store_true")
-    ap.add_argument("--methods", default="STR,rSTR-U,rSTR-L,TR-ALS Hot,TR-ALS Cold")
+    ap.add_argument("--methods", default="STR,rSTR-U,rSTR-L,rSTR-K,TR-ALS Hot,TR-ALS Cold")
     ap.add_argument("--max-steps", type=int, default=0)
     ap.add_argument("--seed", type=int, default=2307)
     ap.add_argument("--contract", default="3xtf32", choices=["3xtf32", "f64"])
