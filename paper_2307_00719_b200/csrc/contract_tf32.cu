@@ -43,10 +43,7 @@ constexpr int kBM = 128;       // UMMA M
 constexpr int kMT = 2;         // M-tiles per CTA (share every B stage)
 constexpr int kBK = 32;        // K per stage (one 128-byte swizzle row of fp32)
 constexpr int kABytes = kBM * kBK * 4;   // 16 KB per X tile
-constexpr uint32_t kASlot0 = 256;        // N > 64: accumulators at mt * 128, 2 A slots at [256, 512): slot a, M-tile
-                                         // mt at 256 + (2a + mt) * 64.  N <= 64: accumulators at mt * 64 and 3 A
-                                         // slots at [128, 512) (one more unit of converter -> MMA slack)
-constexpr int kMaxASlots = 3;
+constexpr uint32_t kASlot0 = 256;        // A slots at [256, 512): slot a, M-tile mt at 256 + (2a + mt) * 64
 // epilogue staging: per lane quarter one dense [32 rows][W] fp32 box (W <= 128) -> one M-tile
 __host__ __device__ constexpr int ystage_box_bytes(int W) { return (32 * W * 4 + 1023) / 1024 * 1024; }
 __host__ __device__ constexpr int ystage_bytes(int W) { return 4 * ystage_box_bytes(W); }
@@ -136,9 +133,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t *xempty = xfull + SX;
   uint64_t *bfull = xempty + SX;
   uint64_t *bempty = bfull + SB;
-  uint64_t *conv = bempty + SB;    // [NA] A slot filled (converters -> MMA)
-  uint64_t *aempty = conv + kMaxASlots;   // [NA] A slot free   (MMA -> converters)
-  uint64_t *accf = aempty + kMaxASlots;    // accumulators complete (MMA -> epilogue)
+  uint64_t *conv = bempty + SB;    // [2] A slot filled (converters -> MMA)
+  uint64_t *aempty = conv + 2;     // [2] A slot free   (MMA -> converters)
+  uint64_t *accf = aempty + 2;     // accumulators complete (MMA -> epilogue)
   uint64_t *acce = accf + 1;       // [2] accumulator of M-tile mt drained (epilogue -> MMA)
   uint32_t *tslot = (uint32_t *)(acce + 2);
 
@@ -158,7 +155,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::mbar_init(&bfull[s], 1);
       tc::mbar_init(&bempty[s], 1);
     }
-    for (int a = 0; a < kMaxASlots; ++a) {
+    for (int a = 0; a < 2; ++a) {
       tc::mbar_init(&conv[a], 8);
       tc::mbar_init(&aempty[a], 1);
     }
@@ -184,8 +181,6 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   __syncthreads();
   tc::tc_fence_after();
   const uint32_t tbase = __shfl_sync(0xffffffffu, *tslot, 0);
-  const int NA = p.Npad <= 64 ? 3 : 2;                       // TMEM A slots (see kASlot0)
-  const uint32_t accst = NA == 3 ? 64u : 128u, aslot0 = NA == 3 ? 128u : kASlot0;
   if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 1] = gtimer();
 
   if ((p.dbg_flags & 256) && warp != 1 && !(p.dbg_flags & 512)) {
@@ -255,11 +250,11 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         const uint32_t b0 = tc::smem_u32(bbuf);
         long long t0 = clock64();
         for (int64_t u = u0; u < u1; ++u) {
-          const int a = (int)(u % NA);
+          const int a = (int)(u & 1);
 #pragma unroll
           for (int mt = 0; mt < kMT; ++mt) {
-            const uint32_t d = tbase + (uint32_t)mt * accst;
-            const uint32_t ahi = tbase + aslot0 + (uint32_t)((2 * a + mt) * 64);
+            const uint32_t d = tbase + (uint32_t)(mt * 128);
+            const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * a + mt) * 64);
 #pragma unroll
             for (int ks = 0; ks < kBK / 8; ++ks) {
               const uint64_t bhi = tc::smem_desc_sw128(b0 + ks * 32, 16, 1024);
@@ -270,7 +265,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             }
           }
           mma_commit_elect(&bempty[(int)((u - u0) % SB)]);
-          mma_commit_elect(&aempty[(int)((u - u0) % NA)]);
+          mma_commit_elect(&aempty[(int)((u - u0) & 1)]);
         }
         mma_commit_elect(accf);
         tc::mbar_wait(accf, 0);
@@ -312,8 +307,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             __syncwarp();
             tc::tc_fence_after();
           }
-          const uint32_t d = tbase + (uint32_t)mt * accst;
-          const uint32_t ahi = tbase + aslot0 + (uint32_t)((2 * au + mt) * 64);
+          const uint32_t d = tbase + (uint32_t)(mt * 128);
+          const uint32_t ahi = tbase + kASlot0 + (uint32_t)((2 * au + mt) * 64);
 #pragma unroll
           for (int ks = 0; ks < kBK / 8; ++ks) {
             const uint64_t bhi = bd + (uint64_t)(ks * 2), blo = bd + (uint64_t)(lostep + ks * 2);
@@ -329,7 +324,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         pend_accf = last;
         if (dbgcta && u - u0 < 64) p.dbg[(u - u0) * 16 + 7] = clock64();
         if (++s == SB) s = 0;
-        if (++a == NA) { a = 0; pha ^= 1; }
+        if (++a == 2) { a = 0; pha ^= 1; }
       }
       if (pend_accf) mma_commit_elect(accf);
       if (p.dbg && lane == 0) p.dbg[1024 + blockIdx.x * 4 + 2] = gtimer();
@@ -380,7 +375,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&xempty[s]);   // the X slot is free once the tile sits in registers
-      const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + aslot0 + (uint32_t)((2 * a + mt) * 64);
+      const uint32_t ta = tbase + ((uint32_t)(q * 32) << 16) + kASlot0 + (uint32_t)((2 * a + mt) * 64);
       if (!(p.dbg_flags & 4) && present) {
         tmem_st32(ta, hi);
         tmem_st32(ta + 32, lo);
@@ -393,7 +388,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       __syncwarp();
       if (lane == 0) tc::mbar_arrive(&conv[a]);
       if (++s == SX) { s = 0; ph ^= 1; }
-      if (++a == NA) { a = 0; pha ^= 1; }
+      if (++a == 2) { a = 0; pha ^= 1; }
       if (++sb == SB) { sb = 0; phb ^= 1; }
     }
   } else if (warp >= 12) {
@@ -428,7 +423,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
           t = g / p.mt_per_t;
           r0 = (g - t * p.mt_per_t) * kBM;
         }
-        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)mt * accst;
+        const uint32_t taddr = tbase + ((uint32_t)(q * 32) << 16) + (uint32_t)(mt * 128);
         if (p.yred) {
           uint8_t *box = (lastseg && mt == 1 ? xbuf : ystage) + q * ybox;
           if (pending && box != xbuf + q * ybox) {
@@ -655,7 +650,7 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   const int ybytes = p.yred ? ystage_bytes(W) : 0;
   p.bstages = 2;
   if (const char *ev = getenv("STR_TF_BSTAGES")) p.bstages = std::max(2, atoi(ev));   // tuning knob
-  p.stages = std::min(6, (int)((227 * 1024 - 1024 - 512 - ybytes - p.bstages * bbytes) / (kMT * kABytes)));
+  p.stages = std::min(6, (int)((227 * 1024 - 1024 - 256 - ybytes - p.bstages * bbytes) / (kMT * kABytes)));
   if (p.stages < 2) {
     h->err = "3xTF32 contraction: shared memory too small for the ring depths";
     return -1;
@@ -695,7 +690,7 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
     k_zero_f32<<<(unsigned)std::min<int64_t>(296, (n4 + 255) / 256), 256, 0, st>>>((float4 *)p.Y, n4);
     tl_mark(h, "zero_y");
   }
-  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 512;   // 512: barriers + TMEM slot
+  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 256;
   prof_mark(h, 2 * (pass - 1));
   if (pass == 1)
     k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, ymap, p);
