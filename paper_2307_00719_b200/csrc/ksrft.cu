@@ -303,6 +303,8 @@ __global__ void __launch_bounds__(256) k_mix_pq(const void *const *__restrict__ 
     }
   }
   __syncthreads();
+  const bool pow2 = (WF & (WF - 1)) == 0;
+  const int lgWF = 31 - __clz(WF);
   // complex MAC on packed fp32 pairs: acc += x w = x (w.x, w.x) + (-x.y, x.x) (w.y, w.y)  (2 FFMA2)
   {
     float2 wxx[P], wyy[P];                               // w_P^j = w^{Q j}
@@ -313,7 +315,14 @@ __global__ void __launch_bounds__(256) k_mix_pq(const void *const *__restrict__ 
       wyy[j] = make_float2(w.y, w.y);
     }
     for (int it = threadIdx.x; it < WF * Q; it += 256) {   // stage 1, item (f, n2)
-      const int f = it % WF, n2 = it / WF;
+      int f, n2;
+      if constexpr (P * Q <= 32) {   // short modes: cheap items, power-of-two tile widths use shifts
+        f = pow2 ? (it & (WF - 1)) : it % WF;
+        n2 = pow2 ? (it >> lgWF) : it / WF;
+      } else {
+        f = it % WF;
+        n2 = it / WF;
+      }
       float2 x[P], xr[P];
 #pragma unroll
       for (int n1 = 0; n1 < P; ++n1) {
@@ -354,7 +363,14 @@ __global__ void __launch_bounds__(256) k_mix_pq(const void *const *__restrict__ 
       wyy[j] = make_float2(w.y, w.y);
     }
     for (int it = threadIdx.x; it < WF * P; it += 256) {   // stage 2, item (f, k1)
-      const int f = it % WF, k1 = it / WF;
+      int f, k1;
+      if constexpr (P * Q <= 32) {
+        f = pow2 ? (it & (WF - 1)) : it % WF;
+        k1 = pow2 ? (it >> lgWF) : it / WF;
+      } else {
+        f = it % WF;
+        k1 = it / WF;
+      }
       float2 t[Q], tr[Q];
 #pragma unroll
       for (int n2 = 0; n2 < Q; ++n2) {
