@@ -172,3 +172,33 @@ def test_m_below_rank_product_rejected():
     s = make_stream("R4")
     with pytest.raises(ValueError):
         KSRFTStreamingTR(paper_view(s.init_slab()), s.init_cores(), 3, seed=1)
+
+
+def test_ksrft_sketch_is_unbiased():
+    """Monte-Carlo pin: for fixed signs D, uniform rows of the unitary-mixed problem give
+    E[Re(X~_S conj G^_S)] = (m/J) X_[n] G^{≠n}_[2] and E[Re(G^_S^T conj G^_S)] = (m/J) G^{≠n T} G^{≠n}
+    (unitarity of ⊗ F_j D_j), checked against the ⊠₂ subchain route over seeded index draws."""
+    rng = np.random.default_rng(22)
+    dims, ranks = (4, 3, 5), (2, 3, 2)
+    N, m, n = 3, 6, 1
+    cores = _tiny_cores(rng, dims, ranks)
+    X = rng.standard_normal(dims)
+    Ws = mixing_matrices(sign_flips(5, 1, N, dims))
+    Xh = mix_tensor(X, Ws)
+    mixed = [mix_core(G, W) for G, W in zip(cores, Ws)]
+    J = int(np.prod([d for k, d in enumerate(dims) if k != n - 1]))
+    Gsub = unfold2(subchain(cores, n))
+    P_ref = (m / J) * unfold(X, n, "mode") @ Gsub
+    Q_ref = (m / J) * Gsub.T @ Gsub
+    P_sum = np.zeros_like(P_ref)
+    Q_sum = np.zeros_like(Q_ref)
+    trials = 3000
+    for s in range(trials):
+        idxs = np.stack([draw_uniform(2000 + s, 0, k, N, dims[k - 1], m) for k in range(1, N + 1)], axis=1)
+        samp = [G[:, idxs[:, k], :] for k, G in enumerate(mixed)]
+        GS2 = unfold2(sampled_subchain(samp, N, n))
+        XS = unmix_fibers(sampled_fibers(Xh, idxs, n), Ws[n - 1])
+        P_sum += np.real(XS @ GS2.conj())
+        Q_sum += np.real(GS2.T @ GS2.conj())
+    assert np.linalg.norm(P_sum / trials - P_ref) / np.linalg.norm(P_ref) < 0.05
+    assert np.linalg.norm(Q_sum / trials - Q_ref) / np.linalg.norm(Q_ref) < 0.05

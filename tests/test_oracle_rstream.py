@@ -127,3 +127,33 @@ def test_rstr_requires_enough_rows():
     s = make_stream("T4")
     with pytest.raises(ValueError):
         RandomizedStreamingTR(paper_view(s.init_slab()), s.init_cores(), 5, "uniform", seed=1)
+
+
+def test_uniform_sketch_is_unbiased():
+    """Monte-Carlo pin of the sampled normal equations (Alg. 7 l.15-16 with uniform rows drawn with
+    replacement, no rescaling, reading R8): over the seeded draws, E[X_S G_S] = (m/J) X_[n] G^{≠n}_[2]
+    and E[G_S^T G_S] = (m/J) G^{≠n T} G^{≠n} with J = prod_{j≠n} I_j, the exact products built by
+    the independent ⊠₂ subchain route."""
+    from oracle.rstream import sampled_fibers, sampled_subchain
+    from oracle.tensor import unfold
+    rng = np.random.default_rng(21)
+    dims, ranks = (4, 3, 5), (2, 3, 2)
+    N, m, n = 3, 6, 2
+    cores = [rng.standard_normal((ranks[k], dims[k], ranks[(k + 1) % N])) for k in range(N)]
+    X = rng.standard_normal(dims)
+    J = int(np.prod([d for k, d in enumerate(dims) if k != n - 1]))
+    Gsub = unfold2(subchain(cores, n))
+    P_ref = (m / J) * unfold(X, n, "mode") @ Gsub
+    Q_ref = (m / J) * Gsub.T @ Gsub
+    P_sum = np.zeros_like(P_ref)
+    Q_sum = np.zeros_like(Q_ref)
+    trials = 3000
+    for s in range(trials):
+        idxs = np.stack([draw_uniform(1000 + s, 0, k, N, dims[k - 1], m) for k in range(1, N + 1)], axis=1)
+        samp = [G[:, idxs[:, k], :] for k, G in enumerate(cores)]
+        GS2 = unfold2(sampled_subchain(samp, N, n))
+        P_sum += sampled_fibers(X, idxs, n) @ GS2
+        Q_sum += GS2.T @ GS2
+    # the mean of `trials` i.i.d. sketches: relative error ~ 1/sqrt(trials m) ~ 0.8%
+    assert np.linalg.norm(P_sum / trials - P_ref) / np.linalg.norm(P_ref) < 0.05
+    assert np.linalg.norm(Q_sum / trials - Q_ref) / np.linalg.norm(Q_ref) < 0.05
