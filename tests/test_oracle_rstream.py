@@ -157,3 +157,37 @@ def test_uniform_sketch_is_unbiased():
     # the mean of `trials` i.i.d. sketches: relative error ~ 1/sqrt(trials m) ~ 0.8%
     assert np.linalg.norm(P_sum / trials - P_ref) / np.linalg.norm(P_ref) < 0.05
     assert np.linalg.norm(Q_sum / trials - Q_ref) / np.linalg.norm(Q_ref) < 0.05
+
+
+def test_leverage_sketch_expectation():
+    """Monte-Carlo pin of Alg. 8's sampled normal equations (rows drawn with replacement from the
+    product of the per-mode leverage distributions p_k = l(G_k(2))/rank, Lemma 1; no rescaling,
+    reading R8): E[X_S G_S] = m X_[n] diag(q) G^{≠n}_[2] and E[G_S^T G_S] = m G^{≠n T} diag(q) G^{≠n},
+    q(i) = prod_{j≠n} p_j(i_j) over the subchain rows (first chain index fastest), brute force."""
+    from oracle.rstream import sampled_fibers, sampled_subchain
+    from oracle.tensor import unfold
+    rng = np.random.default_rng(23)
+    dims, ranks = (7, 6, 8), (1, 2, 1)          # I_k > R_k R_{k+1}: non-uniform leverage scores
+    N, m, n = 3, 5, 1
+    cores = [rng.standard_normal((ranks[k], dims[k], ranks[(k + 1) % N])) * rng.uniform(0.2, 3.0, (1, dims[k], 1))
+             for k in range(N)]
+    X = rng.standard_normal(dims)
+    p = [leverage_distribution(core_unfold(G)) for G in cores]
+    assert max(np.max(pk) * len(pk) for pk in p) > 1.3        # genuinely non-uniform
+    order = list(range(n + 1, N + 1)) + list(range(1, n))
+    q = np.array([np.prod([p[j - 1][i] for j, i in zip(order, tuple(reversed(idx)))])
+                  for idx in itertools.product(*[range(dims[j - 1]) for j in reversed(order)])])
+    Gsub = unfold2(subchain(cores, n))
+    P_ref = m * unfold(X, n, "mode") @ (q[:, None] * Gsub)
+    Q_ref = m * Gsub.T @ (q[:, None] * Gsub)
+    P_sum = np.zeros_like(P_ref)
+    Q_sum = np.zeros_like(Q_ref)
+    trials = 3000
+    for s in range(trials):
+        idxs = np.stack([draw_weighted(3000 + s, 0, k, N, p[k - 1], m) for k in range(1, N + 1)], axis=1)
+        samp = [G[:, idxs[:, k], :] for k, G in enumerate(cores)]
+        GS2 = unfold2(sampled_subchain(samp, N, n))
+        P_sum += sampled_fibers(X, idxs, n) @ GS2
+        Q_sum += GS2.T @ GS2
+    assert np.linalg.norm(P_sum / trials - P_ref) / np.linalg.norm(P_ref) < 0.06
+    assert np.linalg.norm(Q_sum / trials - Q_ref) / np.linalg.norm(Q_ref) < 0.06
