@@ -72,6 +72,8 @@ int launch_mix_mode(const void *const *xslot, bool x_f64, void *Xh, bool f64, co
                     const double *d, cudaStream_t st);
 int launch_mix_sample(const double *G, int64_t I, int S, const int32_t *idx, int64_t m, const double *d, double2 *out,
                       double2 *core_ws, cudaStream_t st);   // returns the number of launches (< 0: error)
+int launch_mix_sample_draw(const double *G, int64_t I, int S, uint64_t seed, const int64_t *tau, int k, int N, int64_t m,
+                           const double *d, double2 *out, double2 *core_ws, int32_t *idx, cudaStream_t st);
 int launch_chain_complex(const double2 *const *G, const int *Ra, const int *Rb, int nf, int64_t m, double *out,
                          cudaStream_t st);
 int launch_gather_unmix(const void *Xh, bool f64, const int64_t *dims, int N, int n, const int32_t *idx, int64_t m,

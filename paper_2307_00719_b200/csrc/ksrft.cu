@@ -727,6 +727,35 @@ int launch_mix_sample(const double *G, int64_t I, int S, const int32_t *idx, int
   return 1;
 }
 
+// the mixed core, then the uniform draw fused with the gather of its sampled rows (draw s of the
+// stream (seed, tau, k) recomputed per thread, counter-based; idx[s] written by c == 0)
+__global__ void k_draw_gather_crows(uint64_t seed, const int64_t *__restrict__ tau, int k, int N, int64_t I, int64_t m,
+                                    const double2 *__restrict__ Gh, int S, int32_t *__restrict__ idx,
+                                    double2 *__restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * S) return;
+  const int64_t s = e / S;
+  const int c = (int)(e - s * S);
+  const uint64_t key = seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(1 + (*tau) * (N + 1) + k));
+  const int64_t ix = (int64_t)__umul64hi(ks_splitmix_at(key, (uint64_t)s), (uint64_t)I);
+  if (c == 0) idx[s] = (int32_t)ix;
+  out[e] = Gh[ix * S + c];
+}
+
+int launch_mix_sample_draw(const double *G, int64_t I, int S, uint64_t seed, const int64_t *tau, int k, int N, int64_t m,
+                           const double *d, double2 *out, double2 *core_ws, int32_t *idx, cudaStream_t st) {
+  const size_t smem = sizeof(double2) * (size_t)I;
+  if (smem > 200 * 1024 || !core_ws) return -1;
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(k_mix_core, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    attr = true;
+  }
+  k_mix_core<<<(unsigned)cdiv(I * S, 128), 128, smem, st>>>(G, (int)I, S, d, core_ws);
+  k_draw_gather_crows<<<(unsigned)cdiv(m * S, 256), 256, 0, st>>>(seed, tau, k, N, I, m, core_ws, S, idx, out);
+  return 2;
+}
+
 int launch_chain_complex(const double2 *const *G, const int *Ra, const int *Rb, int nf, int64_t m, double *out,
                          cudaStream_t st) {
   if (nf < 1 || nf > kMaxFactors) return -1;

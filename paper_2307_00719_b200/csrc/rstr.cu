@@ -83,13 +83,19 @@ __device__ __forceinline__ uint64_t draw_key(uint64_t seed, int64_t tau, int k, 
 
 __global__ void k_tau_advance(int64_t *tau) { *tau += 1; }
 
-// uniform on [I): (u * I) >> 64
-__global__ void k_draw_uniform(uint64_t seed, const int64_t *__restrict__ tau, int k, int N, int64_t I, int64_t m,
-                               int32_t *__restrict__ out) {
-  const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (j >= m) return;
-  const uint64_t u = splitmix_at(draw_key(seed, *tau, k, N), (uint64_t)j);
-  out[j] = (int32_t)__umul64hi(u, (uint64_t)I);
+// uniform draw fused with the gather of the sampled rows (one node fewer per draw): thread (s, c)
+// recomputes draw s (counter-based), writes idx[s] when c == 0 and copies G[idx_s][c]
+__global__ void k_draw_gather_uniform(uint64_t seed, const int64_t *__restrict__ tau, int k, int N, int64_t I,
+                                      int64_t m, const double *__restrict__ G, int S, int32_t *__restrict__ idx,
+                                      double *__restrict__ out) {
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (e >= m * S) return;
+  const int64_t s = e / S;
+  const int c = (int)(e - s * S);
+  const uint64_t u = splitmix_at(draw_key(seed, *tau, k, N), (uint64_t)s);
+  const int64_t ix = (int64_t)__umul64hi(u, (uint64_t)I);
+  if (c == 0) idx[s] = (int32_t)ix;
+  out[e] = G[ix * S + c];
 }
 
 // weighted by p (nullptr: 1/I each): one CTA; the CDF is summed by one thread in index order (as the
@@ -346,20 +352,34 @@ static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t
   const int S = RRr(h, k) * RRr(h, k + 1);
   int32_t *dix = (int32_t *)h->sIdxDev.p + (int64_t)(k - 1) * h->m;
   const int64_t *tau = (const int64_t *)h->dTau.p;
-  if (h->variant != STR_SAMPLE_LEVERAGE) {
-    k_draw_uniform<<<(unsigned)cdiv(h->m, 256), 256, 0, h->st>>>(h->seed, tau, k, h->N, I, h->m, dix);
-    tl_mark(h, "draw_uniform");
-  } else {
-    const double *pd = nullptr;
-    RTRY(leverage_probs_dev(h, rows, I, S, &pd));
-    k_draw_weighted<<<1, 1024, sizeof(double) * I, h->st>>>(pd, I, h->seed, tau, k, h->N, h->m, dix);
-    tl_mark(h, "draw_weighted");
+  ModeBuf &mbu = h->md[std::min(k, h->N - 1) - 1];
+  double *dstu = (k == h->N) ? (double *)h->sG.p : (double *)mbu.samp.p;
+  if (h->variant == STR_SAMPLE_UNIFORM) {   // draw + gather in one kernel
+    h->idx_dev[k] = true;
+    k_draw_gather_uniform<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(h->seed, tau, k, h->N, I, h->m, rows, S,
+                                                                             dix, dstu);
+    tl_mark(h, "draw_gather");
+    return STR_OK;
   }
+  if (h->variant == STR_SAMPLE_KSRFT) {     // mixed core, then draw + gather of its sampled rows
+    h->idx_dev[k] = true;
+    const int nl = launch_mix_sample_draw(rows, I, S, h->seed, tau, k, h->N, h->m,
+                                          (const double *)h->ksSign.p + h->ks_off[k - 1], (double2 *)dstu,
+                                          (double2 *)h->ksCore.p, dix, h->st);
+    if (nl < 0) {
+      h->err = "KSRFT: mode too long for the sampled mixing kernel";
+      return STR_E_ARG;
+    }
+    tl_mark(h, "mix_sample_draw", nl);
+    return STR_OK;
+  }
+  // leverage: probabilities, weighted draw (one CTA, CDF in shared memory), gather
+  const double *pd = nullptr;
+  RTRY(leverage_probs_dev(h, rows, I, S, &pd));
+  k_draw_weighted<<<1, 1024, sizeof(double) * I, h->st>>>(pd, I, h->seed, tau, k, h->N, h->m, dix);
+  tl_mark(h, "draw_weighted");
   h->idx_dev[k] = true;
-  ModeBuf &mb = h->md[std::min(k, h->N - 1) - 1];
-  double *dst = (k == h->N) ? (double *)h->sG.p : (double *)mb.samp.p;
-  if (h->ksrft()) return ks_sample(h, k, rows, I, dst);
-  k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dst);
+  k_gather_rows<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(rows, S, dix, h->m, dstu);
   tl_mark(h, "k_gather_rows");
   return STR_OK;
 }
