@@ -12,7 +12,8 @@
  * per processed time step), the complementary matrices P_n (I_n x R_nR_{n+1}) and
  * Q_n (R_nR_{n+1} x R_nR_{n+1}) of Eq. (partial), and the Gram tensors Z_n of
  * Alg. 4 l.2.  rSTR (Alg. 6; Alg. 7; Alg. 8)
- * keeps the same P_n/Q_n built from sampled rows and the sampled core slices.
+ * keeps the same P_n/Q_n built from sampled rows and the sampled core slices; rSTR-K (Alg. 9
+ * P:1194-1258) builds them from rows of the KSRFT-mixed problem (real parts, R17-R22).
  *
  * Conventions
  *   - Modes are numbered 1..N as in the paper; mode N is time.  All indices are 0-based.
@@ -27,7 +28,7 @@
  *   - Device work is enqueued on the stream given in the config (or an internal stream when
  *     NULL) and the call returns without waiting; call str_sync() to wait.  Host-side argument
  *     errors are reported immediately.  Device-side numerical failures (a non-positive
- *     pivot in a Cholesky factorization of Q_n) are reported by the next str_sync(),
+ *     pivot in the SPD inversion of Q_n or of a temporal Gram) are reported by the next str_sync(),
  *     str_get_cores(), str_get_temporal_rows() or str_fit() as STR_E_NUMERIC, after which
  *     the handle is poisoned (every later call returns STR_E_POISONED).
  *   - A handle is used by one host thread at a time.  Distinct handles may run
@@ -56,7 +57,7 @@ typedef enum {
   STR_E_ARG = 1,       /* invalid argument (NULL pointer, bad mode, capacity too small) */
   STR_E_SHAPE = 2,     /* shape mismatch */
   STR_E_PRECOND = 3,   /* rSTR with m < max_n R_nR_{n+1}, I_1 % world_size != 0 */
-  STR_E_NUMERIC = 4,   /* Cholesky of Q_n (or the sketched temporal Gram) failed */
+  STR_E_NUMERIC = 4,   /* SPD inversion of Q_n (or of a temporal Gram) met a non-positive pivot */
   STR_E_CUDA = 5,      /* CUDA runtime error */
   STR_E_NCCL = 6,      /* NCCL error (multi-GPU) */
   STR_E_OOM = 7,       /* device allocation failed */
