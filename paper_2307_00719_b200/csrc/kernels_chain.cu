@@ -626,6 +626,10 @@ __host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
 template <bool AL16, bool TA>
 __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restrict__ A, const double *__restrict__ B,
                                                          double *__restrict__ C, int M, int N, int K, QEpi q) {
+  // programmatic dependent launch (when launched with the PDL attribute): let the next kernel of
+  // the stream start scheduling now, and wait for the previous one's results before reading
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   extern __shared__ __align__(16) double gsm[];
   const int Ka = TA ? 0 : gemm_ka(K), K4 = (K + 3) / 4 * 4;
   double *As = gsm;                 // [16][Ka], or TA: [K4][kGbS]
@@ -770,6 +774,10 @@ __global__ void k_fit_perm_tr(const double *__restrict__ TR, int Ra, int Rb, int
 }
 
 // ||X - TL TR^T||^2 and ||X||^2 of tn slices on the fragment GEMM with the fit epilogue.
+template <bool AL16, bool TA>
+static void launch_dmma_pdl(dim3 gd, size_t smd, cudaStream_t s, const double *A, const double *B, double *C, int M,
+                            int N, int K, QEpi q);
+
 int launch_fit_gemm(const void *X, bool x_is_f64, const double *TLf, const double *TR, int Ra, int Rb, int64_t L,
                     int64_t Rr, int64_t tn, double *TRp, double2 *partials, double *acc2, cudaStream_t s) {
   prepare_kernel_attrs();
@@ -786,13 +794,34 @@ int launch_fit_gemm(const void *X, bool x_is_f64, const double *TLf, const doubl
   const size_t smd = gemm_dmma_smem(W);
   const bool al16 = (W % 2 == 0) && (N % 2 == 0);
   if (al16)
-    k_chain_gemm_dmma<true, false><<<gd, 256, smd, s>>>(TLf, TRp, nullptr, M, N, W, q);
+    launch_dmma_pdl<true, false>(gd, smd, s, TLf, TRp, nullptr, M, N, W, q);
   else
-    k_chain_gemm_dmma<false, false><<<gd, 256, smd, s>>>(TLf, TRp, nullptr, M, N, W, q);
+    launch_dmma_pdl<false, false>(gd, smd, s, TLf, TRp, nullptr, M, N, W, q);
   launch_fit_reduce(partials, (int64_t)gd.x * gd.y, acc2, s);
   return 3;
 }
 size_t fit_gemm_partials(int64_t L, int64_t Rr, int64_t tn) { return (size_t)cdiv(Rr, 16) * cdiv(L * tn, 16); }
+
+// k_chain_gemm_dmma with the programmatic-stream-serialization attribute (PDL; STR_PDL=0 disables)
+template <bool AL16, bool TA>
+static void launch_dmma_pdl(dim3 gd, size_t smd, cudaStream_t s, const double *A, const double *B, double *C, int M,
+                            int N, int K, QEpi q) {
+  static const bool on = [] {
+    const char *e = getenv("STR_PDL");
+    return !(e && e[0] == '0');
+  }();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = gd;
+  cfg.blockDim = dim3(256);
+  cfg.dynamicSmemBytes = smd;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, k_chain_gemm_dmma<AL16, TA>, A, B, C, M, N, K, q);
+}
 
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
   if (g_dbg_skip & 16) return;
@@ -803,9 +832,9 @@ void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N
     dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
     const size_t smd = gemm_dmma_smem(K);
     if (al16)
-      k_chain_gemm_dmma<true, false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+      launch_dmma_pdl<true, false>(gd, smd, s, A, B, C, M, N, K, q);
     else
-      k_chain_gemm_dmma<false, false><<<gd, 256, smd, s>>>(A, B, C, M, N, K, q);
+      launch_dmma_pdl<false, false>(gd, smd, s, A, B, C, M, N, K, q);
     return;
   }
   const size_t sm = (size_t)2 * K * 32 * sizeof(double);
@@ -871,9 +900,9 @@ void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int 
     dim3 gd((unsigned)cdiv(S, 16), (unsigned)cdiv(S, 16));
     const QEpi q{Zm, Ra, Rb, 3};
     if (S % 2 == 0 && (uintptr_t)G % 16 == 0)
-      k_chain_gemm_dmma<true, true><<<gd, 256, smd, s>>>(G, G, nullptr, S, S, (int)I, q);
+      launch_dmma_pdl<true, true>(gd, smd, s, G, G, nullptr, S, S, (int)I, q);
     else
-      k_chain_gemm_dmma<false, true><<<gd, 256, smd, s>>>(G, G, nullptr, S, S, (int)I, q);
+      launch_dmma_pdl<false, true>(gd, smd, s, G, G, nullptr, S, S, (int)I, q);
     return;
   }
   const int n = Ra * Ra * Rb * Rb;
