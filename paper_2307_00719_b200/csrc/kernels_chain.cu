@@ -19,6 +19,42 @@
 
 namespace strb200 {
 
+// Launch with the programmatic-stream-serialization attribute (programmatic dependent launch): the
+// kernel may start while its predecessor in the stream finishes; kernels launched this way begin
+// with griddepcontrol.launch_dependents + griddepcontrol.wait (PDL_PROLOGUE) before touching
+// memory.  STR_PDL=<mask> selects the kernel classes (0: none).
+#define PDL_PROLOGUE()                                              \
+  do {                                                              \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+  } while (0)
+// Kernel classes for the PDL mask (STR_PDL = bitmask; default kPdlDefault)
+constexpr int kPdlDmma = 1, kPdlAbsorb = 2, kPdlInv = 4;
+constexpr int kPdlDefault = kPdlDmma | kPdlInv;   // measured: PDL on the absorbs slows C5 (their early CTAs crowd the passes)
+static int pdl_mask() {
+  static const int m = [] {
+    const char *e = getenv("STR_PDL");
+    return e ? atoi(e) : kPdlDefault;
+  }();
+  return m;
+}
+template <typename... KArgs, typename... Args>
+static void pdl_launch(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  const bool on = (pdl_mask() & cls) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
+
 int g_dbg_skip = 0;
 int g_gemm_stage = -1;
 int g_table_v3 = 1;
@@ -301,6 +337,7 @@ constexpr int kInvCDiag = 4;       // diagonal tiles of warp 0 (nt <= 16)
 
 __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1)
     k_spd_inv_cl(const double *__restrict__ Q, int S, double *__restrict__ Qinv, int *info) {
+  PDL_PROLOGUE();
   namespace cg = cooperative_groups;
   cg::cluster_group cl = cg::this_cluster();
   __shared__ __align__(16) double Vb[2][STR_MAXW * kVS];   // pivot panels V (double-buffered)
@@ -493,7 +530,7 @@ void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_
   if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
   if (g_inv_cluster && S <= STR_MAXW && S > 8) {
-    k_spd_inv_cl<<<kInvNC, kInvCThreads, 0, s>>>(Q, S, Qinv, info);
+    pdl_launch(kPdlInv, k_spd_inv_cl, dim3(kInvNC), dim3(kInvCThreads), 0, s, Q, S, Qinv, info);
     return;
   }
   if (S <= 104)
@@ -626,10 +663,7 @@ __host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
 template <bool AL16, bool TA>
 __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restrict__ A, const double *__restrict__ B,
                                                          double *__restrict__ C, int M, int N, int K, QEpi q) {
-  // programmatic dependent launch (when launched with the PDL attribute): let the next kernel of
-  // the stream start scheduling now, and wait for the previous one's results before reading
-  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
-  asm volatile("griddepcontrol.wait;" ::: "memory");
+  PDL_PROLOGUE();
   extern __shared__ __align__(16) double gsm[];
   const int Ka = TA ? 0 : gemm_ka(K), K4 = (K + 3) / 4 * 4;
   double *As = gsm;                 // [16][Ka], or TA: [K4][kGbS]
@@ -806,10 +840,7 @@ size_t fit_gemm_partials(int64_t L, int64_t Rr, int64_t tn) { return (size_t)cdi
 template <bool AL16, bool TA>
 static void launch_dmma_pdl(dim3 gd, size_t smd, cudaStream_t s, const double *A, const double *B, double *C, int M,
                             int N, int K, QEpi q) {
-  static const bool on = [] {
-    const char *e = getenv("STR_PDL");
-    return !(e && e[0] == '0');
-  }();
+  const bool on = (pdl_mask() & kPdlDmma) != 0;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = gd;
   cfg.blockDim = dim3(256);
@@ -1107,6 +1138,7 @@ __global__ void __launch_bounds__(256) k_absorb5(AbsorbDesc ad, const TY *__rest
 template <typename TY, bool LEFT>
 __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
                                                  int accumulate, int before, int I, int nrest, int RB, int ic, int KW) {
+  PDL_PROLOGUE();
   extern __shared__ __align__(16) double asm6[];
   const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
   const int Cb = LEFT ? ad.Q : ad.P;        // free rank carried along the large dimension
@@ -1242,9 +1274,11 @@ static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int a
   if (smem > 160 * 1024) return false;
   const unsigned grid = (unsigned)cdiv(nrest, RB);
   if (left)
-    k_absorb6<TY, true><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic, KW);
+    pdl_launch(kPdlAbsorb, k_absorb6<TY, true>, grid, dim3(threads), smem, s, ad, Y, out, accumulate, (int)before, (int)I, (int)nrest,
+               RB, ic, KW);
   else
-    k_absorb6<TY, false><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic, KW);
+    pdl_launch(kPdlAbsorb, k_absorb6<TY, false>, grid, dim3(threads), smem, s, ad, Y, out, accumulate, (int)before, (int)I,
+               (int)nrest, RB, ic, KW);
   return true;
 }
 
