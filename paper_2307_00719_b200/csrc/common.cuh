@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <cstdlib>
 #include <stdint.h>
 
 #ifndef __CUDA_ARCH__
@@ -69,5 +70,41 @@ struct QEpi {
 };
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Launch with the programmatic-stream-serialization attribute (programmatic dependent launch): the
+// kernel may start while its predecessor in the stream finishes; kernels launched this way begin
+// with griddepcontrol.launch_dependents + griddepcontrol.wait (PDL_PROLOGUE) before touching
+// memory.  STR_PDL=<mask> selects the kernel classes (0: none).
+#define PDL_PROLOGUE()                                              \
+  do {                                                              \
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
+    asm volatile("griddepcontrol.wait;" ::: "memory");              \
+  } while (0)
+// Kernel classes for the PDL mask (STR_PDL = bitmask; default kPdlDefault)
+constexpr int kPdlDmma = 1, kPdlAbsorb = 2, kPdlInv = 4, kPdlRstr = 8;
+constexpr int kPdlDefault = kPdlDmma | kPdlInv | kPdlRstr;   // measured: PDL on the absorbs slows C5 (their early CTAs crowd the passes)
+static int pdl_mask() {
+  static const int m = [] {
+    const char *e = getenv("STR_PDL");
+    return e ? atoi(e) : kPdlDefault;
+  }();
+  return m;
+}
+template <typename... KArgs, typename... Args>
+static void pdl_launch(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args... args) {
+  const bool on = (pdl_mask() & cls) != 0;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = on ? 1 : 0;
+  cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
+}
 
 }  // namespace strb200

@@ -19,41 +19,7 @@
 
 namespace strb200 {
 
-// Launch with the programmatic-stream-serialization attribute (programmatic dependent launch): the
-// kernel may start while its predecessor in the stream finishes; kernels launched this way begin
-// with griddepcontrol.launch_dependents + griddepcontrol.wait (PDL_PROLOGUE) before touching
-// memory.  STR_PDL=<mask> selects the kernel classes (0: none).
-#define PDL_PROLOGUE()                                              \
-  do {                                                              \
-    asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); \
-    asm volatile("griddepcontrol.wait;" ::: "memory");              \
-  } while (0)
-// Kernel classes for the PDL mask (STR_PDL = bitmask; default kPdlDefault)
-constexpr int kPdlDmma = 1, kPdlAbsorb = 2, kPdlInv = 4;
-constexpr int kPdlDefault = kPdlDmma | kPdlInv;   // measured: PDL on the absorbs slows C5 (their early CTAs crowd the passes)
-static int pdl_mask() {
-  static const int m = [] {
-    const char *e = getenv("STR_PDL");
-    return e ? atoi(e) : kPdlDefault;
-  }();
-  return m;
-}
-template <typename... KArgs, typename... Args>
-static void pdl_launch(int cls, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
-                       Args... args) {
-  const bool on = (pdl_mask() & cls) != 0;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = grid;
-  cfg.blockDim = block;
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = on ? 1 : 0;
-  cudaLaunchKernelEx(&cfg, kern, ((KArgs)args)...);
-}
+
 
 int g_dbg_skip = 0;
 int g_gemm_stage = -1;
@@ -1720,6 +1686,7 @@ constexpr int kSkKC = 32;
 __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, int64_t sai, int64_t sak,
                                                  const double *__restrict__ B, int64_t sbk, int64_t sbj, int M, int N,
                                                  int64_t K, int64_t kper, double *__restrict__ part) {
+  PDL_PROLOGUE();
   // two chunk buffers: the cp.async of chunk c+1 is in flight while chunk c is multiplied
   __shared__ __align__(16) double As[2][kSkKC][34], Bs[2][kSkKC][32];   // As rows padded (transposed loads)
   const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
@@ -1775,6 +1742,7 @@ __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, i
 // to the increment (equal to symmetrizing the sum when C is symmetric).
 __global__ void k_reduce_sk(const double *__restrict__ part, int KS, int64_t n, int N, double *__restrict__ C, int acc,
                             int sym) {
+  PDL_PROLOGUE();
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
   // all partials are loaded before the (fixed-order) sums, so the loads overlap
@@ -1810,9 +1778,10 @@ int launch_gemm_sk(const double *A, int64_t sai, int64_t sak, const double *B, i
   const int64_t kper = cdiv(cdiv(K, KS), kSkKC) * kSkKC;
   KS = (int)cdiv(K, kper);
   dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32), (unsigned)KS);
-  k_gemm_sk<<<grid, 256, 0, s>>>(A, sai, sak, B, sbk, sbj, M, N, K, kper, ws);
+  pdl_launch(kPdlRstr, k_gemm_sk, grid, dim3(256), 0, s, A, sai, sak, B, sbk, sbj, M, N, K, kper, ws);
   const int64_t n = (int64_t)M * N;
-  k_reduce_sk<<<(unsigned)cdiv(n, 256), 256, 0, s>>>(ws, KS, n, N, C, acc, sym);
+  pdl_launch(kPdlRstr, k_reduce_sk, dim3((unsigned)cdiv(n, 256)), dim3(256), 0, s, (const double *)ws, KS, n, N, C, acc,
+             sym);
   return 2;
 }
 

@@ -34,6 +34,7 @@ namespace strb200 {
 // out[s][c] = G[idx[s]][c]  (rows of a G(2) matrix with S columns)
 __global__ void k_gather_rows(const double *__restrict__ G, int S, const int32_t *__restrict__ idx, int64_t m,
                               double *__restrict__ out) {
+  PDL_PROLOGUE();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m * S) return;
   int64_t s = e / S;
@@ -52,6 +53,7 @@ struct GatherDesc {
 template <typename T>
 __global__ void k_gather_fibers(const void *const *__restrict__ Xp, const int32_t *__restrict__ idx, GatherDesc gd,
                                 double *__restrict__ XS) {
+  PDL_PROLOGUE();
   int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= gd.In * gd.m) return;
   const T *__restrict__ X = (const T *)*Xp;   // the batch, through the device slot set_x fills
@@ -88,6 +90,7 @@ __global__ void k_tau_advance(int64_t *tau) { *tau += 1; }
 __global__ void k_draw_gather_uniform(uint64_t seed, const int64_t *__restrict__ tau, int k, int N, int64_t I,
                                       int64_t m, const double *__restrict__ G, int S, int32_t *__restrict__ idx,
                                       double *__restrict__ out) {
+  PDL_PROLOGUE();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (e >= m * S) return;
   const int64_t s = e / S;
@@ -356,8 +359,8 @@ static str_status draw_mode_dev(str_state *h, int k, const double *rows, int64_t
   double *dstu = (k == h->N) ? (double *)h->sG.p : (double *)mbu.samp.p;
   if (h->variant == STR_SAMPLE_UNIFORM) {   // draw + gather in one kernel
     h->idx_dev[k] = true;
-    k_draw_gather_uniform<<<(unsigned)cdiv(h->m * S, 256), 256, 0, h->st>>>(h->seed, tau, k, h->N, I, h->m, rows, S,
-                                                                             dix, dstu);
+    pdl_launch(kPdlRstr, k_draw_gather_uniform, dim3((unsigned)cdiv(h->m * S, 256)), dim3(256), 0, h->st, h->seed, tau,
+               k, h->N, I, h->m, rows, S, dix, dstu);
     tl_mark(h, "draw_gather");
     return STR_OK;
   }
@@ -496,9 +499,11 @@ static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, 
   gd.m = h->m;
   const unsigned grid = (unsigned)cdiv(gd.In * gd.m, 256);
   if (h->dtype == STR_F64)
-    k_gather_fibers<double><<<grid, 256, 0, h->st>>>((const void *const *)h->dX.p, (const int32_t *)h->sIdxDev.p, gd, XS);
+    pdl_launch(kPdlRstr, k_gather_fibers<double>, dim3(grid), dim3(256), 0, h->st, (const void *const *)h->dX.p,
+               (const int32_t *)h->sIdxDev.p, gd, XS);
   else
-    k_gather_fibers<float><<<grid, 256, 0, h->st>>>((const void *const *)h->dX.p, (const int32_t *)h->sIdxDev.p, gd, XS);
+    pdl_launch(kPdlRstr, k_gather_fibers<float>, dim3(grid), dim3(256), 0, h->st, (const void *const *)h->dX.p,
+               (const int32_t *)h->sIdxDev.p, gd, XS);
   tl_mark(h, "gather_fibers");
   return STR_OK;
 }
