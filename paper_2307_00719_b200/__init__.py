@@ -34,15 +34,19 @@ _DTYPES = {"f32": STR_F32, "f64": STR_F64}
 
 
 class Handle:
-    """Owns a ``str_state*`` and the host-side config arrays it was created from."""
+    """Owns a ``str_state*``, the host-side config arrays it was created from and the CUDA stream
+    the library enqueues on (a torch stream object, so that device buffers handed to the library
+    can be recorded on it: the caching allocator then keeps them alive until the enqueued work
+    that reads them has finished — include/str.h's lifetime rule for X)."""
 
-    def __init__(self, ptr, N, dims, ranks, dtype, keep):
+    def __init__(self, ptr, N, dims, ranks, dtype, keep, stream=None):
         self.ptr = ptr
         self.N = N
         self.dims = tuple(dims)
         self.ranks = tuple(ranks)
         self.dtype = dtype
         self._keep = keep
+        self.stream = stream
 
     def __del__(self):
         try:
@@ -69,6 +73,19 @@ def _dev_ptr(x, expect_numel: int, dtype: str) -> int:
     return x.data_ptr()
 
 
+def _enter(h: Optional[Handle], x, stream=None):
+    """Orders the library stream after the caller's current stream (which produced x) and records
+    x on the library stream (argument marshalling only: no data is touched)."""
+    import torch
+    st = stream if stream is not None else h.stream
+    if st is None:
+        return
+    cur = torch.cuda.current_stream(x.device)
+    if cur.cuda_stream != st.cuda_stream:
+        st.wait_stream(cur)
+    x.record_stream(st)
+
+
 def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_init: int,
              init_cores: Sequence[np.ndarray], *, dtype: str = "f32", contract: str = "3xtf32",
              variant: str = "det", sketch_rows: int = 0, seed: int = 0, t_capacity: int = 0, split_k: int = 0,
@@ -80,8 +97,10 @@ def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_in
     N = int(order)
     dims_a = (C.c_int64 * (N - 1))(*[int(d) for d in dims])
     ranks_a = (C.c_int32 * N)(*[int(r) for r in ranks])
-    if stream is None:
-        stream = torch.cuda.current_stream(device).cuda_stream
+    # the library's stream: the caller's (wrapped so buffers can be recorded on it) or a dedicated
+    # stream of this handle
+    tstream = (torch.cuda.Stream(device) if not stream else torch.cuda.ExternalStream(int(stream), device=device))
+    stream = tstream.cuda_stream
     nid = None
     if nccl_id is not None:
         nid = C.create_string_buffer(bytes(nccl_id), len(nccl_id))
@@ -93,11 +112,12 @@ def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_in
     local = [int(d) for d in dims]
     local[0] //= int(world_size)
     xptr = _dev_ptr(X_init, int(np.prod(local)) * int(t_init), dtype)
+    _enter(None, X_init, tstream)
     cores = [np.ascontiguousarray(np.asarray(G, dtype=np.float64).reshape(-1, order="F")) for G in init_cores]
     arr = (C.POINTER(C.c_double) * N)(*[c.ctypes.data_as(C.POINTER(C.c_double)) for c in cores])
     out = C.c_void_p()
     st = _lib.lib.str_init(C.byref(cfg), C.c_void_p(xptr), int(t_init), arr, C.byref(out))
-    h = Handle(out, N, dims, ranks, dtype, keep=(dims_a, ranks_a, nid))
+    h = Handle(out, N, dims, ranks, dtype, keep=(dims_a, ranks_a, nid), stream=tstream)
     if st != 0:
         msg = _lib.lib.str_error_string(out).decode() if out.value else ""
         if out.value:
@@ -114,6 +134,7 @@ def str_update_batch(h: Handle, X_new, t_new: Optional[int] = None) -> None:
     if t_new is None:
         t_new = X_new.numel() // h.local_slice
     ptr = _dev_ptr(X_new, h.local_slice * int(t_new), h.dtype)
+    _enter(h, X_new)
     _check(h, _lib.lib.str_update_batch(h.ptr, C.c_void_p(ptr), int(t_new)))
 
 
@@ -150,6 +171,7 @@ def str_get_temporal_rows(h: Handle, t0: int, t: int) -> np.ndarray:
 
 def str_fit(h: Handle, X, t0: int, t: int) -> float:
     ptr = _dev_ptr(X, h.local_slice * int(t), h.dtype)
+    _enter(h, X)
     v = C.c_double()
     _check(h, _lib.lib.str_fit(h.ptr, C.c_void_p(ptr), int(t0), int(t), C.byref(v)))
     return v.value
@@ -160,6 +182,7 @@ def str_tr_als(h: Handle, X, t: int, sweeps: int) -> float:
     handle holds, then the streaming state rebuilt from X (device, t slices).  Returns the fit
     ||X - TR(G)|| / ||X|| after the last sweep."""
     ptr = _dev_ptr(X, h.local_slice * int(t), h.dtype)
+    _enter(h, X)
     v = C.c_double()
     _check(h, _lib.lib.str_tr_als(h.ptr, C.c_void_p(ptr), int(t), int(sweeps), C.byref(v)))
     return v.value

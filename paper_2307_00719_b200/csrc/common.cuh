@@ -5,6 +5,9 @@
 #include <cstdlib>
 #include <stdint.h>
 
+#include <mutex>
+#include <utility>
+
 #ifndef __CUDA_ARCH__
 #include <string>
 #endif
@@ -70,6 +73,19 @@ struct QEpi {
 };
 
 __host__ __device__ inline int64_t cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// Function attributes (dynamic shared-memory opt-ins, carve-out preferences) are per device and
+// handles on different devices may be created concurrently: run the setup once per device ordinal.
+constexpr int kMaxDevices = 64;
+struct PerDeviceOnce {
+  std::once_flag f[kMaxDevices];
+};
+template <class F>
+inline void once_per_device(PerDeviceOnce &o, F &&fn) {
+  int d = 0;
+  if (cudaGetDevice(&d) != cudaSuccess || d < 0 || d >= kMaxDevices) d = 0;
+  std::call_once(o.f[d], std::forward<F>(fn));
+}
 
 // Launch with the programmatic-stream-serialization attribute (programmatic dependent launch): the
 // kernel may start while its predecessor in the stream finishes; kernels launched this way begin

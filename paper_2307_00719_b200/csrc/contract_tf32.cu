@@ -524,24 +524,24 @@ str_status tf32_prepare(str_state *h) {
              "multiple of 4 (16-byte TMA row stride); use STR_CONTRACT_F64 or another split_k";
     return STR_E_ARG;
   }
-  if (!g_encode) {
+  static std::once_flag enc_once;
+  std::call_once(enc_once, [] {
     cudaDriverEntryPointQueryResult q;
     void *fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
-        q != cudaDriverEntryPointSuccess || !fn)
-      return tf_fail(h, "cuTensorMapEncodeTiled unavailable");
-    g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
-  }
-  static bool attr = false;
-  if (!attr) {
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess && fn)
+      g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+  });
+  if (!g_encode) return tf_fail(h, "cuTensorMapEncodeTiled unavailable");
+  static PerDeviceOnce attr_once;
+  once_per_device(attr_once, [&] {
     cudaFuncSetAttribute(k_contract_tf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     cudaFuncSetAttribute(k_contract_tf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
     prefer_max_smem(k_contract_tf32<1>);
     prefer_max_smem(k_zero_f32);
     prefer_max_smem(k_contract_tf32<2>);
     // (Npad <= 128 keeps 2 Npad x 128 B of table per stage; 3 stages fit)
-    attr = true;
-  }
+  });
   h->tf32_ready = true;
   return STR_OK;
 }
@@ -558,7 +558,10 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
   size_t yf = ((size_t)std::max<int64_t>(h->L * tn, h->Rr) * W * sizeof(float) + 15) / 16 * 16;
   auto grow = [&](DevBuf &b, size_t bytes) -> bool {
     if (b.bytes >= bytes) return true;
-    if (b.p) cudaFree(b.p);
+    if (b.p) {   // captured graphs may hold the old pointer
+      h->reset_graphs();
+      cudaFree(b.p);
+    }
     b.p = nullptr;
     b.bytes = 0;
     if (cudaMalloc(&b.p, bytes) != cudaSuccess) return false;
@@ -612,15 +615,16 @@ static bool encode_y_map(str_state *h, CUtensorMap *ymap, float *Y, int pass, in
 str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn) {
   CUtensorMap tmap, ymap;
   if (!encode_x_map(h, &tmap, X, pass, tn)) return STR_E_CUDA;
-  memcpy(&ymap, h->tf_ymap[pass - 1], sizeof(CUtensorMap));
+  const str_state::GraphSlot &g = h->gs[slot];
+  memcpy(&ymap, g.tf_ymap[pass - 1], sizeof(CUtensorMap));
   TcParams p;
-  memcpy(&p, h->tf_params[pass - 1], sizeof(TcParams));
+  memcpy(&p, g.tf_params[pass - 1], sizeof(TcParams));
   void *args[3] = {&tmap, &ymap, &p};
   cudaKernelNodeParams kp = {};
   kp.func = pass == 1 ? (void *)k_contract_tf32<1> : (void *)k_contract_tf32<2>;
-  kp.gridDim = dim3(h->tf_grid[pass - 1]);
+  kp.gridDim = dim3(g.tf_grid[pass - 1]);
   kp.blockDim = dim3(kTcThreads);
-  kp.sharedMemBytes = (unsigned)h->tf_smem[pass - 1];
+  kp.sharedMemBytes = (unsigned)g.tf_smem[pass - 1];
   kp.kernelParams = args;
   kp.extra = nullptr;
   cudaError_t e = cudaGraphExecKernelNodeSetParams(h->gs[slot].exec, h->gs[slot].tf[pass - 1], &kp);
@@ -664,9 +668,8 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.U = blocks * p.KT;
   // persistent grid: every SM but the kInvNC that the side stream's cluster inverse occupies while
   // a pass runs (a pass CTA waiting for such an SM would hold the whole pass back)
-  static int nsm = 0;
-  if (!nsm && cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->device) != cudaSuccess) nsm = 148;
-  int maxg = std::max(1, nsm - (g_inv_cluster ? kInvClusterCTAs : 0));
+  const int nsm = h->nsm;
+  int maxg = std::max(1, nsm - kInvClusterCTAs);
   if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(nsm, atoi(ev)));   // tuning knob
   int grid = (int)std::min<int64_t>(maxg, p.U);
   p.upc = cdiv(p.U, grid);
@@ -676,10 +679,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.dbg = h->tf_dbg ? h->tf_dbg + (pass - 1) * str_state::kTfDbgWords : nullptr;
   p.dbg_flags = 0;
   if (g_dbg_skip & 4) p.U = 0;   // what-if diagnostic: every CTA exits at once
-  if (h->tf_dbg) {
+#ifdef STR_DIAG
+  if (h->tf_dbg) {   // pipeline what-if flags (wrong results; tools/gpu_flags2.sh, diagnostic builds only)
     const char *ev = getenv("STR_TF_DBGFLAGS");
     if (ev) p.dbg_flags = atoi(ev);
   }
+#endif
   CUtensorMap ymap;
   memset(&ymap, 0, sizeof(ymap));
   if (p.yred && !encode_y_map(h, &ymap, Y, pass, W, tn)) return -1;
@@ -705,12 +710,13 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
       h->err = "cannot locate the captured contraction node";
       return -1;
     }
-    h->gs[h->cur_slot].tf[pass - 1] = deps[0];
-    static_assert(sizeof(TcParams) <= sizeof(h->tf_params[0]), "TcParams too large");
-    memcpy(h->tf_params[pass - 1], &p, sizeof(TcParams));
-    memcpy(h->tf_ymap[pass - 1], &ymap, sizeof(CUtensorMap));
-    h->tf_grid[pass - 1] = grid;
-    h->tf_smem[pass - 1] = smem;
+    str_state::GraphSlot &g = h->gs[h->cur_slot];
+    g.tf[pass - 1] = deps[0];
+    static_assert(sizeof(TcParams) <= sizeof(g.tf_params[0]), "TcParams too large");
+    memcpy(g.tf_params[pass - 1], &p, sizeof(TcParams));
+    memcpy(g.tf_ymap[pass - 1], &ymap, sizeof(CUtensorMap));
+    g.tf_grid[pass - 1] = grid;
+    g.tf_smem[pass - 1] = smem;
   }
   tl_mark(h, pass == 1 ? "contract_tf32_p1" : "contract_tf32_p2");
   prof_mark(h, 2 * (pass - 1) + 1);

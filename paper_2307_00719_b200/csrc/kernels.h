@@ -8,28 +8,20 @@
 
 namespace strb200 {
 
-// Diagnostic what-if knob (STR_DBG_SKIP, read at str_init; 0 in production): launchers whose bit
-// is set enqueue nothing, so a timing run shows how much of the step each kernel class holds.
-// Results are meaningless while it is non-zero.  1 spd_inv, 2 tables, 4 contraction, 8 absorbs,
-// 16 chain GEMMs, 32 row GEMMs, 64 Z Grams.
+// Diagnostic what-if knob, compiled in only with -DSTR_DIAG (tools/gpu_whatif.sh builds such a
+// library; STR_DBG_SKIP is read at str_init): launchers whose bit is set enqueue nothing, so a
+// timing run shows how much of the step each kernel class holds.  Results are meaningless while
+// it is non-zero.  1 spd_inv, 2 tables, 4 contraction, 8 absorbs, 16 chain GEMMs, 32 row GEMMs,
+// 64 Z Grams.  Release builds: the constant 0 (every skip test folds away).
+#ifdef STR_DIAG
 extern int g_dbg_skip;
-extern int g_gemm_stage;
-extern int g_absorb_v5;
-extern int g_absorb_cps;
-extern int g_table_v3;
-extern int g_inv_cluster;
+#else
+constexpr int g_dbg_skip = 0;
+#endif
 constexpr int kInvClusterCTAs = 4;   // CTAs of the cluster inverse (k_spd_inv_cl)
 
-// kernels_small.cu
-void launch_build_table(const FactorList &fl, int64_t E, double *out, cudaStream_t s);
-void launch_absorb(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);
-void launch_gram_z(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
-void launch_dgemm(const double *A, const double *B, double *C, int M, int N, int K, cudaStream_t s);
-void launch_q_accum(const double *Hm, int Rn, int Rn1, double *Q, int accumulate, cudaStream_t s);
-void launch_axpy(const double *x, double *y, int64_t n, cudaStream_t s);
-void launch_set_identity(double *A, int n, cudaStream_t s);
-
 // kernels_chain.cu
+void launch_set_identity(double *A, int n, cudaStream_t s);
 void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s);
 void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s);
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s);

@@ -21,12 +21,10 @@ namespace strb200 {
 
 
 
+#ifdef STR_DIAG
 int g_dbg_skip = 0;
-int g_gemm_stage = -1;
-int g_table_v3 = 1;
-int g_inv_cluster = 1;    // diagnostic switch: 0 keeps the single-CTA inverse       // diagnostic switch: 0 keeps the generic table kernel
-int g_absorb_v5 = 1;
-int g_absorb_cps = 3;     // target absorb CTAs per SM (several CTAs overlap staging with compute)      // diagnostic switch: 1 k_absorb6 (tensor-core fragments), 2 k_absorb5, 0 k_absorb4   // diagnostic override of the chain-GEMM staging mode (-1: automatic)
+#endif
+constexpr int kAbsorbCps = 3;   // target absorb CTAs per SM (several CTAs overlap staging with compute)
 
 void prepare_kernel_attrs();
 
@@ -495,7 +493,7 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
 void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {
   if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
-  if (g_inv_cluster && S <= STR_MAXW && S > 8) {
+  if (S <= STR_MAXW && S > 8) {
     pdl_launch(kPdlInv, k_spd_inv_cl, dim3(kInvNC), dim3(kInvCThreads), 0, s, Q, S, Qinv, info);
     return;
   }
@@ -506,115 +504,12 @@ void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_
 }
 
 // ------------------------------------------------------------------------------------------
-// C = A (M x K) B (K x N), row-major fp64, K <= 256: one 32x32 output tile per CTA with the whole
-// A row block and B column block staged in shared memory by cp.async (every load in flight at
-// once; these small products are latency-bound).  Thread (tx, ty) owns rows 4ty..4ty+3 of
-// column tx; A is stored k-major so a thread's 4 rows are two 16-byte broadcast loads.
-// Epilogue (q.mode): 0 store C; 1 Q = H_<2>; 2 Q += H_<2>, where C is the chain matrix Hm
-// (rows (i1 + Rn r1), columns (i2 + Rn1 r2)) and H_<2>[i1 + Rn i2][r1 + Rn r2] = Hm[..][..]
-// (Def. 1 P:126 applied to the chain result).  Q is left unsymmetrized; k_spd_inv symmetrizes.
-// Used for the Gram-chain links and for G = P Q^{-1} (M = I rows).
-
+// 16-byte cp.async (16-byte aligned source and destination)
 __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
                : "memory");
 }
 
-// STAGE 0: 8-byte cp.async; 1: 16-byte cp.async (16-byte aligned rows); 2: cp.async.bulk row copies
-template <int STAGE>
-__global__ void __launch_bounds__(256) k_chain_gemm(const double *__restrict__ A, const double *__restrict__ B,
-                                                    double *__restrict__ C, int M, int N, int K, QEpi q) {
-  extern __shared__ __align__(16) double gsm[];
-  // BULK: A rows [32][K] and B rows [K][32] arrive by cp.async.bulk row copies (16-byte aligned rows);
-  // otherwise by 8-byte cp.async.  A is read row-major (4 broadcast loads per k), B per lane.
-  double *As = gsm;             // [32][K]
-  double *Bs = gsm + 32 * K;    // [K][32]
-  __shared__ __align__(8) uint64_t bar;
-  const int tx = threadIdx.x & 31, ty = threadIdx.x >> 5;
-  const int row0 = blockIdx.y * 32, col0 = blockIdx.x * 32;
-  const int mr = min(32, M - row0), nc = min(32, N - col0);
-  if (STAGE == 2) {
-    if (threadIdx.x == 0) {
-      tc::mbar_init(&bar, 1);
-      tc::fence_barrier_init();
-    }
-    // zero what no copy writes (rows of A beyond M, columns of B beyond N)
-    for (int e = threadIdx.x; e < (32 - mr) * K; e += 256) As[mr * K + e] = 0.0;
-    if (nc < 32)
-      for (int e = threadIdx.x; e < K * (32 - nc); e += 256) Bs[(e / (32 - nc)) * 32 + nc + e % (32 - nc)] = 0.0;
-    __syncthreads();
-    if (threadIdx.x < 32) {
-      if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&bar, (uint32_t)((mr * K + K * nc) * 8));
-      __syncwarp();
-      for (int r = threadIdx.x; r < mr; r += 32)
-        tc::bulk_load(As + r * K, A + (int64_t)(row0 + r) * K, (uint32_t)(K * 8), &bar);
-      for (int k = threadIdx.x; k < K; k += 32)
-        tc::bulk_load(Bs + k * 32, B + (int64_t)k * N + col0, (uint32_t)(nc * 8), &bar);
-    }
-    tc::mbar_wait(&bar, 0);
-  } else if (STAGE == 1) {
-    const int K2 = K >> 1;   // 16-byte chunks per A row
-    for (int e = threadIdx.x; e < 32 * K2; e += 256) {
-      const int r = e / K2;
-      if (r < mr) cp_async16(As + 2 * e, A + (int64_t)row0 * K + 2 * e);
-      else *(double2 *)(As + 2 * e) = make_double2(0.0, 0.0);
-    }
-    for (int e = threadIdx.x; e < 16 * K; e += 256) {
-      const int kk = e >> 4, c = 2 * (e & 15);
-      if (c < nc) cp_async16(Bs + kk * 32 + c, B + (int64_t)kk * N + col0 + c);
-      else *(double2 *)(Bs + kk * 32 + c) = make_double2(0.0, 0.0);
-    }
-    cp_async_wait_all();
-    __syncthreads();
-  } else {
-    for (int e = threadIdx.x; e < 32 * K; e += 256) {
-      const int r = e / K;
-      if (r < mr) cp_async8(As + e, A + (int64_t)row0 * K + e);
-      else As[e] = 0.0;
-    }
-    for (int e = threadIdx.x; e < 32 * K; e += 256) {
-      const int k = e >> 5, c = e & 31;
-      if (c < nc) cp_async8(Bs + k * 32 + c, B + (int64_t)k * N + col0 + c);
-      else Bs[k * 32 + c] = 0.0;
-    }
-    cp_async_wait_all();
-    __syncthreads();
-  }
-  // two interleaved k-halves (even / odd k): eight independent FMA chains of length K/2
-  double acc[4] = {0.0, 0.0, 0.0, 0.0}, acd[4] = {0.0, 0.0, 0.0, 0.0};
-  const double *a0 = As + (4 * ty) * K;
-  int k = 0;
-#pragma unroll 2
-  for (; k + 1 < K; k += 2) {
-    const double b = Bs[k * 32 + tx], b1 = Bs[(k + 1) * 32 + tx];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      acc[u] = fma(a0[u * K + k], b, acc[u]);
-      acd[u] = fma(a0[u * K + k + 1], b1, acd[u]);
-    }
-  }
-  if (k < K) {
-    const double b = Bs[k * 32 + tx];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) acc[u] = fma(a0[u * K + k], b, acc[u]);
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u) acc[u] += acd[u];
-#pragma unroll
-  for (int u = 0; u < 4; ++u) {
-    const int row = row0 + 4 * ty + u, col = col0 + tx;
-    if (row < M && col < N) {
-      if (q.mode == 0) {
-        C[(int64_t)row * N + col] = acc[u];
-      } else {
-        const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
-        const int S = q.Rn * q.Rn1;
-        double *dst = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
-        *dst = (q.mode == 1) ? acc[u] : *dst + acc[u];
-      }
-    }
-  }
-}
 
 // C = A B (fp64, row-major) on the FP64 tensor-core fragments (mma.sync m8n8k4): one 16 x 16
 // output tile per CTA (2 x 2 DMMA tiles), 8 warps = 4 tiles x 2 halves of K, so each warp runs one
@@ -823,26 +718,19 @@ static void launch_dmma_pdl(dim3 gd, size_t smd, cudaStream_t s, const double *A
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s) {
   if (g_dbg_skip & 16) return;
   prepare_kernel_attrs();
-  dim3 grid((unsigned)cdiv(N, 32), (unsigned)cdiv(M, 32));
-  const bool al16 = (K % 2 == 0) && (N % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
-  if (g_gemm_stage < 0 || g_gemm_stage == 3) {   // default: FP64 tensor-core fragments
-    dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
-    const size_t smd = gemm_dmma_smem(K);
-    if (al16)
-      launch_dmma_pdl<true, false>(gd, smd, s, A, B, C, M, N, K, q);
-    else
-      launch_dmma_pdl<false, false>(gd, smd, s, A, B, C, M, N, K, q);
+  constexpr int kMaxRows = 65535 * 16;   // gridDim.y limit: taller plain products run in row chunks
+  if (M > kMaxRows && q.mode == 0) {
+    for (int r0 = 0; r0 < M; r0 += kMaxRows)
+      launch_chain_gemm(A + (int64_t)r0 * K, B, C + (int64_t)r0 * N, std::min(kMaxRows, M - r0), N, K, q, s);
     return;
   }
-  const size_t sm = (size_t)2 * K * 32 * sizeof(double);
-  int mode = al16 ? 1 : 0;
-  if (g_gemm_stage >= 0 && (al16 || g_gemm_stage == 0)) mode = g_gemm_stage;
-  if (mode == 2)
-    k_chain_gemm<2><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
-  else if (mode == 1)
-    k_chain_gemm<1><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
+  const bool al16 = (K % 2 == 0) && (N % 2 == 0) && ((uintptr_t)A % 16 == 0) && ((uintptr_t)B % 16 == 0);
+  dim3 gd((unsigned)cdiv(N, 16), (unsigned)cdiv(M, 16));
+  const size_t smd = gemm_dmma_smem(K);
+  if (al16)
+    launch_dmma_pdl<true, false>(gd, smd, s, A, B, C, M, N, K, q);
   else
-    k_chain_gemm<0><<<grid, 256, sm, s>>>(A, B, C, M, N, K, q);
+    launch_dmma_pdl<false, false>(gd, smd, s, A, B, C, M, N, K, q);
 }
 
 void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s) {
@@ -1015,86 +903,6 @@ __global__ void __launch_bounds__(256) k_absorb4(AbsorbDesc ad, const TY *__rest
   }
 }
 
-// Absorb, one thread per output element: CTA = RB consecutive rests x O = Po Qo outputs each.
-// The Y blocks (rest, i) of the CTA (contiguous P x Q entries each) and the slices A(i) are staged in
-// shared memory in chunks of ic contracted indices; every thread runs four interleaved FMA chains
-// over (i, contracted rank).  left: out[u][q] = sum_i sum_p A(i)[u][p] Y(i)[p][q] (A(i)[u][p] at
-// u + Ra p); right: out[p][v] = sum_i sum_q Y(i)[p][q] A(i)[q][v] (A(i)[q][v] at q + Ra v).
-template <typename TY, bool LEFT>
-__global__ void __launch_bounds__(256) k_absorb5(AbsorbDesc ad, const TY *__restrict__ Y, double *__restrict__ out,
-                                                 int accumulate, int before, int I, int nrest, int RB, int ic) {
-  extern __shared__ __align__(16) double asm5[];
-  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
-  const int Po = LEFT ? ad.Ra : ad.P, Qo = LEFT ? ad.Q : ad.Rb, O = Po * Qo;
-  const int C = LEFT ? ad.P : ad.Q;   // contracted rank
-  double *As = asm5;                                       // [ic][AB]
-  TY *Ys = (TY *)(asm5 + ((ic * AB + 1) & ~1));            // [RB][ic][PQ]
-  const int rest0 = blockIdx.x * RB;
-  const int rl = threadIdx.x / O, o = threadIdx.x - rl * O;
-  const int rest = rest0 + rl;
-  const bool act = rl < RB && rest < nrest;
-  const int x = o / Qo, y = o - x * Qo;   // left: (u, q); right: (p, v)
-  double acc[4] = {0.0, 0.0, 0.0, 0.0};
-  __shared__ __align__(8) uint64_t bar;
-  const bool bulk = ((PQ * (int)sizeof(TY)) % 16 == 0) && ((AB * 8) % 16 == 0) && ((uintptr_t)Y % 16 == 0) &&
-                    ((uintptr_t)ad.A % 16 == 0);
-  if (bulk && threadIdx.x == 0) {
-    tc::mbar_init(&bar, 1);
-    tc::fence_barrier_init();
-  }
-  uint32_t ph = 0;
-  const int nr = min(RB, nrest - rest0);
-  for (int i0 = 0; i0 < I; i0 += ic) {
-    const int icn = min(ic, I - i0);
-    __syncthreads();
-    if (bulk) {
-      // one copy for the A chunk, one per (rest, i) block of P x Q entries
-      if (threadIdx.x < 32) {
-        if (threadIdx.x == 0)
-          tc::mbar_arrive_expect_tx(&bar, (uint32_t)(icn * AB * 8 + nr * icn * PQ * (int)sizeof(TY)));
-        __syncwarp();
-        if (threadIdx.x == 0) tc::bulk_load(As, ad.A + (int64_t)i0 * AB, (uint32_t)(icn * AB * 8), &bar);
-        for (int e = threadIdx.x; e < nr * icn; e += 32) {
-          const int r = e / icn, ii = e - r * icn, rr = rest0 + r;
-          const int b0 = rr % before, a0 = rr / before;
-          tc::bulk_load(Ys + (r * ic + ii) * PQ, Y + ((int64_t)b0 + (int64_t)before * (i0 + ii + (int64_t)I * a0)) * PQ,
-                        (uint32_t)(PQ * sizeof(TY)), &bar);
-        }
-      }
-      tc::mbar_wait(&bar, ph);
-      ph ^= 1;
-    } else {
-      for (int e = threadIdx.x; e < icn * AB; e += blockDim.x) cp_async8(As + e, ad.A + (int64_t)i0 * AB + e);
-      for (int e = threadIdx.x; e < nr * icn * PQ; e += blockDim.x) {
-        const int r = e / (icn * PQ), w = e - r * (icn * PQ), ii = w / PQ, el = w - ii * PQ;
-        const int rr = rest0 + r;
-        const int b0 = rr % before, a0 = rr / before;
-        cp_async_el(Ys + (r * ic + ii) * PQ + el, Y + ((int64_t)b0 + (int64_t)before * (i0 + ii + (int64_t)I * a0)) * PQ + el);
-      }
-      cp_async_wait_all();
-      __syncthreads();
-    }
-    if (act) {
-      const TY *yb = Ys + rl * ic * PQ;
-      for (int ii = 0; ii < icn; ++ii) {
-        const double *Ai = As + ii * AB;
-        const TY *Yi = yb + ii * PQ;
-        if (LEFT) {
-#pragma unroll 4
-          for (int c = 0; c < C; ++c) acc[c & 3] = fma(Ai[x + ad.Ra * c], (double)Yi[c * ad.Q + y], acc[c & 3]);
-        } else {
-#pragma unroll 4
-          for (int c = 0; c < C; ++c) acc[c & 3] = fma((double)Yi[x * ad.Q + c], Ai[c + ad.Ra * y], acc[c & 3]);
-        }
-      }
-    }
-  }
-  if (!act) return;
-  const double v = (acc[0] + acc[1]) + (acc[2] + acc[3]);
-  double *dst = out + (int64_t)rest * O + o;
-  *dst = accumulate ? *dst + v : v;
-}
-
 // Absorb on the FP64 tensor-core fragments (mma.sync m8n8k4).  For a CTA of RB rests the absorb is
 // a GEMM whose large dimension stacks (rest, free rank) and whose small dimension is the new rank:
 //   left:  D[u][(r, q)] = sum_{(i, p)} A(i)[u][p] Y(r, i)[p][q]     (M = Ra small, N = RB Q)
@@ -1229,7 +1037,7 @@ static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int a
   if ((PQ * (int)sizeof(TY)) % 16 != 0 || (AB * 8) % 16 != 0 || (uintptr_t)Y % 16 != 0 || (uintptr_t)ad.A % 16 != 0)
     return false;
   // rests per CTA: enough CTAs to cover the GPU, at most 8 big tiles (one warp each)
-  int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / (148 * g_absorb_cps), 64 / std::max(1, Cb)));
+  int RB = (int)std::max<int64_t>(1, std::min<int64_t>(nrest / (148 * kAbsorbCps), 64 / std::max(1, Cb)));
   const int nbt = (RB * Cb + 7) / 8;
   const int KW = (int)std::max<int64_t>(1, std::min<int64_t>(8 / nbt, I));
   const int threads = std::max(32, std::min(256, nbt * KW * 32));
@@ -1245,27 +1053,6 @@ static bool absorb6_launch(const AbsorbDesc &ad, const TY *Y, double *out, int a
   else
     pdl_launch(kPdlAbsorb, k_absorb6<TY, false>, grid, dim3(threads), smem, s, ad, Y, out, accumulate, (int)before, (int)I,
                (int)nrest, RB, ic, KW);
-  return true;
-}
-
-template <typename TY>
-static bool absorb5_launch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest, int64_t before,
-                           int64_t I, cudaStream_t s) {
-  const bool left = ad.left != 0;
-  const int O = (left ? ad.Ra : ad.P) * (left ? ad.Q : ad.Rb);
-  if (O > 256 || nrest >= ((int64_t)1 << 31) || before * I * nrest >= ((int64_t)1 << 40)) return false;
-  const int RB = std::max(1, 256 / O);
-  const int threads = (int)std::min<int64_t>(256, cdiv((int64_t)RB * O, 32) * 32);
-  const int AB = ad.Ra * ad.Rb, PQ = ad.P * ad.Q;
-  const size_t per_i = sizeof(double) * AB + sizeof(TY) * (size_t)RB * PQ;
-  int ic = (int)std::min<int64_t>(I, std::max<int64_t>(1, (96 * 1024) / (int64_t)per_i));
-  const size_t smem = sizeof(double) * (((size_t)ic * AB + 1) & ~1) + sizeof(TY) * (size_t)RB * ic * PQ;
-  if (smem > 160 * 1024) return false;
-  const unsigned grid = (unsigned)cdiv(nrest, RB);
-  if (left)
-    k_absorb5<TY, true><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic);
-  else
-    k_absorb5<TY, false><<<grid, threads, smem, s>>>(ad, Y, out, accumulate, (int)before, (int)I, (int)nrest, RB, ic);
   return true;
 }
 
@@ -1298,8 +1085,9 @@ static void absorb_launch(const AbsorbDesc &ad, const TY *Y, double *out, int ac
 template <typename TY>
 static void absorb_dispatch(const AbsorbDesc &ad, const TY *Y, double *out, int accumulate, int64_t nrest,
                             int64_t before, int64_t I, cudaStream_t s) {
-  if (g_absorb_v5 == 1 && absorb6_launch<TY>(ad, Y, out, accumulate, nrest, before, I, s)) return;
-  if (g_absorb_v5 == 2 && absorb5_launch<TY>(ad, Y, out, accumulate, nrest, before, I, s)) return;
+  // k_absorb6 (FP64 tensor-core fragments) unless the shape or alignment rules it out (e.g. fp32 Y
+  // blocks that are not a whole number of 16-byte chunks); then the register-blocked k_absorb4
+  if (absorb6_launch<TY>(ad, Y, out, accumulate, nrest, before, I, s)) return;
   // MR bounds both the accumulator length (Ra | Rb) and the contracted rank (P | Q)
   const int L = std::max(ad.left ? ad.Ra : ad.Rb, ad.left ? ad.P : ad.Q);
   if (L <= 4)
@@ -1319,10 +1107,6 @@ static void absorb_attrs() {
   cudaFuncSetAttribute(k_absorb6<TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   prefer_max_smem(k_absorb6<TY, true>);
   prefer_max_smem(k_absorb6<TY, false>);
-  cudaFuncSetAttribute(k_absorb5<TY, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  cudaFuncSetAttribute(k_absorb5<TY, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-  prefer_max_smem(k_absorb5<TY, true>);
-  prefer_max_smem(k_absorb5<TY, false>);
   cudaFuncSetAttribute(k_absorb4<TY, 4, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, 4, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
   cudaFuncSetAttribute(k_absorb4<TY, 8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -1637,7 +1421,7 @@ int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaSt
     bool uni = (R == 4 || R == 8 || R == 10 || R == 16);
     for (int f = 0; f < td.fl.n && uni; ++f)
       uni = td.fl.f[f].Ra == R && td.fl.f[f].Rb == R && (uintptr_t)td.fl.f[f].G % 16 == 0;
-    if (uni && g_table_v3) {
+    if (uni) {
       const int th = (int)cdiv(16 * R, 32) * 32;
       if (R == 4) k_build_table3<4><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
       else if (R == 8) k_build_table3<8><<<(unsigned)units, th, smem, s>>>(td, out64, tiles);
@@ -1658,6 +1442,17 @@ int launch_build_table2(const TableDesc &td, double *out64, float *tiles, cudaSt
   else
     k_build_table2<STR_MAXR><<<(unsigned)units, threads, smem, s>>>(td, out64, tiles);
   return 0;
+}
+
+// ------------------------------------------------------------------------------------------
+// A = I (n x n): the identity chain matrix (an empty Gram-chain product).
+__global__ void k_set_identity(double *A, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n * n) A[i] = (i / n == i % n) ? 1.0 : 0.0;
+}
+
+void launch_set_identity(double *A, int n, cudaStream_t s) {
+  k_set_identity<<<(unsigned)cdiv((int64_t)n * n, 256), 256, 0, s>>>(A, n);
 }
 
 // ------------------------------------------------------------------------------------------
@@ -1787,13 +1582,10 @@ int launch_gemm_sk(const double *A, int64_t sai, int64_t sak, const double *B, i
 
 // Dynamic shared-memory opt-ins, done once outside any stream capture.
 void prepare_kernel_attrs() {
-  static bool done = false;
-  if (done) return;
+  static PerDeviceOnce once;
+  once_per_device(once, [] {
   cudaFuncSetAttribute(k_spd_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
   cudaFuncSetAttribute(k_spd_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
-  cudaFuncSetAttribute(k_chain_gemm<0>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
-  cudaFuncSetAttribute(k_chain_gemm<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
-  cudaFuncSetAttribute(k_chain_gemm<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 2 * 256 * 32 * 8);
   cudaFuncSetAttribute(k_chain_gemm_dmma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
   cudaFuncSetAttribute(k_chain_gemm_dmma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
   cudaFuncSetAttribute(k_chain_gemm_dmma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -1818,9 +1610,6 @@ void prepare_kernel_attrs() {
   prefer_max_smem(k_build_table3<16>);
   prefer_max_smem(k_spd_inv<5>);
   prefer_max_smem(k_spd_inv<8>);
-  prefer_max_smem(k_chain_gemm<0>);
-  prefer_max_smem(k_chain_gemm<1>);
-  prefer_max_smem(k_chain_gemm<2>);
   prefer_max_smem(k_gram_z2);
   prefer_max_smem(k_build_table2<4>);
   prefer_max_smem(k_build_table2<8>);
@@ -1831,7 +1620,7 @@ void prepare_kernel_attrs() {
   prefer_max_smem(k_gemm_sk);
   prefer_max_smem(k_reduce_sk);
   prepare_f64_attrs();
-  done = true;
+  });
 }
 
 }  // namespace strb200

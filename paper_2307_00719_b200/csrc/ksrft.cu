@@ -666,8 +666,8 @@ int launch_mix_mode(const void *const *xslot, bool x_f64, void *Xh, bool f64, co
   md.d = d;
   const int64_t tiles = md.nA * cdiv(md.B, md.WB);
   const unsigned grid = (unsigned)tiles;
-  static bool attr = false;   // once, before any capture (the first call comes from the uncaptured init)
-  if (!attr) {
+  static PerDeviceOnce attr_once;   // once, before any capture (the first call comes from the uncaptured init)
+  once_per_device(attr_once, [&] {
     const int mx = 227 * 1024;
     cudaFuncSetAttribute(k_mix_mode<double, double, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_mix_mode<double, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
@@ -675,18 +675,16 @@ int launch_mix_mode(const void *const *xslot, bool x_f64, void *Xh, bool f64, co
     cudaFuncSetAttribute(k_mix_mode<float, float, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_mix_mode<double, double, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
     cudaFuncSetAttribute(k_mix_mode<float, float, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, mx);
-    attr = true;
-  }
+  });
   if (!f64) {   // the fp32 mixing path: compile-time p x q kernels where the factorization is listed
-    static bool pq_attr = false;
-    if (!pq_attr) {
+    static PerDeviceOnce pq_once;
+    once_per_device(pq_once, [&] {
       for (const MixPQEntry &e : kMixPQ) {
         cudaFuncSetAttribute(e.first_f32, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(e.first_f64, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         cudaFuncSetAttribute(e.rest, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
       }
-      pq_attr = true;
-    }
+    });
     for (const MixPQEntry &e : kMixPQ) {
       if (e.p != md.p || e.q != md.q) continue;
       MixPQFn fn = j > 0 ? e.rest : (x_f64 ? e.first_f64 : e.first_f32);
@@ -712,12 +710,11 @@ int launch_mix_sample(const double *G, int64_t I, int S, const int32_t *idx, int
                       double2 *core_ws, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (size_t)I;
   if (smem > 200 * 1024) return -1;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr_once;
+  once_per_device(attr_once, [&] {
     cudaFuncSetAttribute(k_mix_sample, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_mix_core, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  });
   if (core_ws && I <= m) {
     k_mix_core<<<(unsigned)cdiv(I * S, 128), 128, smem, st>>>(G, (int)I, S, d, core_ws);
     k_gather_crows<<<(unsigned)cdiv(m * S, 256), 256, 0, st>>>(core_ws, S, idx, m, out);
@@ -746,11 +743,10 @@ int launch_mix_sample_draw(const double *G, int64_t I, int S, uint64_t seed, con
                            const double *d, double2 *out, double2 *core_ws, int32_t *idx, cudaStream_t st) {
   const size_t smem = sizeof(double2) * (size_t)I;
   if (smem > 200 * 1024 || !core_ws) return -1;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr_once;
+  once_per_device(attr_once, [&] {
     cudaFuncSetAttribute(k_mix_core, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  });
   k_mix_core<<<(unsigned)cdiv(I * S, 128), 128, smem, st>>>(G, (int)I, S, d, core_ws);
   k_draw_gather_crows<<<(unsigned)cdiv(m * S, 256), 256, 0, st>>>(seed, tau, k, N, I, m, core_ws, S, idx, out);
   return 2;
@@ -787,12 +783,11 @@ int launch_gather_unmix(const void *Xh, bool f64, const int64_t *dims, int N, in
   ud.d = d;
   const size_t smem = sizeof(double2) * (size_t)(kUnmixSB + 1) * ud.I;
   if (smem > 200 * 1024) return -1;
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr_once;
+  once_per_device(attr_once, [&] {
     cudaFuncSetAttribute(k_gather_unmix<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     cudaFuncSetAttribute(k_gather_unmix<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  });
   const unsigned grid = (unsigned)cdiv(m, kUnmixSB);
   if (f64) k_gather_unmix<double><<<grid, 128, smem, st>>>((const double2 *)Xh, ud, out);
   else k_gather_unmix<float><<<grid, 128, smem, st>>>((const float2 *)Xh, ud, out);

@@ -1,12 +1,14 @@
 // rstr.cu — randomized streaming TR (rSTR) with uniform (Alg. 7) and
 // leverage-score (Alg. 8) row sampling.
 //
-// Per draw (mode k, time step tau) the host draws m indices with replacement from a SplitMix64
-// stream keyed by (seed, tau, k) (reading R11; the oracle re-implements the same
-// generator independently).  Leverage probabilities p_k(i) = l_i(G_k(2)) / rank (Lemma 1,
-// P:567) are computed on the device (Gram + SPD inverse: l_i = g_i^T (G^T G)^{-1} g_i when
-// I_k > R_kR_{k+1}; uniform when I_k <= R_kR_{k+1}, reading R10) and copied to the host for the
-// inverse-CDF draw.  Everything else runs in device kernels:
+// Per draw (mode k, time step tau) m indices are drawn with replacement from a SplitMix64 stream
+// keyed by (seed, tau, k) (reading R11; the oracle re-implements the same generator
+// independently).  The draws run ON THE DEVICE in counter form (draw j = mix(key + (j+1) GOLDEN)),
+// bit-identical to the host sampler, which is kept only for index tables the caller injects
+// (str_set_index_table) and for the STR_RSTR_HOST_DRAWS=1 diagnostic.  Leverage probabilities
+// p_k(i) = l_i(G_k(2)) / rank (Lemma 1) are computed on the device (Gram + SPD inverse:
+// l_i = g_i^T (G^T G)^{-1} g_i when I_k > R_kR_{k+1}; uniform when I_k <= R_kR_{k+1}, reading R10)
+// and drawn by inverse CDF on the device.  Everything else runs in device kernels:
 //   * sampled slices (G_k)_S = G_k(:, idxs(:,k), :)                       (Alg. 7 l.4)
 //   * sampled subchain G^{≠n}_S by the ⊡₂ chain of sampled slices         (Alg. 3 l.5-7, Def. 7)
 //   * zipped fibers X_S[n] (I_n x m) gathered from X                      (reading R7)
@@ -204,7 +206,15 @@ static inline int RRr(const str_state *h, int n) { return h->R[(n - 1) % h->N]; 
 
 static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
   if (b.bytes >= bytes) return STR_OK;
-  if (b.p) cudaFree(b.p);
+  if (h->capturing) {   // a cudaFree inside the stream capture would invalidate it (rstr_workspace pre-sizes)
+    h->err = "internal: rSTR workspace grows during graph capture";
+    h->poisoned = true;
+    return STR_E_CUDA;
+  }
+  if (b.p) {   // captured graphs may hold the old pointer
+    h->reset_graphs();
+    cudaFree(b.p);
+  }
   b.p = nullptr;
   b.bytes = 0;
   if (cudaMalloc(&b.p, bytes) != cudaSuccess) {
@@ -509,11 +519,10 @@ static str_status gather_fibers(str_state *h, const void *X, int n, int64_t tn, 
 }
 
 static str_status rstr_workspace(str_state *h, int64_t tn) {
-  static bool attr = false;
-  if (!attr) {
+  static PerDeviceOnce attr_once;
+  once_per_device(attr_once, [&] {
     cudaFuncSetAttribute(k_draw_weighted, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(kDevCdfMax * 8));
-    attr = true;
-  }
+  });
   if (!h->idx_pinned) {
     RCU(cudaMallocHost(&h->idx_pinned, sizeof(int32_t) * h->N * h->m));
     for (int k = 0; k <= h->N; ++k) RCU(cudaEventCreateWithFlags(&h->idx_ev[k], cudaEventDisableTiming));
@@ -536,6 +545,7 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
   RTRY(ensure_dev(h, h->sG, sizeof(double) * h->m * maxS * cw));
   RTRY(ensure_dev(h, h->sidx, sizeof(double) * h->m * maxS * cw));   // G_S[2]
   RTRY(ensure_dev(h, h->sGram, sizeof(double) * maxS * maxS));
+  RTRY(ensure_dev(h, h->sTmp, sizeof(double) * (maxI * maxS + maxI)));   // leverage scores (leverage_probs_dev)
   RTRY(ensure_dev(h, h->sSk,
                   sizeof(double) * gemm_sk_ws_doubles((int)std::max<int64_t>(maxI, maxS), maxS, h->m * cw)));
   RTRY(ensure_dev(h, h->sSk2, sizeof(double) * gemm_sk_ws_doubles(maxS, maxS, h->m * cw)));

@@ -54,7 +54,10 @@ static str_status fail(str_state *h, str_status s, const std::string &msg) {
 
 static str_status ensure(str_state *h, DevBuf &b, size_t bytes) {
   if (b.bytes >= bytes) return STR_OK;
-  if (b.p) cudaFree(b.p);
+  if (b.p) {   // captured graphs may hold the old pointer
+    h->reset_graphs();
+    cudaFree(b.p);
+  }
   b.p = nullptr;
   b.bytes = 0;
   if (bytes == 0) return STR_OK;
@@ -369,8 +372,7 @@ str_status ensure_temporal_capacity(str_state *h, int64_t need) {
   cudaFree(h->GN.p);
   h->GN = nb;
   h->Tcap = cap;
-  h->gs[0].reset();   // the captured append nodes point at the old buffer
-  h->gs[1].reset();
+  h->reset_graphs();   // the captured append nodes point at the old buffer
   return STR_OK;
 }
 
@@ -731,7 +733,7 @@ static str_status deferred_check(str_state *h) {
   int info = 0;
   e = cudaMemcpy(&info, h->d_info, sizeof(int), cudaMemcpyDeviceToHost);
   if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("info: ") + cudaGetErrorString(e));
-  if (info && !g_dbg_skip) return fail(h, STR_E_NUMERIC, "Cholesky of Q_n failed (non-positive pivot)");
+  if (info && !g_dbg_skip) return fail(h, STR_E_NUMERIC, "SPD inversion of Q_n met a non-positive pivot");
   return STR_OK;
 }
 
@@ -799,17 +801,20 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   }
   h->xbytes = cfg->dtype == STR_F64 ? 8 : 4;
 
+#ifdef STR_DIAG
   if (const char *sk = getenv("STR_DBG_SKIP")) {   // what-if timing diagnostic (tools/gpu_whatif.sh)
     g_dbg_skip = atoi(sk);
     if (g_dbg_skip)
       fprintf(stderr, "libstr: STR_DBG_SKIP=%d skips kernel classes: results are WRONG (what-if timing only)\n",
               g_dbg_skip);
   }
+#endif
   cudaError_t e = cudaSetDevice(cfg->device);
   if (e != cudaSuccess) {
     delete h;
     return STR_E_CUDA;
   }
+  if (cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess) h->nsm = 148;
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
@@ -820,7 +825,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     h->st = (cudaStream_t)cfg->stream;
     h->own_stream = false;
   } else {
-    if (cudaStreamCreateWithFlags(&h->st, cudaStreamNonBlocking) != cudaSuccess) {
+    // blocking w.r.t. the legacy default stream, so X produced there is ordered before the step
+    if (cudaStreamCreateWithFlags(&h->st, cudaStreamDefault) != cudaSuccess) {
       delete h;
       return STR_E_CUDA;
     }
@@ -1065,7 +1071,8 @@ extern "C" str_status str_fit(str_state *h, const void *X, int64_t t0, int64_t t
     const char *xp = (const char *)X + (size_t)h->L * h->Rr * c0 * h->xbytes;
     // X^hat = T_L T_R^T on the FP64 tensor-core fragments, residual sums in the epilogue (the row
     // GEMM needs L tn and R_r below 2^31 and the ranks' W <= 256)
-    const bool fg = h->L * tn < ((int64_t)1 << 31) && h->Rr < ((int64_t)1 << 31) && Ra * Rb <= 256;
+    const bool fg = h->L * tn < ((int64_t)1 << 31) && cdiv(h->L * tn, 16) <= 65535 && h->Rr < ((int64_t)1 << 31) &&
+                    Ra * Rb <= 256;
     int nf = fg ? launch_fit_gemm(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
                                   h->Rr, tn, (double *)trp.p, (double2 *)parts.p, (double *)acc.p, h->st)
                 : launch_fit(xp, h->dtype == STR_F64, (const double *)tl.p, (const double *)tr.p, Ra, Rb, h->L,
@@ -1115,8 +1122,7 @@ extern "C" STR_API str_status strdbg_tftrace(str_state *h, int32_t enable, long 
     if (host_out) CU(cudaMemcpy(host_out, h->tf_dbg, 2 * str_state::kTfDbgWords * sizeof(long long), cudaMemcpyDeviceToHost));
     cudaFree(h->tf_dbg);
     h->tf_dbg = nullptr;
-    h->gs[0].reset();   // captured contraction nodes may point at the freed trace buffer
-    h->gs[1].reset();
+    h->reset_graphs();   // captured contraction nodes may point at the freed trace buffer
   }
   return STR_OK;
 }

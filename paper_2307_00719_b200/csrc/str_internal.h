@@ -40,6 +40,7 @@ struct str_state {
   uint64_t seed = 0;
   int k = 1;                        // two-pass split
   int p = 1, rank = 0, device = 0;
+  int nsm = 148;                    // SMs of the device
   int xbytes = 4;
   int64_t i1_off = 0;
   cudaStream_t st = nullptr;
@@ -82,6 +83,12 @@ struct str_state {
     cudaGraphExec_t exec = nullptr;
     int64_t tn = 0, launches = 0;
     cudaGraphNode_t setx = nullptr, tf[2] = {nullptr, nullptr};
+    // launch parameters of the captured contraction nodes (per pass), re-used when a replay is
+    // re-pointed at new X (tf32_graph_update)
+    alignas(16) unsigned char tf_params[2][256];
+    alignas(64) unsigned char tf_ymap[2][128];   // CUtensorMap of the pass outputs (TMA reduce epilogue)
+    int tf_grid[2] = {0, 0};
+    size_t tf_smem[2] = {0, 0};
     void reset() {
       if (exec) cudaGraphExecDestroy(exec);
       if (graph) cudaGraphDestroy(graph);
@@ -95,11 +102,12 @@ struct str_state {
   cudaEvent_t pev[4] = {};          // profiling: pass-1 begin/end, pass-2 begin/end
   double prof_ms[2] = {0.0, 0.0};
   int64_t prof_n[2] = {0, 0};
-  alignas(16) unsigned char tf_params[2][256];
-  alignas(64) unsigned char tf_ymap[2][128];   // CUtensorMap of the pass outputs (TMA reduce epilogue)
-  int tf_grid[2] = {0, 0};
-  size_t tf_smem[2] = {0, 0};
   bool capturing = false;
+  // every captured graph holds raw device pointers: any (re)allocation of a buffer invalidates both
+  void reset_graphs() {
+    gs[0].reset();
+    gs[1].reset();
+  }
   long long *tf_dbg = nullptr;      // device buffer for the contraction pipeline trace (diagnostic)
   static constexpr int kTfDbgWords = 1024 + 4 * 160;   // per pass
 

@@ -182,3 +182,22 @@ def make_stream(cfg) -> Stream:
     if isinstance(cfg, str):
         cfg = get_config(cfg)
     return Stream(cfg)
+
+
+P_ALS_START = 7
+
+
+def als_start_cores(cfg) -> List[np.ndarray]:
+    """Random starting cores for batch TR-ALS on X_init (the initialization protocol of P:734,
+    P:752): i.i.d. N(0, 1) entries scaled by 1/sqrt(R_n R_{n+1}), seeded
+    by (seed, purpose 7, n); the temporal core has t_init rows.  Paper layout (R_n, I_n, R_{n+1})."""
+    if isinstance(cfg, str):
+        cfg = get_config(cfg)
+    N, R = cfg.N, cfg.ranks
+    sizes = list(cfg.dims) + [cfg.t_init]
+    out = []
+    for n in range(1, N + 1):
+        Rn, Rn1 = R[n - 1], R[n % N]
+        g = _rng(cfg.seed, P_ALS_START, n).standard_normal((Rn, sizes[n - 1], Rn1))
+        out.append(g / np.sqrt(Rn * Rn1))
+    return out
