@@ -132,9 +132,26 @@ def pinv_sym(Q: np.ndarray, rcond: float = 1e-12) -> np.ndarray:
     return (V * inv) @ V.T
 
 
-def solve_right(P: np.ndarray, Q: np.ndarray) -> np.ndarray:
-    """G = P Q^† (Alg. 4 l.9, l.17)."""
-    return P @ pinv_sym(Q)
+def solve_right(P: np.ndarray, Q: np.ndarray, refine: int = 2) -> np.ndarray:
+    """G = P Q^† (Alg. 4 l.9, l.17) with Q^† of pinv_sym (reading R3), evaluated to
+    full fp64 accuracy: G_0 = P Q^†, then ``refine`` steps of iterative refinement
+    G_{k+1} = G_k + (P - G_k Q) Q^† with the residual formed in extended precision (np.longdouble).
+    The plain product P Q^† carries an error of order cond(Q)·eps — about 1e-9 relative at the
+    cond(Q) ~ 1e7 that C3 reaches from its TR-ALS init, the size of the fp64 parity bar itself —
+    while the refined solution is accurate to about eps_ld·cond(Q) (eps_ld = 2^-64: ~1e-12 at
+    cond 1e7; tests/test_oracle_tralg.py pins it against exact and 60-digit solutions).  P's rows lie in the
+    range of Q (P = X G^{≠n}, Q = G^{≠n T} G^{≠n}), so the corrections stay in it and a
+    rank-deficient Q still gets the minimum-norm solution."""
+    Qs = symmetrize(Q)
+    Qp = pinv_sym(Qs)
+    G = P @ Qp
+    if refine:
+        Ql = Qs.astype(np.longdouble)
+        Pl = np.asarray(P, dtype=np.longdouble)
+        for _ in range(refine):
+            R = (Pl - G.astype(np.longdouble) @ Ql).astype(np.float64)
+            G = G + R @ Qp
+    return G
 
 
 def symmetrize(Q: np.ndarray) -> np.ndarray:

@@ -22,7 +22,11 @@ constexpr int kInvClusterCTAs = 4;   // CTAs of the cluster inverse (k_spd_inv_c
 
 // kernels_chain.cu
 void launch_set_identity(double *A, int n, cudaStream_t s);
-void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s);
+// Q^{-1} of an SPD S x S matrix (S <= STR_MAXW); ws: spd_inv_ws_doubles(S) doubles of scratch
+// (V = L^{-1} and the pivot-block inverses of the block LDL^T), not shared by concurrent calls.
+void launch_spd_inv(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s);
+size_t spd_inv_ws_doubles(int S);
+void launch_spd_inv_chol(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s);
 void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s);
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s);
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);

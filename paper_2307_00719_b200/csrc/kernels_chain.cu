@@ -490,9 +490,17 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
   }
 }
 
-void launch_spd_inv(const double *Q, int S, double *Qinv, int *info, cudaStream_t s) {
+void launch_spd_inv(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s) {
   if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
+  static const int old = [] {   // A/B knob: STR_INV=0 runs the previous Gauss-Jordan cluster sweep
+    const char *e = getenv("STR_INV");
+    return e ? atoi(e) == 0 : 0;
+  }();
+  if (!old) {
+    launch_spd_inv_chol(Q, S, Qinv, ws, info, s);
+    return;
+  }
   if (S <= STR_MAXW && S > 8) {
     pdl_launch(kPdlInv, k_spd_inv_cl, dim3(kInvNC), dim3(kInvCThreads), 0, s, Q, S, Qinv, info);
     return;

@@ -230,7 +230,7 @@ static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
 // out = B A^{-1} for SPD A (S x S) and `rows` rows of B: the cluster inverse, then a row GEMM on the
 // FP64 tensor-core fragments (the "†" of reading R3/R4 on the device).  Ai: S x S scratch.
 static void solve_right(str_state *h, const double *A, int S, double *Ai, const double *B, int64_t rows, double *out) {
-  launch_spd_inv(A, S, Ai, h->d_info, h->st);
+  launch_spd_inv(A, S, Ai, (double *)h->Vws_t.p, h->d_info, h->st);
   tl_mark(h, "spd_inv");
   launch_rows_mm(B, Ai, S, rows, out, h->st);
   tl_mark(h, "rows_mm");
@@ -578,7 +578,7 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   RTRY(rs_fork(h));
   gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1, true);   // Q_n += sym(G_S^T G_S)
   if (solve) {
-    launch_spd_inv((const double *)mb.Q.p, S, (double *)mb.Qi.p, h->d_info, h->st);
+    launch_spd_inv((const double *)mb.Q.p, S, (double *)mb.Qi.p, (double *)mb.Vws.p, h->d_info, h->st);
     tl_mark(h, "spd_inv");
   }
   rs_main(h);
@@ -649,7 +649,7 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R22)
   RTRY(rs_fork(h));   // the Gram and its inverse beside X_S G_S
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1, true);
-  launch_spd_inv(K, SN, (double *)h->Hi.p, h->d_info, h->st);
+  launch_spd_inv(K, SN, (double *)h->Hi.p, (double *)h->Vws_q.p, h->d_info, h->st);
   tl_mark(h, "spd_inv");
   rs_main(h);
   gemm(h, XS, h->ksrft() ? 2 * h->m : h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);

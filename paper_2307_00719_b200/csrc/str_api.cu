@@ -432,7 +432,7 @@ static void right_modes(const str_state *h, std::vector<int> &modes, std::vector
 // Q_j^{-1} by the blocked sweep (the "^{-1}" of Alg. 4 l.17).
 static str_status invert_mode(str_state *h, int j) {
   ModeBuf &m = h->md[j - 1];
-  launch_spd_inv((const double *)m.Q.p, m.Ra * m.Rb, (double *)m.Qi.p, h->d_info, h->st);
+  launch_spd_inv((const double *)m.Q.p, m.Ra * m.Rb, (double *)m.Qi.p, (double *)m.Vws.p, h->d_info, h->st);
   tl_mark(h, "spd_inv");
   return check_launch(h, "spd_inv");
 }
@@ -486,7 +486,7 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     launch_chain_gemm((const double *)h->Sf[1].p, (const double *)h->md[0].Zm.p, nullptr, M, Nc, K,
                       QEpi{(double *)h->Hq.p, RR(h, N), RR(h, 1), 1}, h->st);
     tl_mark(h, "chain_gemm_q");
-    launch_spd_inv((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, h->d_info, h->st);
+    launch_spd_inv((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, (double *)h->Vws_q.p, h->d_info, h->st);
     tl_mark(h, "spd_inv");
   }
   main_again(h);
@@ -875,6 +875,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     TRY(ensure(h, m.Q, sizeof(double) * S * S));
     TRY(ensure(h, m.Zm, sizeof(double) * S * S));
     TRY(ensure(h, m.Qi, sizeof(double) * S * S));
+    TRY(ensure(h, m.Vws, sizeof(double) * spd_inv_ws_doubles(S)));
   }
   h->Tcap = std::max<int64_t>(cfg->t_capacity > 0 ? cfg->t_capacity : 4096, t_init);
   TRY(ensure(h, h->GN, sizeof(double) * h->Tcap * h->SN));
@@ -890,6 +891,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   TRY(ensure(h, h->H, sizeof(double) * sq));
   TRY(ensure(h, h->Hq, sizeof(double) * STR_MAXW * STR_MAXW));
   TRY(ensure(h, h->Hi, sizeof(double) * STR_MAXW * STR_MAXW));
+  TRY(ensure(h, h->Vws_q, sizeof(double) * spd_inv_ws_doubles(STR_MAXW)));
+  TRY(ensure(h, h->Vws_t, sizeof(double) * spd_inv_ws_doubles(STR_MAXW)));
   {
     DevBuf info;
     TRY(ensure(h, info, sizeof(int)));
@@ -1245,4 +1248,50 @@ extern "C" STR_API str_status strdbg_contract_repeat(str_state *h, const void *X
   cudaEventDestroy(e0);
   cudaEventDestroy(e1);
   return STR_OK;
+}
+
+// Test hook (not part of include/str.h): Q^{-1} of `count` SPD S x S matrices (host, row-major)
+// through the library's SPD-inverse kernel on `device`; returns the pivot-failure flag in *info.
+extern "C" STR_API str_status strdbg_spd_inv(int32_t device, int32_t S, int32_t count, const double *Q_host,
+                                              double *Qinv_host, int32_t *info_host, int32_t reps, float *us) {
+  if (S < 1 || S > STR_MAXW || count < 1 || !Q_host || !Qinv_host) return STR_E_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return STR_E_CUDA;
+  const size_t n = (size_t)S * S;
+  double *dQ = nullptr, *dQi = nullptr, *ws = nullptr;
+  int *dinfo = nullptr;
+  str_status st = STR_OK;
+  if (cudaMalloc(&dQ, n * count * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&dQi, n * count * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&ws, spd_inv_ws_doubles(S) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&dinfo, sizeof(int)) != cudaSuccess) {
+    st = STR_E_OOM;
+  } else {
+    cudaMemcpy(dQ, Q_host, n * count * sizeof(double), cudaMemcpyHostToDevice);
+    cudaMemset(dinfo, 0, sizeof(int));
+    for (int c = 0; c < count; ++c) launch_spd_inv(dQ + c * n, S, dQi + c * n, ws, dinfo, 0);
+    if (cudaDeviceSynchronize() != cudaSuccess) st = STR_E_CUDA;
+    if (reps > 0 && us && st == STR_OK) {   // average time per inverse, back-to-back launches
+      cudaEvent_t e0, e1;
+      cudaEventCreate(&e0);
+      cudaEventCreate(&e1);
+      cudaEventRecord(e0, 0);
+      for (int r = 0; r < reps; ++r) launch_spd_inv(dQ, S, dQi, ws, dinfo, 0);
+      cudaEventRecord(e1, 0);
+      cudaEventSynchronize(e1);
+      float ms = 0.f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      *us = 1000.f * ms / reps;
+      cudaEventDestroy(e0);
+      cudaEventDestroy(e1);
+    }
+    cudaMemcpy(Qinv_host, dQi, n * count * sizeof(double), cudaMemcpyDeviceToHost);
+    int inf = 0;
+    cudaMemcpy(&inf, dinfo, sizeof(int), cudaMemcpyDeviceToHost);
+    if (info_host) *info_host = inf;
+  }
+  cudaFree(dQ);
+  cudaFree(dQi);
+  cudaFree(ws);
+  cudaFree(dinfo);
+  return st;
 }

@@ -23,6 +23,7 @@ struct ModeBuf {
   DevBuf Q;             // (Ra*Rb)^2 (Eq. partial)
   DevBuf Zm;            // Gram tensor Z_n as chain matrix: Rb^2 x Ra^2
   DevBuf Qi;            // Q_n^{-1} (full symmetric)
+  DevBuf Vws;           // scratch of the SPD inverse of Q_n (block LDL^T factors)
   // rSTR
   DevBuf samp;          // sampled slices (G_n)_S: m x Ra*Rb (G(2) layout rows)
   std::vector<int32_t> idx_host;
@@ -60,6 +61,7 @@ struct str_state {
   DevBuf ZmN;                       // Z_N^new (update) / Z_N (init): R_1^2 x R_N^2
   std::vector<DevBuf> Sf;           // suffix chains Sf_n (index n)
   DevBuf Lp[2], T1, H, Hq, Hi;       // Hq = H^{≠N}_<2> (temporal normal matrix), Hi = Hq^{-1}
+  DevBuf Vws_q, Vws_t;              // SPD-inverse scratch: Hq, and the rSTR leverage solves
 
   // workspaces
   int64_t ws_t = 0;
@@ -144,11 +146,11 @@ struct str_state {
       b.bytes = 0;
     };
     for (auto &m : md) {
-      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.Qi); fr(m.samp);
+      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.Qi); fr(m.samp); fr(m.Vws);
     }
     fr(GN); fr(ZmN);
     for (auto &b : Sf) fr(b);
-    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi);
+    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi); fr(Vws_q); fr(Vws_t);
     fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
     fr(tab_split); fr(tf_part); fr(tf_part2);
     fr(GNnew); fr(dT); fr(dX);

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 from oracle.tensor import fold, tr_full_bruteforce, unfold
-from oracle.tralg import (chain_order, core_fold, core_unfold, gram_chain, gram_core, gram_unfold, pinv_sym,
+from oracle.tralg import (chain_order, core_fold, core_unfold, gram_chain, gram_core, gram_unfold, pinv_sym, solve_right,
                           slices_hadamard, subchain, subchain_order, subchain_product, unfold2)
 
 CASES = [((3, 4, 2), (2, 3, 4)), ((3, 2, 4, 2), (2, 3, 4, 2)), ((2, 3, 2, 2, 3), (2, 3, 2, 4, 3))]
@@ -124,3 +124,47 @@ def test_pinv_sym():
     np.testing.assert_allclose(Qd @ Pd @ Qd, Qd, atol=1e-10)
     np.testing.assert_allclose(Pd @ Qd @ Pd, Pd, atol=1e-10)
     np.testing.assert_allclose(Pd, np.linalg.pinv(Qd, rcond=1e-10), atol=1e-10)
+
+
+def _unimodular_spd(S, rng, spread=3):
+    """Q = L L^T with L unit lower triangular with integer entries: an SPD integer matrix whose
+    inverse L^{-T} L^{-1} is an integer matrix too (det L = 1), with a large condition number."""
+    L = np.tril(rng.integers(-spread, spread + 1, (S, S)), -1) + np.eye(S, dtype=np.int64)
+    return L @ L.T
+
+
+@pytest.mark.parametrize("S,spread,seed", [(6, 3, 0), (12, 3, 1), (16, 2, 0), (20, 2, 1), (24, 1, 2)])
+def test_solve_right_exact_on_unimodular_systems(S, spread, seed):
+    """Closed form: with Q = L L^T (L unimodular, integer) and an integer G, P = G Q is exact in fp64
+    and the solution of G Q = P is G itself.  The refined solve reaches it to a few ulps even where
+    cond(Q) (1e6-2e7, the range C3 reaches) makes the plain P Q^† miss it by cond·eps ~ 1e-9."""
+    rng = np.random.default_rng(seed)
+    Q = _unimodular_spd(S, rng, spread)
+    G = rng.integers(-5, 6, (4, S))
+    P = G @ Q
+    assert np.abs(P).max() < 2 ** 52 and np.abs(Q).max() < 2 ** 52
+    Qf, Pf = Q.astype(np.float64), P.astype(np.float64)
+    cond = np.linalg.cond(Qf)
+    assert 1e6 < cond < 1e8
+    err = np.linalg.norm(solve_right(Pf, Qf) - G) / np.linalg.norm(G)
+    assert err < 1e-13, (S, cond, err)
+    err0 = np.linalg.norm(solve_right(Pf, Qf, refine=0) - G) / np.linalg.norm(G)
+    assert err0 > 100 * err
+
+
+def test_solve_right_matches_mpmath_on_random_ill_conditioned():
+    """Reference solution in 60-digit arithmetic (mpmath LU) for an SPD Q of cond 1e7."""
+    import mpmath
+    rng = np.random.default_rng(5)
+    S = 10
+    U, _ = np.linalg.qr(rng.standard_normal((S, S)))
+    Q = (U * np.logspace(0, 7, S)) @ U.T
+    Q = 0.5 * (Q + Q.T)
+    P = rng.standard_normal((3, S)) @ Q + 1e-3 * rng.standard_normal((3, S))
+    mpmath.mp.dps = 60
+    Qm = mpmath.matrix(Q.tolist())
+    ref = np.array([[float(v) for v in (mpmath.lu_solve(Qm, mpmath.matrix(P[i].tolist())))] for i in range(3)])
+    err = np.linalg.norm(solve_right(P, Q) - ref) / np.linalg.norm(ref)
+    assert err < 1e-13, err
+    err0 = np.linalg.norm(solve_right(P, Q, refine=0) - ref) / np.linalg.norm(ref)
+    assert err0 > 100 * err
