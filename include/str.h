@@ -69,6 +69,9 @@ typedef enum { STR_CONTRACT_3XTF32 = 0, STR_CONTRACT_F64 = 1 } str_contract;
 /* STR (Alg. 4); rSTR-U (Alg. 7), rSTR-L (Alg. 8); rSTR-K: KSRFT mixing + uniform rows (Def. 10
    P:614-627, Alg. 9; readings R17-R22) */
 typedef enum { STR_DET = 0, STR_SAMPLE_UNIFORM = 1, STR_SAMPLE_LEVERAGE = 2, STR_SAMPLE_KSRFT = 3 } str_variant;
+/* Collectives of the sharded step (world_size > 1): NCCL between processes (one per GPU), or an
+   in-process loopback group (the ranks are handles of one process sharing one GPU; tests) */
+typedef enum { STR_COMM_NCCL = 0, STR_COMM_LOOPBACK = 1 } str_comm;
 
 typedef struct {
   int32_t order;          /* N >= 3 */
@@ -85,9 +88,12 @@ typedef struct {
   int32_t split_k;        /* two-pass split point k in [1, N-2] (0 = automatic) */
   int32_t world_size;     /* >= 1: X is sharded along mode 1 across world_size processes */
   int32_t rank;           /* this process' shard: rows [rank*I_1/p, (rank+1)*I_1/p) of mode 1 */
-  const void *nccl_id;    /* 128-byte ncclUniqueId shared by all ranks (ignored if world_size == 1) */
+  const void *nccl_id;    /* STR_COMM_NCCL: 128-byte ncclUniqueId shared by all ranks; STR_COMM_LOOPBACK:
+                             the group from str_loopback_create (ignored if world_size == 1) */
   int32_t device;         /* CUDA device ordinal */
-  void *stream;           /* cudaStream_t to enqueue on, or NULL for an internal stream */
+  void *stream;           /* cudaStream_t to enqueue on, or NULL for an internal stream (created
+                             blocking with respect to the legacy default stream) */
+  int32_t comm;           /* str_comm (0 = NCCL) */
 } str_config;
 
 /* Alg. 4 l.1-5, Alg. 7 l.1-16, Alg. 8 l.1-17.
@@ -101,8 +107,13 @@ STR_API str_status str_init(const str_config *cfg, const void *X_init, int64_t t
 
 /* One time step (Alg. 4 l.7-19; Alg. 7 l.17-41; Alg. 8 l.18-43).
  * X_new: DEVICE pointer to this rank's shard (I_1/p x ... x I_{N-1} x t_new), t_new >= 1.
- * Not retained after the enqueued work completes: the method never revisits old data
- * (SPEC S:438).  Collective when world_size > 1 (every rank calls with the same t_new). */
+ * Lifetime: the call returns before the step has run; the caller must keep X_new valid and
+ * unchanged until the enqueued work has completed (str_sync, any call documented as waiting, or an
+ * event recorded on the library's stream after this call).  X_new must be produced before the call
+ * in the stream order of the library's stream (or of the legacy default stream when the library's
+ * internal stream is used).  The library never retains X_new after the step: the method never
+ * revisits old data.  Collective when world_size > 1 (every rank calls with the same
+ * t_new). */
 STR_API str_status str_update_batch(str_state *h, const void *X_new, int64_t t_new);
 
 /* Same step with X_new in HOST memory (pinned for full speed): the library copies it to the
@@ -152,6 +163,12 @@ STR_API int64_t str_kernel_launches(const str_state *h);
 STR_API str_status str_set_profiling(str_state *h, int32_t enable);
 STR_API str_status str_profile(str_state *h, double *pass1_ms, int64_t *pass1_launches, double *pass2_ms,
                        int64_t *pass2_launches);
+
+/* In-process loopback group of world_size ranks (STR_COMM_LOOPBACK): the ranks' handles are created
+ * by str_init with cfg.comm = STR_COMM_LOOPBACK and cfg.nccl_id = group, from concurrent host
+ * threads (str_init is collective); destroy the group after its handles. */
+STR_API str_status str_loopback_create(int32_t world_size, void **group);
+STR_API void str_loopback_destroy(void *group);
 
 /* rSTR test hooks: the index table drawn for mode k (1..N) at the most
  * recent draw (m entries), or force the table used at the next draw of mode k. */

@@ -24,6 +24,7 @@ from ._lib import (STR_CONTRACT_3XTF32, STR_CONTRACT_F64, STR_DET, STR_F32, STR_
 __all__ = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",
            "str_fit", "str_sync", "str_processed", "str_error_string", "str_destroy", "str_kernel_launches",
            "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "str_tr_als", "Handle",
+           "str_loopback_create", "str_loopback_destroy",
            "StrError",
            "LIB_PATH"]
 
@@ -90,7 +91,7 @@ def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_in
              init_cores: Sequence[np.ndarray], *, dtype: str = "f32", contract: str = "3xtf32",
              variant: str = "det", sketch_rows: int = 0, seed: int = 0, t_capacity: int = 0, split_k: int = 0,
              world_size: int = 1, rank: int = 0, nccl_id: Optional[bytes] = None, device: int = 0,
-             stream: Optional[int] = None) -> Handle:
+             stream: Optional[int] = None, loopback_group: Optional[int] = None) -> Handle:
     """Alg. 4 l.1-5 / Alg. 7-8 init.  ``dims`` are the GLOBAL I_1..I_{N-1}; X_init is this rank's
     shard; ``init_cores`` are global paper-layout cores (core N has t_init rows)."""
     import torch
@@ -104,11 +105,16 @@ def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_in
     nid = None
     if nccl_id is not None:
         nid = C.create_string_buffer(bytes(nccl_id), len(nccl_id))
+    comm = _lib.STR_COMM_NCCL
+    gptr = None
+    if loopback_group is not None:   # in-process ranks sharing one GPU (str_loopback_create)
+        comm = _lib.STR_COMM_LOOPBACK
+        gptr = C.c_void_p(int(loopback_group))
     cfg = str_config(order=N, dims=dims_a, ranks=ranks_a, dtype=_DTYPES[dtype], contract=_CONTRACTS[contract],
                      variant=_VARIANTS[variant], sketch_rows=int(sketch_rows), seed=int(seed) & (2 ** 64 - 1),
                      t_capacity=int(t_capacity), split_k=int(split_k), world_size=int(world_size), rank=int(rank),
-                     nccl_id=C.cast(nid, C.c_void_p) if nid is not None else None, device=int(device),
-                     stream=C.c_void_p(stream))
+                     nccl_id=(gptr if gptr is not None else (C.cast(nid, C.c_void_p) if nid is not None else None)),
+                     device=int(device), stream=C.c_void_p(stream), comm=comm)
     local = [int(d) for d in dims]
     local[0] //= int(world_size)
     xptr = _dev_ptr(X_init, int(np.prod(local)) * int(t_init), dtype)
@@ -127,6 +133,17 @@ def str_init(order: int, dims: Sequence[int], ranks: Sequence[int], X_init, t_in
     h.world_size = int(world_size)
     h.local_slice = int(np.prod(local))
     return h
+
+
+def str_loopback_create(world_size: int) -> int:
+    """In-process loopback group of world_size ranks (include/str.h): returns the group pointer."""
+    g = C.c_void_p()
+    _check(None, _lib.lib.str_loopback_create(int(world_size), C.byref(g)))
+    return int(g.value)
+
+
+def str_loopback_destroy(group: int) -> None:
+    _lib.lib.str_loopback_destroy(C.c_void_p(int(group)))
 
 
 def str_update_batch(h: Handle, X_new, t_new: Optional[int] = None) -> None:

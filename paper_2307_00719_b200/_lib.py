@@ -17,11 +17,13 @@ STATUS_NAMES = ["STR_OK", "STR_E_ARG", "STR_E_SHAPE", "STR_E_PRECOND", "STR_E_NU
 STR_F32, STR_F64 = 0, 1
 STR_CONTRACT_3XTF32, STR_CONTRACT_F64 = 0, 1
 STR_DET, STR_SAMPLE_UNIFORM, STR_SAMPLE_LEVERAGE, STR_SAMPLE_KSRFT = 0, 1, 2, 3
+STR_COMM_NCCL, STR_COMM_LOOPBACK = 0, 1
 
 # Every symbol include/str.h declares (checked by tests/test_abi.py without a GPU).
 EXPORTS = ["str_init", "str_update_batch", "str_update_batch_host", "str_get_cores", "str_get_temporal_rows",
            "str_fit", "str_sync", "str_processed", "str_error_string", "str_destroy", "str_kernel_launches",
-           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "str_tr_als"]
+           "str_set_profiling", "str_profile", "str_get_index_table", "str_set_index_table", "str_tr_als",
+           "str_loopback_create", "str_loopback_destroy"]
 
 
 class str_config(C.Structure):
@@ -41,6 +43,7 @@ class str_config(C.Structure):
         ("nccl_id", C.c_void_p),
         ("device", C.c_int32),
         ("stream", C.c_void_p),
+        ("comm", C.c_int32),
     ]
 
 
@@ -76,6 +79,8 @@ def _load():
                                   C.POINTER(C.c_int64)]),
         "str_get_index_table": (C.c_int, [P, C.c_int32, C.POINTER(C.c_int32), C.c_int64]),
         "str_set_index_table": (C.c_int, [P, C.c_int32, C.POINTER(C.c_int32), C.c_int64]),
+        "str_loopback_create": (C.c_int, [C.c_int32, C.POINTER(P)]),
+        "str_loopback_destroy": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(lib, name)

@@ -107,6 +107,46 @@ __device__ __forceinline__ bool warp_sweep8(double (&d)[2], int g, int tg) {
   return bad;
 }
 
+// The same symmetric sweep in ONE thread's registers on an 8 x 8 SPD block in shared memory
+// (row-major, ld 8, both triangles): M <- -M^{-1}.  No shuffles on the pivot chain (one reciprocal
+// and one dependent update per pivot), one copy of the code.  Returns true on a bad pivot.
+__device__ __noinline__ bool sweep8_1(double *M) {
+  double a[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j <= i; ++j) a[i][j] = M[i * 8 + j];
+  bool bad = false;
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    const double piv = a[m][m];
+    bad = bad || !(piv > 0.0);
+    const double p = rcp_nr(piv);
+    double col[8], sc[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      col[i] = (i > m) ? a[i][m] : a[m][i];
+      sc[i] = col[i] * p;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j <= i; ++j)
+        if (i != m && j != m) a[i][j] = fma(-sc[i], col[j], a[i][j]);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      if (i > m) a[i][m] = sc[i];
+      else if (i < m) a[m][i] = sc[i];
+    }
+    a[m][m] = -p;
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) M[i * 8 + j] = (j <= i) ? a[i][j] : a[j][i];
+  return bad;
+}
+
 // SLOTS = off-diagonal tiles per warp: ceil(nt(nt-1)/2 / (32 - nt)) = 5 for nt <= 13, 8 for nt <= 16
 // The step loop runs from kb = -1 (the prologue: publish V_0, invert tile (0,0)) so that the pivot
 // sweep is instantiated once; tile coordinates come from a shared table (no register arrays).
@@ -308,6 +348,8 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
   __shared__ __align__(16) double Wb[STR_MAXW * kVS];      // W = V D
   __shared__ __align__(16) double Db[2][64];               // pivot inverses D
   __shared__ short s_off[7][kInvCSlots][2];                // off-diagonal tiles of warps 1-7
+  __shared__ __align__(16) double sw8[64];                  // the pivot block of the look-ahead sweep
+  __shared__ int s_bad8;
   const int c = (int)cl.block_rank();
   const int nt = (S + 7) >> 3;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -430,9 +472,15 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
 #ifdef INV_PROBE
           const long long qs = clock64();
 #endif
-          double d[2] = {cc[sl][0], cc[sl][1]};
-          bad = warp_sweep8(d, g, tg) || bad;
-          put2(Dn, g * 8 + 2 * tg, -d[0], -d[1]);
+          // the 8-pivot sweep in one lane (no shuffles on the pivot chain)
+          sw8[g * 8 + 2 * tg] = cc[sl][0];
+          sw8[g * 8 + 2 * tg + 1] = cc[sl][1];
+          __syncwarp();
+          if (lane == 0) s_bad8 = sweep8_1(sw8) ? 1 : 0;
+          __syncwarp();
+          bad = bad || s_bad8 != 0;
+          put2(Dn, g * 8 + 2 * tg, -sw8[g * 8 + 2 * tg], -sw8[g * 8 + 2 * tg + 1]);
+          __syncwarp();
 #ifdef INV_PROBE
           ps += clock64() - qs;
 #endif
@@ -493,11 +541,11 @@ __global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1
 void launch_spd_inv(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s) {
   if (g_dbg_skip & 1) return;
   prepare_kernel_attrs();
-  static const int old = [] {   // A/B knob: STR_INV=0 runs the previous Gauss-Jordan cluster sweep
+  static const int chol = [] {   // A/B knob: STR_INV=1 runs the single-CTA block-Cholesky inverse
     const char *e = getenv("STR_INV");
-    return e ? atoi(e) == 0 : 0;
+    return e ? atoi(e) == 1 : 0;
   }();
-  if (!old) {
+  if (chol) {
     launch_spd_inv_chol(Q, S, Qinv, ws, info, s);
     return;
   }

@@ -21,6 +21,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "common.cuh"
@@ -76,49 +77,13 @@ static str_status check_launch(str_state *h, const char *what) {
   return STR_OK;
 }
 
-// ------------------------------------------------------------------------------------ NCCL (dlopen)
-#include <nccl.h>
-struct NcclApi {
-  void *lib = nullptr;
-  ncclResult_t (*commInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
-  ncclResult_t (*allReduce)(const void *, void *, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
-                            cudaStream_t) = nullptr;
-  ncclResult_t (*allGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
-  ncclResult_t (*commDestroy)(ncclComm_t) = nullptr;
-  const char *(*getErrorString)(ncclResult_t) = nullptr;
-};
-static NcclApi g_nccl;
-
-static bool load_nccl(std::string &why) {
-  if (g_nccl.lib) return true;
-  const char *names[] = {"libnccl.so.2", "libnccl.so"};
-  for (const char *nm : names) {
-    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
-    if (g_nccl.lib) break;
-  }
-  if (!g_nccl.lib) {
-    why = "cannot dlopen libnccl.so.2";
-    return false;
-  }
-  g_nccl.commInitRank = (decltype(g_nccl.commInitRank))dlsym(g_nccl.lib, "ncclCommInitRank");
-  g_nccl.allReduce = (decltype(g_nccl.allReduce))dlsym(g_nccl.lib, "ncclAllReduce");
-  g_nccl.allGather = (decltype(g_nccl.allGather))dlsym(g_nccl.lib, "ncclAllGather");
-  g_nccl.commDestroy = (decltype(g_nccl.commDestroy))dlsym(g_nccl.lib, "ncclCommDestroy");
-  g_nccl.getErrorString = (decltype(g_nccl.getErrorString))dlsym(g_nccl.lib, "ncclGetErrorString");
-  if (!g_nccl.commInitRank || !g_nccl.allReduce || !g_nccl.allGather || !g_nccl.commDestroy) {
-    why = "libnccl is missing symbols";
-    return false;
-  }
-  return true;
-}
-
-// Sum-allreduce of device data across the mode-1 shards (no-op on one GPU).
+// ------------------------------------------------------------------------------------ collectives
+// Sum-allreduce of device data across the mode-1 shards (no-op on one GPU), on the handle's current
+// stream: NCCL or the in-process loopback group (comm.cu).
 static str_status allreduce(str_state *h, void *buf, size_t n, bool f32 = false) {
   if (h->p == 1 || n == 0) return STR_OK;
-  ncclResult_t r = g_nccl.allReduce(buf, buf, n, f32 ? ncclFloat32 : ncclFloat64, ncclSum, (ncclComm_t)h->comm, h->st);
-  if (r != ncclSuccess)
-    return fail(h, STR_E_NCCL, std::string("ncclAllReduce: ") +
-                                   (g_nccl.getErrorString ? g_nccl.getErrorString(r) : "error"));
+  const std::string e = h->comm->allreduce(buf, n, f32, h->st);
+  if (!e.empty()) return fail(h, STR_E_NCCL, e);
   h->collectives++;
   return STR_OK;
 }
@@ -669,6 +634,82 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
   return STR_OK;
 }
 
+// ------------------------------------------------------------------------------------ loopback driver
+// Test hook (not part of include/str.h): one STR step of all p in-process ranks of a loopback group
+// (STR_COMM_LOOPBACK).  graph = 0: every rank's step is enqueued eagerly by its own host thread (the
+// ranks meet at the collective sites on the host).  graph = 1: the p steps are captured once into
+// ONE CUDA graph — p stream branches joined by the collective sites' sum nodes — and replayed; the
+// X buffers must then be the same on every call (the graph holds their addresses).
+extern "C" STR_API str_status strdbg_loopback_step(str_state **hs, int32_t p, const void **X, int64_t tn,
+                                                   int32_t graph) {
+  if (!hs || !X || p < 1 || tn < 1) return STR_E_ARG;
+  for (int r = 0; r < p; ++r)
+    if (!hs[r] || hs[r]->poisoned || hs[r]->p != p || !hs[r]->loop_group || hs[r]->variant != STR_DET)
+      return STR_E_ARG;
+  std::vector<str_status> st(p, STR_OK);
+  if (!graph) {
+    std::vector<std::thread> th;
+    for (int r = 0; r < p; ++r) th.emplace_back([&, r] { st[r] = str_update_batch(hs[r], X[r], tn); });
+    for (auto &t : th) t.join();
+    for (int r = 0; r < p; ++r)
+      if (st[r] != STR_OK) return st[r];
+    return STR_OK;
+  }
+  str_state *h = hs[0];
+  cudaSetDevice(h->device);
+  int64_t *etn = nullptr;
+  std::vector<const void *> *ex = nullptr;
+  cudaGraphExec_t &exec = loopback_exec(loopback_group_of(h->comm), &etn, &ex);
+  bool fresh = false;
+  for (int r = 0; r < p; ++r) {
+    const void *old = hs[r]->GN.p;
+    TRY(ensure_workspace(hs[r], tn));
+    TRY(ensure_temporal_capacity(hs[r], hs[r]->T + tn));
+    if (hs[r]->GN.p != old) fresh = true;   // (the group's graph holds the old temporal buffer)
+  }
+  bool same = exec && *etn == tn && !fresh && (int)ex->size() == p;
+  for (int r = 0; same && r < p; ++r) same = (*ex)[r] == X[r];
+  if (!same) {
+    if (exec) cudaGraphExecDestroy(exec);
+    exec = nullptr;
+    cudaEvent_t fork_ev, join_ev[16];
+    CU(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+    for (int r = 0; r < p; ++r) CU(cudaEventCreateWithFlags(&join_ev[r], cudaEventDisableTiming));
+    CU(cudaStreamBeginCapture(h->st, cudaStreamCaptureModeRelaxed));
+    cudaEventRecord(fork_ev, h->st);
+    for (int r = 1; r < p; ++r) cudaStreamWaitEvent(hs[r]->st, fork_ev, 0);
+    std::vector<std::thread> th;
+    for (int r = 0; r < p; ++r)
+      th.emplace_back([&, r] {
+        cudaSetDevice(hs[r]->device);
+        st[r] = update_det_enqueue(hs[r], X[r], tn);
+      });
+    for (auto &t : th) t.join();
+    for (int r = 1; r < p; ++r) {
+      cudaEventRecord(join_ev[r], hs[r]->st);
+      cudaStreamWaitEvent(h->st, join_ev[r], 0);
+    }
+    cudaGraph_t g = nullptr;
+    cudaError_t e = cudaStreamEndCapture(h->st, &g);
+    cudaEventDestroy(fork_ev);
+    for (int r = 0; r < p; ++r) cudaEventDestroy(join_ev[r]);
+    for (int r = 0; r < p; ++r)
+      if (st[r] != STR_OK) {
+        if (g) cudaGraphDestroy(g);
+        return st[r];
+      }
+    if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("loopback capture: ") + cudaGetErrorString(e));
+    e = cudaGraphInstantiate(&exec, g, 0);
+    cudaGraphDestroy(g);
+    if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("loopback instantiate: ") + cudaGetErrorString(e));
+    *etn = tn;
+    ex->assign(X, X + p);
+  }
+  CU(cudaGraphLaunch(exec, h->st));
+  for (int r = 0; r < p; ++r) hs[r]->T += tn;
+  return STR_OK;
+}
+
 // ------------------------------------------------------------------------------------ init (STR)
 // Alg. 4 l.1-5: Z_1..Z_N, P_n = X_init[n] G^{≠n}_[2], Q_n = H^{≠n}_<2> with all init cores.
 static str_status init_det(str_state *h, const void *X, int64_t tn) {
@@ -834,19 +875,18 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   }
   if (p > 1) {
     std::string why;
-    if (!cfg->nccl_id || !load_nccl(why)) {
-      h->err = why.empty() ? "nccl_id required" : why;
-      str_destroy(h);
-      return STR_E_NCCL;
+    if (cfg->comm == STR_COMM_LOOPBACK) {
+      h->comm = comm_loopback(const_cast<void *>(cfg->nccl_id), p, cfg->rank, h, why);
+      h->loop_group = const_cast<void *>(cfg->nccl_id);
+      h->use_graph_forced_off = true;   // the group captures all ranks' steps into one graph
+    } else {
+      h->comm = comm_nccl(p, cfg->rank, cfg->nccl_id, why);
     }
-    ncclUniqueId id;
-    memcpy(&id, cfg->nccl_id, sizeof(id));
-    ncclComm_t comm;
-    if (g_nccl.commInitRank(&comm, p, id, cfg->rank) != ncclSuccess) {
-      str_destroy(h);
-      return STR_E_NCCL;
+    if (!h->comm) {
+      h->err = why;
+      *out = h;   // the caller reads str_error_string, then str_destroy
+      return cfg->comm == STR_COMM_LOOPBACK ? STR_E_ARG : STR_E_NCCL;
     }
-    h->comm = comm;
   }
   *out = h;
 
@@ -906,7 +946,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   prepare_kernel_attrs();
   {
     const char *ev = getenv("STR_NO_GRAPH");
-    h->use_graph = !(ev && ev[0] == '1');
+    h->use_graph = !(ev && ev[0] == '1') && !h->use_graph_forced_off;
     const char *hd = getenv("STR_RSTR_HOST_DRAWS");   // diagnostic: the host sampler for rSTR draws
     h->rstr_dev = !(hd && hd[0] == '1');
   }
@@ -1023,13 +1063,22 @@ extern "C" str_status str_get_cores(str_state *h, int32_t n, double *host_out, i
   const int S = m.Ra * m.Rb;
   if (capacity < m.I_glob * S) return fail(h, STR_E_ARG, "capacity too small");
   std::vector<double> buf((size_t)m.I_glob * S);
-  if (n == 1 && h->p > 1) {
+  if (n == 1 && h->p > 1 && h->loop_group) {
+    // in-process ranks: read every rank's shard of G_1 directly (no collective: the callers are
+    // not concurrent here)
+    for (int r = 0; r < h->p; ++r) {
+      str_state *o = loopback_member(h->loop_group, r);
+      if (!o) return fail(h, STR_E_ARG, "loopback rank missing");
+      TRY(deferred_check(o));
+      CU(cudaMemcpy(buf.data() + (size_t)r * m.I * S, o->md[0].G.p, sizeof(double) * m.I * S, cudaMemcpyDeviceToHost));
+    }
+  } else if (n == 1 && h->p > 1) {
     DevBuf gathered;
     TRY(ensure(h, gathered, sizeof(double) * m.I_glob * S));
-    ncclResult_t r = g_nccl.allGather(m.G.p, gathered.p, (size_t)m.I * S, ncclFloat64, (ncclComm_t)h->comm, h->st);
-    if (r != ncclSuccess) {
+    const std::string e = h->comm->allgather((const double *)m.G.p, (double *)gathered.p, (size_t)m.I * S, h->st);
+    if (!e.empty()) {
       cudaFree(gathered.p);
-      return fail(h, STR_E_NCCL, "ncclAllGather failed");
+      return fail(h, STR_E_NCCL, e);
     }
     CU(cudaStreamSynchronize(h->st));
     CU(cudaMemcpy(buf.data(), gathered.p, sizeof(double) * buf.size(), cudaMemcpyDeviceToHost));
@@ -1185,7 +1234,8 @@ extern "C" void str_destroy(str_state *h) {
   cudaSetDevice(h->device);
   cudaStreamSynchronize(h->st);
   h->free_all();
-  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy((ncclComm_t)h->comm);
+  delete h->comm;
+  h->comm = nullptr;
   if (h->st2) {
     cudaStreamSynchronize(h->st2);
     cudaStreamDestroy(h->st2);

@@ -9,6 +9,25 @@
 
 #include "str.h"
 
+// Collective backend of the mode-1-sharded step (comm.cu): NCCL across processes or an in-process
+// loopback group.  Every call enqueues on stream s; the return value is "" or an error message.
+struct Comm {
+  int p = 1, rank = 0;
+  virtual ~Comm() = default;
+  virtual std::string allreduce(void *buf, size_t n, bool f32, cudaStream_t s) = 0;          // sum, in place
+  virtual std::string allgather(const double *send, double *recv, size_t n, cudaStream_t s) = 0;  // rank-major
+  virtual bool loopback() const { return false; }
+};
+struct str_state;
+namespace strb200 {
+Comm *comm_nccl(int p, int rank, const void *nccl_id, std::string &why);
+Comm *comm_loopback(void *group, int p, int rank, str_state *h, std::string &why);
+str_state *loopback_member(void *group, int rank);
+struct LoopbackGroup;
+LoopbackGroup *loopback_group_of(Comm *c);
+cudaGraphExec_t &loopback_exec(LoopbackGroup *g, int64_t **tn, std::vector<const void *> **xs);
+}  // namespace strb200
+
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
@@ -48,7 +67,8 @@ struct str_state {
   bool own_stream = false;
   cudaStream_t st2 = nullptr, st_main = nullptr;   // side stream for the independent branches
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  void *comm = nullptr;             // ncclComm_t
+  Comm *comm = nullptr;             // collectives when p > 1 (comm.cu)
+  void *loop_group = nullptr;       // loopback group (in-process ranks), if any
 
   // geometry (local)
   int64_t L = 1, Rr = 1;            // prod of left dims (modes 1..k), right dims (k+1..N-1)
@@ -80,6 +100,7 @@ struct str_state {
   // appended at the device-side row counter dT.
   DevBuf GNnew, dT, dX;
   bool use_graph = true;
+  bool use_graph_forced_off = false;   // loopback ranks: the group owns the step graph
   struct GraphSlot {
     cudaGraph_t graph = nullptr;
     cudaGraphExec_t exec = nullptr;
