@@ -22,6 +22,8 @@
 // A non-positive (or NaN) pivot sets *info = 1.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "common.cuh"
 #include "dmma.cuh"
 #include "kernels.h"
@@ -66,17 +68,29 @@ __device__ __noinline__ void chol8_inv1(const double *M, int ldm, double *Tout, 
 #pragma unroll
     for (int j = 0; j <= i; ++j) a[i][j] = M[i * ldm + j];
   double r[8];
+  // pivots in pairs: for the leading 2 x 2 block [[x, y], [y, z]] of the current Schur complement,
+  // L = [[sqrt x, 0], [y / sqrt x, sqrt(d / x)]] with d = x z - y^2, so both reciprocal square roots
+  // (of x and of d) start together: half the dependent rsqrt latencies of the scalar recursion
 #pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const double piv = a[m][m];
-    bad = bad || !(piv > 0.0);
-    r[m] = rsqrt_full(piv);
+  for (int m = 0; m < 8; m += 2) {
+    const double x = a[m][m], y = a[m + 1][m], z = a[m + 1][m + 1];
+    const double d = fma(x, z, -y * y);
+    bad = bad || !(x > 0.0) || !(d > 0.0);
+    const double rx = rsqrt_full(x), rdd = rsqrt_full(d);
+    const double l10 = y * rx;               // L[m+1][m]
+    r[m] = rx;                               // 1 / L[m][m]
+    r[m + 1] = rdd * (x * rx);               // 1 / L[m+1][m+1] = sqrt(x) / sqrt(d)
 #pragma unroll
-    for (int i = m + 1; i < 8; ++i) a[i][m] *= r[m];   // column m of L
+    for (int i = m + 2; i < 8; ++i) {
+      a[i][m] *= rx;                                          // L[i][m]
+      a[i][m + 1] = fma(-a[i][m], l10, a[i][m + 1]) * r[m + 1];   // L[i][m+1]
+    }
 #pragma unroll
-    for (int i = m + 1; i < 8; ++i)
+    for (int i = m + 2; i < 8; ++i)
 #pragma unroll
-      for (int j = m + 1; j <= i; ++j) a[i][j] = fma(-a[i][m], a[j][m], a[i][j]);
+      for (int j = m + 2; j <= i; ++j)
+        a[i][j] = fma(-a[i][m + 1], a[j][m + 1], fma(-a[i][m], a[j][m], a[i][j]));
+    a[m + 1][m] = l10;
   }
   // T = L^{-1}: T[i][i] = r_i, T[i][j] = -r_i sum_{j<=k<i} L[i][k] T[k][j]
   double tt[8][8];
@@ -97,9 +111,12 @@ __device__ __noinline__ void chol8_inv1(const double *M, int ldm, double *Tout, 
     for (int j = 0; j < 8; ++j) Tout[i * kPL + j] = (j <= i) ? tt[i][j] : 0.0;
 }
 
-// Block Cholesky of sym(Q) (S x S, row-major, global) on one CTA, V = L^{-1} alongside, and
-// Q^{-1} = V^T V (S x S, row-major, global).  Shared memory: fc_smem_bytes.  Returns bad.
-__device__ bool cta_bchol_inv(const double *__restrict__ Q, int S, double *sm, double *__restrict__ Qinv) {
+// Block Cholesky of sym(Q) (S x S, row-major, global) on one CTA with V = L^{-1} alongside, written
+// to Vout (Sp x Sp, row-major; Sp = S rounded up to 8, identity padding) row block by row block as
+// it is formed: only the blocks on and below the block diagonal are written (the diagonal blocks
+// T_p are lower triangular with explicit zeros), so Q^{-1} = V^T V.  Shared memory: fc_smem_bytes.
+// Returns bad.
+__device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, double *__restrict__ Vout) {
   const int nt = (S + 7) >> 3, Sp = nt * 8, LD = ld_frag(Sp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   double *As = sm;                    // [Sp][LD]
@@ -125,25 +142,20 @@ __device__ bool cta_bchol_inv(const double *__restrict__ Q, int S, double *sm, d
   cpa_commit();
   cpa_wait<0>();
   __syncthreads();
-  {
-    // lower tile (ti, tj) per warp iteration; lane -> 2 elements (a, b), (a + 4, b) of the tile
-    const int ntl = nt * (nt + 1) / 2;
-    for (int e = warp; e < ntl; e += kFcThreads / 32) {
-      int ti = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-      while ((ti + 1) * (ti + 2) / 2 <= e) ++ti;
-      while (ti * (ti + 1) / 2 > e) --ti;
-      const int tj = e - ti * (ti + 1) / 2;
+  FCP(44);
+  // lower triangle only (the factorization never reads above the diagonal): row i per warp, all
+  // loads of a row before its stores (the lanes write only lower elements, which no lane reads)
+  for (int i = warp; i < Sp; i += kFcThreads / 32) {
+    double v[4];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int a = (lane >> 3) + 4 * h, b = lane & 7;
-        const int i = 8 * ti + a, j = 8 * tj + b;
-        if (ti == tj && j > i) continue;
-        double v;
-        if (i < S && j < S) v = 0.5 * (As[i * LD + j] + As[j * LD + i]);
-        else v = (i == j) ? 1.0 : 0.0;
-        As[i * LD + j] = v;
-        if (ti == tj) As[j * LD + i] = v;
-      }
+    for (int q = 0; q < 4; ++q) {
+      const int j = lane + 32 * q;
+      v[q] = (i < S && j < S && j <= i) ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : (i == j ? 1.0 : 0.0);
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int j = lane + 32 * q;
+      if (j <= i) As[i * LD + j] = v[q];
     }
   }
   __syncthreads();
@@ -152,54 +164,90 @@ __device__ bool cta_bchol_inv(const double *__restrict__ Q, int S, double *sm, d
   if (threadIdx.x == 0) chol8_inv1(As, LD, Ds, bad);
   FCP(40);
   __syncthreads();
+  if (warp == 0)
+    for (int e = lane; e < 64; e += 32) Vout[(int64_t)(e >> 3) * Sp + (e & 7)] = Ds[(e >> 3) * kPL + (e & 7)];
   FCP(41);
+  // Step p (after the CTA barrier of step p-1):
+  //   warp 0   L_{p+1,p} = A_{p+1,p} T_p^T (its own panel row) -> named-barrier arrive -> the pivot
+  //            block A_{p+1,p+1} -= L_{p+1,p} L_{p+1,p}^T -> T_{p+1} (one lane) -> V_{p+1,p+1}
+  //   workers  copy step p-1's panel into the lower tiles, the rest of the panel L_ip (i >= p+2),
+  //            named barrier (the whole panel is there), trailing update, V's row block p
+  //   CTA barrier
+  // so the pivot chain (warp 0) never waits for the panel copies or the trailing updates of step p.
   for (int p = 0; p < nt; ++p) {
     const double *Tp = Ds + p * 8 * kPL;
     double *Wp = Wp0 + (p & 1) * Sp * kPL;
-    // (alpha) panel L_ip = A_ip T_p^T, i > p (warp 0 takes the next pivot row block)
-    {
-      const int first = (warp == 0) ? p + 1 : p + 2 + (warp - 1);
-      const int step = (warp == 0) ? nt : 7;
-      for (int i = first; i < nt; i += step) {
+    if (warp == 0) {
+      if (p + 1 < nt) {
+        const int q = p + 1;
+        double c[2] = {0.0, 0.0};
+        dmma8_tn(c, As + (8 * q) * LD + 8 * p, LD, Tp, kPL, g, t);
+        frag_store(c, Wp + 8 * q * kPL, kPL, g, t);
+        __syncwarp();
+        asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
+        double d[2];
+        frag_load(d, As + (8 * q) * LD + 8 * q, LD, g, t);
+        const double *pw = Wp + 8 * q * kPL;
+        dmma(d[0], d[1], -pw[g * kPL + t], pw[g * kPL + t]);
+        dmma(d[0], d[1], -pw[g * kPL + 4 + t], pw[g * kPL + 4 + t]);
+        frag_store(d, As + (8 * q) * LD + 8 * q, LD, g, t);
+        __syncwarp();
+        if (lane == 0) chol8_inv1(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
+        __syncwarp();
+        for (int e = lane; e < 64; e += 32)   // V_qq = T_q
+          Vout[(int64_t)(8 * q + (e >> 3)) * Sp + 8 * q + (e & 7)] = Ds[q * 8 * kPL + (e >> 3) * kPL + (e & 7)];
+      } else {
+        asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
+      }
+    } else {
+      // the previous step's panel replaces A_{i,p-1} (read below as L_{p,p-1} by V's row block p)
+      if (p > 0) {
+        const double *Wq = Wp0 + ((p - 1) & 1) * Sp * kPL;
+        for (int e = threadIdx.x - 32; e < (nt - p) * 64; e += kFcThreads - 32) {
+          const int i = 8 * p + (e >> 3), b = e & 7;
+          As[i * LD + 8 * (p - 1) + b] = Wq[i * kPL + b];
+        }
+      }
+      for (int i = p + 2 + (warp - 1); i < nt; i += 7) {   // panel L_ip = A_ip T_p^T, i >= p+2
         double c[2] = {0.0, 0.0};
         dmma8_tn(c, As + (8 * i) * LD + 8 * p, LD, Tp, kPL, g, t);
         frag_store(c, Wp + 8 * i * kPL, kPL, g, t);
       }
-    }
-    if (p == 0) FCP(42);
-    __syncthreads();
-    if (p == 0) FCP(43);
-    if (warp == 0) {
-      // (beta, pivot warp) A_{p+1,p+1} -= L_{p+1,p} L_{p+1,p}^T, then factor it (look-ahead)
-      if (p + 1 < nt) {
-        const int q = p + 1;
-        double c[2];
-        frag_load(c, As + (8 * q) * LD + 8 * q, LD, g, t);
-        const double *pw = Wp + 8 * q * kPL;
-        dmma(c[0], c[1], -pw[g * kPL + t], pw[g * kPL + t]);
-        dmma(c[0], c[1], -pw[g * kPL + 4 + t], pw[g * kPL + 4 + t]);
-        frag_store(c, As + (8 * q) * LD + 8 * q, LD, g, t);
-        __syncwarp();
-        if (lane == 0) chol8_inv1(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
-        __syncwarp();
-      }
-    } else {
-      // (beta, workers) trailing update A_ij -= L_ip L_jp^T, p < j <= i, except (p+1, p+1)
+      asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");
+      // (beta, workers) trailing update A_ij -= L_ip L_jp^T, p < j <= i, except (p+1, p+1); pairs
+      // (ii, jj), jj <= ii < m, enumerated row by row, two tiles per iteration (independent chains)
       const int m = nt - 1 - p;
-      const int npairs = m * (m + 1) / 2;
-      for (int e = warp - 1; e < npairs; e += 7) {
-        int ii = (int)((sqrtf(8.0f * (float)e + 1.0f) - 1.0f) * 0.5f);
-        while ((ii + 1) * (ii + 2) / 2 <= e) ++ii;
-        while (ii * (ii + 1) / 2 > e) --ii;
-        const int jj = e - ii * (ii + 1) / 2;
-        const int i = p + 1 + ii, j = p + 1 + jj;
-        if (i == p + 1 && j == p + 1) continue;
-        double c[2];
-        frag_load(c, As + (8 * i) * LD + 8 * j, LD, g, t);
-        const double *pa = Wp + 8 * i * kPL, *pb = Wp + 8 * j * kPL;
-        dmma(c[0], c[1], -pa[g * kPL + t], pb[g * kPL + t]);
-        dmma(c[0], c[1], -pa[g * kPL + 4 + t], pb[g * kPL + 4 + t]);
-        frag_store(c, As + (8 * i) * LD + 8 * j, LD, g, t);
+      auto norm = [](int &ii, int &jj) {
+        while (jj > ii) {
+          jj -= ii + 1;
+          ++ii;
+        }
+      };
+      int ii = 0, jj = warp - 1;
+      norm(ii, jj);
+      while (ii < m) {
+        int ii2 = ii, jj2 = jj + 7;
+        norm(ii2, jj2);
+        const bool one = !(ii == 0 && jj == 0), two = ii2 < m;
+        const int i1 = p + 1 + ii, j1 = p + 1 + jj, i2 = p + 1 + ii2, j2 = p + 1 + jj2;
+        double c1[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+        if (one) frag_load(c1, As + (8 * i1) * LD + 8 * j1, LD, g, t);
+        if (two) frag_load(c2, As + (8 * i2) * LD + 8 * j2, LD, g, t);
+        if (one) {
+          const double *pa = Wp + 8 * i1 * kPL, *pb = Wp + 8 * j1 * kPL;
+          dmma(c1[0], c1[1], -pa[g * kPL + t], pb[g * kPL + t]);
+          dmma(c1[0], c1[1], -pa[g * kPL + 4 + t], pb[g * kPL + 4 + t]);
+        }
+        if (two) {
+          const double *pa = Wp + 8 * i2 * kPL, *pb = Wp + 8 * j2 * kPL;
+          dmma(c2[0], c2[1], -pa[g * kPL + t], pb[g * kPL + t]);
+          dmma(c2[0], c2[1], -pa[g * kPL + 4 + t], pb[g * kPL + 4 + t]);
+        }
+        if (one) frag_store(c1, As + (8 * i1) * LD + 8 * j1, LD, g, t);
+        if (two) frag_store(c2, As + (8 * i2) * LD + 8 * j2, LD, g, t);
+        ii = ii2;
+        jj = jj2 + 7;
+        norm(ii, jj);
       }
       // (beta, workers) V row block p: V_pk = -T_p sum_{k<=m<p} L_pm V_mk (V_kk = T_k), stored
       // transposed in the upper tile (k, p): As[8k + a][8p + b] = V[8p + b][8k + a]
@@ -216,57 +264,14 @@ __device__ bool cta_bchol_inv(const double *__restrict__ Q, int S, double *sm, d
         __syncwarp();
 #pragma unroll
         for (int e2 = 0; e2 < 2; ++e2) As[(8 * k + 2 * t + e2) * LD + 8 * p + g] = -v[e2];
+        *(double2 *)(Vout + (int64_t)(8 * p + g) * Sp + 8 * k + 2 * t) = make_double2(-v[0], -v[1]);   // V_pk
       }
     }
     __syncthreads();
     FCP(4 + p);
-    // (gamma) L_ip replaces A_ip; the next alpha reads column p+1 only
-    for (int e = threadIdx.x; e < (nt - 1 - p) * 64; e += kFcThreads) {
-      const int i = 8 * (p + 1) + (e >> 3), b = e & 7;
-      As[i * LD + 8 * p + b] = Wp[i * kPL + b];
-    }
   }
   __syncthreads();
   FCP(2);
-  // Q^{-1} = V^T V, tile (r, c), r <= c: sum_{b >= c} V_br^T V_bc, with V_bb = T_b (Ds) and, for b > k,
-  // V_bk stored transposed in the upper tile (k, b): V_bk[kk][n] = As[8k + n][8b + kk].  A warp owns a
-  // column tile c and keeps the accumulators of every r <= c (independent DMMA chains).
-  for (int c = warp; c < nt; c += kFcThreads / 32) {
-    double acc[16][2];
-#pragma unroll
-    for (int r = 0; r < 16; ++r) acc[r][0] = acc[r][1] = 0.0;
-    // b = c: r < c: V_cr^T T_c (V_cr^T rows at As[8r][8c]); r = c: T_c^T T_c
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      if (r < c) dmma8_nn(acc[r], As + (8 * r) * LD + 8 * c, LD, Ds + c * 8 * kPL, kPL, g, t);
-      else if (r == c) dmma8_tnn(acc[r], Ds + r * 8 * kPL, kPL, Ds + c * 8 * kPL, kPL, g, t);
-    }
-    for (int bb = c + 1; bb < nt; ++bb) {   // B = V_bc (transposed rows As[8c][8bb]), fragments reused over r
-      const double *pb = As + (8 * c) * LD + 8 * bb;
-      const double b0 = pb[g * LD + t], b1 = pb[g * LD + 4 + t];
-#pragma unroll
-      for (int r = 0; r < 16; ++r) {
-        if (r <= c) {
-          const double *pa = As + (8 * r) * LD + 8 * bb;   // A = V_br^T rows
-          dmma(acc[r][0], acc[r][1], pa[g * LD + t], b0);
-          dmma(acc[r][0], acc[r][1], pa[g * LD + 4 + t], b1);
-        }
-      }
-    }
-#pragma unroll
-    for (int r = 0; r < 16; ++r) {
-      if (r > c) continue;
-      const int row = 8 * r + g;
-#pragma unroll
-      for (int e2 = 0; e2 < 2; ++e2) {
-        const int col = 8 * c + 2 * t + e2;
-        if (row < S && col < S) {
-          Qinv[(int64_t)row * S + col] = acc[r][e2];
-          if (r != c) Qinv[(int64_t)col * S + row] = acc[r][e2];
-        }
-      }
-    }
-  }
   FCP(3);
   return bad;
 }
@@ -276,29 +281,101 @@ size_t fc_smem_bytes(int S) {
   return sizeof(double) * ((size_t)Sp * ld_frag(Sp) + (size_t)(nt * 8 + 2 * Sp + 64) * kPL);
 }
 
-// Q^{-1} for one SPD matrix (S <= STR_MAXW) on one CTA.
+// The factor V = L^{-1} of one SPD matrix (S <= STR_MAXW) on one CTA.
 __global__ void __launch_bounds__(kFcThreads, 1)
-    k_spd_inv_chol(const double *__restrict__ Q, int S, double *__restrict__ Qinv, int *info) {
+    k_spd_factor(const double *__restrict__ Q, int S, double *__restrict__ V, int *info) {
   PDL_PROLOGUE();
   extern __shared__ __align__(16) double fsm[];
-  const bool bad = cta_bchol_inv(Q, S, fsm, Qinv);
+  const bool bad = cta_bchol(Q, S, fsm, V);
   if (bad && threadIdx.x == 0 && info) atomicExch(info, 1);
 }
 
-size_t spd_inv_ws_doubles(int S) {
-  const int nt = (S + 7) / 8, Sp = 8 * nt;
-  (void)nt;
+size_t spd_factor_doubles(int S) {
+  const int Sp = (S + 7) / 8 * 8;
   return (size_t)Sp * Sp;
 }
 
-void launch_spd_inv_chol(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s) {
+void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_t s) {
+  if (g_dbg_skip & 1) return;
   static PerDeviceOnce once;
   once_per_device(once, [] {
-    cudaFuncSetAttribute(k_spd_inv_chol, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem_bytes(STR_MAXW));
-    prefer_max_smem(k_spd_inv_chol);
+    cudaFuncSetAttribute(k_spd_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem_bytes(STR_MAXW));
+    prefer_max_smem(k_spd_factor);
   });
-  (void)ws;
-  pdl_launch(kPdlInv, k_spd_inv_chol, dim3(1), dim3(kFcThreads), fc_smem_bytes(S), s, Q, S, Qinv, info);
+  pdl_launch(kPdlInv, k_spd_factor, dim3(1), dim3(kFcThreads), fc_smem_bytes(S), s, Q, S, V, info);
+}
+
+// ------------------------------------------------------------------------------------------
+// out = P Q^{-1} = (P V^T) V for I rows of P (I x S, row-major) with the factor V of
+// launch_spd_factor (the G_n(2) = P_n Q_n^{-1} of Alg. 4 l.17 P:379 and G_N^new = M_N (H^{≠N}_<2>)^{-1}
+// of l.9 P:370).  One CTA per 8-row tile: V's lower blocks staged in shared memory (cp.async), then
+// Y = P V^T column tile by column tile over the 8 warps (Y[:, c] = sum_{k <= c} P[:, k] V[c][k]),
+// then out = Y V (out[:, c] = sum_{k >= c} Y[:, k] V[k][c]).
+__global__ void __launch_bounds__(kFcThreads, 1)
+    k_rows_solve(const double *__restrict__ P, const double *__restrict__ V, int S, int64_t I,
+                 double *__restrict__ out) {
+  PDL_PROLOGUE();
+  extern __shared__ __align__(16) double rsm[];
+  const int nt = (S + 7) >> 3, Sp = nt * 8, LD = ld_frag(Sp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  double *Vs = rsm;              // [Sp][LD]  (blocks on and below the diagonal)
+  double *Ps = Vs + Sp * LD;     // [8][LD]  the P rows, then Y
+  const int64_t r0 = (int64_t)blockIdx.x * 8;
+  const int nr = (int)((I - r0) < 8 ? (I - r0) : 8);
+  for (int e = threadIdx.x; e < Sp * (Sp / 2); e += kFcThreads) {
+    const int i = e / (Sp / 2), j = 2 * (e - i * (Sp / 2));
+    if ((j >> 3) <= (i >> 3)) cpa16cg(Vs + i * LD + j, V + (int64_t)i * Sp + j);
+  }
+  for (int e = threadIdx.x; e < 8 * Sp; e += kFcThreads) {
+    const int i = e / Sp, j = e - (e / Sp) * Sp;
+    if (i < nr && j < S) cpa8(Ps + i * LD + j, P + (r0 + i) * S + j);
+    else Ps[i * LD + j] = 0.0;
+  }
+  cpa_commit();
+  cpa_wait<0>();
+  __syncthreads();
+  double y[2][2];
+  int cc[2] = {-1, -1};
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {   // Y[:, c] = sum_{k <= c} P[:, k] V[c][k]  (B[k][n] = V[n][k]: tn, V rows at c)
+    const int c = warp + 8 * q;
+    y[q][0] = y[q][1] = 0.0;
+    if (c < nt) {
+      cc[q] = c;
+      for (int k = 0; k <= c; ++k) dmma8_tn(y[q], Ps + 8 * k, LD, Vs + (8 * c) * LD + 8 * k, LD, g, t);
+    }
+  }
+  __syncthreads();   // every warp has read P
+#pragma unroll
+  for (int q = 0; q < 2; ++q)
+    if (cc[q] >= 0) frag_store(y[q], Ps + 8 * cc[q], LD, g, t);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 2; ++q) {   // out[:, c] = sum_{k >= c} Y[:, k] V[k][c]  (B = V rows at k: nn)
+    const int c = cc[q];
+    if (c < 0) continue;
+    double o[2] = {0.0, 0.0};
+    for (int k = c; k < nt; ++k) dmma8_nn(o, Ps + 8 * k, LD, Vs + (8 * k) * LD + 8 * c, LD, g, t);
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = 8 * c + 2 * t + e;
+      if (g < nr && col < S) out[(r0 + g) * S + col] = o[e];
+    }
+  }
+}
+
+void launch_rows_solve(const double *P, const double *V, int S, int64_t I, double *out, cudaStream_t s) {
+  if (g_dbg_skip & 32) return;
+  if (I <= 0) return;
+  const int Sp = (S + 7) / 8 * 8;
+  const size_t smem = sizeof(double) * (size_t)(Sp + 8) * ld_frag(Sp);
+  static PerDeviceOnce once;
+  once_per_device(once, [] {
+    cudaFuncSetAttribute(k_rows_solve, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(sizeof(double) * (STR_MAXW + 8) * ld_frag(STR_MAXW)));
+    prefer_max_smem(k_rows_solve);
+  });
+  pdl_launch(kPdlDmma, k_rows_solve, dim3((unsigned)cdiv(I, 8)), dim3(kFcThreads), smem, s, P, V, S, I, out);
 }
 
 }  // namespace strb200

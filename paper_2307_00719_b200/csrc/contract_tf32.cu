@@ -554,7 +554,7 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
   const int Np = npad_of(W);
   const int64_t kt1 = cdiv(h->Rr, 32);
   const int64_t kt2 = tn * cdiv(h->L, 32);
-  size_t tiles = (size_t)std::max(kt1, kt2) * 2 * Np * 32 * sizeof(float);
+  const size_t tiles1 = (size_t)kt1 * 2 * Np * 32 * sizeof(float), tiles2 = (size_t)kt2 * 2 * Np * 32 * sizeof(float);
   size_t yf = ((size_t)std::max<int64_t>(h->L * tn, h->Rr) * W * sizeof(float) + 15) / 16 * 16;
   auto grow = [&](DevBuf &b, size_t bytes) -> bool {
     if (b.bytes >= bytes) return true;
@@ -568,7 +568,7 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
     b.bytes = bytes;
     return true;
   };
-  if (!grow(h->tab_split, tiles) || !grow(h->tf_part, yf) || !grow(h->tf_part2, yf)) {
+  if (!grow(h->tab_split, tiles1) || !grow(h->tab_split2, tiles2) || !grow(h->tf_part, yf) || !grow(h->tf_part2, yf)) {
     h->err = "cudaMalloc failed (3xTF32 workspace)";
     return STR_E_OOM;
   }
@@ -666,15 +666,15 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   const int64_t blocks = cdiv(p.mtiles, kMT);   // M-blocks (tile pairs; pass 1 pairs across t)
   p.KT = pass == 1 ? cdiv(Rr, kBK) : tn * p.nlb;
   p.U = blocks * p.KT;
-  // persistent grid: every SM but the kInvNC that the side stream's cluster inverse occupies while
-  // a pass runs (a pass CTA waiting for such an SM would hold the whole pass back)
+  // persistent grid: every SM but the kSideSMs that the side stream's factorization occupies while a
+  // pass runs (a pass CTA waiting for such an SM would hold the whole pass back)
   const int nsm = h->nsm;
-  int maxg = std::max(1, nsm - kInvClusterCTAs);
+  int maxg = std::max(1, nsm - kSideSMs);
   if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(nsm, atoi(ev)));   // tuning knob
   int grid = (int)std::min<int64_t>(maxg, p.U);
   p.upc = cdiv(p.U, grid);
   grid = (int)cdiv(p.U, p.upc);
-  p.Btiles = (const float *)h->tab_split.p;
+  p.Btiles = (const float *)(pass == 1 ? h->tab_split.p : h->tab_split2.p);
   p.Y = Y;
   p.dbg = h->tf_dbg ? h->tf_dbg + (pass - 1) * str_state::kTfDbgWords : nullptr;
   p.dbg_flags = 0;

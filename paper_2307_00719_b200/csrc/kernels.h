@@ -18,16 +18,19 @@ extern int g_dbg_skip;
 #else
 constexpr int g_dbg_skip = 0;
 #endif
-constexpr int kInvClusterCTAs = 4;   // CTAs of the cluster inverse (k_spd_inv_cl)
+// SMs the contraction's persistent grid leaves to the side stream's concurrent kernels (the Gram
+// chain links and the single-CTA factorizations run beside a pass)
+constexpr int kSideSMs = 4;
 
 // kernels_chain.cu
 void launch_set_identity(double *A, int n, cudaStream_t s);
-// Q^{-1} of an SPD S x S matrix (S <= STR_MAXW); ws: spd_inv_ws_doubles(S) doubles of scratch
-// (V = L^{-1} and the pivot-block inverses of the block LDL^T), not shared by concurrent calls.
-void launch_spd_inv(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s);
-size_t spd_inv_ws_doubles(int S);
-void launch_spd_inv_chol(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s);
-void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s);
+// chain_factor.cu: the factor V = L^{-1} (Sp x Sp, Sp = S rounded up to 8, blocks on and below the
+// diagonal; sym(Q) = L L^T) of an SPD S x S matrix (S <= STR_MAXW), so Q^{-1} = V^T V; a non-positive
+// pivot sets *info = 1.
+void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_t s);
+size_t spd_factor_doubles(int S);
+// out = P Q^{-1} = (P V^T) V for I rows of P (I x S, row-major).
+void launch_rows_solve(const double *P, const double *V, int S, int64_t I, double *out, cudaStream_t s);
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s);
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
 void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);

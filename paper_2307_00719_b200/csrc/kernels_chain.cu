@@ -1,9 +1,5 @@
 // kernels_chain.cu — the fp64 kernels on the serial part of an STR batch (everything R^2-sized):
-//   k_spd_inv      Q^{-1} of the SPD normal-equation matrix by an in-place symmetric sweep
-//                  (Gauss-Jordan without pivoting; pivots are Schur-complement diagonals, > 0 for
-//                  SPD Q), one CTA, register-resident 4x4 tiles of the lower triangle;
-//   (rows_mm)      G = P Q^{-1} row blocks (the "G_n(2) = P_n Q_n^†" of Alg. 4 l.9/l.17);
-//   k_chain_gemm   Gram-chain links (×_{2,4}^{1,3} as a matrix product, Def. 5 / Prop. 1)
+//   k_chain_gemm_dmma Gram-chain links (×_{2,4}^{1,3} as a matrix product, Def. 5 / Prop. 1)
 //                  with the Q_n (+)= H_<2> epilogue (Alg. 4 l.16);
 //   k_gram_z2      core Grams Z_n (Alg. 4 l.2/l.18);
 //   k_absorb2      second-level contractions of the two-pass intermediates with core slices;
@@ -14,12 +10,11 @@
 #include <cooperative_groups.h>
 
 #include "common.cuh"
+#include "dmma.cuh"
 #include "kernels.h"
 #include "tc_ptx.cuh"
 
 namespace strb200 {
-
-
 
 #ifdef STR_DIAG
 int g_dbg_skip = 0;
@@ -45,521 +40,6 @@ __device__ __forceinline__ void cp_async_wait_all() {
 }
 
 // ------------------------------------------------------------------------------------------
-// Q^{-1} of an SPD matrix (S <= 128) by the blocked symmetric sweep (Gauss-Jordan without
-// pivoting on 8x8 pivot blocks; the pivot blocks are Schur complements of an SPD matrix, hence
-// SPD).  Step kb with pivot block P (tile kb), V = A[:, P], D = A_PP^{-1}, W = V D:
-//   A_RR -= W_R V_R^T,   A_RP = W_R,   A_PR = W_R^T,   A_PP = -D          (R = the other indices)
-// after the last step A = -Q^{-1}.  The lower-triangle 8x8 tiles live in registers as FP64
-// tensor-core accumulator fragments (mma.sync m8n8k4 f64: lane holds C[lane/4][2(lane%4)+{0,1}]),
-// so the rank-8 update of a tile is two DMMAs with W and V fragments read from shared memory.
-// Warp w < nt owns diagonal tile (w, w) only; the off-diagonal tiles are spread over the other
-// warps.  Look-ahead: in step kb the owner of tile (kb+1, kb+1) updates it first and inverts it at
-// once (8-pivot scalar sweep in registers, shuffles) while the other warps update their tiles;
-// the next pivot column block V' is published by its owners, then all threads form W' = V' D'.
-// Q is staged in shared memory (coalesced) and symmetrized on load ((Q + Q^T)/2, DESIGN.md
-// reading R5); the result goes out through shared memory as well.  A non-positive or NaN pivot
-// sets *info = 1.
-constexpr int kInvThreads = 1024;              // 32 warps
-#ifdef INV_PROBE
-__device__ long long g_inv_probe[8];
-#endif
-
-__device__ __forceinline__ void dmma884(double &c0, double &c1, double a, double b) {
-  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-               : "+d"(c0), "+d"(c1)
-               : "d"(a), "d"(b));
-}
-
-__device__ __forceinline__ double rcp_nr(double d) {
-  // reciprocal: hardware approximation + two Newton steps (full double precision for normal d)
-  double r;
-  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(d));
-  r = fma(r, fma(-d, r, 1.0), r);
-  r = fma(r, fma(-d, r, 1.0), r);
-  return r;
-}
-
-// In-register inverse of the SPD 8x8 block held by one warp in accumulator layout
-// (lane (g, t) holds M[g][2t], M[g][2t+1]): 8-pivot scalar sweep; returns -M^{-1} in d.
-__device__ __forceinline__ bool warp_sweep8(double (&d)[2], int g, int tg) {
-  bool bad = false;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const int src = m >> 1;
-    const double piv = __shfl_sync(0xffffffffu, d[m & 1], m * 4 + src);
-    const double vg = __shfl_sync(0xffffffffu, d[m & 1], g * 4 + src);
-    const double v0 = __shfl_sync(0xffffffffu, d[m & 1], (2 * tg) * 4 + src);
-    const double v1 = __shfl_sync(0xffffffffu, d[m & 1], (2 * tg + 1) * 4 + src);
-    bad = bad || !(piv > 0.0);
-    const double p = rcp_nr(piv);
-    const double sg = vg * p;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int j = 2 * tg + e;
-      const double vj = e ? v1 : v0;
-      double nv = fma(-sg, vj, d[e]);
-      if (j == m) nv = sg;
-      if (g == m) nv = vj * p;
-      if (g == m && j == m) nv = -p;
-      d[e] = nv;
-    }
-  }
-  return bad;
-}
-
-// The same symmetric sweep in ONE thread's registers on an 8 x 8 SPD block in shared memory
-// (row-major, ld 8, both triangles): M <- -M^{-1}.  No shuffles on the pivot chain (one reciprocal
-// and one dependent update per pivot), one copy of the code.  Returns true on a bad pivot.
-__device__ __noinline__ bool sweep8_1(double *M) {
-  double a[8][8];
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j <= i; ++j) a[i][j] = M[i * 8 + j];
-  bool bad = false;
-#pragma unroll
-  for (int m = 0; m < 8; ++m) {
-    const double piv = a[m][m];
-    bad = bad || !(piv > 0.0);
-    const double p = rcp_nr(piv);
-    double col[8], sc[8];
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      col[i] = (i > m) ? a[i][m] : a[m][i];
-      sc[i] = col[i] * p;
-    }
-#pragma unroll
-    for (int i = 0; i < 8; ++i)
-#pragma unroll
-      for (int j = 0; j <= i; ++j)
-        if (i != m && j != m) a[i][j] = fma(-sc[i], col[j], a[i][j]);
-#pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      if (i > m) a[i][m] = sc[i];
-      else if (i < m) a[m][i] = sc[i];
-    }
-    a[m][m] = -p;
-  }
-#pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) M[i * 8 + j] = (j <= i) ? a[i][j] : a[j][i];
-  return bad;
-}
-
-// SLOTS = off-diagonal tiles per warp: ceil(nt(nt-1)/2 / (32 - nt)) = 5 for nt <= 13, 8 for nt <= 16
-// The step loop runs from kb = -1 (the prologue: publish V_0, invert tile (0,0)) so that the pivot
-// sweep is instantiated once; tile coordinates come from a shared table (no register arrays).
-// Row stride of the V / W panels is kVS doubles (12: the 8-byte fragment loads of a half-warp hit
-// 32 distinct banks).
-constexpr int kVS = 12;
-template <int kInvMaxSlots>
-__global__ void __launch_bounds__(kInvThreads, 1) k_spd_inv(const double *__restrict__ Q, int S,
-                                                              double *__restrict__ Qinv, int *info) {
-  extern __shared__ __align__(16) double ism[];
-  double *Qs = ism;                                   // S x S staging (in and out)
-  double *Vs0 = Qs + ((S * S + 1) & ~1);              // [2][128][kVS] pivot column blocks V[i][m]
-  double *Ws = Vs0 + 2 * STR_MAXW * kVS;              // [128][kVS] W = V D
-  double *Ds0 = Ws + STR_MAXW * kVS;                  // [2][64] D = A_PP^{-1}
-  __shared__ int s_bad;
-  __shared__ short s_tile[kInvMaxSlots][32][2];       // (I, J) of slot sl of warp w; I = -1: none
-  const int nt = (S + 7) >> 3, Sp = nt * 8;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tg = lane & 3;
-  const int noff = nt * (nt - 1) / 2, nwoff = 32 - nt;
-  if (threadIdx.x == 0) s_bad = 0;
-  if (threadIdx.x < kInvMaxSlots * 32) {
-    const int sl = threadIdx.x / 32, w = threadIdx.x % 32;
-    int I = -1, J = 0;
-    if (w < nt) {
-      if (sl == 0) I = J = w;
-    } else {
-      const int tt = (w - nt) + nwoff * sl;          // off-diagonal tiles, row-major (I > J)
-      if (tt < noff) {
-        I = 1;
-        while (I * (I + 1) / 2 <= tt) ++I;
-        J = tt - I * (I - 1) / 2;
-      }
-    }
-    s_tile[sl][w][0] = (short)I;
-    s_tile[sl][w][1] = (short)J;
-  }
-#ifdef INV_PROBE
-  long long tp0 = clock64();
-#endif
-  for (int e = threadIdx.x; e < S * S; e += kInvThreads) cp_async8(Qs + e, Q + e);
-  cp_async_wait_all();
-  __syncthreads();
-  // ---- owned tiles in registers (accumulator layout), symmetrized on load
-  double c[kInvMaxSlots][2];
-#pragma unroll
-  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
-    const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
-      c[sl][e] = (I >= 0 && i < S && j < S) ? 0.5 * (Qs[i * S + j] + Qs[j * S + i]) : (i == j ? 1.0 : 0.0);
-    }
-  }
-#ifdef INV_PROBE
-  long long tp1 = clock64();
-  long long pa = 0, pb = 0, pc = 0, pd = 0;
-#endif
-  const bool diag = warp < nt;
-  for (int kb = -1; kb < nt; ++kb) {
-#ifdef INV_PROBE
-    long long q0 = clock64();
-#endif
-    const int cur = (kb + 2) & 1, nxt = cur ^ 1;
-    const double *V = Vs0 + cur * STR_MAXW * kVS;
-    double *Vn = Vs0 + nxt * STR_MAXW * kVS;
-    const double *D = Ds0 + cur * 64;
-    double *Dn = Ds0 + nxt * 64;
-    const int kn = kb + 1;
-    if (diag && warp == kn) {
-      // look-ahead warp: bring its tile (kn, kn) up to date, publish it, invert it at once
-      if (kb >= 0) {
-        const double a0 = Ws[(8 * kn + g) * kVS + tg], b0 = V[(8 * kn + g) * kVS + tg];
-        const double a1 = Ws[(8 * kn + g) * kVS + 4 + tg], b1 = V[(8 * kn + g) * kVS + 4 + tg];
-        dmma884(c[0][0], c[0][1], -a0, b0);
-        dmma884(c[0][0], c[0][1], -a1, b1);
-      }
-      Vn[(8 * kn + g) * kVS + 2 * tg] = c[0][0];
-      Vn[(8 * kn + g) * kVS + 2 * tg + 1] = c[0][1];
-      double d[2] = {c[0][0], c[0][1]};
-      if (warp_sweep8(d, g, tg) && lane == 0) s_bad = 1;
-      Dn[g * 8 + 2 * tg] = -d[0];
-      Dn[g * 8 + 2 * tg + 1] = -d[1];
-    } else {
-#pragma unroll
-      for (int sl = 0; sl < kInvMaxSlots; ++sl) {
-        const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
-        if (I < 0) continue;
-        if (kb >= 0) {
-          if (I != kb && J != kb) {
-            const double a0 = Ws[(8 * I + g) * kVS + tg], b0 = V[(8 * J + g) * kVS + tg];
-            const double a1 = Ws[(8 * I + g) * kVS + 4 + tg], b1 = V[(8 * J + g) * kVS + 4 + tg];
-            dmma884(c[sl][0], c[sl][1], -a0, b0);
-            dmma884(c[sl][0], c[sl][1], -a1, b1);
-          } else if (I != kb) {          // J == kb: A_RP = W_R
-            c[sl][0] = Ws[(8 * I + g) * kVS + 2 * tg];
-            c[sl][1] = Ws[(8 * I + g) * kVS + 2 * tg + 1];
-          } else if (J != kb) {          // I == kb: A_PR = W_R^T
-            c[sl][0] = Ws[(8 * J + 2 * tg) * kVS + g];
-            c[sl][1] = Ws[(8 * J + 2 * tg + 1) * kVS + g];
-          } else {                        // pivot block: -D
-            c[sl][0] = -D[g * 8 + 2 * tg];
-            c[sl][1] = -D[g * 8 + 2 * tg + 1];
-          }
-        }
-        if (kn < nt) {
-          if (J == kn) {                 // (I == kn == J is the look-ahead warp's tile)
-            Vn[(8 * I + g) * kVS + 2 * tg] = c[sl][0];
-            Vn[(8 * I + g) * kVS + 2 * tg + 1] = c[sl][1];
-          } else if (I == kn) {          // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
-            Vn[(8 * J + 2 * tg) * kVS + g] = c[sl][0];
-            Vn[(8 * J + 2 * tg + 1) * kVS + g] = c[sl][1];
-          }
-        }
-      }
-    }
-#ifdef INV_PROBE
-    long long q1 = clock64();
-#endif
-    __syncthreads();
-#ifdef INV_PROBE
-    long long q2 = clock64();
-#endif
-    if (kn < nt) {
-      if (threadIdx.x < Sp * 8) {
-        const int e = threadIdx.x, i = e >> 3, m = e & 7;
-        double acc = 0.0;
-#pragma unroll
-        for (int l = 0; l < 8; ++l) acc = fma(Vn[i * kVS + l], Dn[l * 8 + m], acc);
-        Ws[i * kVS + m] = acc;
-      }
-#ifdef INV_PROBE
-      pc += clock64() - q2;
-#endif
-      __syncthreads();
-    }
-#ifdef INV_PROBE
-    pa += q1 - q0;
-    pb += q2 - q1;
-    pd += clock64() - q0;
-    if (warp == (kn < nt ? kn : 0) && lane == 0) {   // the look-ahead warp of this step
-      atomicAdd((unsigned long long *)&g_inv_probe[4], (unsigned long long)(q1 - q0));
-    }
-#endif
-  }
-#ifdef INV_PROBE
-  if (threadIdx.x == 32 * 20) { g_inv_probe[3] = pa; g_inv_probe[5] = pb; g_inv_probe[6] = pc; g_inv_probe[7] = pd; }
-  long long tp2 = clock64();
-#endif
-  if (threadIdx.x == 0 && s_bad && info) atomicExch(info, 1);
-  // ---- -A -> Qinv through shared memory (both triangles), coalesced store
-#pragma unroll
-  for (int sl = 0; sl < kInvMaxSlots; ++sl) {
-    const int I = s_tile[sl][warp][0], J = s_tile[sl][warp][1];
-    if (I < 0) continue;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
-      if (i < S && j < S && (I != J || j <= i)) {
-        const double xv = -c[sl][e];
-        Qs[i * S + j] = xv;
-        Qs[j * S + i] = xv;
-      }
-    }
-  }
-  __syncthreads();
-  for (int e = threadIdx.x; e < S * S; e += kInvThreads) Qinv[e] = Qs[e];
-#ifdef INV_PROBE
-  __syncthreads();
-  if (threadIdx.x == 0) { g_inv_probe[0] = tp1 - tp0; g_inv_probe[1] = tp2 - tp1; g_inv_probe[2] = clock64() - tp2; }
-#endif
-}
-
-size_t spd_inv_smem(int S) {
-  return sizeof(double) * ((size_t)((S * S + 1) & ~1) + 3 * STR_MAXW * kVS + 2 * 64);
-}
-
-// ------------------------------------------------------------------------------------------
-// Q^{-1} by the same blocked symmetric sweep, spread over a cluster of kInvNC CTAs (distributed
-// shared memory).  CTA c owns the lower-triangle tile rows I = c (mod kInvNC) in registers (warp 0:
-// its diagonal tiles; warps 1-7: its off-diagonal tiles).  Step kb: every CTA forms W = V D for all
-// row blocks from its local copy of the pivot panel V and pivot inverse D, updates its tiles,
-// and the owners of the next pivot column write their tiles (the next panel V') into EVERY CTA's
-// shared memory; the owner of the next pivot block updates it first, inverts it (8-pivot sweep)
-// and broadcasts D'.  One cluster barrier (release / acquire) ends the step.  The FP64 update
-// work per step is split four ways, and the pivot sweep runs on an SM whose pipe carries only a
-// quarter of the trailing update.
-constexpr int kInvNC = kInvClusterCTAs;   // CTAs per cluster
-constexpr int kInvCThreads = 256;  // 8 warps
-constexpr int kInvCSlots = 6;      // off-diagonal tiles per warp (nt <= 16: <= 36 per CTA over 7 warps)
-constexpr int kInvCDiag = 4;       // diagonal tiles of warp 0 (nt <= 16)
-
-__global__ void __cluster_dims__(kInvNC, 1, 1) __launch_bounds__(kInvCThreads, 1)
-    k_spd_inv_cl(const double *__restrict__ Q, int S, double *__restrict__ Qinv, int *info) {
-  PDL_PROLOGUE();
-  namespace cg = cooperative_groups;
-  cg::cluster_group cl = cg::this_cluster();
-  __shared__ __align__(16) double Vb[2][STR_MAXW * kVS];   // pivot panels V (double-buffered)
-  __shared__ __align__(16) double Wb[STR_MAXW * kVS];      // W = V D
-  __shared__ __align__(16) double Db[2][64];               // pivot inverses D
-  __shared__ short s_off[7][kInvCSlots][2];                // off-diagonal tiles of warps 1-7
-  __shared__ __align__(16) double sw8[64];                  // the pivot block of the look-ahead sweep
-  __shared__ int s_bad8;
-  const int c = (int)cl.block_rank();
-  const int nt = (S + 7) >> 3;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tg = lane & 3;
-  if (threadIdx.x == 0) {
-    int t = 0;
-    for (int w = 0; w < 7; ++w)
-      for (int sl = 0; sl < kInvCSlots; ++sl) s_off[w][sl][0] = -1;
-    for (int I = c; I < nt; I += kInvNC)
-      for (int J = 0; J < I; ++J, ++t) {
-        s_off[t % 7][t / 7][0] = (short)I;
-        s_off[t % 7][t / 7][1] = (short)J;
-      }
-  }
-  __syncthreads();
-  // owned tiles -> registers (symmetrized, identity padding beyond S)
-  constexpr int NSL = kInvCSlots > kInvCDiag ? kInvCSlots : kInvCDiag;
-  int TI[NSL], TJ[NSL];
-  double cc[NSL][2];
-#pragma unroll
-  for (int sl = 0; sl < NSL; ++sl) {
-    int I = -1, J = -1;
-    if (warp == 0) {
-      if (sl < kInvCDiag && c + kInvNC * sl < nt) I = J = c + kInvNC * sl;
-    } else if (sl < kInvCSlots) {
-      I = s_off[warp - 1][sl][0];
-      J = s_off[warp - 1][sl][1];
-    }
-    TI[sl] = __shfl_sync(0xffffffffu, I, 0);
-    TJ[sl] = __shfl_sync(0xffffffffu, J, 0);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = 8 * TI[sl] + g, j = 8 * TJ[sl] + 2 * tg + e;
-      cc[sl][e] = (TI[sl] >= 0 && i < S && j < S) ? 0.5 * (Q[(int64_t)i * S + j] + Q[(int64_t)j * S + i])
-                                                 : (i == j ? 1.0 : 0.0);
-    }
-  }
-  // broadcast helpers: write 2 doubles of a panel / D entry into every CTA of the cluster
-  auto put2 = [&](double *local, int idx, double v0, double v1) {
-#pragma unroll
-    for (int r = 0; r < kInvNC; ++r) {
-      double *rem = cl.map_shared_rank(local, r);
-      rem[idx] = v0;
-      rem[idx + 1] = v1;
-    }
-  };
-  auto put1 = [&](double *local, int idx, double v) {
-#pragma unroll
-    for (int r = 0; r < kInvNC; ++r) cl.map_shared_rank(local, r)[idx] = v;
-  };
-  bool bad = false;
-  cl.sync();   // every CTA's shared memory exists before the first remote store
-#ifdef INV_PROBE
-  long long pw = 0, pu = 0, pb = 0, ps = 0;
-#endif
-  for (int kb = -1; kb < nt; ++kb) {
-#ifdef INV_PROBE
-    const long long q0 = clock64();
-#endif
-    const int cur = (kb + 2) & 1, nxt = cur ^ 1, kn = kb + 1;
-    const double *V = Vb[cur];
-    double *Vn = Vb[nxt];
-    const double *D = Db[cur];
-    double *Dn = Db[nxt];
-    // W = V D for a row block (DMMA: A = V block rows, B = D) into Wb
-    auto wrow = [&](int I) {
-      double w0 = 0.0, w1 = 0.0;
-      dmma884(w0, w1, V[(8 * I + g) * kVS + tg], D[tg * 8 + g]);
-      dmma884(w0, w1, V[(8 * I + g) * kVS + 4 + tg], D[(4 + tg) * 8 + g]);
-      Wb[(8 * I + g) * kVS + 2 * tg] = w0;
-      Wb[(8 * I + g) * kVS + 2 * tg + 1] = w1;
-    };
-    if (kb >= 0 && warp > 0) {
-      // warps 1-7: every row block (the pivot-row / pivot-column cases read other rows), then a
-      // named barrier among these 224 threads only: warp 0 (the diagonal tiles, the look-ahead
-      // sweep) forms the rows it needs itself and never waits for this phase
-      for (int I = warp - 1; I < nt; I += kInvCThreads / 32 - 1) wrow(I);
-      asm volatile("bar.sync 1, %0;" ::"n"(kInvCThreads - 32) : "memory");
-    }
-#ifdef INV_PROBE
-    const long long q1 = clock64();
-#endif
-    // one tile: step-kb update, then its share of the next panel
-    auto tile = [&](double (&t)[2], int I, int J) {
-      if (kb >= 0) {
-        if (I != kb && J != kb) {
-          const double *wp = Wb + (8 * I + g) * kVS + tg, *vp = V + (8 * J + g) * kVS + tg;
-          dmma884(t[0], t[1], -wp[0], vp[0]);
-          dmma884(t[0], t[1], -wp[4], vp[4]);
-        } else if (I != kb) {   // J == kb: A_RP = W_R
-          t[0] = Wb[(8 * I + g) * kVS + 2 * tg];
-          t[1] = Wb[(8 * I + g) * kVS + 2 * tg + 1];
-        } else if (J != kb) {   // I == kb: A_PR = W_R^T
-          t[0] = Wb[(8 * J + 2 * tg) * kVS + g];
-          t[1] = Wb[(8 * J + 2 * tg + 1) * kVS + g];
-        } else {                // pivot block: -D
-          t[0] = -D[g * 8 + 2 * tg];
-          t[1] = -D[g * 8 + 2 * tg + 1];
-        }
-      }
-      if (kn < nt) {
-        if (J == kn) {
-          put2(Vn, (8 * I + g) * kVS + 2 * tg, t[0], t[1]);
-        } else if (I == kn) {   // J < kn: V'[8J + j][g] = A[8kn + g][8J + j]
-          put1(Vn, (8 * J + 2 * tg) * kVS + g, t[0]);
-          put1(Vn, (8 * J + 2 * tg + 1) * kVS + g, t[1]);
-        }
-      }
-    };
-    if (warp == 0) {
-      // the next pivot block first (if it lives here): its W row, update, publish, invert, broadcast
-#pragma unroll
-      for (int sl = 0; sl < kInvCDiag; ++sl)
-        if (TI[sl] == kn) {
-          if (kb >= 0) {
-            wrow(kn);
-            __syncwarp();
-          }
-          tile(cc[sl], kn, kn);
-#ifdef INV_PROBE
-          const long long qs = clock64();
-#endif
-          // the 8-pivot sweep in one lane (no shuffles on the pivot chain)
-          sw8[g * 8 + 2 * tg] = cc[sl][0];
-          sw8[g * 8 + 2 * tg + 1] = cc[sl][1];
-          __syncwarp();
-          if (lane == 0) s_bad8 = sweep8_1(sw8) ? 1 : 0;
-          __syncwarp();
-          bad = bad || s_bad8 != 0;
-          put2(Dn, g * 8 + 2 * tg, -sw8[g * 8 + 2 * tg], -sw8[g * 8 + 2 * tg + 1]);
-          __syncwarp();
-#ifdef INV_PROBE
-          ps += clock64() - qs;
-#endif
-        }
-#pragma unroll
-      for (int sl = 0; sl < kInvCDiag; ++sl)
-        if (TI[sl] >= 0 && TI[sl] != kn) {
-          if (kb >= 0 && TI[sl] != kb) {   // the diagonal update needs only its own W row
-            wrow(TI[sl]);
-            __syncwarp();
-          }
-          tile(cc[sl], TI[sl], TI[sl]);
-        }
-    } else {
-#pragma unroll
-      for (int sl = 0; sl < kInvCSlots; ++sl)
-        if (TI[sl] >= 0) tile(cc[sl], TI[sl], TJ[sl]);
-    }
-#ifdef INV_PROBE
-    const long long q2 = clock64();
-#endif
-    cl.sync();
-#ifdef INV_PROBE
-    const long long q3 = clock64();
-    pw += q1 - q0;
-    pu += q2 - q1;
-    pb += q3 - q2;
-#endif
-  }
-#ifdef INV_PROBE
-  // per-CTA totals of warp 0 (W phase, updates incl. look-ahead sweep, cluster barrier) and the
-  // look-ahead sweeps this CTA ran
-  if (threadIdx.x == 0) {
-    g_inv_probe[0 + 0] = 0;
-    atomicAdd((unsigned long long *)&g_inv_probe[1], (unsigned long long)pw);
-    atomicAdd((unsigned long long *)&g_inv_probe[2], (unsigned long long)pu);
-    atomicAdd((unsigned long long *)&g_inv_probe[3], (unsigned long long)pb);
-    atomicAdd((unsigned long long *)&g_inv_probe[4], (unsigned long long)ps);
-  }
-#endif
-  if (bad && lane == 0 && info) atomicExch(info, 1);
-  // -A = Q^{-1}: both triangles straight to global memory
-#pragma unroll
-  for (int sl = 0; sl < NSL; ++sl) {
-    const int I = TI[sl], J = TJ[sl];
-    if (I < 0) continue;
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int i = 8 * I + g, j = 8 * J + 2 * tg + e;
-      if (i < S && j < S && (I != J || j <= i)) {
-        Qinv[(int64_t)i * S + j] = -cc[sl][e];
-        Qinv[(int64_t)j * S + i] = -cc[sl][e];
-      }
-    }
-  }
-}
-
-void launch_spd_inv(const double *Q, int S, double *Qinv, double *ws, int *info, cudaStream_t s) {
-  if (g_dbg_skip & 1) return;
-  prepare_kernel_attrs();
-  static const int chol = [] {   // A/B knob: STR_INV=1 runs the single-CTA block-Cholesky inverse
-    const char *e = getenv("STR_INV");
-    return e ? atoi(e) == 1 : 0;
-  }();
-  if (chol) {
-    launch_spd_inv_chol(Q, S, Qinv, ws, info, s);
-    return;
-  }
-  if (S <= STR_MAXW && S > 8) {
-    pdl_launch(kPdlInv, k_spd_inv_cl, dim3(kInvNC), dim3(kInvCThreads), 0, s, Q, S, Qinv, info);
-    return;
-  }
-  if (S <= 104)
-    k_spd_inv<5><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
-  else
-    k_spd_inv<8><<<1, kInvThreads, spd_inv_smem(S), s>>>(Q, S, Qinv, info);
-}
-
-// ------------------------------------------------------------------------------------------
 // 16-byte cp.async (16-byte aligned source and destination)
 __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)), "l"(g)
@@ -571,7 +51,10 @@ __device__ __forceinline__ void cp_async16(void *smem, const void *g) {
 // output tile per CTA (2 x 2 DMMA tiles), 8 warps = 4 tiles x 2 halves of K, so each warp runs one
 // accumulator chain over ceil(K/8) k-steps and the halves meet in shared memory.  A rows (stride
 // Ka = K rounded to 4 mod 16) and B rows (stride 20) make the fragment loads of a half-warp hit 32
-// distinct banks.  Epilogue as k_chain_gemm (q.mode).
+// distinct banks.  Epilogue (q.mode): 0 store C; 1 Q = H_<2>; 2 Q += H_<2>, where C is the chain
+// matrix Hm (rows (i1 + Rn r1), columns (i2 + Rn1 r2)) and H_<2>[i1 + Rn i2][r1 + Rn r2] = Hm[..][..]
+// (Def. 1 P:126 applied to the chain result; Q is left unsymmetrized, the factorization symmetrizes);
+// 3 the Gram regrouping below; 4 the fit sums of str_fit.
 constexpr int kGbS = 20;   // B row stride (doubles)
 __host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
 // TA: A is given transposed (K x M row-major, A_eff[m][k] = A[k M + m]) and staged like B.
@@ -645,11 +128,11 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
   if (TA) {
     const double *ap = As + tg * kGbS + 8 * ti + g;
 #pragma unroll 4
-    for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks * kGbS], bp[4 * ks * kGbS]);
+    for (int ks = ks0; ks < ks1; ++ks) dmma(c0, c1, ap[4 * ks * kGbS], bp[4 * ks * kGbS]);
   } else {
     const double *ap = As + (8 * ti + g) * Ka + tg;
 #pragma unroll 4
-    for (int ks = ks0; ks < ks1; ++ks) dmma884(c0, c1, ap[4 * ks], bp[4 * ks * kGbS]);
+    for (int ks = ks0; ks < ks1; ++ks) dmma(c0, c1, ap[4 * ks], bp[4 * ks * kGbS]);
   }
   if (half) {
     Rs[(tile * 32 + lane) * 2] = c0;
@@ -688,6 +171,8 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
           make_double2((Rs[256] + Rs[258]) + (Rs[260] + Rs[262]), (Rs[257] + Rs[259]) + (Rs[261] + Rs[263]));
     return;
   }
+  double *qd[2] = {nullptr, nullptr};
+  double qv[2] = {0.0, 0.0}, qo[2] = {0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int col = col0 + 8 * tj + 2 * tg + e;
@@ -702,10 +187,16 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
       } else {
         const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
         const int S = q.Rn * q.Rn1;
-        double *dst = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
-        *dst = (q.mode == 1) ? v : *dst + v;
+        qd[e] = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
+        qv[e] = v;
+        if (q.mode == 2) qo[e] = *qd[e];
       }
     }
+  }
+  if (q.mode == 1 || q.mode == 2) {   // (the old values were all loaded before the first store)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (qd[e]) *qd[e] = qo[e] + qv[e];
   }
 }
 
@@ -789,11 +280,6 @@ void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N
     launch_dmma_pdl<false, false>(gd, smd, s, A, B, C, M, N, K, q);
 }
 
-void launch_rows_mm(const double *P, const double *B, int S, int64_t I, double *out, cudaStream_t s) {
-  if (g_dbg_skip & 32) return;
-  if (I <= 0) return;
-  launch_chain_gemm(P, B, out, (int)I, S, S, QEpi{nullptr, 0, 0, 0}, s);
-}
 
 // ------------------------------------------------------------------------------------------
 // Gram tensor as a chain matrix: Zm[(a + Rb c)][(b + Ra d)] = sum_i G(i)(b,a) G(i)(d,c) (Z of
@@ -1030,10 +516,10 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
           const bool cv = 4 * j + tg < C;
           const double yv = (nbv && cv) ? (double)yi[j * ystep] : 0.0;
           const double av0 = (sm0 < Sm && cv) ? Ai[aoff0 + j * astep] : 0.0;
-          if (LEFT) dmma884(c[0][0], c[0][1], av0, yv); else dmma884(c[0][0], c[0][1], yv, av0);
+          if (LEFT) dmma(c[0][0], c[0][1], av0, yv); else dmma(c[0][0], c[0][1], yv, av0);
           if (two) {
             const double av1 = (sm1 < Sm && cv) ? Ai[aoff1 + j * astep] : 0.0;
-            if (LEFT) dmma884(c[1][0], c[1][1], av1, yv); else dmma884(c[1][0], c[1][1], yv, av1);
+            if (LEFT) dmma(c[1][0], c[1][1], av1, yv); else dmma(c[1][0], c[1][1], yv, av1);
           }
         }
       }
@@ -1059,11 +545,15 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
   } else if (!wact) {
     return;
   }
-  // accumulator fragment: row g, columns 2 tg + e of the 8 x 8 tile
+  // accumulator fragment: row g, columns 2 tg + e of the 8 x 8 tile; every old value is loaded before
+  // any store (a load-add-store per element would serialize on the possible aliasing)
+  double *dsts[2][2];
+  double olds[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
   for (int s2 = 0; s2 < 2; ++s2) {
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
+      dsts[s2][e] = nullptr;
       int rest, idx;
       if (LEFT) {   // D[u][n]: u = 8 s2 + g, n = 8 bt + 2 tg + e
         const int u = 8 * s2 + g, n = 8 * bt + 2 * tg + e, r = n / Cb, q = n - r * Cb;
@@ -1076,11 +566,15 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
         rest = rest0 + rb;
         idx = cb * ad.Rb + v;
       }
-      double *dst = out + (int64_t)rest * O + idx;
-      const double val = c[s2][e];
-      *dst = accumulate ? *dst + val : val;
+      dsts[s2][e] = out + (int64_t)rest * O + idx;
+      if (accumulate) olds[s2][e] = *dsts[s2][e];
     }
   }
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2)
+#pragma unroll
+    for (int e = 0; e < 2; ++e)
+      if (dsts[s2][e]) *dsts[s2][e] = olds[s2][e] + c[s2][e];
 }
 
 template <typename TY>
@@ -1640,8 +1134,6 @@ int launch_gemm_sk(const double *A, int64_t sai, int64_t sak, const double *B, i
 void prepare_kernel_attrs() {
   static PerDeviceOnce once;
   once_per_device(once, [] {
-  cudaFuncSetAttribute(k_spd_inv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
-  cudaFuncSetAttribute(k_spd_inv<8>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)spd_inv_smem(STR_MAXW));
   cudaFuncSetAttribute(k_chain_gemm_dmma<true, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
   cudaFuncSetAttribute(k_chain_gemm_dmma<false, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_dmma_smem(256));
   cudaFuncSetAttribute(k_chain_gemm_dmma<true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
@@ -1664,8 +1156,6 @@ void prepare_kernel_attrs() {
   prefer_max_smem(k_build_table3<8>);
   prefer_max_smem(k_build_table3<10>);
   prefer_max_smem(k_build_table3<16>);
-  prefer_max_smem(k_spd_inv<5>);
-  prefer_max_smem(k_spd_inv<8>);
   prefer_max_smem(k_gram_z2);
   prefer_max_smem(k_build_table2<4>);
   prefer_max_smem(k_build_table2<8>);

@@ -227,13 +227,13 @@ static str_status ensure_dev(str_state *h, DevBuf &b, size_t bytes) {
   return STR_OK;
 }
 
-// out = B A^{-1} for SPD A (S x S) and `rows` rows of B: the cluster inverse, then a row GEMM on the
-// FP64 tensor-core fragments (the "†" of reading R3/R4 on the device).  Ai: S x S scratch.
+// out = B A^{-1} for SPD A (S x S) and `rows` rows of B: the block-Cholesky factor V^T of A, then the
+// two triangular products (B V^T) V (the "†" of reading R3/R4 on the device).  Ai: factor scratch.
 static void solve_right(str_state *h, const double *A, int S, double *Ai, const double *B, int64_t rows, double *out) {
-  launch_spd_inv(A, S, Ai, (double *)h->Vws_t.p, h->d_info, h->st);
-  tl_mark(h, "spd_inv");
-  launch_rows_mm(B, Ai, S, rows, out, h->st);
-  tl_mark(h, "rows_mm");
+  launch_spd_factor(A, S, Ai, h->d_info, h->st);
+  tl_mark(h, "spd_factor");
+  launch_rows_solve(B, Ai, S, rows, out, h->st);
+  tl_mark(h, "rows_solve");
 }
 
 static void gemm(str_state *h, const double *A, int64_t sai, int64_t sak, const double *B, int64_t sbk, int64_t sbj,
@@ -578,15 +578,15 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   RTRY(rs_fork(h));
   gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1, true);   // Q_n += sym(G_S^T G_S)
   if (solve) {
-    launch_spd_inv((const double *)mb.Q.p, S, (double *)mb.Qi.p, (double *)mb.Vws.p, h->d_info, h->st);
-    tl_mark(h, "spd_inv");
+    launch_spd_factor((const double *)mb.Q.p, S, (double *)mb.Qi.p, h->d_info, h->st);
+    tl_mark(h, "spd_factor");
   }
   rs_main(h);
   gemm(h, XS, K, 1, GS, S, 1, (double *)mb.P.p, (int)mb.I, S, K, acc);
   RTRY(rs_join(h));
   if (solve) {
-    launch_rows_mm((const double *)mb.P.p, (const double *)mb.Qi.p, S, mb.I, (double *)mb.G.p, h->st);
-    tl_mark(h, "rows_mm");
+    launch_rows_solve((const double *)mb.P.p, (const double *)mb.Qi.p, S, mb.I, (double *)mb.G.p, h->st);
+    tl_mark(h, "rows_solve");
   }
   return STR_OK;
 }
@@ -649,13 +649,13 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R22)
   RTRY(rs_fork(h));   // the Gram and its inverse beside X_S G_S
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1, true);
-  launch_spd_inv(K, SN, (double *)h->Hi.p, (double *)h->Vws_q.p, h->d_info, h->st);
-  tl_mark(h, "spd_inv");
+  launch_spd_factor(K, SN, (double *)h->Hi.p, h->d_info, h->st);
+  tl_mark(h, "spd_factor");
   rs_main(h);
   gemm(h, XS, h->ksrft() ? 2 * h->m : h->m, 1, GS, SN, 1, M, (int)tn, SN, h->m, 0);
   RTRY(rs_join(h));
-  launch_rows_mm(M, (const double *)h->Hi.p, SN, tn, GN_new, h->st);
-  tl_mark(h, "rows_mm");
+  launch_rows_solve(M, (const double *)h->Hi.p, SN, tn, GN_new, h->st);
+  tl_mark(h, "rows_solve");
   // idxs(:,N) over [t_new]; (G_N^new)_S  (Alg. 7 l.24-25; Alg. 8 l.25-27, reading R9)
   RTRY(draw_mode(h, N, GN_new, tn));
   for (int n = 1; n < N; ++n) {

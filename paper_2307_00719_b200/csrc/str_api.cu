@@ -265,28 +265,39 @@ static TableDesc desc_TL(const str_state *h, int64_t t0, int64_t tn) {
 }
 
 // ------------------------------------------------------------------------------------ contraction
-// One pass of the two-pass schedule over X: builds the pass's table operand
-// (pass 1: T_R from the current = old cores; pass 2: T_L from the new temporal rows [t0, t0+tn)
-// and the updated left cores), contracts, and returns the output Y (fp32 in 3xTF32 mode).
-// trows: the tn temporal rows that pass 2 contracts with (unused by pass 1).  The f64 path reads X
-// through the device slot h->dX, which the caller has set (set_x).
-static str_status contract(str_state *h, const void *X, int pass, const double *trows, int64_t tn, const void **Y,
-                           bool *y_f32) {
+// One pass of the two-pass schedule over X.  The pass's table operand (pass 1: T_R from
+// the current cores; pass 2: T_L from the new temporal rows [trows, +tn) and the updated left cores) is
+// built by build_pass_table — on the step graph's third branch, overlapping other work: T_L beside
+// Z_k's Gram, and the NEXT step's T_R at the end of this step beside Z_{N-1}'s Gram and the append
+// (the right-group cores are final by then) — and run_pass contracts.  For 3xTF32 the table kernel also
+// clears the pass output (the contraction accumulates into it with TMA reduce-adds); pass 1's output
+// is cleared at its full capacity, since the next step's t_new is not known when it is built.
+static str_status build_pass_table(str_state *h, int pass, const double *trows, int64_t tn) {
   const int W = RR(h, h->k + 1) * RR(h, h->N);
   TableDesc td = pass == 1 ? desc_TR(h) : desc_TL_at(h, trows, tn);
   if (h->contract == STR_CONTRACT_3XTF32) {
     td.Npad = tf32_npad(W);
+    td.zero = (float4 *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
+    td.zero_n4 = ((pass == 1 ? h->L * h->ws_t : h->Rr) * W + 3) / 4;
+    TRY(build_table(h, td, nullptr, (float *)(pass == 1 ? h->tab_split.p : h->tab_split2.p),
+                    pass == 1 ? "table_TR" : "table_TL"));
+  } else {
+    TRY(build_table(h, td, (double *)(pass == 1 ? h->TR.p : h->TL.p), nullptr, pass == 1 ? "table_TR" : "table_TL"));
+  }
+  if (pass == 1) h->tr_ready = true;
+  return STR_OK;
+}
+
+static str_status run_pass(str_state *h, const void *X, int pass, int64_t tn, const void **Y, bool *y_f32) {
+  const int W = RR(h, h->k + 1) * RR(h, h->N);
+  if (h->contract == STR_CONTRACT_3XTF32) {
     float *out = (float *)(pass == 1 ? h->tf_part.p : h->tf_part2.p);
-    td.zero = (float4 *)out;   // the table kernel clears the pass output
-    td.zero_n4 = ((pass == 1 ? h->L * tn : h->Rr) * W + 3) / 4;
-    TRY(build_table(h, td, nullptr, (float *)h->tab_split.p, pass == 1 ? "table_TR" : "table_TL"));
     if (launch_contract_tf32(h, X, pass, W, tn, out, true) != 0)
       return fail(h, STR_E_CUDA, "tf32 contraction launch failed: " + h->err);
     *Y = out;
     *y_f32 = true;
   } else {
-    double *tab = (double *)(pass == 1 ? h->TR.p : h->TL.p);
-    TRY(build_table(h, td, tab, nullptr, pass == 1 ? "table_TR" : "table_TL"));
+    const double *tab = (const double *)(pass == 1 ? h->TR.p : h->TL.p);
     double *out = (double *)(pass == 1 ? h->YL.p : h->YR.p);
     prof_mark(h, 2 * (pass - 1));
     int nl = launch_contract_f64((const void *const *)h->dX.p, h->dtype == STR_F64, pass, tab, W, h->L, h->Rr, tn,
@@ -296,12 +307,21 @@ static str_status contract(str_state *h, const void *X, int pass, const double *
     *Y = out;
     *y_f32 = false;
   }
+  if (pass == 1) h->tr_ready = false;   // the pass-1 output now holds this pass's sums
   return check_launch(h, pass == 1 ? "contract pass 1" : "contract pass 2");
+}
+
+// Table build and pass in sequence on the current stream (init, test hooks).
+static str_status contract(str_state *h, const void *X, int pass, const double *trows, int64_t tn, const void **Y,
+                           bool *y_f32) {
+  TRY(build_pass_table(h, pass, trows, tn));
+  return run_pass(h, X, pass, tn, Y, y_f32);
 }
 
 // ------------------------------------------------------------------------------------ workspaces
 static str_status ensure_workspace(str_state *h, int64_t tn) {
   if (tn <= h->ws_t) return STR_OK;
+  h->tr_ready = false;   // the pass outputs may be reallocated (and the pass-1 zeroing covers ws_t)
   const int N = h->N, k = h->k;
   const int W1 = RR(h, k + 1) * RR(h, N);
   const int64_t Lt = h->L * tn;
@@ -394,26 +414,41 @@ static void right_modes(const str_state *h, std::vector<int> &modes, std::vector
   }
 }
 
-// Q_j^{-1} by the blocked sweep (the "^{-1}" of Alg. 4 l.17).
-static str_status invert_mode(str_state *h, int j) {
-  ModeBuf &m = h->md[j - 1];
-  launch_spd_inv((const double *)m.Q.p, m.Ra * m.Rb, (double *)m.Qi.p, (double *)m.Vws.p, h->d_info, h->st);
-  tl_mark(h, "spd_inv");
-  return check_launch(h, "spd_inv");
-}
 
-// G_j = P_j Q_j^{-1} (Alg. 4 l.17) and Z_j (l.18).
-static str_status finish_mode(str_state *h, int j) {
+// G_j = P_j Q_j^{-1} (Alg. 4 l.17).
+static str_status finish_rows(str_state *h, int j) {
   ModeBuf &m = h->md[j - 1];
   const int S = m.Ra * m.Rb;
-  launch_rows_mm((const double *)m.P.p, (const double *)m.Qi.p, S, m.I, (double *)m.G.p, h->st);
-  tl_mark(h, "rows_mm");
-  TRY(check_launch(h, "rows_mm"));
+  launch_rows_solve((const double *)m.P.p, (const double *)m.Qi.p, S, m.I, (double *)m.G.p, h->st);
+  tl_mark(h, "rows_solve");
+  return check_launch(h, "rows_solve");
+}
+
+// Z_j (l.18), reduced across the shards of the row-sharded G_1.
+static str_status finish_gram(str_state *h, int j) {
+  ModeBuf &m = h->md[j - 1];
   launch_gram_z2((const double *)m.G.p, m.I, m.Ra, m.Rb, (double *)m.Zm.p, 0, h->st);
   tl_mark(h, "gram_z");
   TRY(check_launch(h, "gram_z"));
   if (j == 1) TRY(allreduce(h, m.Zm.p, (size_t)m.Ra * m.Ra * m.Rb * m.Rb));   // G_1 row-sharded
   return STR_OK;
+}
+
+static str_status finish_mode(str_state *h, int j) {
+  TRY(finish_rows(h, j));
+  return finish_gram(h, j);
+}
+
+// Q (+)= (A B)_<2> (the last link of a Prop. 1 chain with the l.16 regrouping; the chain GEMM's Q
+// epilogue), then the factor V of sym(Q) (l.17's ^{-1}; chain_factor.cu).
+static str_status gram_link_factor(str_state *h, const double *A, const double *B, int M, int Nc, int K, int Rn,
+                                   int Rn1, int accumulate, double *Q, int S, double *V) {
+  launch_chain_gemm(A, B, nullptr, M, Nc, K, QEpi{Q, Rn, Rn1, accumulate ? 2 : 1}, h->st);
+  tl_mark(h, "chain_gemm_q");
+  TRY(check_launch(h, "chain_gemm_q"));
+  launch_spd_factor(Q, S, V, h->d_info, h->st);
+  tl_mark(h, "spd_factor");
+  return check_launch(h, "spd_factor");
 }
 
 // Fork / join of the side stream (independent branches of one step; graph branches when
@@ -428,6 +463,23 @@ static str_status fork(str_state *h) {
   return STR_OK;
 }
 static void main_again(str_state *h) { h->st = h->st_main; }
+// The third branch (pass tables): fork3() ... main3() enqueues on st3; join3() makes the main
+// stream wait for it.
+static str_status fork3(str_state *h) {
+  h->st_main = h->st;
+  if (h->timeline) return STR_OK;
+  CU(cudaEventRecord(h->ev_fork3, h->st));
+  CU(cudaStreamWaitEvent(h->st3, h->ev_fork3, 0));
+  h->st = h->st3;
+  return STR_OK;
+}
+static void main3(str_state *h) { h->st = h->st_main; }
+static str_status join3(str_state *h) {
+  if (h->timeline) return STR_OK;
+  CU(cudaEventRecord(h->ev_join3, h->st3));
+  CU(cudaStreamWaitEvent(h->st, h->ev_join3, 0));
+  return STR_OK;
+}
 static str_status join(str_state *h) {
   if (h->timeline) return STR_OK;
   CU(cudaEventRecord(h->ev_join, h->st2));
@@ -446,19 +498,17 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   // side: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq, Hq^{-1} (old state only)
   TRY(fork(h));
   TRY(build_suffixes(h));
-  {
+  {   // Hq = (Sf_1 Z_1)_<2> and its factor in one cluster launch
     int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
-    launch_chain_gemm((const double *)h->Sf[1].p, (const double *)h->md[0].Zm.p, nullptr, M, Nc, K,
-                      QEpi{(double *)h->Hq.p, RR(h, N), RR(h, 1), 1}, h->st);
-    tl_mark(h, "chain_gemm_q");
-    launch_spd_inv((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, (double *)h->Vws_q.p, h->d_info, h->st);
-    tl_mark(h, "spd_inv");
+    TRY(gram_link_factor(h, (const double *)h->Sf[1].p, (const double *)h->md[0].Zm.p, M, Nc, K, RR(h, N), RR(h, 1), 0,
+                         (double *)h->Hq.p, h->SN, (double *)h->Hi.p));
   }
   main_again(h);
-  // main: pass 1 with the old cores, then M_N = (G_1...G_k) Y_L summed over l
+  // main: pass 1 with the old cores (its table was built at the end of the previous step, or just
+  // before this step: update_det), then M_N = (G_1...G_k) Y_L summed over l
   const void *YL;
   bool yl32;
-  TRY(contract(h, X, 1, nullptr, tn, &YL, &yl32));
+  TRY(run_pass(h, X, 1, tn, &YL, &yl32));
   std::vector<int> modes;
   std::vector<int64_t> dims;
   left_modes(h, modes, dims);
@@ -471,8 +521,8 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   TRY(allreduce(h, Mt, (size_t)tn * h->SN));                                   // site C1
   TRY(join(h));
   double *GN_new = (double *)h->GNnew.p;
-  launch_rows_mm(Mt, (const double *)h->Hi.p, h->SN, tn, GN_new, h->st);       // l.9
-  tl_mark(h, "rows_mm");
+  launch_rows_solve(Mt, (const double *)h->Hi.p, h->SN, tn, GN_new, h->st);    // l.9
+  tl_mark(h, "rows_solve");
   TRY(check_launch(h, "temporal solve"));
   launch_gram_z2(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);  // Z_N^new
   tl_mark(h, "gram_z");
@@ -488,22 +538,21 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   bool yr32 = false;
   for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
-    // side: Q_j += H_j<2> (l.15-16), Q_j^{-1}
+    // side: Q_j += H_j<2> (l.15-16) and the factor of Q_j (l.17's ^{-1}), one cluster launch
     TRY(fork(h));
     {
-      const QEpi q{(double *)m.Q.p, RR(h, j), RR(h, j + 1), 2};
+      const int S = RR(h, j) * RR(h, j + 1);
       if (j == 1) {   // H_1 = Z_N^new Sf_1  (R_1^2 x R_N^2 . R_N^2 x R_2^2)
         if (N - 1 == 1) return fail(h, STR_E_ARG, "order N >= 3 required");
-        launch_chain_gemm((const double *)h->ZmN.p, (const double *)h->Sf[1].p, nullptr, RR(h, 1) * RR(h, 1),
-                          RR(h, 2) * RR(h, 2), RR(h, N) * RR(h, N), q, h->st);
+        TRY(gram_link_factor(h, (const double *)h->ZmN.p, (const double *)h->Sf[1].p, RR(h, 1) * RR(h, 1),
+                             RR(h, 2) * RR(h, 2), RR(h, N) * RR(h, N), RR(h, j), RR(h, j + 1), 1, (double *)m.Q.p, S,
+                             (double *)m.Qi.p));
       } else {        // H_j = Z_{j-1} B_j  (R_j^2 x R_{j-1}^2 . R_{j-1}^2 x R_{j+1}^2)
-        launch_chain_gemm((const double *)h->md[j - 2].Zm.p, Bj, nullptr, RR(h, j) * RR(h, j),
-                          RR(h, j + 1) * RR(h, j + 1), RR(h, j - 1) * RR(h, j - 1), q, h->st);
+        TRY(gram_link_factor(h, (const double *)h->md[j - 2].Zm.p, Bj, RR(h, j) * RR(h, j),
+                             RR(h, j + 1) * RR(h, j + 1), RR(h, j - 1) * RR(h, j - 1), RR(h, j), RR(h, j + 1), 1,
+                             (double *)m.Q.p, S, (double *)m.Qi.p));
       }
-      tl_mark(h, "chain_gemm_q");
-      TRY(check_launch(h, "chain_gemm_q"));
     }
-    TRY(invert_mode(h, j));
     main_again(h);
     // main: T1_j and B_{j+1} for the next mode (off the critical path)
     if (j + 1 <= N - 1) {
@@ -546,20 +595,32 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
         tl_mark(h, "axpy");
       }
     } else {
-      if (j == k + 1) {   // pass 2 with the new cores
-        TRY(contract(h, X, 2, GN_new, tn, &YR, &yr32));
+      if (j == k + 1) {   // pass 2 with the new cores (table built on the third branch after mode k's rows)
+        TRY(join3(h));
+        TRY(run_pass(h, X, 2, tn, &YR, &yr32));
         TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));   // site C2'
       }
       right_modes(h, modes, dims);
       TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p, 1));
     }
     TRY(join(h));
-    TRY(finish_mode(h, j));
+    TRY(finish_rows(h, j));
+    if (j == k) {            // pass 2's table needs G_N^new and the new G_1..G_k: build it beside Z_k
+      TRY(fork3(h));
+      TRY(build_pass_table(h, 2, GN_new, tn));
+      main3(h);
+    } else if (j == N - 1) {   // the next step's pass-1 table (final right-group cores) beside Z_{N-1}
+      TRY(fork3(h));
+      TRY(build_pass_table(h, 1, nullptr, tn));
+      main3(h);
+    }
+    TRY(finish_gram(h, j));
   }
   // l.10: append the new temporal rows
   launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, h->SN, h->st);
   tl_mark(h, "append");
-  return check_launch(h, "append");
+  TRY(check_launch(h, "append"));
+  return join3(h);
 }
 
 // One STR step: replays the captured graph of update_det_enqueue (capturing it on first use or
@@ -571,6 +632,7 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
   if (h->profiling && !h->pev[0]) {
     for (auto &e : h->pev) CU(cudaEventCreate(&e));
   }
+  if (!h->tr_ready) TRY(build_pass_table(h, 1, nullptr, tn));   // (outside the graph: first step, after init)
   const bool graph = h->use_graph && !h->timeline;
   if (!graph) {
     TRY(update_det_enqueue(h, X, tn));
@@ -663,9 +725,11 @@ extern "C" STR_API str_status strdbg_loopback_step(str_state **hs, int32_t p, co
   bool fresh = false;
   for (int r = 0; r < p; ++r) {
     const void *old = hs[r]->GN.p;
+    const int64_t old_ws = hs[r]->ws_t;
     TRY(ensure_workspace(hs[r], tn));
     TRY(ensure_temporal_capacity(hs[r], hs[r]->T + tn));
-    if (hs[r]->GN.p != old) fresh = true;   // (the group's graph holds the old temporal buffer)
+    if (hs[r]->GN.p != old || hs[r]->ws_t != old_ws) fresh = true;   // (the group's graph holds old buffers)
+    if (!hs[r]->tr_ready) TRY(build_pass_table(hs[r], 1, nullptr, tn));   // first step: pass-1 table
   }
   bool same = exec && *etn == tn && !fresh && (int)ex->size() == p;
   for (int r = 0; same && r < p; ++r) same = (*ex)[r] == X[r];
@@ -857,8 +921,11 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   }
   if (cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess) h->nsm = 148;
   if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+      cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_fork3, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return STR_E_CUDA;
   }
@@ -914,8 +981,7 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     TRY(ensure(h, m.P, sizeof(double) * m.I * S));
     TRY(ensure(h, m.Q, sizeof(double) * S * S));
     TRY(ensure(h, m.Zm, sizeof(double) * S * S));
-    TRY(ensure(h, m.Qi, sizeof(double) * S * S));
-    TRY(ensure(h, m.Vws, sizeof(double) * spd_inv_ws_doubles(S)));
+    TRY(ensure(h, m.Qi, sizeof(double) * spd_factor_doubles(S)));
   }
   h->Tcap = std::max<int64_t>(cfg->t_capacity > 0 ? cfg->t_capacity : 4096, t_init);
   TRY(ensure(h, h->GN, sizeof(double) * h->Tcap * h->SN));
@@ -931,8 +997,6 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   TRY(ensure(h, h->H, sizeof(double) * sq));
   TRY(ensure(h, h->Hq, sizeof(double) * STR_MAXW * STR_MAXW));
   TRY(ensure(h, h->Hi, sizeof(double) * STR_MAXW * STR_MAXW));
-  TRY(ensure(h, h->Vws_q, sizeof(double) * spd_inv_ws_doubles(STR_MAXW)));
-  TRY(ensure(h, h->Vws_t, sizeof(double) * spd_inv_ws_doubles(STR_MAXW)));
   {
     DevBuf info;
     TRY(ensure(h, info, sizeof(int)));
@@ -1240,8 +1304,14 @@ extern "C" void str_destroy(str_state *h) {
     cudaStreamSynchronize(h->st2);
     cudaStreamDestroy(h->st2);
   }
+  if (h->st3) {
+    cudaStreamSynchronize(h->st3);
+    cudaStreamDestroy(h->st3);
+  }
   if (h->ev_fork) cudaEventDestroy(h->ev_fork);
   if (h->ev_join) cudaEventDestroy(h->ev_join);
+  if (h->ev_fork3) cudaEventDestroy(h->ev_fork3);
+  if (h->ev_join3) cudaEventDestroy(h->ev_join3);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
 }
@@ -1307,25 +1377,32 @@ extern "C" STR_API str_status strdbg_spd_inv(int32_t device, int32_t S, int32_t 
   if (S < 1 || S > STR_MAXW || count < 1 || !Q_host || !Qinv_host) return STR_E_ARG;
   if (cudaSetDevice(device) != cudaSuccess) return STR_E_CUDA;
   const size_t n = (size_t)S * S;
-  double *dQ = nullptr, *dQi = nullptr, *ws = nullptr;
+  // Q^{-1} = I Q^{-1} through the factor kernel and the row solve with P = I
+  double *dQ = nullptr, *dQi = nullptr, *ws = nullptr, *dI = nullptr;
   int *dinfo = nullptr;
   str_status st = STR_OK;
   if (cudaMalloc(&dQ, n * count * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&dQi, n * count * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&ws, spd_inv_ws_doubles(S) * sizeof(double)) != cudaSuccess ||
-      cudaMalloc(&dinfo, sizeof(int)) != cudaSuccess) {
+      cudaMalloc(&ws, spd_factor_doubles(S) * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&dI, n * sizeof(double)) != cudaSuccess || cudaMalloc(&dinfo, sizeof(int)) != cudaSuccess) {
     st = STR_E_OOM;
   } else {
+    std::vector<double> eye(n, 0.0);
+    for (int i = 0; i < S; ++i) eye[(size_t)i * S + i] = 1.0;
+    cudaMemcpy(dI, eye.data(), n * sizeof(double), cudaMemcpyHostToDevice);
     cudaMemcpy(dQ, Q_host, n * count * sizeof(double), cudaMemcpyHostToDevice);
     cudaMemset(dinfo, 0, sizeof(int));
-    for (int c = 0; c < count; ++c) launch_spd_inv(dQ + c * n, S, dQi + c * n, ws, dinfo, 0);
+    for (int c = 0; c < count; ++c) {
+      launch_spd_factor(dQ + c * n, S, ws, dinfo, 0);
+      launch_rows_solve(dI, ws, S, S, dQi + c * n, 0);
+    }
     if (cudaDeviceSynchronize() != cudaSuccess) st = STR_E_CUDA;
     if (reps > 0 && us && st == STR_OK) {   // average time per inverse, back-to-back launches
       cudaEvent_t e0, e1;
       cudaEventCreate(&e0);
       cudaEventCreate(&e1);
       cudaEventRecord(e0, 0);
-      for (int r = 0; r < reps; ++r) launch_spd_inv(dQ, S, dQi, ws, dinfo, 0);
+      for (int r = 0; r < reps; ++r) launch_spd_factor(dQ, S, ws, dinfo, 0);
       cudaEventRecord(e1, 0);
       cudaEventSynchronize(e1);
       float ms = 0.f;
@@ -1342,6 +1419,7 @@ extern "C" STR_API str_status strdbg_spd_inv(int32_t device, int32_t S, int32_t 
   cudaFree(dQ);
   cudaFree(dQi);
   cudaFree(ws);
+  cudaFree(dI);
   cudaFree(dinfo);
   return st;
 }

@@ -41,8 +41,7 @@ struct ModeBuf {
   DevBuf P;             // I x Ra*Rb (Eq. partial)
   DevBuf Q;             // (Ra*Rb)^2 (Eq. partial)
   DevBuf Zm;            // Gram tensor Z_n as chain matrix: Rb^2 x Ra^2
-  DevBuf Qi;            // Q_n^{-1} (full symmetric)
-  DevBuf Vws;           // scratch of the SPD inverse of Q_n (block LDL^T factors)
+  DevBuf Qi;            // V^T of Q_n (Q_n^{-1} = VT VT^T; launch_spd_factor)
   // rSTR
   DevBuf samp;          // sampled slices (G_n)_S: m x Ra*Rb (G(2) layout rows)
   std::vector<int32_t> idx_host;
@@ -67,6 +66,9 @@ struct str_state {
   bool own_stream = false;
   cudaStream_t st2 = nullptr, st_main = nullptr;   // side stream for the independent branches
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaStream_t st3 = nullptr;                      // third branch: the contraction passes' tables
+  cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
+  bool tr_ready = false;                           // pass-1 table built for the current cores, output cleared
   Comm *comm = nullptr;             // collectives when p > 1 (comm.cu)
   void *loop_group = nullptr;       // loopback group (in-process ranks), if any
 
@@ -80,8 +82,7 @@ struct str_state {
   int64_t T = 0, Tcap = 0;
   DevBuf ZmN;                       // Z_N^new (update) / Z_N (init): R_1^2 x R_N^2
   std::vector<DevBuf> Sf;           // suffix chains Sf_n (index n)
-  DevBuf Lp[2], T1, H, Hq, Hi;       // Hq = H^{≠N}_<2> (temporal normal matrix), Hi = Hq^{-1}
-  DevBuf Vws_q, Vws_t;              // SPD-inverse scratch: Hq, and the rSTR leverage solves
+  DevBuf Lp[2], T1, H, Hq, Hi;       // Hq = H^{≠N}_<2> (temporal normal matrix), Hi = its factor V^T
 
   // workspaces
   int64_t ws_t = 0;
@@ -91,7 +92,7 @@ struct str_state {
 
   // 3xTF32 path
   bool tf32_ready = false;
-  DevBuf tab_split;                 // hi/lo fp32 table for the tensor-core passes
+  DevBuf tab_split, tab_split2;     // hi/lo fp32 tables of the tensor-core passes 1 and 2
   DevBuf tf_part, tf_part2;         // pass-1 / pass-2 fp32 outputs (stream-K red.add targets)
 
   // CUDA-graph replay of the STR step: the step is captured once per t_new and
@@ -167,13 +168,13 @@ struct str_state {
       b.bytes = 0;
     };
     for (auto &m : md) {
-      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.Qi); fr(m.samp); fr(m.Vws);
+      fr(m.G); fr(m.P); fr(m.Q); fr(m.Zm); fr(m.Qi); fr(m.samp);
     }
     fr(GN); fr(ZmN);
     for (auto &b : Sf) fr(b);
-    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi); fr(Vws_q); fr(Vws_t);
+    fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi);
     fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
-    fr(tab_split); fr(tf_part); fr(tf_part2);
+    fr(tab_split); fr(tab_split2); fr(tf_part); fr(tf_part2);
     fr(GNnew); fr(dT); fr(dX);
     gs[0].reset();
     gs[1].reset();

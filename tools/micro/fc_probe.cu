@@ -106,27 +106,27 @@ int main(int argc, char **argv) {
   double *dQ, *dQi, *ws;
   int *info;
   cudaMalloc(&dQ, S * S * 8);
-  cudaMalloc(&dQi, S * S * 8);
+  cudaMalloc(&dQi, spd_factor_doubles(S) * 8);
   cudaMalloc(&ws, 8);
   cudaMalloc(&info, 4);
   cudaMemcpy(dQ, Q.data(), S * S * 8, cudaMemcpyHostToDevice);
-  for (int it = 0; it < 5; ++it) launch_spd_inv_chol(dQ, S, dQi, ws, info, 0);
+  for (int it = 0; it < 5; ++it) launch_spd_factor(dQ, S, dQi, info, 0);
   cudaDeviceSynchronize();
   long long pr[64];
   cudaMemcpyFromSymbol(pr, g_fc_probe, sizeof(pr));
   const int nt = (S + 7) / 8;
-  printf("S=%d load %lld  steps:", S, pr[1] - pr[0]);
+  printf("S=%d load %lld (copy %lld, sym %lld)  steps:", S, pr[1] - pr[0], pr[44] - pr[0], pr[1] - pr[44]);
   long long prev = pr[1];
   for (int p = 0; p < nt; ++p) {
     printf(" %lld", pr[4 + p] - prev);
     prev = pr[4 + p];
   }
-  printf("\n  tail(last gamma) %lld  qinv %lld  total %lld cycles\n", pr[2] - prev, pr[3] - pr[2], pr[3] - pr[0]);
+  printf("\n  tail(last gamma) %lld  total %lld cycles\n", pr[2] - prev, pr[3] - pr[0]);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0);
-  for (int it = 0; it < 100; ++it) launch_spd_inv_chol(dQ, S, dQi, ws, info, 0);
+  for (int it = 0; it < 100; ++it) launch_spd_factor(dQ, S, dQi, info, 0);
   cudaEventRecord(e1);
   cudaEventSynchronize(e1);
   float ms;
