@@ -12,9 +12,9 @@
 // and Q^{-1} = V^T V.  (The square-root form keeps the multipliers L_ip bounded by ||A||^{1/2}; a block
 // LDL^T with explicitly inverted pivot blocks, W_ip = A_ip D_p^{-1}, is not stable at cond 1e8.)
 //
-// Schedule (one CTA, 256 threads).  The matrix lives in shared memory (lower tiles: A, then L in
+// Schedule (one CTA, kFcThreads = 384 threads).  The matrix lives in shared memory (lower tiles: A, then L in
 // place; upper tiles: V^T; T_p in a panel); warp 0 is the pivot warp — after the panel of step p it
-// updates the next pivot block and factors it at once (look-ahead), while warps 1-7 apply the trailing
+// updates the next pivot block and factors it at once (look-ahead), while warps 1-11 apply the trailing
 // update of step p and form V's row block p.  Two CTA barriers per step; the latency floor is the
 // chain of 8 dependent pivots per block.  Then the CTA assembles Q^{-1} = V^T V from shared memory.
 // The code is kept compact (rolled pivot loop, one copy of the 8 x 8 factorization): the kernel is
@@ -42,7 +42,12 @@ __device__ long long g_fc_probe[64];
   } while (0)
 #endif
 
-constexpr int kFcThreads = 256;
+#ifndef FC_THREADS
+#define FC_THREADS 384
+#endif
+constexpr int kFcThreads = FC_THREADS;          // factor CTA: warp 0 pivots, the rest are workers
+constexpr int kFcWarps = kFcThreads / 32, kFcWorkers = kFcWarps - 1;
+constexpr int kRsThreads = 256;                 // rows-solve CTA (8 warps x 2 column tiles: S <= 128)
 constexpr int kPL = 12;    // leading dimension of 8-wide panels (T blocks, the L panel, scratch): conflict-free
 
 // 1/sqrt(x) to full double precision: hardware approximation + two Newton steps
@@ -123,10 +128,11 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   double *Ds = As + Sp * LD;          // [nt][8][kPL]  T_p = L_pp^{-1}
   double *Wp0 = Ds + nt * 8 * kPL;    // [2][Sp][kPL]  panel L_ip of step p (double-buffered by parity:
                                       // step p+1's panel is written while step p's is still copied)
-  double *Xs = Wp0 + 2 * Sp * kPL;    // [8 warps][8][kPL] scratch
+  double *Xs = Wp0 + 2 * Sp * kPL;    // [kFcWarps][8][kPL] scratch
   FCP(0);
   // Q rows into shared memory (coalesced; 16-byte copies when the rows allow), then
-  // sym(Q) = (Q + Q^T)/2 into the lower tiles (diagonal tiles in full), identity padding beyond S
+  // sym(Q) = (Q + Q^T)/2 into the lower tiles (the factorization never reads above the diagonal),
+  // identity padding beyond S
   if ((S & 1) == 0 && ((uintptr_t)Q & 15) == 0) {
     const int h2 = S >> 1;
     for (int e = threadIdx.x; e < S * h2; e += kFcThreads) {
@@ -142,20 +148,28 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   cpa_commit();
   cpa_wait<0>();
   __syncthreads();
-  FCP(44);
-  // lower triangle only (the factorization never reads above the diagonal): row i per warp, all
-  // loads of a row before its stores (the lanes write only lower elements, which no lane reads)
-  for (int i = warp; i < Sp; i += kFcThreads / 32) {
-    double v[4];
+  // lower triangle only (the factorization never reads above the diagonal): rows i = warp + 12 r,
+  // four rows per batch with every load of a batch issued before its stores (the lanes write only
+  // lower elements, which no lane reads: the reads of the mirrored element As[j][i], j < i, are upper)
+  for (int i0 = warp; i0 < Sp; i0 += 4 * kFcWarps) {
+    double v[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = lane + 32 * q;
-      v[q] = (i < S && j < S && j <= i) ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : (i == j ? 1.0 : 0.0);
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + b * kFcWarps;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = lane + 32 * q;
+        v[b][q] = (i < S && j < S && j <= i) ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : (i == j ? 1.0 : 0.0);
+      }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int j = lane + 32 * q;
-      if (j <= i) As[i * LD + j] = v[q];
+    for (int b = 0; b < 4; ++b) {
+      const int i = i0 + b * kFcWarps;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int j = lane + 32 * q;
+        if (i < Sp && j <= i) As[i * LD + j] = v[b][q];
+      }
     }
   }
   __syncthreads();
@@ -184,6 +198,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         dmma8_tn(c, As + (8 * q) * LD + 8 * p, LD, Tp, kPL, g, t);
         frag_store(c, Wp + 8 * q * kPL, kPL, g, t);
         __syncwarp();
+        if (p == 5) FCP(54);
         asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
         double d[2];
         frag_load(d, As + (8 * q) * LD + 8 * q, LD, g, t);
@@ -192,13 +207,16 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         dmma(d[0], d[1], -pw[g * kPL + 4 + t], pw[g * kPL + 4 + t]);
         frag_store(d, As + (8 * q) * LD + 8 * q, LD, g, t);
         __syncwarp();
+        if (p == 5) FCP(55);
         if (lane == 0) chol8_inv1(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
         __syncwarp();
+        if (p == 5) FCP(56);
         for (int e = lane; e < 64; e += 32)   // V_qq = T_q
           Vout[(int64_t)(8 * q + (e >> 3)) * Sp + 8 * q + (e & 7)] = Ds[q * 8 * kPL + (e >> 3) * kPL + (e & 7)];
       } else {
         asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
       }
+      FCP(20 + p);   // (probe: the pivot warp's work of step p is done)
     } else {
       // the previous step's panel replaces A_{i,p-1} (read below as L_{p,p-1} by V's row block p)
       if (p > 0) {
@@ -208,7 +226,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
           As[i * LD + 8 * (p - 1) + b] = Wq[i * kPL + b];
         }
       }
-      for (int i = p + 2 + (warp - 1); i < nt; i += 7) {   // panel L_ip = A_ip T_p^T, i >= p+2
+      for (int i = p + 2 + (warp - 1); i < nt; i += kFcWorkers) {   // panel L_ip = A_ip T_p^T, i >= p+2
         double c[2] = {0.0, 0.0};
         dmma8_tn(c, As + (8 * i) * LD + 8 * p, LD, Tp, kPL, g, t);
         frag_store(c, Wp + 8 * i * kPL, kPL, g, t);
@@ -226,7 +244,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
       int ii = 0, jj = warp - 1;
       norm(ii, jj);
       while (ii < m) {
-        int ii2 = ii, jj2 = jj + 7;
+        int ii2 = ii, jj2 = jj + kFcWorkers;
         norm(ii2, jj2);
         const bool one = !(ii == 0 && jj == 0), two = ii2 < m;
         const int i1 = p + 1 + ii, j1 = p + 1 + jj, i2 = p + 1 + ii2, j2 = p + 1 + jj2;
@@ -246,13 +264,13 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         if (one) frag_store(c1, As + (8 * i1) * LD + 8 * j1, LD, g, t);
         if (two) frag_store(c2, As + (8 * i2) * LD + 8 * j2, LD, g, t);
         ii = ii2;
-        jj = jj2 + 7;
+        jj = jj2 + kFcWorkers;
         norm(ii, jj);
       }
       // (beta, workers) V row block p: V_pk = -T_p sum_{k<=m<p} L_pm V_mk (V_kk = T_k), stored
       // transposed in the upper tile (k, p): As[8k + a][8p + b] = V[8p + b][8k + a]
       double *xs = Xs + warp * 8 * kPL;
-      for (int k = warp - 1; k < p; k += 7) {
+      for (int k = warp - 1; k < p; k += kFcWorkers) {
         double c[2] = {0.0, 0.0};
         dmma8_nn(c, As + (8 * p) * LD + 8 * k, LD, Ds + k * 8 * kPL, kPL, g, t);   // L_pk T_k
         for (int mm = k + 1; mm < p; ++mm)   // L_pm V_mk, V_mk[kk][n] = As[8k + n][8mm + kk]
@@ -278,7 +296,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
 
 size_t fc_smem_bytes(int S) {
   const int nt = (S + 7) / 8, Sp = 8 * nt;
-  return sizeof(double) * ((size_t)Sp * ld_frag(Sp) + (size_t)(nt * 8 + 2 * Sp + 64) * kPL);
+  return sizeof(double) * ((size_t)Sp * ld_frag(Sp) + (size_t)(nt * 8 + 2 * Sp + 8 * kFcWarps) * kPL);
 }
 
 // The factor V = L^{-1} of one SPD matrix (S <= STR_MAXW) on one CTA.
@@ -311,7 +329,7 @@ void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_
 // of l.9 P:370).  One CTA per 8-row tile: V's lower blocks staged in shared memory (cp.async), then
 // Y = P V^T column tile by column tile over the 8 warps (Y[:, c] = sum_{k <= c} P[:, k] V[c][k]),
 // then out = Y V (out[:, c] = sum_{k >= c} Y[:, k] V[k][c]).
-__global__ void __launch_bounds__(kFcThreads, 1)
+__global__ void __launch_bounds__(kRsThreads, 1)
     k_rows_solve(const double *__restrict__ P, const double *__restrict__ V, int S, int64_t I,
                  double *__restrict__ out) {
   PDL_PROLOGUE();
@@ -322,11 +340,11 @@ __global__ void __launch_bounds__(kFcThreads, 1)
   double *Ps = Vs + Sp * LD;     // [8][LD]  the P rows, then Y
   const int64_t r0 = (int64_t)blockIdx.x * 8;
   const int nr = (int)((I - r0) < 8 ? (I - r0) : 8);
-  for (int e = threadIdx.x; e < Sp * (Sp / 2); e += kFcThreads) {
+  for (int e = threadIdx.x; e < Sp * (Sp / 2); e += kRsThreads) {
     const int i = e / (Sp / 2), j = 2 * (e - i * (Sp / 2));
     if ((j >> 3) <= (i >> 3)) cpa16cg(Vs + i * LD + j, V + (int64_t)i * Sp + j);
   }
-  for (int e = threadIdx.x; e < 8 * Sp; e += kFcThreads) {
+  for (int e = threadIdx.x; e < 8 * Sp; e += kRsThreads) {
     const int i = e / Sp, j = e - (e / Sp) * Sp;
     if (i < nr && j < S) cpa8(Ps + i * LD + j, P + (r0 + i) * S + j);
     else Ps[i * LD + j] = 0.0;
@@ -375,7 +393,7 @@ void launch_rows_solve(const double *P, const double *V, int S, int64_t I, doubl
                          (int)(sizeof(double) * (STR_MAXW + 8) * ld_frag(STR_MAXW)));
     prefer_max_smem(k_rows_solve);
   });
-  pdl_launch(kPdlDmma, k_rows_solve, dim3((unsigned)cdiv(I, 8)), dim3(kFcThreads), smem, s, P, V, S, I, out);
+  pdl_launch(kPdlDmma, k_rows_solve, dim3((unsigned)cdiv(I, 8)), dim3(kRsThreads), smem, s, P, V, S, I, out);
 }
 
 }  // namespace strb200

@@ -7,7 +7,8 @@
 #include <vector>
 using namespace strb200;
 __global__ void k_chol8_bench(int reps) {
-  __shared__ double M[8 * 12], T[8 * 12];
+  __shared__ __align__(16) double M[8 * 12];
+  __shared__ __align__(16) double T[8 * 12];
   const int lane = threadIdx.x;
   for (int i = lane; i < 64; i += 32) M[(i / 8) * 12 + i % 8] = (i / 8 == i % 8) ? 4.0 : 0.1;
   __syncwarp();
@@ -115,12 +116,20 @@ int main(int argc, char **argv) {
   long long pr[64];
   cudaMemcpyFromSymbol(pr, g_fc_probe, sizeof(pr));
   const int nt = (S + 7) / 8;
-  printf("S=%d load %lld (copy %lld, sym %lld)  steps:", S, pr[1] - pr[0], pr[44] - pr[0], pr[1] - pr[44]);
+  printf("S=%d load+sym %lld  steps:", S, pr[1] - pr[0]);
   long long prev = pr[1];
   for (int p = 0; p < nt; ++p) {
     printf(" %lld", pr[4 + p] - prev);
     prev = pr[4 + p];
   }
+  printf("\n  pivot warp busy per step:");
+  prev = pr[1];
+  for (int p = 0; p < nt; ++p) {
+    printf(" %lld", pr[20 + p] - prev);
+    prev = pr[4 + p];
+  }
+  printf("\n  step 5 pivot warp: panel row %lld, diag update %lld, chol8 %lld, V write %lld",
+         pr[54] - pr[8], pr[55] - pr[54], pr[56] - pr[55], pr[25] - pr[56]);
   printf("\n  tail(last gamma) %lld  total %lld cycles\n", pr[2] - prev, pr[3] - pr[0]);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
