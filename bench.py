@@ -39,11 +39,67 @@ N_DISTINCT = 15
 
 
 def load_peaks():
+    """MEASURED_PEAKS.json (driver-written: HBM copy, cuBLAS bf16) plus profiles/r02_measured_peaks.json
+    (tools/measure_peaks.py on this pool's B200: cuBLAS TF32 and FP64 GEMM, burst and sustained)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
-            return json.load(f), "measured"
+            peaks, src = json.load(f), "measured"
     except Exception:
-        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+        peaks, src = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}, "fallback"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_measured_peaks.json")) as f:
+            extra = json.load(f)
+        peaks["tf32_tflops"] = extra["tf32"]["burst_tflops"]
+        peaks["tf32_tflops_sustained"] = extra["tf32"]["sustained_tflops"]
+        peaks["fp64_tflops"] = extra["fp64"]["burst_tflops"]
+        peaks["fp64_tflops_sustained"] = extra["fp64"]["sustained_tflops"]
+    except Exception:
+        pass
+    return peaks, src
+
+
+def host_info():
+    """CPU model, numpy version, BLAS vendor and its thread count (for the cpu_baseline record)."""
+    import platform
+    model = platform.processor() or "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except Exception:
+        pass
+    blas, threads = "unknown", os.cpu_count()
+    try:
+        from threadpoolctl import threadpool_info
+        for d in threadpool_info():
+            if d.get("user_api") == "blas":
+                blas = f"{d.get('internal_api')} {d.get('version')} ({d.get('architecture')})"
+                threads = d.get("num_threads", threads)
+                break
+    except Exception:
+        pass
+    return {"cpu_model": model, "numpy": np.__version__, "blas": blas, "blas_threads": threads,
+            "host_cores": os.cpu_count()}
+
+
+def nccl_summary(path_glob):
+    """What NCCL_DEBUG=INFO said on this rank: version, NVLS use, transport lines (a few)."""
+    import glob
+    lines = []
+    for fn in sorted(glob.glob(path_glob)):
+        try:
+            lines += open(fn).read().splitlines()
+        except Exception:
+            pass
+    if not lines:
+        return None
+    ver = next((l.split("NCCL version", 1)[1].strip() for l in lines if "NCCL version" in l), None)
+    nvls = [l for l in lines if "NVLS" in l]
+    via = sorted({l.split("via", 1)[1].strip() for l in lines if " via " in l})[:4]
+    return {"version": ver, "nvls_lines": len(nvls), "nvls_sample": nvls[:2], "transports": via,
+            "lines": len(lines)}
 
 
 class ClockSampler:
@@ -119,7 +175,14 @@ def bench_ours(args):
     world, rank, local = dist_setup(args.gpus)
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    nccl_glob = None
     if world > 1:
+        # NCCL's own account of the collectives (NVLS / transports), summarised in the JSON line
+        import tempfile
+        ddir = os.environ.get("STR_NCCL_DEBUG_DIR") or tempfile.mkdtemp(prefix="str_nccl_")
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_FILE", os.path.join(ddir, "nccl.%h.%p.log"))
+        nccl_glob = os.path.join(ddir, "nccl.*.log")
         dist.init_process_group("nccl", device_id=dev)
     cfg = get_config(args.config)
     contract = args.contract or cfg.contract
@@ -234,14 +297,30 @@ def bench_ours(args):
     avg_p2 = p2_ms / max(p2_n, 1)
     avg_pass = 0.5 * (avg_p1 + avg_p2)
     if contract == "3xtf32":
-        tf32 = peaks["bf16_tflops"] * 0.5            # nominal tf32/bf16 ratio (1.1 / 2.25 PF dense)
-        peak_tf = tf32 / 3.0                          # 3 tf32 MMAs per algorithmic MAC
+        # the pass kernels run inside a long, back-to-back step: the sustained TF32 figure (measured
+        # cuBLAS TF32 GEMM), / 3 for the three TF32 MMAs per algorithmic multiply-add
+        if "tf32_tflops_sustained" in peaks:
+            peak_tf = peaks["tf32_tflops_sustained"] / 3.0
+            basis = (f"measured cuBLAS TF32 GEMM sustained {peaks['tf32_tflops_sustained']} TF/s "
+                     "(profiles/r02_measured_peaks.json) / 3 (3xTF32)")
+            alt = {"tf32_burst": peaks["tf32_tflops"] / 3.0,
+                   "bf16_burst_x_nominal_ratio": peaks["bf16_tflops"] * 0.5 / 3.0}
+        else:
+            peak_tf = peaks["bf16_tflops"] * 0.5 / 3.0   # nominal tf32/bf16 ratio (1.1 / 2.25 PF dense)
+            basis = f"{peaks_src} bf16 burst {peaks['bf16_tflops']} x 0.5 (tf32/bf16 nominal) / 3 (3xTF32)"
+            alt = {}
         bound, unit = "tensor", "TFLOP/s"
-        basis = f"{peaks_src} bf16 burst {peaks['bf16_tflops']} x 0.5 (tf32/bf16 nominal) / 3 (3xTF32)"
     else:
-        peak_tf = 148 * 64 * 2 * 1.965e9 / 1e12       # FP64 FMA lanes x clock
-        bound, unit = "alu", "TFLOP/s"
-        basis = "FP64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz"
+        # the FP64 path runs on the FP64 tensor cores (DMMA): measured cuBLAS DGEMM, sustained
+        if "fp64_tflops_sustained" in peaks:
+            peak_tf = peaks["fp64_tflops_sustained"]
+            basis = f"measured cuBLAS FP64 GEMM sustained {peak_tf} TF/s (profiles/r02_measured_peaks.json)"
+            alt = {"fp64_derived_clock_x_units": 148 * 64 * 2 * 1.965e9 / 1e12}
+        else:
+            peak_tf = 148 * 64 * 2 * 1.965e9 / 1e12       # FP64 FMA lanes x clock
+            basis = "FP64: 148 SMs x 64 FMA/clk x 2 x 1.965 GHz"
+            alt = {}
+        bound, unit = "tensor", "TFLOP/s"
     if avg_pass <= 0:   # rSTR: no dense contraction pass on the path (sampled GEMMs only)
         avg_pass = float("nan")
     achieved = flops_per_pass / (avg_pass / 1e3) / 1e12
@@ -261,7 +340,27 @@ def bench_ours(args):
             traffic = json.load(open(tpath)).get(f"{args.config}:{contract}")
         except Exception:
             traffic = None
-    if args.variant == "ksrft":
+    if args.variant in ("uniform", "leverage"):
+        # rSTR-U / -L: no dense pass; the HBM traffic of a step is the zipped-fiber gathers X_S[n]
+        # (m fibers per mode).  Sector bytes: mode 1 fibers are contiguous (ceil(I_1 b / 32) sectors),
+        # every other mode's fiber elements sit in separate 32-byte sectors.  Bound = those bytes /
+        # HBM bandwidth, against the whole step (the step is latency-bound: small GEMMs and solves).
+        m = cfg.sketch_rows or 2000
+        xb = 4 if cfg.dtype == "f32" else 8
+        dims_t = list(cfg.dims) + [cfg.t_new]
+        dims_t[0] = dims_t[0] // world
+        sectors = -(-dims_t[0] * xb // 32) + sum(dims_t[1:])
+        sec_bytes = m * 32 * sectors
+        useful = m * xb * sum(dims_t)
+        step_s = ms / args.steps / 1e3
+        ach = sec_bytes / step_s / 1e9
+        roofline = {"bound": "hbm", "achieved": round(ach, 3), "peak": round(peaks["hbm_gbs"], 3), "unit": "GB/s",
+                    "frac": round(ach / peaks["hbm_gbs"], 5), "traffic": None,
+                    "kernel": "whole rSTR step over its gathered fiber sectors (no dense pass on the path)",
+                    "algorithmic_per_step": {"sector_bytes": sec_bytes, "useful_bytes": useful},
+                    "t_hbm_floor_us": round(sec_bytes / (peaks["hbm_gbs"] * 1e9) * 1e6, 3),
+                    "peak_basis": f"{peaks_src} HBM copy bandwidth"}
+    elif args.variant == "ksrft":
         # rSTR-K: the dominant kernels are the N KSRFT mixing passes over the batch (HBM-bound):
         # algorithmic bytes = |X| (in + 8 B complex out) for mode 1 + 16 B per entry for modes 2..N
         mix_ms = p1_ms / max(p1_n, 1)
@@ -281,8 +380,6 @@ def bench_ours(args):
                     "mix_us": round(mix_ms * 1e3, 2),
                     "mix_share_of_step": round(mix_ms / (ms / args.steps), 4),
                     "algorithmic_per_launch": {"bytes": mix_bytes}, "peak_basis": f"{peaks_src} HBM copy bandwidth"}
-    elif args.variant != "det":
-        roofline = {"kernel": "n/a: rSTR has no dense contraction pass (the step is sampled GEMMs and solves)"}
     else:
       roofline = {"bound": bound, "achieved": round(achieved, 3), "peak": round(peak, 3), "unit": unit,
                   "frac": round(achieved / peak, 4), "traffic": traffic, "kernel": "contraction pass (avg of pass 1/2)",
@@ -290,6 +387,12 @@ def bench_ours(args):
                   "pass_share_of_step": round((p1_ms + p2_ms) / max(kp, 1) / (ms / args.steps), 4),
                   "algorithmic_per_launch": {"flops": flops_per_pass, "bytes": bytes_per_pass},
                   "peak_basis": basis,
+                  "frac_vs_other_peaks": ({k: round(achieved / v, 4) for k, v in alt.items()}
+                                          if unit == "TFLOP/s" else {}),
+                  # step-level fraction: the two passes' algorithmic minimum (F_min, or their bytes when
+                  # HBM-bound) over the whole step at this peak
+                  "step_frac": round((2 * flops_per_pass / 1e12 if unit == "TFLOP/s" else 2 * bytes_per_pass / 1e9)
+                                     / (ms / args.steps / 1e3) / peak, 4),
                   # the paper's mode-by-mode work F_paper = N 2|X|R^2 per step vs the
                   # two-pass F_min = 2 passes x 2|X|R^2, both over the measured step time
                   "per_step": {"F_min": 2 * flops_per_pass, "F_paper": cfg.N * flops_per_pass,
@@ -362,6 +465,7 @@ def bench_ours(args):
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline(cfg, variant=args.variant)
     if world > 1:
+        line["nccl"] = nccl_summary(nccl_glob) if nccl_glob else None
         dist.destroy_process_group()
     if rank == 0:
         print(json.dumps(line), flush=True)
@@ -396,9 +500,11 @@ def cpu_baseline(cfg, budget_s=20.0, variant="det"):
         st.update(Xb)
         t_used += time.perf_counter() - t
         steps += 1
-    return {"value": steps * cfg.batch_entries / t_used, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle",
+    hi = host_info()
+    return {"value": steps * cfg.batch_entries / t_used, "unit": UNIT, "cores": hi["blas_threads"], "kind": "oracle",
             "sample": f"{cfg.name} ({variant}): oracle init + {steps} full update steps ({t_used:.1f} s of update time; "
-                      f"numpy BLAS threads = all {os.cpu_count()} host cores)"}
+                      f"numpy BLAS threads = {hi['blas_threads']} of {hi['host_cores']} host cores)",
+            "host": hi}
 
 
 def bench_reference(args):
@@ -431,7 +537,8 @@ def bench_reference(args):
             "data": "synthetic (seeded TR stream, SURVEY.md §8(d).1)",
             "config": {"workload": f"{cfg.name} (same as ours), variant {args.variant}",
                        "global_batch_entries": cfg.batch_entries},
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": os.cpu_count(), "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": host_info()["blas_threads"], "kind": "oracle",
+                             "sample": sample, "host": host_info()},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 

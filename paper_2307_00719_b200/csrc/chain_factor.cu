@@ -12,9 +12,9 @@
 // and Q^{-1} = V^T V.  (The square-root form keeps the multipliers L_ip bounded by ||A||^{1/2}; a block
 // LDL^T with explicitly inverted pivot blocks, W_ip = A_ip D_p^{-1}, is not stable at cond 1e8.)
 //
-// Schedule (one CTA, kFcThreads = 384 threads).  The matrix lives in shared memory (lower tiles: A, then L in
+// Schedule (one CTA, kFcThreads = 512 threads).  The matrix lives in shared memory (lower tiles: A, then L in
 // place; upper tiles: V^T; T_p in a panel); warp 0 is the pivot warp — after the panel of step p it
-// updates the next pivot block and factors it at once (look-ahead), while warps 1-11 apply the trailing
+// updates the next pivot block and factors it at once (look-ahead), while the worker warps apply the trailing
 // update of step p and form V's row block p.  Two CTA barriers per step; the latency floor is the
 // chain of 8 dependent pivots per block.  Then the CTA assembles Q^{-1} = V^T V from shared memory.
 // The code is kept compact (rolled pivot loop, one copy of the 8 x 8 factorization): the kernel is
@@ -43,10 +43,17 @@ __device__ long long g_fc_probe[64];
 #endif
 
 #ifndef FC_THREADS
-#define FC_THREADS 384
+#define FC_THREADS 512
 #endif
 constexpr int kFcThreads = FC_THREADS;          // factor CTA: warp 0 pivots, the rest are workers
-constexpr int kFcWarps = kFcThreads / 32, kFcWorkers = kFcWarps - 1;
+#ifndef FC_EXCL
+#define FC_EXCL 1
+#endif
+// With FC_EXCL the pivot warp has its SM sub-partition to itself (warps 4, 8, ... share warp 0's
+// scheduler and only join the barriers); the other warps are the workers, numbered wid = 0, 1, ...
+constexpr int kFcWarps = kFcThreads / 32;
+constexpr int kFcWorkers = FC_EXCL ? kFcWarps - kFcWarps / 4 : kFcWarps - 1;
+__device__ __forceinline__ int fc_worker_id(int warp) { return FC_EXCL ? ((warp & 3) ? warp - warp / 4 - 1 : -1) : warp - 1; }
 constexpr int kRsThreads = 256;                 // rows-solve CTA (8 warps x 2 column tiles: S <= 128)
 constexpr int kPL = 12;    // leading dimension of 8-wide panels (T blocks, the L panel, scratch): conflict-free
 
@@ -124,6 +131,7 @@ __device__ __noinline__ void chol8_inv1(const double *M, int ldm, double *Tout, 
 __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, double *__restrict__ Vout) {
   const int nt = (S + 7) >> 3, Sp = nt * 8, LD = ld_frag(Sp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  const int wid = fc_worker_id(warp);
   double *As = sm;                    // [Sp][LD]
   double *Ds = As + Sp * LD;          // [nt][8][kPL]  T_p = L_pp^{-1}
   double *Wp0 = Ds + nt * 8 * kPL;    // [2][Sp][kPL]  panel L_ip of step p (double-buffered by parity:
@@ -217,16 +225,18 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
       }
       FCP(20 + p);   // (probe: the pivot warp's work of step p is done)
+    } else if (wid < 0) {
+      asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");   // idle warp on the pivot warp's sub-partition
     } else {
       // the previous step's panel replaces A_{i,p-1} (read below as L_{p,p-1} by V's row block p)
       if (p > 0) {
         const double *Wq = Wp0 + ((p - 1) & 1) * Sp * kPL;
-        for (int e = threadIdx.x - 32; e < (nt - p) * 64; e += kFcThreads - 32) {
+        for (int e = wid * 32 + lane; e < (nt - p) * 64; e += kFcWorkers * 32) {
           const int i = 8 * p + (e >> 3), b = e & 7;
           As[i * LD + 8 * (p - 1) + b] = Wq[i * kPL + b];
         }
       }
-      for (int i = p + 2 + (warp - 1); i < nt; i += kFcWorkers) {   // panel L_ip = A_ip T_p^T, i >= p+2
+      for (int i = p + 2 + wid; i < nt; i += kFcWorkers) {   // panel L_ip = A_ip T_p^T, i >= p+2
         double c[2] = {0.0, 0.0};
         dmma8_tn(c, As + (8 * i) * LD + 8 * p, LD, Tp, kPL, g, t);
         frag_store(c, Wp + 8 * i * kPL, kPL, g, t);
@@ -241,7 +251,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
           ++ii;
         }
       };
-      int ii = 0, jj = warp - 1;
+      int ii = 0, jj = wid;
       norm(ii, jj);
       while (ii < m) {
         int ii2 = ii, jj2 = jj + kFcWorkers;
@@ -270,7 +280,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
       // (beta, workers) V row block p: V_pk = -T_p sum_{k<=m<p} L_pm V_mk (V_kk = T_k), stored
       // transposed in the upper tile (k, p): As[8k + a][8p + b] = V[8p + b][8k + a]
       double *xs = Xs + warp * 8 * kPL;
-      for (int k = warp - 1; k < p; k += kFcWorkers) {
+      for (int k = wid; k < p; k += kFcWorkers) {
         double c[2] = {0.0, 0.0};
         dmma8_nn(c, As + (8 * p) * LD + 8 * k, LD, Ds + k * 8 * kPL, kPL, g, t);   // L_pk T_k
         for (int mm = k + 1; mm < p; ++mm)   // L_pm V_mk, V_mk[kk][n] = As[8k + n][8mm + kk]

@@ -188,15 +188,19 @@ static str_status chain_mul(str_state *h, const double *A, bool A_id, const doub
   return check_launch(h, "chain_gemm");
 }
 
+// Suffix Sf_n (1 <= n <= N-2).  Sf_{N-2} = Z_{N-1} itself (no copy): Z_{N-1} changes only at the
+// last mode's Gram refresh, after every use of the suffixes in the step.
+static const double *sf(const str_state *h, int n) {
+  return (const double *)(n == h->N - 2 ? h->md[h->N - 2].Zm.p : h->Sf[n].p);
+}
+
 // Sf_n = Z_{N-1} ... Z_{n+1} (Sf_{N-1} = I), from the current Z's (Alg. 4 l.15 right part).
 static str_status build_suffixes(str_state *h) {
   const int N = h->N;
-  for (int n = N - 2; n >= 1; --n) {
+  for (int n = N - 3; n >= 1; --n) {
     // Sf_n = Sf_{n+1} * Zm_{n+1};  Sf_{n+1}: R_N^2 x R_{n+2}^2, Zm_{n+1}: R_{n+2}^2 x R_{n+1}^2
     int M = RR(h, N) * RR(h, N), K = RR(h, n + 2) * RR(h, n + 2), Nc = RR(h, n + 1) * RR(h, n + 1);
-    bool id = (n + 1 == N - 1);
-    TRY(chain_mul(h, (const double *)h->Sf[n + 1].p, id, (const double *)h->md[n].Zm.p, false,
-                  (double *)h->Sf[n].p, M, Nc, K));
+    TRY(chain_mul(h, sf(h, n + 1), false, (const double *)h->md[n].Zm.p, false, (double *)h->Sf[n].p, M, Nc, K));
   }
   return STR_OK;
 }
@@ -210,12 +214,12 @@ static str_status q_update(str_state *h, int n, const double *Lp, bool Lp_id, co
   bool Sf_id = (n == N - 1);
   QEpi q{Qout, RR(h, n), RR(h, n + 1), accumulate ? 2 : 1};
   if (Lp_id) {
-    launch_chain_gemm(Zmid, (const double *)h->Sf[n].p, nullptr, b, d, c, q, h->st);
+    launch_chain_gemm(Zmid, sf(h, n), nullptr, b, d, c, q, h->st);
   } else if (Sf_id) {
     launch_chain_gemm(Lp, Zmid, nullptr, a, c, b, q, h->st);
   } else {
     TRY(chain_mul(h, Lp, false, Zmid, false, (double *)h->T1.p, a, c, b));
-    launch_chain_gemm((const double *)h->T1.p, (const double *)h->Sf[n].p, nullptr, a, d, c, q, h->st);
+    launch_chain_gemm((const double *)h->T1.p, sf(h, n), nullptr, a, d, c, q, h->st);
   }
   tl_mark(h, "chain_gemm_q");
   return check_launch(h, "chain_gemm_q");
@@ -487,6 +491,15 @@ static str_status join(str_state *h) {
   return STR_OK;
 }
 
+// The step's first side-branch work: suffix chains and Hq = (Sf_1 Z_1)_<2> with its factor.
+static str_status side_start(str_state *h) {
+  const int N = h->N;
+  TRY(build_suffixes(h));
+  int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
+  return gram_link_factor(h, sf(h, 1), (const double *)h->md[0].Zm.p, M, Nc, K, RR(h, N), RR(h, 1), 0,
+                          (double *)h->Hq.p, h->SN, (double *)h->Hi.p);
+}
+
 // ------------------------------------------------------------------------------------ update (STR)
 // Enqueues one STR step (no host synchronization, no host-side T): the new temporal rows go to the
 // scratch GNnew and are appended at the device row counter at the end.  The Gram-chain / inverse
@@ -495,14 +508,12 @@ static str_status join(str_state *h) {
 static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   const int N = h->N, k = h->k;
   TRY(set_x(h, X));
-  // side: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq, Hq^{-1} (old state only)
+  // side: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq and its factor (old state only).
+  // (Forking the side branch only once every pass-1 CTA is resident — a gate kernel launched
+  // programmatically dependent on the pass — shortened pass 1 by ~1 µs but delayed the side branch:
+  // C5 step 0.211 -> 0.229 ms; profiles/r02_side_gate.txt.)
   TRY(fork(h));
-  TRY(build_suffixes(h));
-  {   // Hq = (Sf_1 Z_1)_<2> and its factor in one cluster launch
-    int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
-    TRY(gram_link_factor(h, (const double *)h->Sf[1].p, (const double *)h->md[0].Zm.p, M, Nc, K, RR(h, N), RR(h, 1), 0,
-                         (double *)h->Hq.p, h->SN, (double *)h->Hi.p));
-  }
+  TRY(side_start(h));
   main_again(h);
   // main: pass 1 with the old cores (its table was built at the end of the previous step, or just
   // before this step: update_det), then M_N = (G_1...G_k) Y_L summed over l
@@ -544,7 +555,7 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
       const int S = RR(h, j) * RR(h, j + 1);
       if (j == 1) {   // H_1 = Z_N^new Sf_1  (R_1^2 x R_N^2 . R_N^2 x R_2^2)
         if (N - 1 == 1) return fail(h, STR_E_ARG, "order N >= 3 required");
-        TRY(gram_link_factor(h, (const double *)h->ZmN.p, (const double *)h->Sf[1].p, RR(h, 1) * RR(h, 1),
+        TRY(gram_link_factor(h, (const double *)h->ZmN.p, sf(h, 1), RR(h, 1) * RR(h, 1),
                              RR(h, 2) * RR(h, 2), RR(h, N) * RR(h, N), RR(h, j), RR(h, j + 1), 1, (double *)m.Q.p, S,
                              (double *)m.Qi.p));
       } else {        // H_j = Z_{j-1} B_j  (R_j^2 x R_{j-1}^2 . R_{j-1}^2 x R_{j+1}^2)
@@ -568,7 +579,7 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
       } else {        // B_{j+1} = T1_j Sf_{j+1}  (R_j^2 x R_N^2 . R_N^2 x R_{j+2}^2)
         // (ping-pong: the side stream may still be reading B_j while B_{j+1} is formed)
         double *bn = (double *)((j & 1) ? h->T1.p : h->H.p);
-        TRY(chain_mul(h, T1cur, false, (const double *)h->Sf[j + 1].p, false, bn, RR(h, j) * RR(h, j),
+        TRY(chain_mul(h, T1cur, false, sf(h, j + 1), false, bn, RR(h, j) * RR(h, j),
                       RR(h, j + 2) * RR(h, j + 2), RR(h, N) * RR(h, N)));
         Bj = bn;
       }
