@@ -25,6 +25,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-fvisibility=hidden",
                 "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+if os.environ.get("STR_BUILD_DIAG") == "1":   # diagnostic build: STR_DBG_SKIP / STR_TF_DBGFLAGS active
+    FLAGS = FLAGS + ["-DSTR_DIAG"]
+    OBJ = os.path.join(HERE, "build_diag")
 
 
 def _nccl_include():

@@ -455,42 +455,6 @@ static str_status gram_link_factor(str_state *h, const double *A, const double *
   return check_launch(h, "spd_factor");
 }
 
-// Fork / join of the side stream (independent branches of one step; graph branches when
-// capturing).  Between fork() and main_again() launches go to the side stream.
-static str_status fork(str_state *h) {
-  h->st_main = h->st;
-  if (h->timeline) return STR_OK;   // the diagnostic timeline serializes everything on one stream
-  CU(cudaEventRecord(h->ev_fork, h->st));
-  CU(cudaStreamWaitEvent(h->st2, h->ev_fork, 0));
-  h->st_main = h->st;
-  h->st = h->st2;
-  return STR_OK;
-}
-static void main_again(str_state *h) { h->st = h->st_main; }
-// The third branch (pass tables): fork3() ... main3() enqueues on st3; join3() makes the main
-// stream wait for it.
-static str_status fork3(str_state *h) {
-  h->st_main = h->st;
-  if (h->timeline) return STR_OK;
-  CU(cudaEventRecord(h->ev_fork3, h->st));
-  CU(cudaStreamWaitEvent(h->st3, h->ev_fork3, 0));
-  h->st = h->st3;
-  return STR_OK;
-}
-static void main3(str_state *h) { h->st = h->st_main; }
-static str_status join3(str_state *h) {
-  if (h->timeline) return STR_OK;
-  CU(cudaEventRecord(h->ev_join3, h->st3));
-  CU(cudaStreamWaitEvent(h->st, h->ev_join3, 0));
-  return STR_OK;
-}
-static str_status join(str_state *h) {
-  if (h->timeline) return STR_OK;
-  CU(cudaEventRecord(h->ev_join, h->st2));
-  CU(cudaStreamWaitEvent(h->st, h->ev_join, 0));
-  return STR_OK;
-}
-
 // The step's first side-branch work: suffix chains and Hq = (Sf_1 Z_1)_<2> with its factor.
 static str_status side_start(str_state *h) {
   const int N = h->N;
@@ -502,21 +466,45 @@ static str_status side_start(str_state *h) {
 
 // ------------------------------------------------------------------------------------ update (STR)
 // Enqueues one STR step (no host synchronization, no host-side T): the new temporal rows go to the
-// scratch GNnew and are appended at the device row counter at the end.  The Gram-chain / inverse
-// work of each mode (which needs only Z's) runs on the side stream, concurrently with the
-// contraction / absorb work (which needs X and the cores); the two join before G_n = P_n Q_n^{-1}.
+// scratch GNnew and are appended at the device row counter at the end.
+//
+// Two streams (graph branches when capturing) plus a third for the pass tables.  The serial chain
+// of the step — per mode: H_j = Z_{j-1} B_j with Q_j += H_<2>, the factor of Q_j, the rows
+// G_j = P_j Q_j^{-1}, the Gram Z_j — runs on the CHAIN stream (h->st2) as one sequence of
+// programmatically dependent launches; the X-dependent work (passes, absorbs, allreduces) and the
+// off-path chain products T1 / B run on the DATA stream (h->st at entry).  They meet through
+// events: the data stream hands over M_N / P_j (evP) and B_{j+1} (evB); the chain stream hands over
+// G_j (evR) and Z_j (evZ).  So the chain's kernel-to-kernel edges are same-stream (their launch
+// latency hides behind the predecessor), and the data stream's waits sit off the critical path.
 static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   const int N = h->N, k = h->k;
+  const bool serial = h->timeline != 0;   // the diagnostic timeline runs everything on one stream
+  cudaStream_t D = h->st;
+  cudaStream_t C = serial ? D : h->st2;
+  cudaStream_t T3 = serial ? D : h->st3;
+  auto rec = [&](cudaEvent_t e, cudaStream_t s) -> cudaError_t {
+    return serial ? cudaSuccess : cudaEventRecord(e, s);
+  };
+  auto wait = [&](cudaStream_t s, cudaEvent_t e) -> cudaError_t {
+    return serial ? cudaSuccess : cudaStreamWaitEvent(s, e, 0);
+  };
+  cudaEvent_t evP = h->ev_fork, evB = h->ev_join, evZ = h->ev_z;
+  struct Restore {   // the handle's stream is D again on every exit path
+    str_state *h;
+    cudaStream_t d;
+    ~Restore() { h->st = d; }
+  } restore{h, D};
+
+  h->st = D;
   TRY(set_x(h, X));
-  // side: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq and its factor (old state only).
-  // (Forking the side branch only once every pass-1 CTA is resident — a gate kernel launched
-  // programmatically dependent on the pass — shortened pass 1 by ~1 µs but delayed the side branch:
-  // C5 step 0.211 -> 0.229 ms; profiles/r02_side_gate.txt.)
-  TRY(fork(h));
+  // chain: suffix chains, H^{≠N} = Sf_1 Z_1 (Alg. 4 l.8) -> Hq and its factor (old state only)
+  CU(rec(evP, D));
+  CU(wait(C, evP));
+  h->st = C;
   TRY(side_start(h));
-  main_again(h);
-  // main: pass 1 with the old cores (its table was built at the end of the previous step, or just
+  // data: pass 1 with the old cores (its table was built at the end of the previous step, or just
   // before this step: update_det), then M_N = (G_1...G_k) Y_L summed over l
+  h->st = D;
   const void *YL;
   bool yl32;
   TRY(run_pass(h, X, 1, tn, &YL, &yl32));
@@ -530,18 +518,23 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   double *Mt = (double *)h->Mt.p;
   TRY(run_absorbs(h, YL, yl32, modes, dims, RR(h, k + 1), RR(h, N), ops, Mt, 0));
   TRY(allreduce(h, Mt, (size_t)tn * h->SN));                                   // site C1
-  TRY(join(h));
+  CU(rec(evP, D));
+  // chain: G_N^new = M_N Hq^{-1} (l.9) and Z_N^new
+  h->st = C;
+  CU(wait(C, evP));
   double *GN_new = (double *)h->GNnew.p;
   launch_rows_solve(Mt, (const double *)h->Hi.p, h->SN, tn, GN_new, h->st);    // l.9
   tl_mark(h, "rows_solve");
   TRY(check_launch(h, "temporal solve"));
   launch_gram_z2(GN_new, tn, RR(h, N), RR(h, 1), (double *)h->ZmN.p, 0, h->st);  // Z_N^new
   tl_mark(h, "gram_z");
+  TRY(check_launch(h, "gram_z"));
+  CU(rec(evZ, C));   // (also certifies G_N^new)
   // modes 1..N-1 in order (Gauss-Seidel).  Gram chain of mode j (Prop. 1 with the new Z's before
   // j and the old ones after): H_j = Lp_j Z_N^new Sf_j, Lp_j = Z_{j-1} ... Z_1.  Carried as
   // T1_j = Lp_j Z_N^new (T1_1 = Z_N^new, T1_{j+1} = Z_j T1_j) and B_{j+1} = T1_j Sf_{j+1}, both
-  // formed on the main stream while mode j's inverse runs, so that once Z_j is known the critical
-  // path to Q_{j+1} is the single product H_{j+1} = Z_j B_{j+1}.
+  // formed on the data stream while mode j's factor runs, so that once Z_j is known the chain's
+  // only product before Q_{j+1}'s factor is H_{j+1} = Z_j B_{j+1}.
   const double *T1cur = (const double *)h->ZmN.p;   // T1_j (R_j^2 x R_N^2)
   int t1buf = 0;
   const double *Bj = nullptr;                       // B_j (R_{j-1}^2 x R_{j+1}^2), j >= 2
@@ -549,23 +542,22 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   bool yr32 = false;
   for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
-    // side: Q_j += H_j<2> (l.15-16) and the factor of Q_j (l.17's ^{-1}), one cluster launch
-    TRY(fork(h));
-    {
-      const int S = RR(h, j) * RR(h, j + 1);
-      if (j == 1) {   // H_1 = Z_N^new Sf_1  (R_1^2 x R_N^2 . R_N^2 x R_2^2)
-        if (N - 1 == 1) return fail(h, STR_E_ARG, "order N >= 3 required");
-        TRY(gram_link_factor(h, (const double *)h->ZmN.p, sf(h, 1), RR(h, 1) * RR(h, 1),
-                             RR(h, 2) * RR(h, 2), RR(h, N) * RR(h, N), RR(h, j), RR(h, j + 1), 1, (double *)m.Q.p, S,
-                             (double *)m.Qi.p));
-      } else {        // H_j = Z_{j-1} B_j  (R_j^2 x R_{j-1}^2 . R_{j-1}^2 x R_{j+1}^2)
-        TRY(gram_link_factor(h, (const double *)h->md[j - 2].Zm.p, Bj, RR(h, j) * RR(h, j),
-                             RR(h, j + 1) * RR(h, j + 1), RR(h, j - 1) * RR(h, j - 1), RR(h, j), RR(h, j + 1), 1,
-                             (double *)m.Q.p, S, (double *)m.Qi.p));
-      }
+    const int S = RR(h, j) * RR(h, j + 1);
+    // chain: Q_j += H_j<2> (l.15-16) and the factor of Q_j (l.17's ^{-1})
+    h->st = C;
+    if (j == 1) {   // H_1 = Z_N^new Sf_1  (R_1^2 x R_N^2 . R_N^2 x R_2^2)
+      if (N - 1 == 1) return fail(h, STR_E_ARG, "order N >= 3 required");
+      TRY(gram_link_factor(h, (const double *)h->ZmN.p, sf(h, 1), RR(h, 1) * RR(h, 1), RR(h, 2) * RR(h, 2),
+                           RR(h, N) * RR(h, N), RR(h, j), RR(h, j + 1), 1, (double *)m.Q.p, S, (double *)m.Qi.p));
+    } else {        // H_j = Z_{j-1} B_j  (R_j^2 x R_{j-1}^2 . R_{j-1}^2 x R_{j+1}^2)
+      CU(wait(C, evB));
+      TRY(gram_link_factor(h, (const double *)h->md[j - 2].Zm.p, Bj, RR(h, j) * RR(h, j),
+                           RR(h, j + 1) * RR(h, j + 1), RR(h, j - 1) * RR(h, j - 1), RR(h, j), RR(h, j + 1), 1,
+                           (double *)m.Q.p, S, (double *)m.Qi.p));
     }
-    main_again(h);
-    // main: T1_j and B_{j+1} for the next mode (off the critical path)
+    // data: T1_j and B_{j+1} for the next mode (need Z_{j-1}, or Z_N^new for j = 1)
+    h->st = D;
+    CU(wait(D, evZ));
     if (j + 1 <= N - 1) {
       if (j >= 2) {   // T1_j = Z_{j-1} T1_{j-1}
         double *t1n = (double *)h->Lp[t1buf].p;
@@ -577,14 +569,16 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
       if (j + 1 == N - 1) {
         Bj = T1cur;   // Sf_{N-1} = I
       } else {        // B_{j+1} = T1_j Sf_{j+1}  (R_j^2 x R_N^2 . R_N^2 x R_{j+2}^2)
-        // (ping-pong: the side stream may still be reading B_j while B_{j+1} is formed)
+        // (ping-pong: the chain stream may still be reading B_j while B_{j+1} is formed)
         double *bn = (double *)((j & 1) ? h->T1.p : h->H.p);
         TRY(chain_mul(h, T1cur, false, sf(h, j + 1), false, bn, RR(h, j) * RR(h, j),
                       RR(h, j + 2) * RR(h, j + 2), RR(h, N) * RR(h, N)));
         Bj = bn;
       }
+      CU(rec(evB, D));
     }
-    // main: P_j += X_new[j] G^{≠j}_new (l.13-14)
+    // data: P_j += X_new[j] G^{≠j}_new (l.13-14), with the new G_1..G_{j-1} (evZ above also
+    // certifies G_{j-1}: the chain stream writes Z_{j-1} after G_{j-1})
     if (j <= k) {
       left_modes(h, modes, dims);
       if (j == 1) {
@@ -607,31 +601,40 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
       }
     } else {
       if (j == k + 1) {   // pass 2 with the new cores (table built on the third branch after mode k's rows)
-        TRY(join3(h));
+        if (!serial) CU(cudaStreamWaitEvent(D, h->ev_join3, 0));
         TRY(run_pass(h, X, 2, tn, &YR, &yr32));
         TRY(allreduce(h, const_cast<void *>(YR), (size_t)h->Rr * RR(h, k + 1) * RR(h, N), yr32));   // site C2'
       }
       right_modes(h, modes, dims);
       TRY(run_absorbs(h, YR, yr32, modes, dims, RR(h, N), RR(h, k + 1), right_ops(h, j), (double *)m.P.p, 1));
     }
-    TRY(join(h));
+    CU(rec(evP, D));
+    // chain: G_j = P_j Q_j^{-1} (l.17), then Z_j (l.18)
+    h->st = C;
+    CU(wait(C, evP));
     TRY(finish_rows(h, j));
-    if (j == k) {            // pass 2's table needs G_N^new and the new G_1..G_k: build it beside Z_k
-      TRY(fork3(h));
-      TRY(build_pass_table(h, 2, GN_new, tn));
-      main3(h);
-    } else if (j == N - 1) {   // the next step's pass-1 table (final right-group cores) beside Z_{N-1}
-      TRY(fork3(h));
-      TRY(build_pass_table(h, 1, nullptr, tn));
-      main3(h);
+    if (j == k || j == N - 1) {
+      // third branch: pass 2's table (G_N^new and the new G_1..G_k) beside Z_k, or the next step's
+      // pass-1 table (final right-group cores) beside Z_{N-1}
+      CU(rec(h->ev_fork3, C));
+      CU(wait(T3, h->ev_fork3));
+      h->st = T3;
+      TRY(build_pass_table(h, j == k ? 2 : 1, j == k ? GN_new : nullptr, tn));
+      CU(rec(h->ev_join3, T3));
+      h->st = C;
     }
     TRY(finish_gram(h, j));
+    CU(rec(evZ, C));
   }
-  // l.10: append the new temporal rows
+  // data: l.10, append the new temporal rows (G_N^new certified by the first evZ wait); then the
+  // step ends when the chain (Z_{N-1}) and the third branch (next pass-1 table) are done
+  h->st = D;
   launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, h->SN, h->st);
   tl_mark(h, "append");
   TRY(check_launch(h, "append"));
-  return join3(h);
+  CU(wait(D, evZ));
+  CU(wait(D, h->ev_join3));
+  return STR_OK;
 }
 
 // One STR step: replays the captured graph of update_det_enqueue (capturing it on first use or
@@ -936,7 +939,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork3, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_z, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return STR_E_CUDA;
   }
@@ -1323,6 +1327,7 @@ extern "C" void str_destroy(str_state *h) {
   if (h->ev_join) cudaEventDestroy(h->ev_join);
   if (h->ev_fork3) cudaEventDestroy(h->ev_fork3);
   if (h->ev_join3) cudaEventDestroy(h->ev_join3);
+  if (h->ev_z) cudaEventDestroy(h->ev_z);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
 }

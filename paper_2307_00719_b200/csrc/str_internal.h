@@ -68,6 +68,7 @@ struct str_state {
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   cudaStream_t st3 = nullptr;                      // third branch: the contraction passes' tables
   cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
+  cudaEvent_t ev_z = nullptr;       // STR step: the chain stream's Z_j (and G_j) handed to the data stream
   bool tr_ready = false;                           // pass-1 table built for the current cores, output cleared
   Comm *comm = nullptr;             // collectives when p > 1 (comm.cu)
   void *loop_group = nullptr;       // loopback group (in-process ranks), if any
