@@ -68,12 +68,15 @@ __device__ __forceinline__ double rsqrt_full(double x) {
 }
 
 // Cholesky factor and its inverse of the SPD 8 x 8 block M (shared memory, row-major, leading
-// dimension ldm; the lower triangle is read) in ONE thread's registers: M = L L^T, T = L^{-1}
-// (written lower-triangular, zeros above, to Tout with leading dimension kPL).  No shuffles on the
-// pivot chain: per pivot one full-precision reciprocal square root and one dependent update; the
-// inverse rows are independent FMA chains the scheduler interleaves with the later pivots.  A
-// non-positive or NaN pivot sets bad.
-__device__ __noinline__ void chol8_inv1(const double *M, int ldm, double *Tout, bool &bad) {
+// dimension ldm; the lower triangle is read): M = L L^T, T = L^{-1} (written lower-triangular, zeros
+// above, to Tout with leading dimension kPL).  Called by lanes 0..7 of one warp: every lane runs the
+// factorization in its own registers (one instruction stream, broadcast shared-memory reads, no
+// shuffles on the pivot chain: per pivot one full-precision reciprocal square root and one dependent
+// update), then lane c solves L x = e_c for column c of T — 8 independent forward substitutions in
+// parallel instead of the whole triangular inverse in one thread.  Called by a whole warp (lanes
+// 8-31 duplicate lanes 0-7 and store nothing).  A non-positive or NaN pivot sets bad (on every lane).
+__device__ __noinline__ void chol8_inv8(const double *M, int ldm, double *Tout, bool &bad) {
+  const int c = threadIdx.x & 7;
   double a[8][8];
 #pragma unroll
   for (int i = 0; i < 8; ++i)
@@ -104,23 +107,19 @@ __device__ __noinline__ void chol8_inv1(const double *M, int ldm, double *Tout, 
         a[i][j] = fma(-a[i][m + 1], a[j][m + 1], fma(-a[i][m], a[j][m], a[i][j]));
     a[m + 1][m] = l10;
   }
-  // T = L^{-1}: T[i][i] = r_i, T[i][j] = -r_i sum_{j<=k<i} L[i][k] T[k][j]
-  double tt[8][8];
+  // column c of T = L^{-1}: x_i = r_i (delta_ic - sum_{k<i} L[i][k] x_k) (x_i = 0 for i < c); the
+  // sum runs k ascending so that x_{i-1}, the latest operand, enters last
+  double xv[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    tt[i][i] = r[i];
+    double s = (i == c) ? 1.0 : 0.0;
 #pragma unroll
-    for (int j = 0; j < i; ++j) {
-      double s = 0.0;
-#pragma unroll
-      for (int k = j; k < i; ++k) s = fma(a[i][k], tt[k][j], s);
-      tt[i][j] = -r[i] * s;
-    }
+    for (int k = 0; k < i; ++k) s = fma(-a[i][k], xv[k], s);
+    xv[i] = s * r[i];
   }
+  if ((threadIdx.x & 31) < 8)
 #pragma unroll
-  for (int i = 0; i < 8; ++i)
-#pragma unroll
-    for (int j = 0; j < 8; ++j) Tout[i * kPL + j] = (j <= i) ? tt[i][j] : 0.0;
+    for (int i = 0; i < 8; ++i) Tout[i * kPL + c] = xv[i];
 }
 
 // Block Cholesky of sym(Q) (S x S, row-major, global) on one CTA with V = L^{-1} alongside, written
@@ -138,9 +137,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
                                       // step p+1's panel is written while step p's is still copied)
   double *Xs = Wp0 + 2 * Sp * kPL;    // [kFcWarps][8][kPL] scratch
   FCP(0);
-  // Q rows into shared memory (coalesced; 16-byte copies when the rows allow), then
-  // sym(Q) = (Q + Q^T)/2 into the lower tiles (the factorization never reads above the diagonal),
-  // identity padding beyond S
+  // Q rows into shared memory (coalesced; 16-byte copies when the rows allow)
   if ((S & 1) == 0 && ((uintptr_t)Q & 15) == 0) {
     const int h2 = S >> 1;
     for (int e = threadIdx.x; e < S * h2; e += kFcThreads) {
@@ -156,34 +153,32 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   cpa_commit();
   cpa_wait<0>();
   __syncthreads();
-  // lower triangle only (the factorization never reads above the diagonal): rows i = warp + 12 r,
-  // four rows per batch with every load of a batch issued before its stores (the lanes write only
-  // lower elements, which no lane reads: the reads of the mirrored element As[j][i], j < i, are upper)
-  for (int i0 = warp; i0 < Sp; i0 += 4 * kFcWarps) {
-    double v[4][4];
+  // sym(Q) = (Q + Q^T)/2 into the lower tiles (the factorization never reads above the diagonal; the
+  // upper halves of the diagonal tiles are zeroed), identity padding beyond S.  One 8 x 8 lower tile
+  // per warp iteration, lane (a, b) = (lane / 8, lane % 8) on (8I + a (+4), 8J + b): both the tile
+  // and its mirror are read at most two-way bank-conflicted (a row walk would be eight-way).  Every
+  // lane reads before any lane of the warp writes (a diagonal tile's upper half is zeroed while its
+  // lower half reads it); no other warp touches the tile or its mirror.
+  {
+    const int a0 = lane >> 3, b0 = lane & 7;
+    for (int tt = warp; tt < nt * (nt + 1) / 2; tt += kFcWarps) {
+      int I = 0, J = tt;
+      while (J > I) { J -= I + 1; ++I; }
+      double v[2];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = i0 + b * kFcWarps;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = lane + 32 * q;
-        v[b][q] = (i < S && j < S && j <= i) ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : (i == j ? 1.0 : 0.0);
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const int i = 8 * I + a0 + 4 * h2, j = 8 * J + b0;
+        v[h2] = (i < S && j < S) ? (j <= i ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : 0.0) : (i == j ? 1.0 : 0.0);
       }
-    }
+      __syncwarp();
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int i = i0 + b * kFcWarps;
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int j = lane + 32 * q;
-        if (i < Sp && j <= i) As[i * LD + j] = v[b][q];
-      }
+      for (int h2 = 0; h2 < 2; ++h2) As[(8 * I + a0 + 4 * h2) * LD + 8 * J + b0] = v[h2];
     }
   }
   __syncthreads();
   FCP(1);
   bool bad = false;
-  if (threadIdx.x == 0) chol8_inv1(As, LD, Ds, bad);
+  if (warp == 0) chol8_inv8(As, LD, Ds, bad);
   FCP(40);
   __syncthreads();
   if (warp == 0)
@@ -191,9 +186,10 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   FCP(41);
   // Step p (after the CTA barrier of step p-1):
   //   warp 0   L_{p+1,p} = A_{p+1,p} T_p^T (its own panel row) -> named-barrier arrive -> the pivot
-  //            block A_{p+1,p+1} -= L_{p+1,p} L_{p+1,p}^T -> T_{p+1} (one lane) -> V_{p+1,p+1}
-  //   workers  copy step p-1's panel into the lower tiles, the rest of the panel L_ip (i >= p+2),
-  //            named barrier (the whole panel is there), trailing update, V's row block p
+  //            block A_{p+1,p+1} -= L_{p+1,p} L_{p+1,p}^T -> T_{p+1} (lanes 0-7 store)
+  //   workers  V_pp = T_p (one warp), copy step p-1's panel into the lower tiles, the rest of the
+  //            panel L_ip (i >= p+2), named barrier (the whole panel is there), trailing update,
+  //            V's row block p
   //   CTA barrier
   // so the pivot chain (warp 0) never waits for the panel copies or the trailing updates of step p.
   for (int p = 0; p < nt; ++p) {
@@ -216,11 +212,9 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         frag_store(d, As + (8 * q) * LD + 8 * q, LD, g, t);
         __syncwarp();
         if (p == 5) FCP(55);
-        if (lane == 0) chol8_inv1(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
+        chol8_inv8(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
         __syncwarp();
         if (p == 5) FCP(56);
-        for (int e = lane; e < 64; e += 32)   // V_qq = T_q
-          Vout[(int64_t)(8 * q + (e >> 3)) * Sp + 8 * q + (e & 7)] = Ds[q * 8 * kPL + (e >> 3) * kPL + (e & 7)];
       } else {
         asm volatile("bar.arrive 1, %0;" ::"n"(kFcThreads) : "memory");
       }
@@ -228,6 +222,9 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
     } else if (wid < 0) {
       asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");   // idle warp on the pivot warp's sub-partition
     } else {
+      if (p > 0 && wid == kFcWorkers - 1)   // V_pp = T_p (factored by the pivot warp in step p-1)
+        for (int e = lane; e < 64; e += 32)
+          Vout[(int64_t)(8 * p + (e >> 3)) * Sp + 8 * p + (e & 7)] = Ds[p * 8 * kPL + (e >> 3) * kPL + (e & 7)];
       // the previous step's panel replaces A_{i,p-1} (read below as L_{p,p-1} by V's row block p)
       if (p > 0) {
         const double *Wq = Wp0 + ((p - 1) & 1) * Sp * kPL;
@@ -241,7 +238,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         dmma8_tn(c, As + (8 * i) * LD + 8 * p, LD, Tp, kPL, g, t);
         frag_store(c, Wp + 8 * i * kPL, kPL, g, t);
       }
-      asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");   // the whole panel is there
       // (beta, workers) trailing update A_ij -= L_ip L_jp^T, p < j <= i, except (p+1, p+1); pairs
       // (ii, jj), jj <= ii < m, enumerated row by row, two tiles per iteration (independent chains)
       const int m = nt - 1 - p;

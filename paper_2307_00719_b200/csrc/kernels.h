@@ -31,6 +31,7 @@ void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_
 size_t spd_factor_doubles(int S);
 // out = P Q^{-1} = (P V^T) V for I rows of P (I x S, row-major).
 void launch_rows_solve(const double *P, const double *V, int S, int64_t I, double *out, cudaStream_t s);
+
 void launch_chain_gemm(const double *A, const double *B, double *C, int M, int N, int K, QEpi q, cudaStream_t s);
 void launch_gram_z2(const double *G, int64_t I, int Ra, int Rb, double *Zm, int accumulate, cudaStream_t s);
 void launch_absorb2(const AbsorbDesc &ad, const void *Y, bool y_f32, double *out, int accumulate, cudaStream_t s);

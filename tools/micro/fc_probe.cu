@@ -15,7 +15,7 @@ __global__ void k_chol8_bench(int reps) {
   bool bad = false;
   long long t0 = clock64();
   for (int r = 0; r < reps; ++r) {
-    if (lane == 0) chol8_inv1(M, 12, T, bad);
+    chol8_inv8(M, 12, T, bad);
     __syncwarp();
     if (lane == 0) M[0] = 4.0 + T[0] * 1e-30;
     __syncwarp();
