@@ -27,6 +27,7 @@
 #include "common.cuh"
 #include "dmma.cuh"
 #include "kernels.h"
+#include "tc_ptx.cuh"
 
 namespace strb200 {
 
@@ -46,6 +47,12 @@ __device__ long long g_fc_probe[64];
 #define FC_THREADS 512
 #endif
 constexpr int kFcThreads = FC_THREADS;          // factor CTA: warp 0 pivots, the rest are workers
+#ifndef FC_BULK
+#define FC_BULK 0
+#endif
+#ifndef FC_WHATIF
+#define FC_WHATIF 0
+#endif
 #ifndef FC_EXCL
 #define FC_EXCL 1
 #endif
@@ -137,7 +144,22 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
                                       // step p+1's panel is written while step p's is still copied)
   double *Xs = Wp0 + 2 * Sp * kPL;    // [kFcWarps][8][kPL] scratch
   FCP(0);
-  // Q rows into shared memory (coalesced; 16-byte copies when the rows allow)
+  // Q rows into shared memory: one bulk (TMA) copy per row when the rows are 16-byte multiples,
+  // else 16- / 8-byte cp.async
+#if FC_BULK
+  __shared__ __align__(8) uint64_t qbar;
+  if ((S & 1) == 0 && ((uintptr_t)Q & 15) == 0) {
+    if (threadIdx.x == 0) {
+      tc::mbar_init(&qbar, 1);
+      tc::fence_barrier_init();
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) tc::mbar_arrive_expect_tx(&qbar, (uint32_t)(S * S * 8));
+    __syncthreads();
+    if (threadIdx.x < S) tc::bulk_load(As + threadIdx.x * LD, Q + (int64_t)threadIdx.x * S, (uint32_t)(S * 8), &qbar);
+    tc::mbar_wait(&qbar, 0);
+  } else
+#endif
   if ((S & 1) == 0 && ((uintptr_t)Q & 15) == 0) {
     const int h2 = S >> 1;
     for (int e = threadIdx.x; e < S * h2; e += kFcThreads) {
@@ -153,26 +175,38 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   cpa_commit();
   cpa_wait<0>();
   __syncthreads();
+  FCP(44);
   // sym(Q) = (Q + Q^T)/2 into the lower tiles (the factorization never reads above the diagonal; the
   // upper halves of the diagonal tiles are zeroed), identity padding beyond S.  One 8 x 8 lower tile
   // per warp iteration, lane (a, b) = (lane / 8, lane % 8) on (8I + a (+4), 8J + b): both the tile
   // and its mirror are read at most two-way bank-conflicted (a row walk would be eight-way).  Every
   // lane reads before any lane of the warp writes (a diagonal tile's upper half is zeroed while its
   // lower half reads it); no other warp touches the tile or its mirror.
+#ifdef FC_SYM2   // (probe only: the pass twice, the second timed on warm code; wrong results)
+  for (int rep = 0; rep < 2; ++rep) {
+    if (rep == 1) {
+      __syncthreads();
+      FCP(45);
+    }
+#else
   {
-    const int a0 = lane >> 3, b0 = lane & 7;
-    for (int tt = warp; tt < nt * (nt + 1) / 2; tt += kFcWarps) {
-      int I = 0, J = tt;
-      while (J > I) { J -= I + 1; ++I; }
-      double v[2];
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const int i = 8 * I + a0 + 4 * h2, j = 8 * J + b0;
-        v[h2] = (i < S && j < S) ? (j <= i ? 0.5 * (As[i * LD + j] + As[j * LD + i]) : 0.0) : (i == j ? 1.0 : 0.0);
-      }
+#endif
+    const int a0 = lane >> 3, b0 = lane & 7, ntl = nt * (nt + 1) / 2;
+    int I = 0, J = warp;   // tile (I, J), J <= I, of the row-major lower enumeration; advanced incrementally
+    while (J > I) { J -= I + 1; ++I; }
+    for (int tt = warp; tt < ntl; tt += kFcWarps) {
+      const int i0 = 8 * I + a0, j = 8 * J + b0;
+      // all four reads first (padding rows / columns read whatever is there and are not selected)
+      const double x0 = As[i0 * LD + j], y0 = As[j * LD + i0];
+      const double x1 = As[(i0 + 4) * LD + j], y1 = As[j * LD + i0 + 4];
+      const bool jin = j < S;
+      const double v0 = (i0 < S && jin) ? (j <= i0 ? 0.5 * (x0 + y0) : 0.0) : (i0 == j ? 1.0 : 0.0);
+      const double v1 = (i0 + 4 < S && jin) ? (j <= i0 + 4 ? 0.5 * (x1 + y1) : 0.0) : (i0 + 4 == j ? 1.0 : 0.0);
       __syncwarp();
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) As[(8 * I + a0 + 4 * h2) * LD + 8 * J + b0] = v[h2];
+      As[i0 * LD + j] = v0;
+      As[(i0 + 4) * LD + j] = v1;
+      J += kFcWarps;
+      while (J > I) { J -= I + 1; ++I; }
     }
   }
   __syncthreads();
@@ -212,6 +246,9 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         frag_store(d, As + (8 * q) * LD + 8 * q, LD, g, t);
         __syncwarp();
         if (p == 5) FCP(55);
+#if FC_WHATIF & 2   // (probe only: timing without the pivot-block factorization; wrong results)
+        if (p < 0)
+#endif
         chol8_inv8(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
         __syncwarp();
         if (p == 5) FCP(56);
@@ -239,6 +276,9 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         frag_store(c, Wp + 8 * i * kPL, kPL, g, t);
       }
       asm volatile("bar.sync 1, %0;" ::"n"(kFcThreads) : "memory");   // the whole panel is there
+#if FC_WHATIF & 1   // (probe only: timing without the trailing update and V's row blocks; wrong results)
+      if (p >= 0) goto step_end;
+#endif
       // (beta, workers) trailing update A_ij -= L_ip L_jp^T, p < j <= i, except (p+1, p+1); pairs
       // (ii, jj), jj <= ii < m, enumerated row by row, two tiles per iteration (independent chains)
       const int m = nt - 1 - p;
@@ -278,10 +318,17 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
       // transposed in the upper tile (k, p): As[8k + a][8p + b] = V[8p + b][8k + a]
       double *xs = Xs + warp * 8 * kPL;
       for (int k = wid; k < p; k += kFcWorkers) {
-        double c[2] = {0.0, 0.0};
+        // two accumulator chains (even / odd m) halve the dependent-DMMA latency of the long rows
+        double c[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
         dmma8_nn(c, As + (8 * p) * LD + 8 * k, LD, Ds + k * 8 * kPL, kPL, g, t);   // L_pk T_k
-        for (int mm = k + 1; mm < p; ++mm)   // L_pm V_mk, V_mk[kk][n] = As[8k + n][8mm + kk]
-          dmma8_tn(c, As + (8 * p) * LD + 8 * mm, LD, As + (8 * k) * LD + 8 * mm, LD, g, t);
+        int mm = k + 1;
+        for (; mm + 1 < p; mm += 2) {   // L_pm V_mk, V_mk[kk][n] = As[8k + n][8mm + kk]
+          dmma8_tn(c2, As + (8 * p) * LD + 8 * mm, LD, As + (8 * k) * LD + 8 * mm, LD, g, t);
+          dmma8_tn(c, As + (8 * p) * LD + 8 * (mm + 1), LD, As + (8 * k) * LD + 8 * (mm + 1), LD, g, t);
+        }
+        if (mm < p) dmma8_tn(c2, As + (8 * p) * LD + 8 * mm, LD, As + (8 * k) * LD + 8 * mm, LD, g, t);
+        c[0] += c2[0];
+        c[1] += c2[1];
         frag_store(c, xs, kPL, g, t);
         __syncwarp();
         double v[2] = {0.0, 0.0};
@@ -292,6 +339,9 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         *(double2 *)(Vout + (int64_t)(8 * p + g) * Sp + 8 * k + 2 * t) = make_double2(-v[0], -v[1]);   // V_pk
       }
     }
+#if FC_WHATIF & 1
+  step_end:
+#endif
     __syncthreads();
     FCP(4 + p);
   }

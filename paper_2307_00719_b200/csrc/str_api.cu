@@ -455,13 +455,52 @@ static str_status gram_link_factor(str_state *h, const double *A, const double *
   return check_launch(h, "spd_factor");
 }
 
-// The step's first side-branch work: suffix chains and Hq = (Sf_1 Z_1)_<2> with its factor.
-static str_status side_start(str_state *h) {
+// The Gram chains that need only the Z's of the previous step (Alg. 4 l.8 and the right parts of
+// l.15): the suffixes Sf_n = Z_{N-1} R_n (n <= N-3; Sf_{N-2} is Z_{N-1} itself) and
+// Hq = H^{≠N}_<2> = (Z_{N-1} R_0)_<2>, with R_n = Z_{N-2} ... Z_{n+1} (R_{N-3} = Z_{N-2}).  A step
+// forms them at its end from its final Z's — R_n on the data stream while the last mode's chain
+// runs (they need Z_1..Z_{N-2} only), then one product per chain after Z_{N-1}, beside the next
+// pass-1 table — so that the next step starts with the factor of Hq alone beside pass 1 (pass-1 CTAs
+// never wait for SMs held by these products).  side_ready: they hold the current Z's.
+static const double *rc(const str_state *h, int n) {
+  return (const double *)(n == h->N - 3 ? h->md[h->N - 3].Zm.p : h->Rc[n].p);
+}
+static str_status side_r_chain(str_state *h) {   // R_n, n = N-4 .. 0 (needs Z_1 .. Z_{N-2})
   const int N = h->N;
-  TRY(build_suffixes(h));
-  int M = RR(h, N) * RR(h, N), K = RR(h, 2) * RR(h, 2), Nc = RR(h, 1) * RR(h, 1);
-  return gram_link_factor(h, sf(h, 1), (const double *)h->md[0].Zm.p, M, Nc, K, RR(h, N), RR(h, 1), 0,
-                          (double *)h->Hq.p, h->SN, (double *)h->Hi.p);
+  for (int n = N - 4; n >= 0; --n) {
+    // R_n = R_{n+1} Z_{n+1}:  R_{N-1}^2 x R_{n+2}^2 . R_{n+2}^2 x R_{n+1}^2
+    TRY(chain_mul(h, rc(h, n + 1), false, (const double *)h->md[n].Zm.p, false, (double *)h->Rc[n].p,
+                  RR(h, N - 1) * RR(h, N - 1), RR(h, n + 1) * RR(h, n + 1), RR(h, n + 2) * RR(h, n + 2)));
+  }
+  return STR_OK;
+}
+static str_status side_sf(str_state *h) {        // Sf_n = Z_{N-1} R_n, n = 1 .. N-3 (needs Z_{N-1})
+  const int N = h->N;
+  for (int n = 1; n <= N - 3; ++n)
+    TRY(chain_mul(h, (const double *)h->md[N - 2].Zm.p, false, rc(h, n), false, (double *)h->Sf[n].p,
+                  RR(h, N) * RR(h, N), RR(h, n + 1) * RR(h, n + 1), RR(h, N - 1) * RR(h, N - 1)));
+  return STR_OK;
+}
+static str_status side_hq(str_state *h) {        // Hq = (Z_{N-1} R_0)_<2>  (needs Z_{N-1})
+  const int N = h->N;
+  launch_chain_gemm((const double *)h->md[N - 2].Zm.p, rc(h, 0), nullptr, RR(h, N) * RR(h, N), RR(h, 1) * RR(h, 1),
+                    RR(h, N - 1) * RR(h, N - 1), QEpi{(double *)h->Hq.p, RR(h, N), RR(h, 1), 1}, h->st);
+  tl_mark(h, "chain_gemm_q");
+  return check_launch(h, "chain_gemm_q (Hq)");
+}
+static str_status side_prepare(str_state *h) {   // all of it, in order, on the current stream
+  TRY(side_r_chain(h));
+  TRY(side_sf(h));
+  TRY(side_hq(h));
+  h->side_ready = true;
+  return STR_OK;
+}
+
+// The step's first side-branch work: the factor of Hq (Alg. 4 l.9's ^{-1}).
+static str_status side_start(str_state *h) {
+  launch_spd_factor((const double *)h->Hq.p, h->SN, (double *)h->Hi.p, h->d_info, h->st);
+  tl_mark(h, "spd_factor");
+  return check_launch(h, "spd_factor (Hq)");
 }
 
 // ------------------------------------------------------------------------------------ update (STR)
@@ -558,6 +597,7 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     // data: T1_j and B_{j+1} for the next mode (need Z_{j-1}, or Z_N^new for j = 1)
     h->st = D;
     CU(wait(D, evZ));
+    if (j == N - 1) TRY(side_r_chain(h));   // next step's chains: R_n (Z_1 .. Z_{N-2} are final)
     if (j + 1 <= N - 1) {
       if (j >= 2) {   // T1_j = Z_{j-1} T1_{j-1}
         double *t1n = (double *)h->Lp[t1buf].p;
@@ -625,14 +665,21 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     }
     TRY(finish_gram(h, j));
     CU(rec(evZ, C));
+    if (j == N - 1) {   // next step's Hq (chain stream, after Z_{N-1})
+      TRY(side_hq(h));
+      CU(rec(h->ev_hq, C));
+    }
   }
-  // data: l.10, append the new temporal rows (G_N^new certified by the first evZ wait); then the
-  // step ends when the chain (Z_{N-1}) and the third branch (next pass-1 table) are done
+  // data: l.10, append the new temporal rows (G_N^new certified by the first evZ wait); the next
+  // step's suffixes after Z_{N-1}; then the step ends when the chain (Hq) and the third branch
+  // (next pass-1 table) are done
   h->st = D;
   launch_append_rows((double *)h->GN.p, (int64_t *)h->dT.p, GN_new, tn, h->SN, h->st);
   tl_mark(h, "append");
   TRY(check_launch(h, "append"));
   CU(wait(D, evZ));
+  TRY(side_sf(h));
+  CU(wait(D, h->ev_hq));
   CU(wait(D, h->ev_join3));
   return STR_OK;
 }
@@ -647,6 +694,7 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
     for (auto &e : h->pev) CU(cudaEventCreate(&e));
   }
   if (!h->tr_ready) TRY(build_pass_table(h, 1, nullptr, tn));   // (outside the graph: first step, after init)
+  if (!h->side_ready) TRY(side_prepare(h));                       // (likewise)
   const bool graph = h->use_graph && !h->timeline;
   if (!graph) {
     TRY(update_det_enqueue(h, X, tn));
@@ -744,6 +792,7 @@ extern "C" STR_API str_status strdbg_loopback_step(str_state **hs, int32_t p, co
     TRY(ensure_temporal_capacity(hs[r], hs[r]->T + tn));
     if (hs[r]->GN.p != old || hs[r]->ws_t != old_ws) fresh = true;   // (the group's graph holds old buffers)
     if (!hs[r]->tr_ready) TRY(build_pass_table(hs[r], 1, nullptr, tn));   // first step: pass-1 table
+    if (!hs[r]->side_ready) TRY(side_prepare(hs[r]));
   }
   bool same = exec && *etn == tn && !fresh && (int)ex->size() == p;
   for (int r = 0; same && r < p; ++r) same = (*ex)[r] == X[r];
@@ -841,6 +890,7 @@ static str_status init_det(str_state *h, const void *X, int64_t tn) {
       Lp_id = false;
     }
   }
+  h->side_ready = false;   // the next step forms Sf_n / Hq from these Z's first
   return STR_OK;
 }
 
@@ -940,7 +990,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork3, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join3, cudaEventDisableTiming) != cudaSuccess ||
-      cudaEventCreateWithFlags(&h->ev_z, cudaEventDisableTiming) != cudaSuccess) {
+      cudaEventCreateWithFlags(&h->ev_z, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&h->ev_hq, cudaEventDisableTiming) != cudaSuccess) {
     delete h;
     return STR_E_CUDA;
   }
@@ -1006,6 +1057,8 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
   TRY(ensure(h, h->ZmN, sizeof(double) * sq));
   h->Sf.resize(N);
   for (int n = 1; n <= N - 1; ++n) TRY(ensure(h, h->Sf[n], sizeof(double) * sq));
+  h->Rc.resize(N);
+  for (int n = 0; n <= N - 4; ++n) TRY(ensure(h, h->Rc[n], sizeof(double) * sq));
   TRY(ensure(h, h->Lp[0], sizeof(double) * sq));
   TRY(ensure(h, h->Lp[1], sizeof(double) * sq));
   TRY(ensure(h, h->T1, sizeof(double) * sq));
@@ -1328,6 +1381,7 @@ extern "C" void str_destroy(str_state *h) {
   if (h->ev_fork3) cudaEventDestroy(h->ev_fork3);
   if (h->ev_join3) cudaEventDestroy(h->ev_join3);
   if (h->ev_z) cudaEventDestroy(h->ev_z);
+  if (h->ev_hq) cudaEventDestroy(h->ev_hq);
   if (h->own_stream) cudaStreamDestroy(h->st);
   delete h;
 }

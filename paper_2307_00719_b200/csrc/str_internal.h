@@ -69,6 +69,8 @@ struct str_state {
   cudaStream_t st3 = nullptr;                      // third branch: the contraction passes' tables
   cudaEvent_t ev_fork3 = nullptr, ev_join3 = nullptr;
   cudaEvent_t ev_z = nullptr;       // STR step: the chain stream's Z_j (and G_j) handed to the data stream
+  cudaEvent_t ev_hq = nullptr;      // STR step: the next step's Hq formed (chain stream, step end)
+  bool side_ready = false;                         // Sf_n and Hq hold the chains of the current Z's
   bool tr_ready = false;                           // pass-1 table built for the current cores, output cleared
   Comm *comm = nullptr;             // collectives when p > 1 (comm.cu)
   void *loop_group = nullptr;       // loopback group (in-process ranks), if any
@@ -83,6 +85,7 @@ struct str_state {
   int64_t T = 0, Tcap = 0;
   DevBuf ZmN;                       // Z_N^new (update) / Z_N (init): R_1^2 x R_N^2
   std::vector<DevBuf> Sf;           // suffix chains Sf_n (index n)
+  std::vector<DevBuf> Rc;           // R_n = Z_{N-2} ... Z_{n+1} (index n <= N-4; R_{N-3} is Z_{N-2})
   DevBuf Lp[2], T1, H, Hq, Hi;       // Hq = H^{≠N}_<2> (temporal normal matrix), Hi = its factor V^T
 
   // workspaces

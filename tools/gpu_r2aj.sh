@@ -1,0 +1,7 @@
+#!/bin/bash
+# side-start chain products on <= 4 CTAs (k_chain_gemm_strip): parity, benches, C5 pass trace
+python paper_2307_00719_b200/build.py 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_edges.py tests/test_gpu_trals.py -m gpu -q -x -p no:cacheprovider > gpurun_out/r2aj_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/r2aj_pytest.log
+for c in C5 C4 C2; do timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 --config $c > gpurun_out/r2aj_b_$c.log 2>&1; done
+timeout 300 python tools/graphtrace.py C5 --prof > gpurun_out/r2aj_gt_C5.log 2>&1

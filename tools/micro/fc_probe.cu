@@ -116,7 +116,7 @@ int main(int argc, char **argv) {
   long long pr[64];
   cudaMemcpyFromSymbol(pr, g_fc_probe, sizeof(pr));
   const int nt = (S + 7) / 8;
-  printf("S=%d load+sym %lld  steps:", S, pr[1] - pr[0]);
+  printf("S=%d load %lld +sym %lld (sym2 split %lld / %lld)  steps:", S, pr[44] - pr[0], pr[1] - pr[44], pr[45] - pr[44], pr[1] - pr[45]);
   long long prev = pr[1];
   for (int p = 0; p < nt; ++p) {
     printf(" %lld", pr[4 + p] - prev);
