@@ -44,8 +44,12 @@ constexpr int kMT = 2;         // M-tiles per CTA (share every B stage)
 constexpr int kBK = 32;        // K per stage (one 128-byte swizzle row of fp32)
 constexpr int kABytes = kBM * kBK * 4;   // 16 KB per X tile
 constexpr uint32_t kASlot0 = 256;        // A slots at [256, 512): slot a, M-tile mt at 256 + (2a + mt) * 64
-// epilogue staging: per lane quarter one dense [32 rows][W] fp32 box (W <= 128) -> one M-tile
-__host__ __device__ constexpr int ystage_box_bytes(int W) { return (32 * W * 4 + 1023) / 1024 * 1024; }
+// epilogue staging: per lane quarter one [32 rows][Wb] fp32 box (W <= 128) -> one M-tile.  Each
+// lane writes its row; the row stride Wb >= W is padded to Wb = 4 (mod 32) floats so that the lanes'
+// 16-byte stores spread over all banks (W = 64 would put every lane on the same four banks).  The
+// TMA box is Wb wide; its columns >= W lie outside the tensor and are clipped by the reduce-add.
+__host__ __device__ constexpr int ybox_w(int W) { return W + ((4 - W) % 32 + 32) % 32; }
+__host__ __device__ constexpr int ystage_box_bytes(int W) { return (32 * ybox_w(W) * 4 + 1023) / 1024 * 1024; }
 __host__ __device__ constexpr int ystage_bytes(int W) { return 4 * ystage_box_bytes(W); }
 
 struct TcParams {
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
             if (lane == 0) tc::bulk_wait_read<0>();
             __syncwarp();
           }
-          float *dst = (float *)box + lane * p.W;
+          float *dst = (float *)box + lane * ybox_w(p.W);
           for (int c0 = 0; c0 < p.W; c0 += 32) {
             float v[32];
             tmem_ld32(taddr + c0, v);   // columns >= Npad are never written by the MMA: not stored
@@ -485,7 +489,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       }
       u = uend;
     }
-    if (p.yred && lane == 0) tc::bulk_wait_all();
+    // the CTA may leave once its reduce-adds have READ their staging (the async-proxy writes are
+    // performed before the grid completes, which every consumer of Y waits for)
+    if (p.yred && lane == 0) tc::bulk_wait_read<0>();
   }
   tc::tc_fence_before();
   __syncthreads();
@@ -601,7 +607,7 @@ static bool encode_y_map(str_state *h, CUtensorMap *ymap, float *Y, int pass, in
   const int64_t rows = pass == 1 ? h->L : h->Rr, tt = pass == 1 ? tn : 1;
   cuuint64_t dims[3] = {(cuuint64_t)W, (cuuint64_t)rows, (cuuint64_t)tt};
   cuuint64_t strides[2] = {(cuuint64_t)W * 4, (cuuint64_t)(rows * W * 4)};
-  cuuint32_t box[3] = {(cuuint32_t)W, 32, 1};
+  cuuint32_t box[3] = {(cuuint32_t)ybox_w(W), 32, 1};   // (columns >= W: out of bounds, clipped)
   cuuint32_t es[3] = {1, 1, 1};
   CUresult r = g_encode(ymap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, Y, dims, strides, box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
                         CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
