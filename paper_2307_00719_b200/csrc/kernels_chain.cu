@@ -63,7 +63,11 @@ __host__ __device__ inline int gemm_ka(int K) { return (K + 11) / 16 * 16 + 4; }
 template <bool AL16, bool TA>
 __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restrict__ A, const double *__restrict__ B,
                                                          double *__restrict__ C, int M, int N, int K, QEpi q) {
-  PDL_PROLOGUE();
+  // PDL: the dependents may launch at once; the old Q values of the accumulate epilogue (written only
+  // by this kernel's instance in the previous step) are fetched before the wait for the predecessor,
+  // A and B after it (under stream capture every dependency of a programmatic launch, event-joined
+  // ones included, becomes programmatic, so no operand is known complete at launch)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   extern __shared__ __align__(16) double gsm[];
   const int Ka = TA ? 0 : gemm_ka(K), K4 = (K + 3) / 4 * 4;
   double *As = gsm;                 // [16][Ka], or TA: [K4][kGbS]
@@ -83,8 +87,43 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
   for (int e = threadIdx.x; e < (K4 - K) * 16; e += 256) Bs[(K + e / 16) * kGbS + e % 16] = 0.0;
   if (nc < 16)
     for (int e = threadIdx.x; e < K * (16 - nc); e += 256) Bs[(e / (16 - nc)) * kGbS + nc + e % (16 - nc)] = 0.0;
+  auto stage_b = [&]() {
+    if (AL16) {
+      const int n2 = nc >> 1;
+      for (int e = threadIdx.x; e < K * n2; e += 256) {
+        const int k = e / n2, c = 2 * (e - k * n2);
+        cp_async16(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
+      }
+    } else {
+      for (int e = threadIdx.x; e < K * nc; e += 256) {
+        const int k = e / nc, c = e - k * nc;
+        cp_async8(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
+      }
+    }
+  };
+  // the accumulate epilogue's old values (warps 0-3 store; Q is not written by the predecessor)
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int g = lane >> 2, tg = lane & 3;
+  const int tile = warp & 3, half = warp >> 2, ti = tile >> 1, tj = tile & 1;
+  const int row = row0 + 8 * ti + g;
+  double *qd[2] = {nullptr, nullptr};
+  double qo[2] = {0.0, 0.0};
+  if (!half && (q.mode == 1 || q.mode == 2)) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int col = col0 + 8 * tj + 2 * tg + e;
+      if (row < M && col < N) {
+        const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
+        const int S = q.Rn * q.Rn1;
+        qd[e] = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
+        if (q.mode == 2) qo[e] = *qd[e];
+      }
+    }
+  }
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  stage_b();
   if (AL16) {
-    const int K2 = K >> 1, n2 = nc >> 1, m2 = mr >> 1;
+    const int K2 = K >> 1, m2 = mr >> 1;
     if (TA) {
       for (int e = threadIdx.x; e < K * m2; e += 256) {
         const int k = e / m2, c = 2 * (e - k * m2);
@@ -95,10 +134,6 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
         const int r = e / K2, c = 2 * (e - r * K2);
         cp_async16(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
       }
-    }
-    for (int e = threadIdx.x; e < K * n2; e += 256) {
-      const int k = e / n2, c = 2 * (e - k * n2);
-      cp_async16(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
     }
   } else {
     if (TA) {
@@ -112,16 +147,9 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
         cp_async8(As + r * Ka + c, A + (int64_t)(row0 + r) * K + c);
       }
     }
-    for (int e = threadIdx.x; e < K * nc; e += 256) {
-      const int k = e / nc, c = e - k * nc;
-      cp_async8(Bs + k * kGbS + c, B + (int64_t)k * N + col0 + c);
-    }
   }
   cp_async_wait_all();
   __syncthreads();
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int g = lane >> 2, tg = lane & 3;
-  const int tile = warp & 3, half = warp >> 2, ti = tile >> 1, tj = tile & 1;
   const int nks = K4 / 4, ks0 = half ? (nks + 1) / 2 : 0, ks1 = half ? nks : (nks + 1) / 2;
   double c0 = 0.0, c1 = 0.0;
   const double *bp = Bs + tg * kGbS + 8 * tj + g;
@@ -142,7 +170,6 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
   if (half) return;
   c0 += Rs[(tile * 32 + lane) * 2];
   c1 += Rs[(tile * 32 + lane) * 2 + 1];
-  const int row = row0 + 8 * ti + g;
   if (q.mode == 4) {   // fit: residual and norm sums of this tile (warps 0-3), fixed-order partials
     double d2 = 0.0, x2 = 0.0;
 #pragma unroll
@@ -171,8 +198,6 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
           make_double2((Rs[256] + Rs[258]) + (Rs[260] + Rs[262]), (Rs[257] + Rs[259]) + (Rs[261] + Rs[263]));
     return;
   }
-  double *qd[2] = {nullptr, nullptr};
-  double qv[2] = {0.0, 0.0}, qo[2] = {0.0, 0.0};
 #pragma unroll
   for (int e = 0; e < 2; ++e) {
     const int col = col0 + 8 * tj + 2 * tg + e;
@@ -185,18 +210,9 @@ __global__ void __launch_bounds__(256) k_chain_gemm_dmma(const double *__restric
         const int a = row / Ra, b = row - a * Ra, c = col / Ra, d = col - c * Ra;
         q.Q[(int64_t)(a + Rb * c) * (Ra * Ra) + (b + Ra * d)] = v;
       } else {
-        const int i1 = row % q.Rn, r1 = row / q.Rn, i2 = col % q.Rn1, r2 = col / q.Rn1;
-        const int S = q.Rn * q.Rn1;
-        qd[e] = q.Q + (int64_t)(i1 + q.Rn * i2) * S + (r1 + q.Rn * r2);
-        qv[e] = v;
-        if (q.mode == 2) qo[e] = *qd[e];
+        *qd[e] = qo[e] + v;   // (modes 1 / 2: every old value of this tile was loaded above)
       }
     }
-  }
-  if (q.mode == 1 || q.mode == 2) {   // (the old values were all loaded before the first store)
-#pragma unroll
-    for (int e = 0; e < 2; ++e)
-      if (qd[e]) *qd[e] = qo[e] + qv[e];
   }
 }
 
