@@ -493,6 +493,34 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
   const int nb = 8 * bt + g;
   const int rb = nb / Cb, cb = nb - rb * Cb;
   const bool nbv = rb < nr;
+  // accumulator fragment: row g, columns 2 tg + e of the 8 x 8 tile.  The destinations and, when
+  // accumulating, their old values (P_n of the previous step: nothing in this step writes them
+  // before this kernel) are fetched here, before the staging and the products, so their latency
+  // overlaps them; every old value is loaded before any store (a load-add-store per element
+  // would serialize on the possible aliasing).  Only the storing warps (kw == 0) fetch.
+  double *dsts[2][2];
+  double olds[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
+#pragma unroll
+  for (int s2 = 0; s2 < 2; ++s2) {
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      dsts[s2][e] = nullptr;
+      int rest, idx;
+      if (LEFT) {   // D[u][n]: u = 8 s2 + g, n = 8 bt + 2 tg + e
+        const int u = 8 * s2 + g, n = 8 * bt + 2 * tg + e, r = n / Cb, q = n - r * Cb;
+        if (u >= Sm || r >= nr) continue;
+        rest = rest0 + r;
+        idx = u * ad.Q + q;
+      } else {      // D[m][v]: m = 8 bt + g, v = 8 s2 + 2 tg + e
+        const int v = 8 * s2 + 2 * tg + e;
+        if (v >= Sm || !nbv) continue;
+        rest = rest0 + rb;
+        idx = cb * ad.Rb + v;
+      }
+      dsts[s2][e] = out + (int64_t)rest * O + idx;
+      if (accumulate && kw == 0 && wact) olds[s2][e] = *dsts[s2][e];
+    }
+  }
   double c[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
   if (threadIdx.x == 0) {
     tc::mbar_init(&bar, 1);
@@ -560,31 +588,6 @@ __global__ void __launch_bounds__(256) k_absorb6(AbsorbDesc ad, const TY *__rest
     }
   } else if (!wact) {
     return;
-  }
-  // accumulator fragment: row g, columns 2 tg + e of the 8 x 8 tile; every old value is loaded before
-  // any store (a load-add-store per element would serialize on the possible aliasing)
-  double *dsts[2][2];
-  double olds[2][2] = {{0.0, 0.0}, {0.0, 0.0}};
-#pragma unroll
-  for (int s2 = 0; s2 < 2; ++s2) {
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      dsts[s2][e] = nullptr;
-      int rest, idx;
-      if (LEFT) {   // D[u][n]: u = 8 s2 + g, n = 8 bt + 2 tg + e
-        const int u = 8 * s2 + g, n = 8 * bt + 2 * tg + e, r = n / Cb, q = n - r * Cb;
-        if (u >= Sm || r >= nr) continue;
-        rest = rest0 + r;
-        idx = u * ad.Q + q;
-      } else {      // D[m][v]: m = 8 bt + g, v = 8 s2 + 2 tg + e
-        const int v = 8 * s2 + 2 * tg + e;
-        if (v >= Sm || !nbv) continue;
-        rest = rest0 + rb;
-        idx = cb * ad.Rb + v;
-      }
-      dsts[s2][e] = out + (int64_t)rest * O + idx;
-      if (accumulate) olds[s2][e] = *dsts[s2][e];
-    }
   }
 #pragma unroll
   for (int s2 = 0; s2 < 2; ++s2)
