@@ -1,0 +1,3 @@
+#!/bin/bash
+# factor what-if: without V's row blocks (FC_WHATIF=4) vs normal
+(cd tools/micro && for w in 0 4; do nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DFC_PROBE -DFC_WHATIF=$w -I../../include -I../../paper_2307_00719_b200/csrc -o fcw_$w fc_probe.cu && echo "== whatif $w" && ./fcw_$w 100 && ./fcw_$w 64; done) > gpurun_out/r2aw_probe.log 2>&1

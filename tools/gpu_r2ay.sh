@@ -1,0 +1,8 @@
+#!/bin/bash
+# factor: V rows on the warps beside the pivot warp; probe, tests, benches
+python paper_2307_00719_b200/build.py 2>&1 | tail -1
+(cd tools/micro && nvcc -gencode arch=compute_100a,code=sm_100a -O3 -DFC_PROBE -I../../include -I../../paper_2307_00719_b200/csrc -o fc_probe fc_probe.cu && ./fc_probe 100 && ./fc_probe 64) > gpurun_out/r2ay_probe.log 2>&1
+timeout 900 python -m pytest tests/test_gpu_spd_inv.py tests/test_gpu_parity.py -m gpu -q -x -p no:cacheprovider > gpurun_out/r2ay_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/r2ay_pytest.log
+for c in C5 C4; do timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 --config $c > gpurun_out/r2ay_b_$c.log 2>&1; done
+timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 --config C4 --variant uniform > gpurun_out/r2ay_b_C4u.log 2>&1
