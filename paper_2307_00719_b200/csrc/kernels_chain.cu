@@ -1106,8 +1106,12 @@ __global__ void __launch_bounds__(256) k_gemm_sk(const double *__restrict__ A, i
 // to the increment (equal to symmetrizing the sum when C is symmetric).
 __global__ void k_reduce_sk(const double *__restrict__ part, int KS, int64_t n, int N, double *__restrict__ C, int acc,
                             int sym) {
-  PDL_PROLOGUE();
+  // PDL: the accumulated value (P_n / Q_n of the previous step: only this kernel writes it) is loaded
+  // before the wait for the split-K products, the partials after it
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const double old = (acc && i < n) ? C[i] : 0.0;
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   if (i >= n) return;
   // all partials are loaded before the (fixed-order) sums, so the loads overlap
   double v[32], w[32];
@@ -1127,7 +1131,7 @@ __global__ void k_reduce_sk(const double *__restrict__ part, int KS, int64_t n, 
       if (k < KS) t += w[k];
     s = 0.5 * (s + t);
   }
-  C[i] = acc ? C[i] + s : s;
+  C[i] = acc ? old + s : s;
 }
 
 size_t gemm_sk_ws_doubles(int M, int N, int64_t K) {
