@@ -23,6 +23,9 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+
+#include <cooperative_groups.h>
 
 #include "common.cuh"
 #include "dmma.cuh"
@@ -129,12 +132,26 @@ __device__ __noinline__ void chol8_inv8(const double *M, int ldm, double *Tout, 
     for (int i = 0; i < 8; ++i) Tout[i * kPL + c] = xv[i];
 }
 
+// st.async of two doubles into another CTA of the cluster (shared::cluster addresses), signalling
+// complete_tx on that CTA's mbarrier: the consumer's mbarrier wait then also makes the data visible.
+__device__ __forceinline__ void st_async_f64x2(uint32_t raddr, double a, double b, uint32_t rbar) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];" ::"r"(raddr),
+               "d"(a), "d"(b), "r"(rbar)
+               : "memory");
+}
+__device__ __forceinline__ uint32_t cluster_map_u32(const void *p, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"((uint32_t)__cvta_generic_to_shared(p)), "r"(rank));
+  return r;
+}
+
 // Block Cholesky of sym(Q) (S x S, row-major, global) on one CTA with V = L^{-1} alongside, written
 // to Vout (Sp x Sp, row-major; Sp = S rounded up to 8, identity padding) row block by row block as
 // it is formed: only the blocks on and below the block diagonal are written (the diagonal blocks
 // T_p are lower triangular with explicit zeros), so Q^{-1} = V^T V.  Shared memory: fc_smem_bytes.
 // Returns bad.
-__device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, double *__restrict__ Vout) {
+__device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, double *__restrict__ Vout,
+                          uint64_t *vbar = nullptr) {
   const int nt = (S + 7) >> 3, Sp = nt * 8, LD = ld_frag(Sp);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
   const int wid = fc_worker_id(warp);
@@ -212,7 +229,22 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
   __syncthreads();
   FCP(1);
   bool bad = false;
+  // split (vbar: the V CTA's per-step mbarriers): L's column blocks and the T_p go to the same
+  // positions of the V CTA's tiles by st.async, step p's bytes counted on its mbarrier vbar[p]
+  const bool split = vbar != nullptr;
+  if (split) asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");   // (phase 0: its barriers are set up)
+  const uint32_t rsm0 = split ? cluster_map_u32(sm, 1) : 0u, rbar0 = split ? cluster_map_u32(vbar, 1) : 0u;
+  auto push_t = [&](int q, int step) {   // T_q (the 8 x 8 of its [8][kPL] block, 512 bytes) by one warp
+    const int r = lane >> 2, c2 = 2 * (lane & 3);
+    const double *src = Ds + q * 8 * kPL + r * kPL + c2;
+    st_async_f64x2(rsm0 + (uint32_t)(sizeof(double) * (Sp * LD + q * 8 * kPL + r * kPL + c2)), src[0], src[1],
+                   rbar0 + 8u * step);
+  };
   if (warp == 0) chol8_inv8(As, LD, Ds, bad);
+  if (split && warp == 0) {
+    __syncwarp();
+    push_t(0, 0);
+  }
   FCP(40);
   __syncthreads();
   if (warp == 0)
@@ -250,6 +282,10 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
         if (p < 0)
 #endif
         chol8_inv8(As + (8 * q) * LD + 8 * q, LD, Ds + q * 8 * kPL, bad);
+        if (split) {   // T_q to the V CTA (counted on step p's barrier)
+          __syncwarp();
+          push_t(q, p);
+        }
         __syncwarp();
         if (p == 5) FCP(56);
       } else {
@@ -269,6 +305,12 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
           const int i = 8 * p + (e >> 3), b = e & 7;
           As[i * LD + 8 * (p - 1) + b] = Wq[i * kPL + b];
         }
+        if (split)   // L's column block p-1, rows >= 8p, to the V CTA: pairs of doubles
+          for (int e = wid * 32 + lane; e < (nt - p) * 32; e += kFcWorkers * 32) {
+            const int i = 8 * p + (e >> 2), b = 2 * (e & 3);
+            st_async_f64x2(rsm0 + (uint32_t)(sizeof(double) * (i * LD + 8 * (p - 1) + b)), Wq[i * kPL + b],
+                           Wq[i * kPL + b + 1], rbar0 + 8u * p);
+          }
       }
       for (int i = p + 2 + wid; i < nt; i += kFcWorkers) {   // panel L_ip = A_ip T_p^T, i >= p+2
         double c[2] = {0.0, 0.0};
@@ -317,7 +359,7 @@ __device__ bool cta_bchol(const double *__restrict__ Q, int S, double *sm, doubl
       // (beta, workers) V row block p: V_pk = -T_p sum_{k<=m<p} L_pm V_mk (V_kk = T_k), stored
       // transposed in the upper tile (k, p): As[8k + a][8p + b] = V[8p + b][8k + a]
       double *xs = Xs + warp * 8 * kPL;
-      for (int k = wid; k < p; k += kFcWorkers) {
+      for (int k = wid; k < (split ? 0 : p); k += kFcWorkers) {   // (split: on the V CTA)
         // two accumulator chains (even / odd m) halve the dependent-DMMA latency of the long rows
         double c[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
         dmma8_nn(c, As + (8 * p) * LD + 8 * k, LD, Ds + k * 8 * kPL, kPL, g, t);   // L_pk T_k
@@ -365,6 +407,75 @@ __global__ void __launch_bounds__(kFcThreads, 1)
   if (bad && threadIdx.x == 0 && info) atomicExch(info, 1);
 }
 
+// The second CTA of the two-CTA factor: V's row blocks (V_pk = -T_p sum_{k<=m<p} L_pm V_mk, k < p),
+// one step behind the factoring CTA.  That CTA pushes L's column blocks and the T_p into this CTA's
+// tiles by st.async (distributed shared memory, the same positions as its own copies), counted in
+// bytes on this CTA's mbarrier of the step, so this CTA waits on its own barriers and reads only its
+// own shared memory.  V^T goes to the upper tiles here (the later rows read it) and V to Vout; the
+// diagonal blocks V_pp = T_p are written by the factoring CTA.  So the factor's worker warps carry
+// only the trailing updates.
+__device__ void cta_vrows(int S, double *sm, double *__restrict__ Vout, uint64_t *vbar) {
+  const int nt = (S + 7) >> 3, Sp = nt * 8, LD = ld_frag(Sp);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, g = lane >> 2, t = lane & 3;
+  double *As = sm, *Ds = As + Sp * LD, *Xs = Ds + nt * 8 * kPL + 2 * Sp * kPL;
+  for (int p = 1; p < nt; ++p) {
+    if (p == 1) tc::mbar_wait(&vbar[0], 0);   // step 0: T_0, T_1
+    tc::mbar_wait(&vbar[p], 0);               // step p: L's column block p-1 (rows >= 8p), T_{p+1}
+    const double *Tp = Ds + p * 8 * kPL;
+    double *xs = Xs + warp * 8 * kPL;
+    for (int k = warp; k < p; k += kFcWarps) {
+      double c[2] = {0.0, 0.0}, c2[2] = {0.0, 0.0};
+      dmma8_nn(c, As + (8 * p) * LD + 8 * k, LD, Ds + k * 8 * kPL, kPL, g, t);   // L_pk T_k
+      int mm = k + 1;
+      for (; mm + 1 < p; mm += 2) {   // L_pm V_mk, V_mk[kk][n] = As[8k + n][8mm + kk]
+        dmma8_tn(c2, As + (8 * p) * LD + 8 * mm, LD, As + (8 * k) * LD + 8 * mm, LD, g, t);
+        dmma8_tn(c, As + (8 * p) * LD + 8 * (mm + 1), LD, As + (8 * k) * LD + 8 * (mm + 1), LD, g, t);
+      }
+      if (mm < p) dmma8_tn(c2, As + (8 * p) * LD + 8 * mm, LD, As + (8 * k) * LD + 8 * mm, LD, g, t);
+      c[0] += c2[0];
+      c[1] += c2[1];
+      frag_store(c, xs, kPL, g, t);
+      __syncwarp();
+      double v[2] = {0.0, 0.0};
+      dmma8_nn(v, Tp, kPL, xs, kPL, g, t);
+      __syncwarp();
+#pragma unroll
+      for (int e2 = 0; e2 < 2; ++e2) As[(8 * k + 2 * t + e2) * LD + 8 * p + g] = -v[e2];
+      *(double2 *)(Vout + (int64_t)(8 * p + g) * Sp + 8 * k + 2 * t) = make_double2(-v[0], -v[1]);   // V_pk
+    }
+    __syncthreads();   // V's row block p is read by the later rows
+  }
+}
+
+// The factor on a cluster of two CTAs: CTA 0 factors (cta_bchol without V's rows), CTA 1 forms V's rows.
+__global__ void __launch_bounds__(kFcThreads, 1)
+    k_spd_factor2(const double *__restrict__ Q, int S, double *__restrict__ V, int *info) {
+  PDL_PROLOGUE();
+  extern __shared__ __align__(16) double fsm[];
+  __shared__ __align__(8) uint64_t vbar[STR_MAXW / 8];   // (CTA 1's copies are used)
+  const unsigned rank = cluster_rank();
+  const int nt = (S + 7) >> 3;
+  if (rank == 1 && threadIdx.x == 0) {   // the bytes each step of CTA 0 pushes here
+    for (int p = 0; p < nt; ++p) {
+      tc::mbar_init(&vbar[p], 1);
+      const uint32_t tbytes = (p + 1 < nt ? 512u : 0u) + (p == 0 ? 512u : 0u), lbytes = p > 0 ? 512u * (nt - p) : 0u;
+      tc::mbar_arrive_expect_tx(&vbar[p], tbytes + lbytes);
+    }
+    tc::fence_barrier_init();
+  }
+  // phase 0 of the cluster barrier: CTA 1's barriers exist before CTA 0 pushes (CTA 0 waits for the
+  // phase only after loading Q, so its factorization starts at once)
+  asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+  if (rank == 0) {
+    const bool bad = cta_bchol(Q, S, fsm, V, vbar);
+    if (bad && threadIdx.x == 0 && info) atomicExch(info, 1);
+  } else {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
+    cta_vrows(S, fsm, V, vbar);
+  }
+  cluster_sync_all();   // (no CTA leaves while the other may still address its shared memory)
+}
+
 size_t spd_factor_doubles(int S) {
   const int Sp = (S + 7) / 8 * 8;
   return (size_t)Sp * Sp;
@@ -377,6 +488,34 @@ void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_
     cudaFuncSetAttribute(k_spd_factor, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem_bytes(STR_MAXW));
     prefer_max_smem(k_spd_factor);
   });
+  static int split = -1;
+  if (split < 0) {
+    const char *e = getenv("STR_FACTOR_SPLIT");   // A/B knob: 0 = the one-CTA factor
+    split = (e && e[0] == '0') ? 0 : 1;
+  }
+  if (split && S > 64) {   // (at S <= 64 the V rows are cheap: one CTA)
+    static PerDeviceOnce once2;
+    once_per_device(once2, [] {
+      cudaFuncSetAttribute(k_spd_factor2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem_bytes(STR_MAXW));
+      prefer_max_smem(k_spd_factor2);
+    });
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(2);
+    cfg.blockDim = dim3(kFcThreads);
+    cfg.dynamicSmemBytes = fc_smem_bytes(S);
+    cfg.stream = s;
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = (pdl_mask() & kPdlInv) ? 2 : 1;
+    if (cudaLaunchKernelEx(&cfg, k_spd_factor2, Q, S, V, info) == cudaSuccess) return;
+    cudaGetLastError();   // (not sticky) fall back to one CTA
+  }
   pdl_launch(kPdlInv, k_spd_factor, dim3(1), dim3(kFcThreads), fc_smem_bytes(S), s, Q, S, V, info);
 }
 
