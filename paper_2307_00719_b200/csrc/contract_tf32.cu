@@ -673,11 +673,11 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.KT = pass == 1 ? cdiv(Rr, kBK) : tn * p.nlb;
   p.U = blocks * p.KT;
   // persistent grid: every SM but those the chain stream's kernels occupy while the pass runs (a pass
-  // CTA waiting for such an SM would hold the whole pass back): beside pass 1 only the one-CTA factor
-  // of Hq runs (the step's other chain products are formed at the previous step's end); beside pass 2
+  // CTA waiting for such an SM would hold the whole pass back): beside pass 1 only the factor of Hq
+  // runs (one CTA, or a two-CTA cluster for S_N > 64) (the step's other chain products are formed at the previous step's end); beside pass 2
   // the next mode's Gram-chain product and factor (kSideSMs)
   const int nsm = h->nsm;
-  int maxg = std::max(1, nsm - (pass == 1 ? 1 : kSideSMs));
+  int maxg = std::max(1, nsm - (pass == 1 ? (h->SN > 64 ? 2 : 1) : kSideSMs));   // (S > 64: two-CTA factor)
   if (const char *ev = getenv("STR_TF_GRID")) maxg = std::max(1, std::min(nsm, atoi(ev)));   // tuning knob
   int grid = (int)std::min<int64_t>(maxg, p.U);
   p.upc = cdiv(p.U, grid);

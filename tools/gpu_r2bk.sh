@@ -1,0 +1,8 @@
+#!/bin/bash
+# pass 1 launched programmatically dependent on the step's first node (early CTA setup)
+python paper_2307_00719_b200/build.py 2>&1 | tail -1
+timeout 1500 python -m pytest tests/test_gpu_contract.py tests/test_gpu_parity.py tests/test_gpu_rstr.py tests/test_gpu_trals.py tests/test_gpu_loopback.py -m gpu -q -x -p no:cacheprovider > gpurun_out/r2bk_pytest.log 2>&1
+echo "rc=$?" >> gpurun_out/r2bk_pytest.log
+for c in C5 C4 C2; do timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 --config $c > gpurun_out/r2bk_b_$c.log 2>&1; done
+STR_PDL=13 timeout 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline --e2e-steps 2 --config C5 > gpurun_out/r2bk_b13_C5.log 2>&1
+timeout 300 python tools/graphtrace.py C5 --prof > gpurun_out/r2bk_gt_C5.log 2>&1
