@@ -185,6 +185,8 @@ def bench_ours(args):
         nccl_glob = os.path.join(ddir, "nccl.*.log")
         dist.init_process_group("nccl", device_id=dev)
     cfg = get_config(args.config)
+    if args.split_k is not None:   # two-pass split point override (tuning)
+        cfg = cfg.with_(split_k=args.split_k)
     contract = args.contract or cfg.contract
     s = make_stream(cfg)
     # inputs: init slab + N_DISTINCT rotating batches, this rank's mode-1 shard, device-resident
@@ -555,6 +557,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--ref-budget", type=float, default=60.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--split-k", type=int, default=None, help="two-pass split point k (default: the config's)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "ours":
         args.warmup = 3
