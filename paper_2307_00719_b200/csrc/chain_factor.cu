@@ -65,6 +65,10 @@ constexpr int kFcWarps = kFcThreads / 32;
 constexpr int kFcWorkers = FC_EXCL ? kFcWarps - kFcWarps / 4 : kFcWarps - 1;
 __device__ __forceinline__ int fc_worker_id(int warp) { return FC_EXCL ? ((warp & 3) ? warp - warp / 4 - 1 : -1) : warp - 1; }
 constexpr int kRsThreads = 256;                 // rows-solve CTA (8 warps x 2 column tiles: S <= 128)
+#ifndef FC_SPLIT_MIN_S
+#define FC_SPLIT_MIN_S 32
+#endif
+constexpr int kSplitMinS = FC_SPLIT_MIN_S;      // the two-CTA factor above this S (measured: gains at S = 64 and 100)
 constexpr int kPL = 12;    // leading dimension of 8-wide panels (T blocks, the L panel, scratch): conflict-free
 
 // 1/sqrt(x) to full double precision: hardware approximation + two Newton steps
@@ -493,7 +497,7 @@ void launch_spd_factor(const double *Q, int S, double *V, int *info, cudaStream_
     const char *e = getenv("STR_FACTOR_SPLIT");   // A/B knob: 0 = the one-CTA factor
     split = (e && e[0] == '0') ? 0 : 1;
   }
-  if (split && S > 64) {   // (at S <= 64 the V rows are cheap: one CTA)
+  if (split && S > kSplitMinS) {
     static PerDeviceOnce once2;
     once_per_device(once2, [] {
       cudaFuncSetAttribute(k_spd_factor2, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fc_smem_bytes(STR_MAXW));
