@@ -1,7 +1,8 @@
-"""Unit test of the library's SPD inverse (block LDL^T + V^T Dinv V on a cluster; the "^{-1}" of
-G_n(2) = P_n Q_n^{-1}, Alg. 4 l.17 P:379) against LAPACK on random SPD matrices of every size class
-(ragged S, one pivot block, the 128 maximum) and condition numbers up to 1e8; a non-SPD matrix
-must raise the pivot-failure flag."""
+"""Unit test of the library's SPD inverse (the "^{-1}" of G_n(2) = P_n Q_n^{-1}, Alg. 4 l.17 P:379:
+a block Cholesky factor V = L^{-1} of sym(Q), Q^{-1} = V^T V; one CTA for S <= 32, a two-CTA cluster
+above) against LAPACK on random SPD matrices of every size class (ragged S, one pivot block, both
+kernel paths, the 128 maximum) and condition numbers up to 1e8; a non-SPD matrix must raise the
+pivot-failure flag."""
 import ctypes as C
 
 import numpy as np
