@@ -57,6 +57,7 @@ struct TableDesc {
   int32_t Npad;
   float4 *zero = nullptr;   // optional: zeroed by the table kernel (the next contraction's output)
   int64_t zero_n4 = 0;      // float4s to zero
+  float *out32 = nullptr;   // optional: the rows also in fp32 (same layout as out64)
 };
 
 // Epilogue of k_chain_gemm: mode 0 = store C; 1 = Q = H_<2>; 2 = Q += H_<2> (Rn = R_n, Rn1 = R_{n+1}).

@@ -39,6 +39,7 @@
 namespace strb200 {
 
 constexpr int kTcThreads = 512;
+constexpr int kTcThreadsGen = 576;   // + warps 16, 17: table generators with warps 2, 3 (fused pass 2)
 constexpr int kBM = 128;       // UMMA M
 constexpr int kMT = 2;         // M-tiles per CTA (share every B stage)
 constexpr int kBK = 32;        // K per stage (one 128-byte swizzle row of fp32)
@@ -64,7 +65,23 @@ struct TcParams {
   float *Y;              // fp32 output rows (zeroed), row stride W (pass 1: row l + L t)
   long long *dbg;        // optional pipeline trace of CTA 0 (diagnostic; nullptr in production)
   int dbg_flags;         // diagnostic: bit0 skip table loads, bit1 skip X loads, bit2 skip TMEM stores, bit3 one commit per unit, bit4 spin waits, bit5 converters skip smem reads (wrong results)
+  // fused table generation (pass 2, GR > 0): T_L[(l, t)] = F[(l mod P) + P t] G_k(l / P)
+  const float *GA;       // fp32 prefix rows F, each R x R row-major ([a][b]), row f + P t
+  const double *GB;      // G_k core slices, R x R column-major (b + R c), slice i at i R^2
+  int P;                 // prefix period Lf = (I_1/p) I_2 ... I_{k-1} (>= 32)
 };
+
+__device__ __forceinline__ void cp_async16(void *smem, const void *g) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(tc::smem_u32(smem)), "l"(g) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_0() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void gen_bar_sync() { asm volatile("bar.sync 1, 128;" ::: "memory"); }   // the 4 generator warps
+
+__device__ __forceinline__ float tf32_rna_f(float x) {   // round to the nearest tf32 (ties away)
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xFFFFE000u);
+}
 
 __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t (&v)[32]) {
   asm volatile(
@@ -118,8 +135,8 @@ __device__ __forceinline__ long long gtimer() {
   return t;
 }
 
-template <int PASS>
-__global__ void __launch_bounds__(kTcThreads, 1)
+template <int PASS, int GR>
+__global__ void __launch_bounds__(GR ? kTcThreadsGen : kTcThreads, 1)
     k_contract_tf32(const __grid_constant__ CUtensorMap tmap, const __grid_constant__ CUtensorMap ymap,
                     const TcParams p) {
   if (p.dbg && threadIdx.x == 0) p.dbg[1024 + blockIdx.x * 4 + 0] = gtimer();
@@ -133,7 +150,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint8_t *xbuf = smem;
   uint8_t *bbuf = smem + (size_t)SX * XSTAGE;
   uint8_t *ystage = bbuf + (size_t)SB * BBYTES;   // one-tile epilogue staging ([q] dense [32][W] fp32 boxes)
-  uint64_t *xfull = (uint64_t *)(ystage + (p.yred ? ystage_bytes(p.W) : 0));
+  // fused generation: two stages of the K-tile's 32 prefix rows F (fp32, R x R each)
+  float *astage = (float *)(ystage + (p.yred ? ystage_bytes(p.W) : 0));
+  uint64_t *xfull = (uint64_t *)((uint8_t *)astage + (GR ? 2 * 32 * GR * GR * 4 : 0));
   uint64_t *xempty = xfull + SX;
   uint64_t *bfull = xempty + SX;
   uint64_t *bempty = bfull + SB;
@@ -141,6 +160,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   uint64_t *aempty = conv + 2;     // [2] A slot free   (MMA -> converters)
   uint64_t *accf = aempty + 2;     // accumulators complete (MMA -> epilogue)
   uint64_t *acce = accf + 1;       // [2] accumulator of M-tile mt drained (epilogue -> MMA)
+  uint64_t *bfree = bempty;
   uint32_t *tslot = (uint32_t *)(acce + 2);
 
   // warp index broadcast from lane 0: provably warp-uniform, so role branches are uniform and the
@@ -156,7 +176,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       tc::mbar_init(&xempty[s], 8);    // one arrival per converter warp
     }
     for (int s = 0; s < SB; ++s) {
-      tc::mbar_init(&bfull[s], 1);
+      tc::mbar_init(&bfull[s], GR ? 4 : 1);   // (fused: one arrival per generator warp)
       tc::mbar_init(&bempty[s], 1);
     }
     for (int a = 0; a < 2; ++a) {
@@ -220,6 +240,93 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         if (++sx == SX) { sx = 0; phx ^= 1; }
       }
     }
+  } else if (GR && (warp == 2 || warp == 3 || warp == 16 || warp == 17)) {
+    // -------------------------------------------------------------- table generators (fused
+    // subchain generation, Def. 3): lane j forms row l = 32 lb + j of the K-tile,
+    // T_L(l, t) = F(l mod P, t) G_k(l / P) (R x R), for its warp's quarter (rows a, columns c) of
+    // the product, splits each entry into tf32 hi / lo and writes both into the table ring in the
+    // 128B-swizzled K-major layout the MMA reads (row n = a R + c, k-column j): the table never
+    // exists in HBM.  The K-tile's prefix rows F are staged by the four warps themselves with
+    // cp.async (two stages, the next unit's rows in flight while this unit is formed).
+    if constexpr (GR > 0) {
+      constexpr int R = GR, H = GR / 2, RR2 = GR * GR, CH = RR2 / 4;   // CH: 16-byte chunks per row
+      const int gi = warp == 2 ? 0 : warp == 3 ? 1 : warp == 16 ? 2 : 3;
+      const int a0 = (gi & 1) * H, c0 = (gi >> 1) * H;
+      const int gt = gi * 32 + lane;
+      const int Lr = (int)p.L;
+      auto stage_rows = [&](int64_t uu, int st) {
+        const int ktu = (int)(uu % p.KT);
+        const int t = ktu / p.nlb, lb = ktu - t * p.nlb;
+        const int j = gt >> 2, l = lb * 32 + j;   // four threads per row
+        if (l < Lr) {
+          float *dst = astage + st * 32 * RR2 + j * RR2;
+          const float *src = p.GA + ((int64_t)(l % p.P) + (int64_t)p.P * t) * RR2;
+          for (int w = gt & 3; w < CH; w += 4) cp_async16(dst + 4 * w, src + 4 * w);
+        }
+        cp_async_commit();
+      };
+      stage_rows(u0, 0);
+      int sb = 0;
+      uint32_t phb = 0;
+      int kt = (int)(u0 % p.KT);
+      const int kk = lane, chunk = kk >> 2, within = kk & 3;
+      for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0) : 0) {
+        const int sa = (int)((u - u0) & 1);
+        const int lb = kt - (kt / p.nlb) * p.nlb;
+        const int l = lb * 32 + lane;
+        const bool valid = l < Lr;
+        // this lane's G_k slice, columns [c0, c0 + H), as fp32 (at most two distinct slices per
+        // tile: L1 broadcasts)
+        float bv[R][H];
+        {
+          const double *gb = p.GB + (int64_t)(valid ? l / p.P : 0) * RR2;
+#pragma unroll
+          for (int c = 0; c < H; ++c)
+#pragma unroll
+            for (int b = 0; b < R; ++b) bv[b][c] = (float)__ldg(gb + b + R * (c0 + c));
+        }
+        gen_bar_sync();                                  // every generator is done with stage sa ^ 1
+        if (u + 1 < u1) stage_rows(u + 1, sa ^ 1); else cp_async_commit();
+        cp_async_wait_1();                               // this thread's rows of unit u have landed
+        gen_bar_sync();                                  // ... and everyone's
+        const float *arow = astage + sa * 32 * RR2 + lane * RR2;
+        float acc[H][H];
+#pragma unroll
+        for (int a = 0; a < H; ++a) {
+          float av[R];
+#pragma unroll
+          for (int b = 0; b < R; b += 2) {
+            const float2 v2 = *(const float2 *)(arow + (a0 + a) * R + b);
+            av[b] = v2.x;
+            av[b + 1] = v2.y;
+          }
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            float x = 0.0f;
+#pragma unroll
+            for (int b = 0; b < R; ++b) x = fmaf(av[b], bv[b][c], x);
+            acc[a][c] = valid ? x : 0.0f;
+          }
+        }
+        tc::mbar_wait(&bfree[sb], phb ^ 1);               // the MMAs two units back have read the slot
+        float *B = (float *)(bbuf + (size_t)sb * BBYTES);
+#pragma unroll
+        for (int a = 0; a < H; ++a)
+#pragma unroll
+          for (int c = 0; c < H; ++c) {
+            const float hi = tf32_rna_f(acc[a][c]);
+            const float lo = tf32_rna_f(acc[a][c] - hi);
+            const int n = (a0 + a) * R + c0 + c, n2 = p.Npad + n;
+            B[n * 32 + ((chunk ^ (n & 7)) << 2) + within] = hi;
+            B[n2 * 32 + ((chunk ^ (n2 & 7)) << 2) + within] = lo;
+          }
+        tc::fence_proxy_async_smem();   // generic-proxy stores -> the MMA's async-proxy reads
+        __syncwarp();
+        if (lane == 0) tc::mbar_arrive(&bfull[sb]);
+        if (++sb == SB) { sb = 0; phb ^= 1; }
+      }
+      cp_async_wait_0();
+    }
   } else if (warp == 3) {
     if (lane == 0) {
       // ------------------------------------------------------------ table-block producer (own
@@ -229,7 +336,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       int kt = (int)(u0 % p.KT);
       const uint64_t pol = tc::policy_evict_last();    // each table block is read by several CTAs
       for (int64_t u = u0; u < u1; ++u, (++kt == (int)p.KT) ? (kt = 0) : 0) {
-        tc::mbar_wait(&bempty[sb], phb ^ 1);
+        tc::mbar_wait(&bfree[sb], phb ^ 1);
         if (p.dbg && blockIdx.x == gridDim.x / 2 && u - u0 < 64) p.dbg[(u - u0) * 16 + 8] = clock64();
         uint8_t *B = bbuf + (size_t)sb * BBYTES;
         {   // only the W real rows of B_hi and B_lo travel; the padding rows stay zero in smem
@@ -395,7 +502,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
       if (++a == 2) { a = 0; pha ^= 1; }
       if (++sb == SB) { sb = 0; phb ^= 1; }
     }
-  } else if (warp >= 12) {
+  } else if (warp >= 12 && warp < 16) {
     // -------------------------------------------------------------- epilogue
     // Lane quarter q of both accumulators.  yred: tile by tile, TMEM -> a dense [32][W] box in the
     // one-tile staging area -> release that tile's accumulator -> one TMA reduce-add (coalesced,
@@ -515,6 +622,31 @@ using namespace strb200;
 
 static PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
 
+// The instantiations: pass 1, pass 2 from the pre-tiled table, pass 2 with the table generated in
+// the kernel (uniform rank 4 / 8 / 10).
+static void *tf_kernel(int pass, int gr) {
+  if (pass == 1) return (void *)k_contract_tf32<1, 0>;
+  switch (gr) {
+    case 4: return (void *)k_contract_tf32<2, 4>;
+    case 8: return (void *)k_contract_tf32<2, 8>;
+    case 10: return (void *)k_contract_tf32<2, 10>;
+    default: return (void *)k_contract_tf32<2, 0>;
+  }
+}
+
+static int64_t gen_period(const str_state *h) {   // Lf = (I_1/p) I_2 ... I_{k-1}
+  int64_t P = 1;
+  for (int i = 0; i < h->k - 1; ++i) P *= h->md[i].I;
+  return P;
+}
+
+int tf32_gen_rank(const str_state *h) {
+  if (!h->tf_gen_opt || h->contract != STR_CONTRACT_3XTF32 || h->k < 2) return 0;
+  const int R = h->R[h->N - 1];
+  if (!(R == 4 || R == 8 || R == 10) || h->R[h->k - 1] != R || h->R[h->k] != R) return 0;
+  return gen_period(h) >= 32 ? R : 0;
+}
+
 static str_status tf_fail(str_state *h, const std::string &m) {
   h->err = m;
   return STR_E_CUDA;
@@ -539,13 +671,18 @@ str_status tf32_prepare(str_state *h) {
       g_encode = (PFN_cuTensorMapEncodeTiled_v12000)fn;
   });
   if (!g_encode) return tf_fail(h, "cuTensorMapEncodeTiled unavailable");
+  {   // opt-in (measured slower than the pre-tiled table): STR_TF_GEN=1 at str_init
+    const char *e = getenv("STR_TF_GEN");
+    h->tf_gen_opt = e && atoi(e) == 1;
+  }
   static PerDeviceOnce attr_once;
   once_per_device(attr_once, [&] {
-    cudaFuncSetAttribute(k_contract_tf32<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    cudaFuncSetAttribute(k_contract_tf32<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-    prefer_max_smem(k_contract_tf32<1>);
+    for (int v = 0; v < 5; ++v) {
+      const void *f = tf_kernel(v == 0 ? 1 : 2, v <= 1 ? 0 : (v == 2 ? 4 : v == 3 ? 8 : 10));
+      cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+      cudaFuncSetAttribute(f, cudaFuncAttributePreferredSharedMemoryCarveout, cudaSharedmemCarveoutMaxShared);
+    }
     prefer_max_smem(k_zero_f32);
-    prefer_max_smem(k_contract_tf32<2>);
     // (Npad <= 128 keeps 2 Npad x 128 B of table per stage; 3 stages fit)
   });
   h->tf32_ready = true;
@@ -574,7 +711,10 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn) {
     b.bytes = bytes;
     return true;
   };
-  if (!grow(h->tab_split, tiles1) || !grow(h->tab_split2, tiles2) || !grow(h->tf_part, yf) || !grow(h->tf_part2, yf)) {
+  const int gr = tf32_gen_rank(h);
+  const size_t f32 = gr ? (size_t)tn * gen_period(h) * gr * gr * sizeof(float) : 16;
+  if (!grow(h->tab_split, tiles1) || !grow(h->tab_split2, gr ? 16 : tiles2) || !grow(h->tf_part, yf) ||
+      !grow(h->tf_part2, yf) || !grow(h->F32, f32)) {
     h->err = "cudaMalloc failed (3xTF32 workspace)";
     return STR_E_OOM;
   }
@@ -627,9 +767,9 @@ str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, in
   memcpy(&p, g.tf_params[pass - 1], sizeof(TcParams));
   void *args[3] = {&tmap, &ymap, &p};
   cudaKernelNodeParams kp = {};
-  kp.func = pass == 1 ? (void *)k_contract_tf32<1> : (void *)k_contract_tf32<2>;
+  kp.func = tf_kernel(pass, g.tf_gen[pass - 1]);
   kp.gridDim = dim3(g.tf_grid[pass - 1]);
-  kp.blockDim = dim3(kTcThreads);
+  kp.blockDim = dim3(g.tf_gen[pass - 1] ? kTcThreadsGen : kTcThreads);
   kp.sharedMemBytes = (unsigned)g.tf_smem[pass - 1];
   kp.kernelParams = args;
   kp.extra = nullptr;
@@ -658,9 +798,12 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   const int bbytes = 2 * Np * 128;
   p.yred = (W % 4 == 0 && W <= 128) ? 1 : 0;   // TMA needs 16-byte row strides; box width <= 256
   const int ybytes = p.yred ? ystage_bytes(W) : 0;
+  const int gr = pass == 2 ? tf32_gen_rank(h) : 0;
+  const int gbytes = gr ? 2 * 32 * gr * gr * 4 : 0;   // the two prefix-row stages (fused generation)
   p.bstages = 2;
   if (const char *ev = getenv("STR_TF_BSTAGES")) p.bstages = std::max(2, atoi(ev));   // tuning knob
-  p.stages = std::min(6, (int)((227 * 1024 - 1024 - 256 - ybytes - p.bstages * bbytes) / (kMT * kABytes)));
+  p.stages = std::min(6, (int)((227 * 1024 - 1024 - 256 - ybytes - gbytes - p.bstages * bbytes) / (kMT * kABytes)));
+
   if (p.stages < 2) {
     h->err = "3xTF32 contraction: shared memory too small for the ring depths";
     return -1;
@@ -683,6 +826,9 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
   p.upc = cdiv(p.U, grid);
   grid = (int)cdiv(p.U, p.upc);
   p.Btiles = (const float *)(pass == 1 ? h->tab_split.p : h->tab_split2.p);
+  p.GA = gr ? (const float *)h->F32.p : nullptr;
+  p.GB = gr ? (const double *)h->md[h->k - 1].G.p : nullptr;
+  p.P = gr ? (int)gen_period(h) : 1;
   p.Y = Y;
   p.dbg = h->tf_dbg ? h->tf_dbg + (pass - 1) * str_state::kTfDbgWords : nullptr;
   p.dbg_flags = 0;
@@ -703,12 +849,16 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
     k_zero_f32<<<(unsigned)std::min<int64_t>(296, (n4 + 255) / 256), 256, 0, st>>>((float4 *)p.Y, n4);
     tl_mark(h, "zero_y");
   }
-  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + 1024 + 256;
+  const size_t smem = (size_t)p.stages * kMT * kABytes + (size_t)p.bstages * bbytes + ybytes + gbytes + 1024 + 256;
   prof_mark(h, 2 * (pass - 1));
-  if (pass == 1)
-    k_contract_tf32<1><<<grid, kTcThreads, smem, st>>>(tmap, ymap, p);
-  else
-    k_contract_tf32<2><<<grid, kTcThreads, smem, st>>>(tmap, ymap, p);
+  {
+    void *args[3] = {&tmap, &ymap, &p};
+    if (cudaLaunchKernel(tf_kernel(pass, gr), dim3(grid), dim3(gr ? kTcThreadsGen : kTcThreads), args, smem, st) !=
+        cudaSuccess) {
+      h->err = "contraction launch failed";
+      return -1;
+    }
+  }
   if (h->capturing) {
     // remember the node so that graph replays can re-point it at new X (tf32_graph_update)
     cudaStreamCaptureStatus cs;
@@ -725,6 +875,7 @@ int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t t
     memcpy(g.tf_ymap[pass - 1], &ymap, sizeof(CUtensorMap));
     g.tf_grid[pass - 1] = grid;
     g.tf_smem[pass - 1] = smem;
+    g.tf_gen[pass - 1] = gr;
   }
   tl_mark(h, pass == 1 ? "contract_tf32_p1" : "contract_tf32_p2");
   prof_mark(h, 2 * (pass - 1) + 1);

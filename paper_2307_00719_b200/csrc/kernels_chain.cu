@@ -820,6 +820,12 @@ __global__ void k_build_table2(TableDesc td, double *__restrict__ out64, float *
       for (int q = 0; q < MR; ++q)
         if (q < Rl) o[q] = v[q];
     }
+    if (td.out32) {
+      float *o = td.out32 + (int64_t)e * W + pr * Rl;
+#pragma unroll
+      for (int q = 0; q < MR; ++q)
+        if (q < Rl) o[q] = (float)v[q];
+    }
     if (tiles) {
       const int kk = el, chunk = kk >> 2, within = kk & 3;
 #pragma unroll
@@ -939,6 +945,14 @@ __global__ void __launch_bounds__(256) k_build_table3(TableDesc td, double *__re
         double *o = out64 + (int64_t)e * AB + (pr + r) * R;
 #pragma unroll
         for (int q = 0; q < R; ++q) o[q] = v[r][q];
+      }
+    }
+    if (td.out32) {
+#pragma unroll
+      for (int r = 0; r < 2; ++r) {
+        float *o = td.out32 + (int64_t)e * AB + (pr + r) * R;
+#pragma unroll
+        for (int q = 0; q < R; ++q) o[q] = (float)v[r][q];
       }
     }
     if (tiles) {

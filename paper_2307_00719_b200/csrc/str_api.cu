@@ -278,6 +278,20 @@ static TableDesc desc_TL(const str_state *h, int64_t t0, int64_t tn) {
 // is cleared at its full capacity, since the next step's t_new is not known when it is built.
 static str_status build_pass_table(str_state *h, int pass, const double *trows, int64_t tn) {
   const int W = RR(h, h->k + 1) * RR(h, h->N);
+  if (pass == 2 && tf32_gen_rank(h) > 0) {
+    // fused generation: only the prefix rows F[(f, t)] = G_N(t) G_1(i_1) ... G_{k-1}(i_{k-1}) (fp32,
+    // tn Lf rows); the contraction multiplies each K-tile's rows by G_k itself
+    TableDesc td = desc_TL_at(h, trows, tn);
+    td.fl.n -= 1;   // drop G_k
+    int64_t Lf = 1;
+    for (int i = 1; i <= h->k - 1; ++i) Lf *= h->md[i - 1].I;
+    td.fl.f[0].stride = Lf;
+    td.Lk = Lf;
+    td.out32 = (float *)h->F32.p;
+    td.zero = (float4 *)h->tf_part2.p;
+    td.zero_n4 = (h->Rr * W + 3) / 4;
+    return build_table(h, td, nullptr, nullptr, "table_F");
+  }
   TableDesc td = pass == 1 ? desc_TR(h) : desc_TL_at(h, trows, tn);
   if (h->contract == STR_CONTRACT_3XTF32) {
     td.Npad = tf32_npad(W);
@@ -579,6 +593,7 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
   const double *Bj = nullptr;                       // B_j (R_{j-1}^2 x R_{j+1}^2), j >= 2
   const void *YR = nullptr;
   bool yr32 = false;
+  const int k2 = tf32_gen_rank(h) > 0 ? k - 1 : k;   // the mode after whose rows pass 2's table is built
   for (int j = 1; j <= N - 1; ++j) {
     ModeBuf &m = h->md[j - 1];
     const int S = RR(h, j) * RR(h, j + 1);
@@ -653,13 +668,14 @@ static str_status update_det_enqueue(str_state *h, const void *X, int64_t tn) {
     h->st = C;
     CU(wait(C, evP));
     TRY(finish_rows(h, j));
-    if (j == k || j == N - 1) {
-      // third branch: pass 2's table (G_N^new and the new G_1..G_k) beside Z_k, or the next step's
-      // pass-1 table (final right-group cores) beside Z_{N-1}
+    if (j == k2 || j == N - 1) {
+      // third branch: pass 2's table (G_N^new and the new G_1..G_k) beside Z_k -- with the fused
+      // generation only its prefix rows (G_N^new, G_1..G_{k-1}), beside Z_{k-1} -- or the next
+      // step's pass-1 table (final right-group cores) beside Z_{N-1}
       CU(rec(h->ev_fork3, C));
       CU(wait(T3, h->ev_fork3));
       h->st = T3;
-      TRY(build_pass_table(h, j == k ? 2 : 1, j == k ? GN_new : nullptr, tn));
+      TRY(build_pass_table(h, j == k2 ? 2 : 1, j == k2 ? GN_new : nullptr, tn));
       CU(rec(h->ev_join3, T3));
       h->st = C;
     }
@@ -1409,6 +1425,10 @@ extern "C" STR_API str_status strdbg_contract(str_state *h, const void *X, int32
   }
   return STR_OK;
 }
+
+// Test hook (not in include/str.h): the uniform rank of pass 2's in-kernel table generation for this
+// handle (0: pass 2 reads the pre-tiled table).
+extern "C" STR_API int32_t strdbg_tf32_gen_rank(const str_state *h) { return h ? tf32_gen_rank(h) : -1; }
 
 // Launch-cost probe (diagnostic, not in include/str.h): builds the pass's table once, then times
 // `reps` back-to-back launches of only the contraction (memset + kernel) between two events on the

@@ -98,6 +98,10 @@ struct str_state {
   bool tf32_ready = false;
   DevBuf tab_split, tab_split2;     // hi/lo fp32 tables of the tensor-core passes 1 and 2
   DevBuf tf_part, tf_part2;         // pass-1 / pass-2 fp32 outputs (stream-K red.add targets)
+  // pass 2 with in-kernel table generation (tf32_gen_rank > 0): the fp32 prefix rows
+  // F[(f, t)] = G_N(t) G_1(i_1) ... G_{k-1}(i_{k-1}); the contraction forms T_L = F G_k per K-tile
+  DevBuf F32;
+  bool tf_gen_opt = false;          // STR_TF_GEN=1 at str_init: pass 2 generates its table in the kernel
 
   // CUDA-graph replay of the STR step: the step is captured once per t_new and
   // replayed; X enters through the device slot dX (f64 path) or by re-pointing the two tensor-core
@@ -117,6 +121,7 @@ struct str_state {
     alignas(64) unsigned char tf_ymap[2][128];   // CUtensorMap of the pass outputs (TMA reduce epilogue)
     int tf_grid[2] = {0, 0};
     size_t tf_smem[2] = {0, 0};
+    int tf_gen[2] = {0, 0};   // rank of the in-kernel table generation (0: pre-tiled table)
     void reset() {
       if (exec) cudaGraphExecDestroy(exec);
       if (graph) cudaGraphDestroy(graph);
@@ -178,7 +183,7 @@ struct str_state {
     for (auto &b : Sf) fr(b);
     fr(Lp[0]); fr(Lp[1]); fr(T1); fr(H); fr(Hq); fr(Hi);
     fr(TR); fr(TL); fr(YL); fr(YR); fr(Wt); fr(tmpA); fr(tmpB); fr(Mt); fr(ws); fr(Xstage); fr(info_buf);
-    fr(tab_split); fr(tab_split2); fr(tf_part); fr(tf_part2);
+    fr(tab_split); fr(tab_split2); fr(tf_part); fr(tf_part2); fr(F32);
     fr(GNnew); fr(dT); fr(dX);
     gs[0].reset();
     gs[1].reset();
@@ -225,5 +230,11 @@ str_status tf32_ensure_workspace(str_state *h, int64_t tn);
 // (zeroed here unless y_zeroed, then accumulated).  Returns 0, or -1 with h->err set.
 int launch_contract_tf32(str_state *h, const void *X, int pass, int W, int64_t tn, float *Y, bool y_zeroed);
 int tf32_npad(int W);
+// Pass 2 forms its table in the contraction kernel (the fused subchain generation) when this returns
+// the uniform rank R (> 0): R_N = R_k = R_{k+1} = R in {4, 8, 10}, k >= 2, and the prefix period
+// Lf = (I_1/p) I_2 ... I_{k-1} >= 32 (a K-tile of 32 rows then spans at most two G_k slices);
+// 0 otherwise (the pre-tiled table path).  Opt-in per handle (STR_TF_GEN=1 at str_init): measured
+// slower than the pre-tiled table at C5.
+int tf32_gen_rank(const str_state *h);
 // Re-point captured contraction node `pass` of exec at new data X (3xTF32 path).
 str_status tf32_graph_update(str_state *h, int slot, int pass, const void *X, int64_t tn);

@@ -69,7 +69,15 @@ def test_contract_f64(name, pass_):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("name", ["P2", "P5"])
+@pytest.mark.parametrize("name", ["P2", "P5", "G4", "G8", "G10"])
 @pytest.mark.parametrize("pass_", [1, 2])
 def test_contract_3xtf32(name, pass_):
     assert _run(name, "3xtf32", pass_) < TOL["3xtf32"]
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("name", ["G4", "G8", "G10"])
+def test_contract_3xtf32_fused_pass2(name, monkeypatch):
+    """Pass 2 with its table formed inside the contraction kernel (opt-in STR_TF_GEN=1 at str_init)."""
+    monkeypatch.setenv("STR_TF_GEN", "1")
+    assert _run(name, "3xtf32", 2) < TOL["3xtf32"]

@@ -65,7 +65,7 @@ int main() {
   cudaFuncSetAttribute(k_probe<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   cudaFuncSetAttribute(k_probe<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int iters = 2000;
-  for (int ce : {0, 1, 2}) for (int N : {112}) {
+  for (int ce : {0, 1}) for (int N : {64, 96, 104, 112, 128, 256}) {
     for (int ts = 1; ts >= 0; --ts) {
       printf("commit every %d: ", ce);
       if (ts) k_probe<true><<<1, 128, 100 * 1024>>>(N, iters, d, ce); else k_probe<false><<<1, 128, 100 * 1024>>>(N, iters, d, ce);

@@ -103,6 +103,14 @@ CONFIGS.update({
     "P6": StreamConfig("P6", (36, 29, 23), (12, 10, 11, 9), 10, 4, 3, "f32", "3xtf32",
                        core_scale=12 ** -0.5, noise_abs=1e-2, seed=61),
     # rSTR parity: I_k > R_kR_{k+1} so leverage scores are non-uniform; m >= max R_nR_{n+1}.
+    # Fused pass-2 table generation (uniform rank R in {4, 8, 10}, k = 2, I_1 >= 32): K-tiles that
+    # cross a multiple of I_1 (G4, G10) or align with it (G8), ragged last K-tile and M-tile.
+    "G4": StreamConfig("G4", (36, 7, 30, 9), (4, 4, 4, 4, 4), 6, 3, 3, "f32", "3xtf32",
+                       core_scale=0.5, noise_abs=1e-2, seed=71, split_k=2),
+    "G8": StreamConfig("G8", (32, 5, 20, 8), (8, 8, 8, 8, 8), 6, 3, 3, "f32", "3xtf32",
+                       core_scale=8 ** -0.5, noise_abs=1e-2, seed=72, split_k=2),
+    "G10": StreamConfig("G10", (40, 6, 13, 11), (10, 10, 10, 10, 10), 6, 2, 3, "f32", "3xtf32",
+                        core_scale=10 ** -0.5, noise_abs=1e-2, seed=73, split_k=2),
     "R4": StreamConfig("R4", (30, 25, 20), (2, 3, 2, 3), 6, 4, 3, "f32", "f64",
                        core_scale=0.7, noise_abs=1e-2, seed=41, sketch_rows=200),
     "R5": StreamConfig("R5", (12, 9, 10, 8), (2, 3, 2, 2, 3), 5, 3, 3, "f64", "f64",
