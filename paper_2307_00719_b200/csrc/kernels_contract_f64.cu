@@ -154,7 +154,7 @@ static void dispatch_w(const void *const *X, const double *B, int W, int64_t L, 
 int contract_f64_splits(int64_t M, int64_t K) {
   int64_t mt = cdiv(M, BM);
   // ~2 CTAs per SM, and K chunks of at most ~640 (long chunks leave the few M-tiles of a
-  // large-K pass latency-bound: C5 FP64 pass 2, 12 -> 20 splits, 347 -> ~250 us; tools/gpu_r2bl.sh)
+  // large-K pass latency-bound: C5 FP64 pass 2, 12 -> 20 splits, 347 -> ~250 us; tools/runs/gpu_r2bl.sh)
   int64_t want = std::max<int64_t>(cdiv(2 * 148, mt), cdiv(K, 640));
   int64_t maxs = cdiv(K, 2 * BK);
   int64_t s = want < maxs ? want : maxs;
