@@ -64,7 +64,7 @@ constexpr int kFcThreads = FC_THREADS;          // factor CTA: warp 0 pivots, th
 constexpr int kFcWarps = kFcThreads / 32;
 constexpr int kFcWorkers = FC_EXCL ? kFcWarps - kFcWarps / 4 : kFcWarps - 1;
 __device__ __forceinline__ int fc_worker_id(int warp) { return FC_EXCL ? ((warp & 3) ? warp - warp / 4 - 1 : -1) : warp - 1; }
-constexpr int kRsThreads = 256;                 // rows-solve CTA (8 warps x 2 column tiles: S <= 128)
+constexpr int kRsThreads = 512;                 // rows-solve CTA (16 warps, one column tile each: S <= 128)
 #ifndef FC_SPLIT_MIN_S
 #define FC_SPLIT_MIN_S 32
 #endif
@@ -552,33 +552,37 @@ __global__ void __launch_bounds__(kRsThreads, 1)
   cpa_commit();
   cpa_wait<0>();
   __syncthreads();
-  double y[2][2];
-  int cc[2] = {-1, -1};
-#pragma unroll
-  for (int q = 0; q < 2; ++q) {   // Y[:, c] = sum_{k <= c} P[:, k] V[c][k]  (B[k][n] = V[n][k]: tn, V rows at c)
-    const int c = warp + 8 * q;
-    y[q][0] = y[q][1] = 0.0;
-    if (c < nt) {
-      cc[q] = c;
-      for (int k = 0; k <= c; ++k) dmma8_tn(y[q], Ps + 8 * k, LD, Vs + (8 * c) * LD + 8 * k, LD, g, t);
+  // one column tile per warp (nt <= 16); each product runs on two accumulator chains (even / odd k)
+  const int c = warp;
+  const bool act = c < nt;
+  double y[2] = {0.0, 0.0}, y2[2] = {0.0, 0.0};
+  if (act) {   // Y[:, c] = sum_{k <= c} P[:, k] V[c][k]  (B[k][n] = V[n][k]: tn, V rows at c)
+    int k = 0;
+    for (; k + 1 <= c; k += 2) {
+      dmma8_tn(y, Ps + 8 * k, LD, Vs + (8 * c) * LD + 8 * k, LD, g, t);
+      dmma8_tn(y2, Ps + 8 * (k + 1), LD, Vs + (8 * c) * LD + 8 * (k + 1), LD, g, t);
     }
+    if (k <= c) dmma8_tn(y, Ps + 8 * k, LD, Vs + (8 * c) * LD + 8 * k, LD, g, t);
+    y[0] += y2[0];
+    y[1] += y2[1];
   }
   __syncthreads();   // every warp has read P
-#pragma unroll
-  for (int q = 0; q < 2; ++q)
-    if (cc[q] >= 0) frag_store(y[q], Ps + 8 * cc[q], LD, g, t);
+  if (act) frag_store(y, Ps + 8 * c, LD, g, t);
   __syncthreads();
+  if (!act) return;
+  double o[2] = {0.0, 0.0}, o2[2] = {0.0, 0.0};   // out[:, c] = sum_{k >= c} Y[:, k] V[k][c]  (B = V rows at k: nn)
+  int k = c;
+  for (; k + 1 < nt; k += 2) {
+    dmma8_nn(o, Ps + 8 * k, LD, Vs + (8 * k) * LD + 8 * c, LD, g, t);
+    dmma8_nn(o2, Ps + 8 * (k + 1), LD, Vs + (8 * (k + 1)) * LD + 8 * c, LD, g, t);
+  }
+  if (k < nt) dmma8_nn(o, Ps + 8 * k, LD, Vs + (8 * k) * LD + 8 * c, LD, g, t);
+  o[0] += o2[0];
+  o[1] += o2[1];
 #pragma unroll
-  for (int q = 0; q < 2; ++q) {   // out[:, c] = sum_{k >= c} Y[:, k] V[k][c]  (B = V rows at k: nn)
-    const int c = cc[q];
-    if (c < 0) continue;
-    double o[2] = {0.0, 0.0};
-    for (int k = c; k < nt; ++k) dmma8_nn(o, Ps + 8 * k, LD, Vs + (8 * k) * LD + 8 * c, LD, g, t);
-#pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      const int col = 8 * c + 2 * t + e;
-      if (g < nr && col < S) out[(r0 + g) * S + col] = o[e];
-    }
+  for (int e = 0; e < 2; ++e) {
+    const int col = 8 * c + 2 * t + e;
+    if (g < nr && col < S) out[(r0 + g) * S + col] = o[e];
   }
 }
 
