@@ -564,6 +564,22 @@ static str_status rstr_workspace(str_state *h, int64_t tn) {
   return STR_OK;
 }
 
+// G_S[2] and X_S[n] of mode n (Alg. 7 l.12-14): both need only the index table.  For rSTR-K the
+// gather (which also unmixes the fibers, Alg. 9 l.27) runs on the side stream beside the complex
+// sampled chain (C4: 0.662 -> 0.628 ms per step); for rSTR-U/L the plain gather is too short to pay
+// for the graph's cross-stream join (measured: 0.163 -> 0.182 ms), so the two stay in stream order.
+static str_status chain_and_fibers(str_state *h, const void *X, int n, int64_t tn, double *GS, double *XS) {
+  if (!h->ksrft()) {
+    RTRY(sampled_chain(h, n, GS));
+    return gather_fibers(h, X, n, tn, XS);
+  }
+  RTRY(rs_fork(h));
+  RTRY(gather_fibers(h, X, n, tn, XS));
+  rs_main(h);
+  RTRY(sampled_chain(h, n, GS));
+  return rs_join(h);
+}
+
 // Accumulate the sampled normal equations of mode n (1..N-1) from X (tn slices): P_n (+)= X_S G_S,
 // Q_n (+)= G_S^T G_S (Alg. 7 l.15-16 / l.36-37); with `solve`, then G_n = P_n Q_n^{-1} (l.38).  The
 // Gram and the inverse run on the side stream beside X_S G_S.
@@ -573,8 +589,7 @@ static str_status sampled_normal_eq(str_state *h, const void *X, int n, int64_t 
   double *GS = (double *)h->sidx.p;
   double *XS = (double *)h->sX.p;
   const int64_t K = h->ksrft() ? 2 * h->m : h->m;   // rSTR-K: [Re X~, Im X~][Re G^; Im G^] (reading R21)
-  RTRY(sampled_chain(h, n, GS));
-  RTRY(gather_fibers(h, X, n, tn, XS));
+  RTRY(chain_and_fibers(h, X, n, tn, GS, XS));
   RTRY(rs_fork(h));
   gemm(h, GS, 1, S, GS, S, 1, (double *)mb.Q.p, S, S, K, acc, 1, true);   // Q_n += sym(G_S^T G_S)
   if (solve) {
@@ -644,8 +659,7 @@ static str_status rstr_enqueue(str_state *h, const void *X, int64_t tn) {
   double *K = (double *)h->sGram.p;
   double *M = (double *)h->Mt.p;
   double *GN_new = (double *)h->GNnew.p;
-  RTRY(sampled_chain(h, N, GS));
-  RTRY(gather_fibers(h, X, N, tn, XS));
+  RTRY(chain_and_fibers(h, X, N, tn, GS, XS));
   // rSTR-K: the real halves only, Re(X~) Re(G^) (Re(G^)^T Re(G^))^{-1} (reading R22)
   RTRY(rs_fork(h));   // the Gram and its inverse beside X_S G_S
   gemm(h, GS, 1, SN, GS, SN, 1, K, SN, SN, h->m, 0, 1, true);
@@ -709,7 +723,7 @@ str_status rstr_update(str_state *h, const void *X, int64_t tn) {
         h->err = std::string("rSTR graph capture: ") + cudaGetErrorString(e);
         return STR_E_CUDA;
       }
-      e = cudaGraphInstantiate(&g.exec, cg, 0);
+      e = cudaGraphInstantiate(&g.exec, cg, h->chain_prio ? cudaGraphInstantiateFlagUseNodePriority : 0);
       if (e != cudaSuccess) {
         cudaGraphDestroy(cg);
         h->err = std::string("rSTR graph instantiate: ") + cudaGetErrorString(e);

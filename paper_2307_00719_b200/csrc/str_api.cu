@@ -732,7 +732,7 @@ static str_status update_det(str_state *h, const void *X, int64_t tn) {
         return st;
       }
       if (e != cudaSuccess) return fail(h, STR_E_CUDA, std::string("graph capture: ") + cudaGetErrorString(e));
-      e = cudaGraphInstantiate(&g.exec, cg, 0);
+      e = cudaGraphInstantiate(&g.exec, cg, h->chain_prio ? cudaGraphInstantiateFlagUseNodePriority : 0);
       if (e != cudaSuccess) {
         cudaGraphDestroy(cg);
         return fail(h, STR_E_CUDA, std::string("graph instantiate: ") + cudaGetErrorString(e));
@@ -1000,7 +1000,13 @@ extern "C" str_status str_init(const str_config *cfg, const void *X_init, int64_
     return STR_E_CUDA;
   }
   if (cudaDeviceGetAttribute(&h->nsm, cudaDevAttrMultiProcessorCount, cfg->device) != cudaSuccess) h->nsm = 148;
-  if (cudaStreamCreateWithFlags(&h->st2, cudaStreamNonBlocking) != cudaSuccess ||
+  // STR_CHAIN_PRIO=1 (A/B knob): the chain stream at the highest priority, kept by the step graph's
+  // kernel nodes (cudaGraphInstantiateFlagUseNodePriority), so the serial chain's small kernels are
+  // placed ahead of queued absorb / table CTAs
+  int prio_lo = 0, prio_hi = 0;
+  cudaDeviceGetStreamPriorityRange(&prio_lo, &prio_hi);
+  h->chain_prio = getenv("STR_CHAIN_PRIO") && getenv("STR_CHAIN_PRIO")[0] == '1';
+  if (cudaStreamCreateWithPriority(&h->st2, cudaStreamNonBlocking, h->chain_prio ? prio_hi : 0) != cudaSuccess ||
       cudaStreamCreateWithFlags(&h->st3, cudaStreamNonBlocking) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_fork, cudaEventDisableTiming) != cudaSuccess ||
       cudaEventCreateWithFlags(&h->ev_join, cudaEventDisableTiming) != cudaSuccess ||

@@ -132,6 +132,7 @@ struct str_state {
   };
   GraphSlot gs[2];                  // [0] production replay, [1] profiling replay (events around the passes)
   int cur_slot = 0;                 // slot being captured / replayed
+  bool chain_prio = false;          // STR_CHAIN_PRIO=1: chain stream at the highest priority (A/B knob)
   cudaEvent_t pev[4] = {};          // profiling: pass-1 begin/end, pass-2 begin/end
   double prof_ms[2] = {0.0, 0.0};
   int64_t prof_n[2] = {0, 0};
