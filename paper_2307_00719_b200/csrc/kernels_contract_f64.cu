@@ -156,11 +156,24 @@ int contract_f64_splits(int64_t M, int64_t K) {
   // ~2 CTAs per SM, and K chunks of at most ~640 (long chunks leave the few M-tiles of a
   // large-K pass latency-bound: C5 FP64 pass 2, 12 -> 20 splits, 347 -> ~250 us; tools/runs/gpu_r2bl.sh)
   int64_t want = std::max<int64_t>(cdiv(2 * 148, mt), cdiv(K, 640));
-  int64_t maxs = cdiv(K, 2 * BK);
+  int64_t maxs = std::min<int64_t>(64, cdiv(K, 2 * BK));
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;
-  if (s > 64) s = 64;
-  return (int)s;
+  // Whole waves: the grid runs in ceil(mt s / slots) waves of 2 x 148 resident CTAs, each as long as
+  // one K chunk, so a split count that just spills into another wave wastes most of it (C5 FP64 pass 1:
+  // 3 splits = 600 CTAs = 2.03 waves, ncu: the FP64 pipe 50% busy; profiles/r02f_ncu_contract_f64.txt).
+  // Among s .. 2s pick the count with the least waves x chunk, plus the split's share of the reduce
+  // (its partial written and read once, in units of one CTA's K step).
+  const int64_t slots = 2 * 148;
+  auto cost = [&](int64_t c) {
+    const int64_t chunk = cdiv(cdiv(K, c), BK) * BK;
+    const int64_t real = cdiv(K, chunk);
+    return (double)(cdiv(mt * real, slots) * chunk) + (real > 1 ? (double)real * (double)M * 4e-3 : 0.0);
+  };
+  int64_t best = s;
+  for (int64_t c = s + 1; c <= std::min<int64_t>(maxs, 2 * s); ++c)
+    if (cost(c) < cost(best) * 0.97) best = c;
+  return (int)best;
 }
 
 // Returns the number of kernel launches.
