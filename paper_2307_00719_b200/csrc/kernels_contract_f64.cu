@@ -159,20 +159,22 @@ int contract_f64_splits(int64_t M, int64_t K) {
   int64_t maxs = std::min<int64_t>(64, cdiv(K, 2 * BK));
   int64_t s = want < maxs ? want : maxs;
   if (s < 1) s = 1;
-  // Whole waves: the grid runs in ceil(mt s / slots) waves of 2 x 148 resident CTAs, each as long as
-  // one K chunk, so a split count that just spills into another wave wastes most of it (C5 FP64 pass 1:
-  // 3 splits = 600 CTAs = 2.03 waves, ncu: the FP64 pipe 50% busy; profiles/r02f_ncu_contract_f64.txt).
-  // Among s .. 2s pick the count with the least waves x chunk, plus the split's share of the reduce
-  // (its partial written and read once, in units of one CTA's K step).
-  const int64_t slots = 2 * 148;
+  // Whole waves: a grid that just spills into another wave of resident CTAs wastes most of it (C5 FP64
+  // pass 1: 3 splits = 600 CTAs = 2.03 waves of 2 x 148, ncu: the FP64 pipe 50% busy;
+  // profiles/r02f_ncu_contract_f64.txt).  Two CTAs resident on an SM share its FP64 pipe, so the
+  // cost of a split count is scored at both granularities — waves of 296 CTAs (residency) and of 148
+  // (one CTA's work per SM) — times the chunk length, plus the split's share of the reduce (its
+  // partial written and read once, in units of one CTA's K step); the best of s .. 2s is taken
+  // (measured: C5 FP64 0.705 -> 0.634 ms per step with 5 / 23 splits, C4 FP64 best with 37 / 3).
   auto cost = [&](int64_t c) {
     const int64_t chunk = cdiv(cdiv(K, c), BK) * BK;
     const int64_t real = cdiv(K, chunk);
-    return (double)(cdiv(mt * real, slots) * chunk) + (real > 1 ? (double)real * (double)M * 4e-3 : 0.0);
+    return (double)((cdiv(mt * real, 296) + cdiv(mt * real, 148)) * chunk) +
+           (real > 1 ? (double)real * (double)M * 4e-3 : 0.0);
   };
   int64_t best = s;
   for (int64_t c = s + 1; c <= std::min<int64_t>(maxs, 2 * s); ++c)
-    if (cost(c) < cost(best) * 0.97) best = c;
+    if (cost(c) < cost(best) * 0.995) best = c;
   return (int)best;
 }
 
